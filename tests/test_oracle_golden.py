@@ -1,0 +1,170 @@
+"""Pin the CPU oracle to the reference: KATs from the reference's own tests
+plus golden vectors produced by running the reference (tests/golden)."""
+
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import tailorkv_oracle as O
+
+GOLD = Path(__file__).resolve().parent / "golden"
+META = json.loads((GOLD / "golden.json").read_text())
+KER = np.load(GOLD / "kernels.npz")
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+# -- known-answer tests restated from the reference suite --------------------
+
+
+def test_bit_order_kats():
+    # test_quantizer.py:118-124
+    assert O.pack_codes([1, 0, 1, 1, 0, 0, 0, 1], 1).tolist() == [0b10001101]
+    assert O.pack_codes([3, 0, 1, 2], 2).tolist() == [0b10010011]
+
+
+def test_param_kats():
+    # test_quantizer.py:41-52
+    assert O.group_scale(0.0, 3.0, 2) == 1.0
+    assert O.group_scale(-1.0, 3.0, 1) == 4.0
+    assert O.group_scale(5.0, 5.0, 1) == 1.0
+    assert O.encode([-1.0, 3.0], -1.0, 4.0, 1).tolist() == [0, 1]
+
+
+def test_key_stream_order_kat():
+    # test_quantizer.py:196-202
+    t = O.quantize_keys(np.arange(8.0).reshape(4, 2), 1, 2)
+    assert O.unpack_codes(O.pack_codes(t.code_stream(), 1), 1, 8).tolist() == [0, 1] * 4
+
+
+def test_channel_score_kats():
+    # test_retriever.py:53-77, 84-103
+    assert O.group_channel_scores(np.array([1.0, -3.0, 0.5]), np.array([2.0, 1.0, 4.0])).tolist() == [2.0, 3.0, 2.0]
+    assert O.group_channel_scores(np.array([[1.0, -1.0], [-2.0, 3.0]]), np.array([1.0, 2.0])).tolist() == [3.0, 8.0]
+    assert O.select_channels(np.array([5.0, 5.0, 1.0]), 1).tolist() == [0]
+    assert O.select_channels(np.array([1.0, 9.0, 3.0, 8.0]), 2).tolist() == [1, 3]
+
+
+def test_topk_kats():
+    # test_retriever.py:151-171
+    assert O.select_tokens(np.zeros(10), 2, 3).tolist() == [5, 6, 7, 8, 9]
+    assert O.select_tokens(np.ones(10), 4, 8).tolist() == list(range(10))
+
+
+def test_pack_roundtrip_random():
+    rng = np.random.default_rng(1)
+    for bits in (1, 2):
+        c = rng.integers(0, 2**bits, size=10_001).astype(np.uint8)
+        assert np.array_equal(O.unpack_codes(O.pack_codes(c, bits), bits, c.size), c)
+
+
+# -- golden vectors from the reference ---------------------------------------
+
+
+@pytest.mark.parametrize("case", cases.PACK_CASES, ids=lambda c: c["name"])
+def test_pack_golden(case):
+    k, v = cases.pack_inputs(case)
+    g = META["pack"][case["name"]]
+    with np.errstate(over="ignore"):
+        kb = O.quantize_keys(k, case["bits"], case["g"]).to_bytes()
+        vb = O.quantize_values(v, case["bits"], case["g"]).to_bytes()
+    assert sha(kb) == g["keys_sha256"] and len(kb) == g["keys_len"]
+    assert sha(vb) == g["values_sha256"] and len(vb) == g["values_len"]
+
+
+def test_incremental_append_matches_batch():
+    # test_quantizer.py:204-222 restated on the oracle
+    rng = np.random.default_rng(5)
+    k = cases.f16(rng.normal(size=(70, 8)))
+    t = O.quantize_keys(k[:69], 1, 16)
+    t.append(k[69])
+    full = O.quantize_keys(k, 1, 16)
+    assert t.to_bytes() == full.to_bytes()
+
+
+@pytest.mark.parametrize("case", cases.DECODE_CASES, ids=lambda c: c["name"])
+def test_quant_decode_golden(case):
+    keys, values, queries = cases.decode_inputs(case)
+    kq, vq = O.quantize_layer(keys, values, case["bits"], case["g"])
+    out = O.quant_layer_decode(queries, kq, vq)
+    np.testing.assert_allclose(out, KER[case["name"] + "/out"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(O.qgemv_scores(queries[0], kq[0]), KER[case["name"] + "/logits0"],
+                               rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("case", cases.TOPK_CASES, ids=lambda c: c["name"])
+def test_topk_golden(case):
+    sel = O.select_tokens(cases.topk_scores(case), case["n_local"], case["n_topk"])
+    assert np.array_equal(sel, KER[case["name"]])
+
+
+@pytest.mark.parametrize("case", cases.CHANNEL_CASES, ids=lambda c: c["name"])
+def test_channels_golden(case):
+    qhat, chmax = cases.channel_inputs(case)
+    sel = O.select_channels(O.group_channel_scores(qhat, chmax), case["d_s"])
+    assert np.array_equal(sel, KER[case["name"]])
+
+
+def test_calibrate_golden():
+    for c in cases.CALIB_CASES:
+        pq, pk = cases.calib_inputs(c)
+        g = META["calibrate"][c["name"]]
+        got = O.calibrate(list(pq), list(pk), g["k"], n_q=c["n_q"], tau=c["tau"])
+        for (hs, m, lab), ref in zip(got, g["layers"]):
+            np.testing.assert_allclose(hs, ref["scores"], rtol=1e-12)
+            assert lab == ref["label"]
+
+
+def load_pipeline_trace():
+    z = np.load(GOLD / "pipeline_trace.npz")
+    T = z["queries"].shape[0]
+    steps = [{"hidden": z["hidden"][t].astype(np.float64), "queries": z["queries"][t].astype(np.float64),
+              "new_keys": z["new_keys"][t].astype(np.float64),
+              "new_values": z["new_values"][t].astype(np.float64)} for t in range(T)]
+    return z, steps
+
+
+@pytest.mark.parametrize("run", list(cases.PIPELINE_CONFIGS), ids=str)
+def test_replay_matches_reference_pipeline(run):
+    z, steps = load_pipeline_trace()
+    ref = META["pipeline"]["runs"][run]
+    cfg = {"bits": 1, "g": 64, "n_local": 64, "n_topk": 128, "d_s": 8}
+    rc = ref["config"]
+    cfg.update({k2: rc[k1] for k1, k2 in (("bits", "bits"), ("n_local", "n_local"),
+                                          ("n_topk", "n_topk"), ("critical_channels", "d_s"))
+                if k1 in rc})
+    labels = ["q" if lab == "quantization_friendly" else "s" for lab in ref["labels"]]
+    res = O.replay(list(z["prefill_keys"].astype(np.float64)), list(z["prefill_values"].astype(np.float64)),
+                   list(z["w_q"].astype(np.float64)), steps, labels, **cfg)
+    for rec in ref["retrieval"]:
+        l, t = rec["layer"], rec["step"]
+        for kvh, ph in enumerate(rec["per_head"]):
+            assert res.channels[(l, t)][kvh].tolist() == ph["channels"]
+            assert np.array_equal(res.selected[(l, t)][kvh], cases.hex_to_indices(ph["selected_hex"]))
+            assert res.fetched[(l, t)][kvh] == ph["fetched"]
+    for t in range(len(steps)):
+        for l in range(len(labels)):
+            a, b = res.outputs[t][l].reshape(-1), res.exact[t][l].reshape(-1)
+            cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+            assert abs(cos - ref["cosine"][l][t]) < 1e-9
+
+
+def test_trace_reader_pins_reference_writer():
+    tr = O.read_trace_file(GOLD / "tiny_trace.hkv")
+    m = META["pipeline"]["tiny_trace"]
+    assert tr["prefill_keys"][0][0, 0, 0] == m["first_key"]
+    assert tr["steps"][-1]["new_values"][-1, -1, -1] == m["last_new_value"]
+    assert abs(sum(w.sum() for w in tr["w_q"]) - m["w_q_sum"]) < 1e-9
+
+
+def test_byte_formulas():
+    # Table-2 bytes at config 2 (test_memsim.py:379-399): 50,331,648 per layer
+    assert O.quant_layer_bytes(131072, 8, 128, 1, 64) == 50_331_648
+    assert O.scorer_bytes(131072, 8, 8) == 16_777_216
+    assert O.gather_bytes(2621 * 8, 128) == 10_735_616
