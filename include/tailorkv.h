@@ -1,0 +1,199 @@
+/*
+ * tailorkv.h -- C ABI of the B200-native TailorKV decode engine.
+ *
+ * Every entry point takes plain device/host pointers, integer sizes and a
+ * cudaStream_t (passed as void*).  No torch types cross this boundary.  The
+ * caller owns every buffer; the library never allocates on the decode path
+ * (the only allocator is tkv_host_store_create, which owns its pinned arena).
+ *
+ * The reference (hybridkv, /root/reference/pkg/src/hybridkv) has no FFI: its
+ * boundary is a Python API.  Each function below names the reference
+ * function(s) it replaces; paper_2505_19586_b200/_lib.py is the ctypes binding
+ * (the "reference-side binding" described in INTEGRATION.md).
+ *
+ * Status codes map 1:1 onto hybridkv/errors.py:9-38 classes.
+ *
+ * Device-resident counters: every cache keeps its token count in device memory
+ * (int32 *len) so a whole decode step can be captured once in a CUDA graph and
+ * replayed; appends advance the counter on the device.
+ */
+#ifndef TAILORKV_H_
+#define TAILORKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TKV_OK = 0,
+  TKV_ERR_SHAPE = 1,       /* ShapeError       (errors.py:13) */
+  TKV_ERR_PARAMETER = 2,   /* ParameterError   (errors.py:25) */
+  TKV_ERR_EMPTY_CACHE = 3, /* EmptyCacheError  (errors.py:17) */
+  TKV_ERR_NUMERIC = 4,     /* NumericError     (errors.py:21) */
+  TKV_ERR_ENCODING = 5,    /* EncodingError    (errors.py:29) */
+  TKV_ERR_SCHEDULING = 6,  /* SchedulingError  (errors.py:33) */
+  TKV_ERR_CUDA = 7         /* CUDA runtime failure (no reference counterpart) */
+};
+
+/* Last error message of the calling thread ("" when none). */
+const char *tkv_last_error(void);
+int tkv_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Quantized layer cache (quantizer.py:187-497)
+ * ------------------------------------------------------------------------
+ * One cache holds `units` KV heads (units = batch * kv_heads on this rank).
+ * Keys are per-channel groups of g tokens with an fp16 residual of < g rows
+ * (quantizer.py:277-293); values are per-token groups of g channels
+ * (quantizer.py:252-275).  Codes live in the MMA-native bit-plane layout
+ * described in DESIGN.md section 3; tkv_qcache_export produces the
+ * reference's GQT1 stream byte-for-byte.
+ */
+typedef struct tkv_qcache {
+  int32_t units, d, bits, g;
+  int64_t capacity;      /* tokens; multiple of the key tile (see tkv_qcache_sizes) */
+  uint32_t *key_codes;   /* [units][capacity/Tk][d/32][32][4] */
+  uint32_t *key_lohi;    /* half2(lo,hi) [units][capacity/g][d] */
+  uint16_t *key_resid;   /* fp16 [units][g][d] */
+  uint32_t *val_codes;   /* [units][capacity/32][sets][32][4] */
+  uint32_t *val_lohi;    /* half2(lo,hi) [units][capacity][ceil(d/g)] */
+  float *val_smax;       /* [units] running max of value group scale */
+  int32_t *len;          /* device scalar: tokens held (all units) */
+  uint32_t *ticket;      /* device scalar scratch for append */
+} tkv_qcache;
+
+/* Byte sizes of each buffer of a cache (same order as the struct pointers:
+ * key_codes, key_lohi, key_resid, val_codes, val_lohi, val_smax).  Returns the
+ * token tile the capacity must be a multiple of in *tile. */
+int tkv_qcache_sizes(int32_t units, int32_t d, int32_t bits, int32_t g, int64_t capacity,
+                     int64_t sizes[6], int32_t *tile);
+
+/* Prefill/compress: quantize keys/values [units][n][d] fp16 into an empty
+ * cache (replaces quantize_layer_kv, quantizer.py:479-497).  Sets *len = n.
+ * `check_finite` != 0 scans the input and fails with TKV_ERR_NUMERIC. */
+int tkv_qcache_pack(const tkv_qcache *c, const uint16_t *keys, const uint16_t *values, int64_t n,
+                    int32_t check_finite, void *stream);
+
+/* Decode-step append of one token per unit (replaces
+ * QuantizedLayerKV.append_token, quantizer.py:445-451). */
+int tkv_qcache_append(const tkv_qcache *c, const uint16_t *new_keys, const uint16_t *new_values,
+                      void *stream);
+
+/* Export unit u as a GQT1 blob (replaces GroupQuantizedTensor.to_bytes,
+ * quantizer.py:358-380).  `which` 0 = keys, 1 = values.  `out` is a DEVICE
+ * buffer of at least tkv_qcache_export_size bytes; n is the host's copy of *len. */
+int64_t tkv_qcache_export_size(const tkv_qcache *c, int32_t which, int64_t n);
+int tkv_qcache_export(const tkv_qcache *c, int32_t unit, int32_t which, int64_t n, uint8_t *out,
+                      void *stream);
+
+/* Dequantize unit u to fp32 [n][d] (replaces GroupQuantizedTensor.dequantize,
+ * quantizer.py:335-352); test/inspection helper. */
+int tkv_qcache_dequant(const tkv_qcache *c, int32_t unit, int32_t which, int64_t n, float *out,
+                       void *stream);
+
+/* Quantized decode attention of one layer (replaces pipeline.py:331-337:
+ * qgemv_scores quantizer.py:505-533 -> softmax(/sqrt d) -> qgemv_output
+ * quantizer.py:536-558).  queries fp16 [units*G][d]; out fp32 [units*G][d].
+ * `workspace` >= tkv_quant_decode_workspace bytes.  impl: 0 = auto,
+ * 1 = reference-shaped SIMT kernel, 2 = tensor-core (IMMA) kernel. */
+int64_t tkv_quant_decode_workspace(const tkv_qcache *c, int32_t G);
+int tkv_quant_decode(const tkv_qcache *c, const uint16_t *queries, int32_t G, float *out,
+                     void *workspace, int32_t impl, void *stream);
+
+/* Raw quantized GEMVs for one unit (replaces qgemv_scores / qgemv_output).
+ * logits fp32 [n] unscaled; weights fp32 [n] -> out fp32 [d]. */
+int tkv_qgemv_scores(const tkv_qcache *c, int32_t unit, int64_t n, const float *query, float *logits,
+                     void *stream);
+int tkv_qgemv_output(const tkv_qcache *c, int32_t unit, int64_t n, const float *weights, float *out,
+                     void *stream);
+
+/* ------------------------------------------------------------------------
+ * Sparsity-friendly layer (retriever.py:84-226, memsim.py:76-252)
+ * ------------------------------------------------------------------------ */
+typedef struct tkv_sparse_layer {
+  int32_t units, d;
+  int64_t capacity;       /* tokens */
+  int64_t local_offset;   /* first token index held by the local mirror */
+  int64_t local_capacity; /* rows of the local mirror */
+  uint16_t *kt;           /* channel-major keys fp16 [units][d][capacity] (scorer) */
+  float *chmax;           /* running max|K| [units][d] (memsim.py:93,109-111) */
+  uint16_t *loc_k;        /* local mirror fp16 [units][local_capacity][d] */
+  uint16_t *loc_v;
+  uint16_t *kdev;         /* optional token-major device keys [units][capacity][d] or NULL */
+  uint16_t *host_kv;      /* pinned host store [units][capacity][2][d] (K row | V row) */
+  int32_t *len;           /* device scalar */
+  uint32_t *ticket;       /* device scalar scratch */
+} tkv_sparse_layer;
+
+/* Prefill/offload (replaces HostPool.offload_layer memsim.py:88-93 and the
+ * local mirror of pipeline.py:183-193): keys/values fp16 [units][n][d] on the
+ * device.  Sets *len = n. */
+int tkv_sparse_prefill(const tkv_sparse_layer *s, const uint16_t *keys, const uint16_t *values,
+                       int64_t n, void *stream);
+/* Append one token per unit (replaces HostPool.append memsim.py:106-111 and
+ * the mirror append pipeline.py:412-413). */
+int tkv_sparse_append(const tkv_sparse_layer *s, const uint16_t *new_keys, const uint16_t *new_values,
+                      void *stream);
+
+/* Stage 1 (replaces estimate_query retriever.py:84-108 + group_channel_scores
+ * :138-148 + select_critical_channels :151-163, caller pipeline.py:271-286).
+ * hidden fp16 [B][hidden]; w_q fp16 [hq][hidden][d] (this rank's q heads);
+ * units = B * hq / G.  Writes q_hat f64 [B][hq][d] (may be NULL) and
+ * channels int32 [units][d_s] sorted ascending. */
+int64_t tkv_stage1_workspace(int32_t B, int32_t hq, int32_t hidden, int32_t d);
+int tkv_stage1(const uint16_t *hidden, const uint16_t *w_q, int32_t B, int32_t hq, int32_t hidden_dim,
+               int32_t d, int32_t G, const float *chmax, int32_t d_s, double *q_hat, int32_t *channels,
+               void *workspace, void *stream);
+
+/* Stage 2 (replaces approx_scores retriever.py:166-189 + select_topk_tokens
+ * :192-211): scores over the channel-major keys with the group-summed true
+ * query, then the exact (score desc, index desc) top-k plus the local window.
+ * sel_idx int32 [units][n_local+n_topk] ascending; sel_count/fetch_count
+ * int32 [units] (fetch_count = selected indices below the local window). */
+int64_t tkv_select_workspace(int32_t units, int64_t capacity);
+int tkv_select_tokens(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
+                      int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
+                      int32_t *fetch_count, double *scores_out, void *workspace, void *stream);
+
+/* Top-k selection over caller-provided f64 scores [units][n] (unit tests of
+ * select_topk_tokens, retriever.py:192-211). */
+int tkv_topk_from_scores(const double *scores, int32_t units, int64_t n, int32_t n_local, int32_t n_topk,
+                         int32_t *sel_idx, int32_t *sel_count, void *workspace, void *stream);
+
+/* Gather + sparse attention (replaces fetch_topk memsim.py:228-252 +
+ * pipeline.py:364-376): rows below the local window come from the pinned host
+ * store over PCIe (keys from kdev when keys_from_device != 0), the rest from
+ * the local mirror.  out fp32 [units*G][d]. */
+int64_t tkv_sparse_attn_workspace(int32_t units, int32_t G, int32_t d, int32_t max_rows);
+int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *sel_idx,
+                         const int32_t *sel_count, int32_t n_local, int32_t max_rows, int32_t keys_from_device,
+                         float *out, void *workspace, void *stream);
+
+/* Pinned, NUMA-local host arena for the KV store (memsim.py:76-135).  numa_node
+ * < 0 leaves placement to the OS.  Returns a host pointer usable by kernels
+ * (UVA) or NULL. */
+void *tkv_host_store_create(size_t bytes, int32_t numa_node);
+int tkv_host_store_destroy(void *ptr, size_t bytes);
+
+/* PCIe H2D probe for the roofline: UVA zero-copy read kernel over `bytes` of a
+ * pinned host buffer, rows of `row_bytes` at random row indices. */
+int tkv_uva_read_probe(const void *host, size_t bytes, int32_t row_bytes, const int32_t *rows, int32_t nrows,
+                       float *sink, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Layer classification (identifier.py:89-187)
+ * ------------------------------------------------------------------------
+ * Per q head: mean over the n_q probe queries of (1 - top-k attention mass)
+ * against all n keys of its KV head.  queries fp16 [hq][n_q][d], keys fp16
+ * [h][n][d]; head_scores f64 [hq]. */
+int64_t tkv_calibrate_workspace(int32_t hq, int32_t n_q, int64_t n);
+int tkv_dense_preference(const uint16_t *queries, const uint16_t *keys, int32_t hq, int32_t h, int32_t n_q,
+                         int64_t n, int32_t d, int64_t k, double *head_scores, void *workspace, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAILORKV_H_ */

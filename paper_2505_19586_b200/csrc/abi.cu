@@ -1,0 +1,237 @@
+// extern "C" boundary: argument validation, status codes (errors.py:9-38),
+// dispatch to the kernels.  See include/tailorkv.h.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "qcache.cuh"
+#include "sparse.cuh"
+
+namespace tkv {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+int check_launch(const char *what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TKV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return TKV_OK;
+}
+
+static int validate_qcache(const tkv_qcache *c) {
+  TKV_REQUIRE(c != nullptr, TKV_ERR_PARAMETER, "null cache");
+  TKV_REQUIRE(c->bits == 1 || c->bits == 2, TKV_ERR_PARAMETER, "bits must be one of (1, 2)");
+  TKV_REQUIRE(c->d >= 32 && c->d <= 256 && c->d % 32 == 0, TKV_ERR_SHAPE,
+              "head_dim must be a multiple of 32 in [32, 256] on the CUDA path");
+  TKV_REQUIRE(c->g == 16 || c->g == 32 || c->g == 64 || (c->g == 128 && c->bits == 1), TKV_ERR_PARAMETER,
+              "group_size must be 16, 32 or 64 (128 at 1 bit) on the CUDA path");
+  TKV_REQUIRE(c->units >= 1, TKV_ERR_SHAPE, "units must be >= 1");
+  TKV_REQUIRE(c->capacity % key_tile_tokens(c->bits) == 0 && c->capacity % c->g == 0, TKV_ERR_PARAMETER,
+              "capacity must be a multiple of the key tile");
+  return TKV_OK;
+}
+
+}  // namespace tkv
+
+using namespace tkv;
+
+extern "C" {
+
+const char *tkv_last_error(void) { return g_err.c_str(); }
+int tkv_abi_version(void) { return 1; }
+
+int tkv_qcache_sizes(int32_t units, int32_t d, int32_t bits, int32_t g, int64_t capacity, int64_t sizes[6],
+                     int32_t *tile) {
+  tkv_qcache c{};
+  c.units = units; c.d = d; c.bits = bits; c.g = g; c.capacity = capacity;
+  const int Tk = (bits == 1 || bits == 2) ? key_tile_tokens(bits) : 1;
+  if (tile) *tile = Tk > g ? Tk : g;
+  if (int r = validate_qcache(&c)) return r;
+  const int nb = (d + g - 1) / g;
+  sizes[0] = (int64_t)units * (capacity / Tk) * (d / 32) * 128 * 4;
+  sizes[1] = (int64_t)units * (capacity / g) * d * 4;
+  sizes[2] = (int64_t)units * g * d * 2;
+  sizes[3] = (int64_t)units * (capacity / 32) * val_sets(d, bits) * 128 * 4;
+  sizes[4] = (int64_t)units * capacity * nb * 4;
+  sizes[5] = (int64_t)units * 4;
+  return TKV_OK;
+}
+
+int tkv_qcache_pack(const tkv_qcache *c, const uint16_t *keys, const uint16_t *values, int64_t n,
+                    int32_t check_finite, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  TKV_REQUIRE(n >= 1, TKV_ERR_EMPTY_CACHE, "cannot quantize an empty cache");
+  TKV_REQUIRE(n <= c->capacity, TKV_ERR_SHAPE, "sequence longer than the cache capacity");
+  return pack(*c, keys, values, n, check_finite, as_stream(stream));
+}
+
+int tkv_qcache_append(const tkv_qcache *c, const uint16_t *nk, const uint16_t *nv, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  return append(*c, nk, nv, as_stream(stream));
+}
+
+int64_t tkv_qcache_export_size(const tkv_qcache *c, int32_t which, int64_t n) { return export_size(*c, which, n); }
+
+int tkv_qcache_export(const tkv_qcache *c, int32_t unit, int32_t which, int64_t n, uint8_t *out, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  TKV_REQUIRE(unit >= 0 && unit < c->units, TKV_ERR_PARAMETER, "unit out of range");
+  TKV_REQUIRE(which == 0 || which == 1, TKV_ERR_PARAMETER, "which must be 0 (keys) or 1 (values)");
+  return export_blob(*c, unit, which, n, out, as_stream(stream));
+}
+
+int tkv_qcache_dequant(const tkv_qcache *c, int32_t unit, int32_t which, int64_t n, float *out, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  TKV_REQUIRE(unit >= 0 && unit < c->units, TKV_ERR_PARAMETER, "unit out of range");
+  return dequant(*c, unit, which, n, out, as_stream(stream));
+}
+
+int64_t tkv_quant_decode_workspace(const tkv_qcache *c, int32_t G) { return quant_decode_workspace(*c, G); }
+
+int tkv_quant_decode(const tkv_qcache *c, const uint16_t *queries, int32_t G, float *out, void *workspace,
+                     int32_t impl, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  TKV_REQUIRE(G >= 1 && G <= 16, TKV_ERR_SHAPE, "query heads per KV head must be in [1, 16]");
+  return quant_decode(*c, queries, G, out, workspace, impl, as_stream(stream));
+}
+
+int tkv_qgemv_scores(const tkv_qcache *c, int32_t unit, int64_t n, const float *query, float *logits, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  return qgemv_scores(*c, unit, n, query, logits, as_stream(stream));
+}
+
+int tkv_qgemv_output(const tkv_qcache *c, int32_t unit, int64_t n, const float *weights, float *out, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  return qgemv_output(*c, unit, n, weights, out, as_stream(stream));
+}
+
+static int validate_sparse(const tkv_sparse_layer *s) {
+  TKV_REQUIRE(s != nullptr, TKV_ERR_PARAMETER, "null layer");
+  TKV_REQUIRE(s->d >= 32 && s->d <= 256 && s->d % 32 == 0, TKV_ERR_SHAPE,
+              "head_dim must be a multiple of 32 in [32, 256] on the CUDA path");
+  TKV_REQUIRE(s->units >= 1 && s->capacity >= 1, TKV_ERR_SHAPE, "empty layer");
+  TKV_REQUIRE(s->host_kv != nullptr, TKV_ERR_PARAMETER, "layer has no host store");
+  return TKV_OK;
+}
+
+int tkv_sparse_prefill(const tkv_sparse_layer *s, const uint16_t *keys, const uint16_t *values, int64_t n,
+                       void *stream) {
+  if (int r = validate_sparse(s)) return r;
+  TKV_REQUIRE(n >= 1, TKV_ERR_EMPTY_CACHE, "cannot offload an empty cache");
+  TKV_REQUIRE(n <= s->capacity, TKV_ERR_SHAPE, "sequence longer than the layer capacity");
+  TKV_REQUIRE(s->local_offset >= 0 && s->local_offset <= n, TKV_ERR_PARAMETER, "bad local offset");
+  return sparse_prefill(*s, keys, values, n, as_stream(stream));
+}
+
+int tkv_sparse_append(const tkv_sparse_layer *s, const uint16_t *nk, const uint16_t *nv, void *stream) {
+  if (int r = validate_sparse(s)) return r;
+  return sparse_append(*s, nk, nv, as_stream(stream));
+}
+
+int64_t tkv_stage1_workspace(int32_t B, int32_t hq, int32_t hidden, int32_t d) {
+  return stage1_workspace(B, hq, hidden, d);
+}
+
+int tkv_stage1(const uint16_t *hidden, const uint16_t *w_q, int32_t B, int32_t hq, int32_t hidden_dim, int32_t d,
+               int32_t G, const float *chmax, int32_t d_s, double *q_hat, int32_t *channels, void *workspace,
+               void *stream) {
+  TKV_REQUIRE(B >= 1 && B <= 16, TKV_ERR_SHAPE, "batch must be in [1, 16] for stage 1");
+  TKV_REQUIRE(d >= 32 && d <= 256 && d % 32 == 0, TKV_ERR_SHAPE, "head_dim must be a multiple of 32 in [32,256]");
+  TKV_REQUIRE(G >= 1 && hq % G == 0, TKV_ERR_SHAPE, "query heads not divisible by the group size");
+  TKV_REQUIRE(d_s >= 1 && d_s <= d, TKV_ERR_PARAMETER, "d_s must lie in [1, head_dim]");
+  return stage1(hidden, w_q, B, hq, hidden_dim, d, G, chmax, d_s, q_hat, channels, workspace, as_stream(stream));
+}
+
+int64_t tkv_select_workspace(int32_t units, int64_t capacity) { return select_workspace(units, capacity); }
+
+int tkv_select_tokens(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
+                      int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
+                      int32_t *fetch_count, double *scores_out, void *workspace, void *stream) {
+  if (int r = validate_sparse(s)) return r;
+  TKV_REQUIRE(n_local >= 0, TKV_ERR_PARAMETER, "n_local must be >= 0");
+  TKV_REQUIRE(n_topk >= 1, TKV_ERR_PARAMETER, "n_topk must be >= 1");
+  TKV_REQUIRE(d_s >= 1 && d_s <= s->d && d_s <= 128, TKV_ERR_PARAMETER, "d_s must lie in [1, min(head_dim,128)]");
+  return select_tokens(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, scores_out,
+                       workspace, as_stream(stream));
+}
+
+int tkv_topk_from_scores(const double *scores, int32_t units, int64_t n, int32_t n_local, int32_t n_topk,
+                         int32_t *sel_idx, int32_t *sel_count, void *workspace, void *stream) {
+  TKV_REQUIRE(n >= 1, TKV_ERR_EMPTY_CACHE, "token selection over an empty cache");
+  TKV_REQUIRE(n_local >= 0 && n_topk >= 1, TKV_ERR_PARAMETER, "token budgets out of range");
+  return topk_from_scores(scores, units, n, n_local, n_topk, sel_idx, sel_count, workspace, as_stream(stream));
+}
+
+int64_t tkv_sparse_attn_workspace(int32_t units, int32_t G, int32_t d, int32_t max_rows) {
+  return sparse_attn_workspace(units, G, d, max_rows);
+}
+
+int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *sel_idx,
+                         const int32_t *sel_count, int32_t n_local, int32_t max_rows, int32_t keys_from_device,
+                         float *out, void *workspace, void *stream) {
+  if (int r = validate_sparse(s)) return r;
+  TKV_REQUIRE(!keys_from_device || s->kdev != nullptr, TKV_ERR_PARAMETER, "keys_from_device needs device keys");
+  return sparse_attention(*s, queries, G, sel_idx, sel_count, n_local, max_rows, keys_from_device, out, workspace,
+                          as_stream(stream));
+}
+
+void *tkv_host_store_create(size_t bytes, int32_t numa_node) {
+  const size_t page = 2u << 20;
+  const size_t len = (bytes + page - 1) / page * page;
+  void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) {
+    set_error("mmap failed for the host KV store");
+    return nullptr;
+  }
+  madvise(p, len, MADV_HUGEPAGE);
+  if (numa_node >= 0 && numa_node < 64) {
+    unsigned long mask = 1ul << numa_node;
+    // MPOL_BIND = 2; ignore failure (single-node hosts, no permission)
+    syscall(SYS_mbind, p, len, 2, &mask, 64, 0);
+  }
+  memset(p, 0, len);  // first touch places pages on the bound node
+  const cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    munmap(p, len);
+    set_error(std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+    return nullptr;
+  }
+  return p;
+}
+
+int tkv_host_store_destroy(void *ptr, size_t bytes) {
+  const size_t page = 2u << 20;
+  const size_t len = (bytes + page - 1) / page * page;
+  cudaHostUnregister(ptr);
+  munmap(ptr, len);
+  return TKV_OK;
+}
+
+int tkv_uva_read_probe(const void *host, size_t bytes, int32_t row_bytes, const int32_t *rows, int32_t nrows,
+                       float *sink, void *stream) {
+  TKV_REQUIRE(row_bytes % 16 == 0, TKV_ERR_PARAMETER, "row_bytes must be a multiple of 16");
+  return uva_probe(host, bytes, row_bytes, rows, nrows, sink, as_stream(stream));
+}
+
+int64_t tkv_calibrate_workspace(int32_t hq, int32_t n_q, int64_t n) { return calibrate_workspace(hq, n_q, n); }
+
+int tkv_dense_preference(const uint16_t *queries, const uint16_t *keys, int32_t hq, int32_t h, int32_t n_q,
+                         int64_t n, int32_t d, int64_t k, double *head_scores, void *workspace, void *stream) {
+  TKV_REQUIRE(h >= 1 && hq % h == 0, TKV_ERR_SHAPE, "query heads not divisible by kv heads");
+  TKV_REQUIRE(n_q >= 1 && n_q <= n, TKV_ERR_PARAMETER, "probe n_q out of range");
+  TKV_REQUIRE(k >= 1 && k <= n, TKV_ERR_PARAMETER, "k must lie in [1, n]");
+  TKV_REQUIRE(d % 2 == 0 && d <= 256, TKV_ERR_SHAPE, "head_dim must be even and <= 256");
+  return dense_preference(queries, keys, hq, h, n_q, n, d, k, head_scores, workspace, as_stream(stream));
+}
+
+}  // extern "C"

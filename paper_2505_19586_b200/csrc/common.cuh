@@ -1,0 +1,134 @@
+// Shared helpers for the TailorKV sm_100a kernels.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "tailorkv.h"
+
+namespace tkv {
+
+// ---- error plumbing (thread-local message, status codes from tailorkv.h) ----
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int check_launch(const char *what);
+
+#define TKV_REQUIRE(cond, code, msg)            \
+  do {                                          \
+    if (!(cond)) return ::tkv::fail((code), (msg)); \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- numeric helpers ----
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+__device__ __forceinline__ double h2d(uint16_t h) { return (double)__half2float(__ushort_as_half(h)); }
+
+__device__ __forceinline__ uint32_t pack_lohi(uint16_t lo, uint16_t hi) {
+  return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+
+// Order-preserving map of an IEEE double onto uint64 (larger double -> larger key).
+// -0.0 and +0.0 compare equal in the reference (numpy lexsort); map both to +0.
+__device__ __forceinline__ uint64_t orderable(double x) {
+  if (x == 0.0) x = 0.0;
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ---- quantization codec, bit-exact with quantizer.py:66-117 ----
+// Codes are computed in float64 exactly as the reference (inputs are fp16,
+// so x-lo, hi-lo, hi+lo are exact in float64).
+//   b=1: code = [hi != lo] && 2x >= hi + lo           (DESIGN.md 3.2 proof)
+//   b=2: fp32 fast path, float64 replay of the reference when the fp32
+//        value lies within 1e-5 of a rounding boundary.
+__device__ __forceinline__ uint32_t encode_code(float xf, float lof, float hif, int bits) {
+  if (hif == lof) return 0u;  // degenerate group: scale 1, code 0 (quantizer.py:94-95)
+  if (bits == 1) {
+    double x2 = 2.0 * (double)xf;
+    double s = __dadd_rn((double)hif, (double)lof);
+    return x2 >= s ? 1u : 0u;
+  }
+  // bits == 2
+  float a = xf - lof;          // relative error <= 2^-24
+  float s = (hif - lof) / 3.0f;
+  float v = a / s + 0.5f;
+  float fl = floorf(v);
+  float fr = v - fl;
+  if (fr > 1e-5f && fr < 1.0f - 1e-5f) {
+    int r = (int)fl;
+    return (uint32_t)min(max(r, 0), 3);
+  }
+  double sd = __ddiv_rn(__dsub_rn((double)hif, (double)lof), 3.0);
+  double vd = __ddiv_rn(__dsub_rn((double)xf, (double)lof), sd);
+  double r = floor(__dadd_rn(fabs(vd), 0.5));
+  if (vd < 0) r = -r;
+  int ri = (int)r;
+  return (uint32_t)min(max(ri, 0), 3);
+}
+
+// Group scale as used by decode: (hi-lo)/(2^b-1), 1 when degenerate.
+__device__ __forceinline__ float group_scale_f(float lo, float hi, int bits) {
+  float s = (hi - lo) / (float)((1 << bits) - 1);
+  return s == 0.0f ? 1.0f : s;
+}
+
+// ---- native (MMA fragment) layouts; DESIGN.md section 3 ----
+// Key tile = 16 * (8/bits) tokens.  Word (tile, ks, lane, role) holds, in byte
+// i at bits [k*b, k*b+b), the code of token 16k + (lane>>2) + 8(role&1) and
+// channel 32ks + 4(lane&3) + i + 16(role>>1).
+__host__ __device__ __forceinline__ int key_tile_tokens(int bits) { return 16 * (8 / bits); }
+
+__device__ __forceinline__ void key_code_pos(int64_t t, int c, int d, int bits, int64_t *word, int *bit) {
+  const int Tk = key_tile_tokens(bits);
+  const int64_t tile = t / Tk;
+  const int tt = (int)(t % Tk);
+  const int k = tt >> 4, row = tt & 15;
+  const int g8 = row & 7, rlo = row >> 3;
+  const int ks = c >> 5, cc = c & 31;
+  const int rhi = cc >> 4, c16 = cc & 15;
+  const int tq = c16 >> 2, i = c16 & 3;
+  const int lane = g8 * 4 + tq, role = rhi * 2 + rlo;
+  *word = ((tile * (d >> 5) + ks) * 32 + lane) * 4 + role;
+  *bit = 8 * i + k * bits;
+}
+
+// Value tile = 32 tokens.  sets = ceil(d / (16*8/bits)).  Word (vtile, set,
+// lane, role) holds in byte i at bits [k*b, k*b+b) the code of token
+// 32*vtile + 4(lane&3) + i + 16(role>>1) and channel
+// set*16*(8/b) + 16k + (lane>>2) + 8(role&1).
+__host__ __device__ __forceinline__ int val_sets(int d, int bits) {
+  const int per = 16 * (8 / bits);
+  return (d + per - 1) / per;
+}
+
+__device__ __forceinline__ void val_code_pos(int64_t t, int c, int d, int bits, int64_t *word, int *bit) {
+  const int per = 16 * (8 / bits);
+  const int64_t vt = t >> 5;
+  const int tt = (int)(t & 31);
+  const int rhi = tt >> 4, t16 = tt & 15;
+  const int tq = t16 >> 2, i = t16 & 3;
+  const int set = c / per, cs = c % per;
+  const int k = cs >> 4, row = cs & 15;
+  const int g8 = row & 7, rlo = row >> 3;
+  const int lane = g8 * 4 + tq, role = rhi * 2 + rlo;
+  *word = ((vt * val_sets(d, bits) + set) * 32 + lane) * 4 + role;
+  *bit = 8 * i + k * bits;
+}
+
+}  // namespace tkv

@@ -1,0 +1,26 @@
+#pragma once
+#include "common.cuh"
+
+namespace tkv {
+
+using QC = tkv_qcache;
+using SL = tkv_sparse_layer;
+
+int pack(const QC &c, const uint16_t *keys, const uint16_t *values, int64_t n, int check_finite, cudaStream_t st);
+int append(const QC &c, const uint16_t *nk, const uint16_t *nv, cudaStream_t st);
+int64_t export_size(const QC &c, int which, int64_t n);
+int export_blob(const QC &c, int u, int which, int64_t n, uint8_t *out, cudaStream_t st);
+int dequant(const QC &c, int u, int which, int64_t n, float *out, cudaStream_t st);
+int qgemv_scores(const QC &c, int u, int64_t n, const float *q, float *logits, cudaStream_t st);
+int qgemv_output(const QC &c, int u, int64_t n, const float *w, float *out, cudaStream_t st);
+
+int64_t quant_decode_workspace(const QC &c, int G);
+int quant_decode(const QC &c, const uint16_t *q, int G, float *out, void *ws, int impl, cudaStream_t st);
+
+// Split-K partial combine shared by the quantized and sparse attention paths:
+// part_m/part_l [units][chunks][G], part_acc [units][chunks][G][d].
+// chunk_count (device, per unit) may be NULL -> all `chunks` valid.
+void launch_combine(const float *part_m, const float *part_l, const float *part_acc, int units, int chunks, int G,
+                    int d, const int32_t *chunk_rows, int rows_per_chunk, float *out, cudaStream_t st);
+
+}  // namespace tkv

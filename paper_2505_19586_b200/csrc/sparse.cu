@@ -1,0 +1,763 @@
+// Sparsity-friendly layers: offload/prefill, append, stage 1 (query estimate +
+// critical channels), stage 2 (proxy scores + exact top-k), gather + sparse
+// attention.  Reference: retriever.py:84-226, memsim.py:76-252,
+// pipeline.py:271-286, 340-376, 405-413.
+#include <cmath>
+
+#include "common.cuh"
+#include "qcache.cuh"
+#include "sparse.cuh"
+
+namespace tkv {
+
+// ===========================================================================
+// Prefill / append (memsim.py:88-93, 106-111; pipeline.py:183-193, 412-413)
+// ===========================================================================
+// kt[u][c][j] = K[u][j][c] and chmax[u][c] = max_j |K[u][j][c]|
+__global__ void transpose_keys_kernel(SL s, const uint16_t *__restrict__ keys, int64_t n) {
+  __shared__ uint16_t tile[32][33];
+  __shared__ float cmax[32];
+  const int u = blockIdx.z;
+  const int64_t j0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  if (ty == 0) cmax[tx] = 0.0f;
+  __syncthreads();
+  float m = 0.0f;
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t j = j0 + r;
+    uint16_t v = 0;
+    if (j < n && c0 + tx < s.d) v = keys[((size_t)u * n + j) * s.d + c0 + tx];
+    tile[r][tx] = v;
+    m = fmaxf(m, fabsf(h2f(v)));
+  }
+  atomicMax(reinterpret_cast<int *>(&cmax[tx]), __float_as_int(m));
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int c = c0 + r;
+    const int64_t j = j0 + tx;
+    if (c < s.d && j < n) s.kt[((size_t)u * s.d + c) * s.capacity + j] = tile[tx][r];
+  }
+  if (ty == 0 && c0 + tx < s.d)
+    atomicMax(reinterpret_cast<int *>(&s.chmax[(size_t)u * s.d + c0 + tx]), __float_as_int(cmax[tx]));
+}
+
+__global__ void copy_rows_kernel(uint16_t *__restrict__ dst, int64_t dst_rows, const uint16_t *__restrict__ src,
+                                 int64_t src_rows, int64_t row0, int64_t nrows, int d) {
+  // dst[u][r][:] = src[u][row0 + r][:] for r < nrows
+  const int u = blockIdx.y;
+  const int64_t total = nrows * d / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (d / 8), v = i % (d / 8);
+    reinterpret_cast<uint4 *>(dst + ((size_t)u * dst_rows + r) * d)[v] =
+        reinterpret_cast<const uint4 *>(src + ((size_t)u * src_rows + row0 + r) * d)[v];
+  }
+}
+
+// host_kv[u][j][0|1][:] <- K|V rows (UVA stores into the pinned arena)
+__global__ void fill_host_kernel(SL s, const uint16_t *__restrict__ keys, const uint16_t *__restrict__ values,
+                                 int64_t n) {
+  const int u = blockIdx.y;
+  const int vpr = s.d / 8;
+  const int64_t total = n * 2 * vpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / (2 * vpr);
+    const int which = (int)((i / vpr) & 1), v = (int)(i % vpr);
+    const uint16_t *src = (which ? values : keys) + ((size_t)u * n + j) * s.d;
+    reinterpret_cast<uint4 *>(s.host_kv + (((size_t)u * s.capacity + j) * 2 + which) * s.d)[v] =
+        reinterpret_cast<const uint4 *>(src)[v];
+  }
+}
+
+__global__ void set_len32_kernel(int32_t *len, int64_t n) { *len = (int32_t)n; }
+
+int sparse_prefill(const SL &s, const uint16_t *keys, const uint16_t *values, int64_t n, cudaStream_t st) {
+  cudaMemsetAsync(s.chmax, 0, sizeof(float) * s.units * s.d, st);
+  {
+    dim3 grid((unsigned)((n + 31) / 32), (s.d + 31) / 32, s.units);
+    transpose_keys_kernel<<<grid, dim3(32, 8), 0, st>>>(s, keys, n);
+  }
+  const int64_t lrows = n - s.local_offset;
+  if (lrows > 0) {
+    dim3 grid(64, s.units);
+    copy_rows_kernel<<<grid, 256, 0, st>>>(s.loc_k, s.local_capacity, keys, n, s.local_offset, lrows, s.d);
+    copy_rows_kernel<<<grid, 256, 0, st>>>(s.loc_v, s.local_capacity, values, n, s.local_offset, lrows, s.d);
+  }
+  if (s.kdev) {
+    dim3 grid(256, s.units);
+    copy_rows_kernel<<<grid, 256, 0, st>>>(s.kdev, s.capacity, keys, n, 0, n, s.d);
+  }
+  {
+    dim3 grid(592, s.units);
+    fill_host_kernel<<<grid, 256, 0, st>>>(s, keys, values, n);
+  }
+  set_len32_kernel<<<1, 1, 0, st>>>(s.len, n);
+  return check_launch("tkv_sparse_prefill");
+}
+
+__global__ void sparse_append_kernel(SL s, const uint16_t *__restrict__ nk, const uint16_t *__restrict__ nv) {
+  const int u = blockIdx.x;
+  const int64_t n = *s.len;
+  for (int c = threadIdx.x; c < s.d; c += blockDim.x) {
+    const uint16_t k = nk[(size_t)u * s.d + c], v = nv[(size_t)u * s.d + c];
+    s.host_kv[(((size_t)u * s.capacity + n) * 2 + 0) * s.d + c] = k;
+    s.host_kv[(((size_t)u * s.capacity + n) * 2 + 1) * s.d + c] = v;
+    s.kt[((size_t)u * s.d + c) * s.capacity + n] = k;
+    float *cm = &s.chmax[(size_t)u * s.d + c];
+    *cm = fmaxf(*cm, fabsf(h2f(k)));
+    const int64_t lr = n - s.local_offset;
+    s.loc_k[((size_t)u * s.local_capacity + lr) * s.d + c] = k;
+    s.loc_v[((size_t)u * s.local_capacity + lr) * s.d + c] = v;
+    if (s.kdev) s.kdev[((size_t)u * s.capacity + n) * s.d + c] = k;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned prev = atomicAdd(s.ticket, 1u);
+    if (prev == (unsigned)gridDim.x - 1) {
+      *s.ticket = 0;
+      __threadfence();
+      *s.len = (int32_t)(n + 1);
+    }
+  }
+}
+
+int sparse_append(const SL &s, const uint16_t *nk, const uint16_t *nv, cudaStream_t st) {
+  sparse_append_kernel<<<s.units, 128, 0, st>>>(s, nk, nv);
+  return check_launch("tkv_sparse_append");
+}
+
+// ===========================================================================
+// Stage 1: q_hat = h . W_q (retriever.py:84-108) then group channel scores and
+// the top-d_s channels, ties to the lower index, ascending
+// (retriever.py:138-163).  float64 accumulation like the reference einsum.
+// ===========================================================================
+constexpr int S1_ROWS_PER_CTA = 128;
+constexpr int S1_MAXB = 16;
+
+__global__ void __launch_bounds__(256) stage1_gemv_kernel(const uint16_t *__restrict__ hidden,
+                                                           const uint16_t *__restrict__ w_q, int B, int H, int d,
+                                                           double *__restrict__ part) {
+  // grid (splits, hq); block 256 = (d/2 column pairs) x rows-in-flight
+  extern __shared__ __align__(16) double s1sm[];
+  const int qh = blockIdx.y, split = blockIdx.x, splits = gridDim.x;
+  const int hq = gridDim.y;
+  const int pairs = d / 2;
+  const int rgroups = blockDim.x / pairs;
+  const int cp = threadIdx.x % pairs, rg = threadIdx.x / pairs;
+  const int i0 = split * S1_ROWS_PER_CTA, i1 = min(H, i0 + S1_ROWS_PER_CTA);
+  double acc0[S1_MAXB], acc1[S1_MAXB];
+#pragma unroll
+  for (int b = 0; b < S1_MAXB; ++b) { acc0[b] = 0.0; acc1[b] = 0.0; }
+  if (rg < rgroups) {
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(w_q + ((size_t)qh * H) * d);
+    for (int i = i0 + rg; i < i1; i += rgroups) {
+      const uint32_t pr = __ldg(&w[(size_t)i * pairs + cp]);
+      const double w0 = h2d(pr & 0xffff), w1 = h2d(pr >> 16);
+#pragma unroll
+      for (int b = 0; b < S1_MAXB; ++b) {
+        if (b < B) {
+          const double hv = h2d(hidden[(size_t)b * H + i]);
+          acc0[b] = fma(hv, w0, acc0[b]);
+          acc1[b] = fma(hv, w1, acc1[b]);
+        }
+      }
+    }
+  }
+  // reduce row groups in a fixed order
+  for (int b = 0; b < B; ++b) {
+    if (rg < rgroups) {
+      s1sm[(rg * pairs + cp) * 2 + 0] = acc0[b];
+      s1sm[(rg * pairs + cp) * 2 + 1] = acc1[b];
+    }
+    __syncthreads();
+    if (rg == 0) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int r = 0; r < rgroups; ++r) {
+        a0 += s1sm[(r * pairs + cp) * 2 + 0];
+        a1 += s1sm[(r * pairs + cp) * 2 + 1];
+      }
+      double *o = part + (((size_t)split * B + b) * hq + qh) * d;
+      o[2 * cp] = a0;
+      o[2 * cp + 1] = a1;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void stage1_select_kernel(const double *__restrict__ part, int splits, int B, int hq, int d, int G,
+                                     const float *__restrict__ chmax, int d_s, double *__restrict__ q_hat,
+                                     int32_t *__restrict__ channels) {
+  // one CTA per unit (b, kvh); blockDim == d
+  __shared__ double score[256];
+  const int u = blockIdx.x;
+  const int hkv = hq / G;
+  const int b = u / hkv, kvh = u % hkv;
+  const int c = threadIdx.x;
+  double sabs = 0.0;
+  for (int j = 0; j < G; ++j) {
+    const int qh = kvh * G + j;
+    double q = 0.0;
+    for (int sp = 0; sp < splits; ++sp) q += part[(((size_t)sp * B + b) * hq + qh) * d + c];
+    if (q_hat) q_hat[((size_t)b * hq + qh) * d + c] = q;
+    sabs += fabs(q);
+  }
+  const double sc = sabs * (double)chmax[(size_t)u * d + c];
+  score[c] = sc;
+  __syncthreads();
+  int rank = 0;
+  for (int j = 0; j < d; ++j) {
+    const double o = score[j];
+    rank += (o > sc) || (o == sc && j < c);
+  }
+  const bool sel = rank < d_s;
+  // ascending position among the selected channels
+  __shared__ int flags[256];
+  flags[c] = sel ? 1 : 0;
+  __syncthreads();
+  if (sel) {
+    int pos = 0;
+    for (int j = 0; j < c; ++j) pos += flags[j];
+    channels[(size_t)u * d_s + pos] = c;
+  }
+}
+
+int64_t stage1_workspace(int B, int hq, int H, int d) {
+  const int splits = (H + S1_ROWS_PER_CTA - 1) / S1_ROWS_PER_CTA;
+  return (int64_t)splits * B * hq * d * 8 + 256;
+}
+
+int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, int d, int G, const float *chmax,
+           int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st) {
+  const int splits = (H + S1_ROWS_PER_CTA - 1) / S1_ROWS_PER_CTA;
+  double *part = reinterpret_cast<double *>(ws);
+  const size_t sm = (size_t)256 * 2 * sizeof(double);
+  stage1_gemv_kernel<<<dim3(splits, hq), 256, sm, st>>>(hidden, w_q, B, H, d, part);
+  stage1_select_kernel<<<B * (hq / G), d, 0, st>>>(part, splits, B, hq, d, G, chmax, d_s, q_hat, channels);
+  return check_launch("tkv_stage1");
+}
+
+// ===========================================================================
+// Stage 2: proxy scores + exact top-k (retriever.py:166-211)
+// ===========================================================================
+// Workspace layout (per call, units x capacity):
+//   keys64 [U][cap] u64 | hist [U][65536] u32 | cand_key [U][CAP] u64 |
+//   cand_idx [U][CAP] u32 | bitmap [U][cap/32+1] u32 | misc [U][8] i32 | len i32
+constexpr int HIST_BINS = 65536;
+constexpr int CAND_CAP = 4096;
+
+struct SelWS {
+  uint64_t *keys;
+  uint32_t *hist;
+  uint64_t *cand_key;
+  uint32_t *cand_idx;
+  uint32_t *bitmap;
+  int32_t *misc;  // [0]=b1 [1]=need [2]=cand_count [3]=mode
+  int32_t *len;
+  int64_t cap;
+};
+
+static SelWS carve(void *ws, int units, int64_t cap) {
+  SelWS w;
+  char *p = reinterpret_cast<char *>(ws);
+  auto take = [&](size_t bytes) {
+    char *r = p;
+    p += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  w.keys = reinterpret_cast<uint64_t *>(take((size_t)units * cap * 8));
+  w.hist = reinterpret_cast<uint32_t *>(take((size_t)units * HIST_BINS * 4));
+  w.cand_key = reinterpret_cast<uint64_t *>(take((size_t)units * CAND_CAP * 8));
+  w.cand_idx = reinterpret_cast<uint32_t *>(take((size_t)units * CAND_CAP * 4));
+  w.bitmap = reinterpret_cast<uint32_t *>(take((size_t)units * (cap / 32 + 1) * 4));
+  w.misc = reinterpret_cast<int32_t *>(take((size_t)units * 8 * 4));
+  w.len = reinterpret_cast<int32_t *>(take(4));
+  w.cap = cap;
+  return w;
+}
+
+int64_t select_workspace(int units, int64_t cap) {
+  SelWS w = carve(nullptr, units, cap);
+  return reinterpret_cast<int64_t>(w.len) + 256;
+}
+
+// The workspace must be zero on first use; every call leaves hist, bitmap and
+// the candidate counter zeroed again (so a captured graph can replay).
+__device__ __forceinline__ bool select_all(int64_t n, int n_local, int n_topk) {
+  return n <= (int64_t)n_local + n_topk;
+}
+
+__global__ void __launch_bounds__(256) score_hist_kernel(SL s, const uint16_t *__restrict__ queries, int G,
+                                                          const int32_t *__restrict__ channels, int d_s,
+                                                          int n_local, int n_topk, SelWS w,
+                                                          double *__restrict__ scores_out) {
+  __shared__ double qsum[128];
+  __shared__ int chs[128];
+  const int u = blockIdx.y;
+  const int64_t n = *s.len;
+  if (select_all(n, n_local, n_topk)) return;
+  const int64_t ncand = n - n_local;
+  for (int i = threadIdx.x; i < d_s; i += blockDim.x) {
+    const int ch = channels[(size_t)u * d_s + i];
+    double q = 0.0;
+    for (int j = 0; j < G; ++j) q += h2d(queries[((size_t)u * G + j) * s.d + ch]);  // group sum (retriever.py:189)
+    qsum[i] = q;
+    chs[i] = ch;
+  }
+  __syncthreads();
+  const uint16_t *kt = s.kt + (size_t)u * s.d * s.capacity;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncand; j += (int64_t)gridDim.x * blockDim.x) {
+    double sc = 0.0;
+    for (int i = 0; i < d_s; ++i) sc = fma(h2d(kt[(size_t)chs[i] * s.capacity + j]), qsum[i], sc);
+    const uint64_t key = orderable(sc);
+    w.keys[(size_t)u * w.cap + j] = key;
+    atomicAdd(&w.hist[(size_t)u * HIST_BINS + (key >> 48)], 1u);
+    if (scores_out) scores_out[(size_t)u * s.capacity + j] = sc;
+  }
+}
+
+__global__ void keys_from_scores_kernel(const double *__restrict__ scores, int64_t n, int n_local, int n_topk,
+                                        SelWS w) {
+  const int u = blockIdx.y;
+  if (select_all(n, n_local, n_topk)) return;
+  const int64_t ncand = n - n_local;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncand; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = orderable(scores[(size_t)u * n + j]);
+    w.keys[(size_t)u * w.cap + j] = key;
+    atomicAdd(&w.hist[(size_t)u * HIST_BINS + (key >> 48)], 1u);
+  }
+}
+
+__global__ void __launch_bounds__(1024) find_bin_kernel(const int32_t *__restrict__ len, int n_local, int n_topk,
+                                                         SelWS w) {
+  __shared__ uint32_t part[1024];
+  const int u = blockIdx.x;
+  const int64_t n = *len;
+  uint32_t *hist = w.hist + (size_t)u * HIST_BINS;
+  if (select_all(n, n_local, n_topk)) return;
+  // thread t owns bins [65535 - 64t - 63, 65535 - 64t] (descending order)
+  const int t = threadIdx.x;
+  uint32_t sum = 0;
+  for (int i = 0; i < 64; ++i) sum += hist[HIST_BINS - 1 - (64 * t + i)];
+  part[t] = sum;
+  __syncthreads();
+  // inclusive scan (Hillis-Steele)
+  for (int off = 1; off < 1024; off <<= 1) {
+    uint32_t v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  const uint32_t K = (uint32_t)n_topk;
+  const uint32_t before = t ? part[t - 1] : 0;
+  if (before < K && part[t] >= K) {
+    uint32_t cum = before;
+    for (int i = 0; i < 64; ++i) {
+      const int bin = HIST_BINS - 1 - (64 * t + i);
+      const uint32_t h = hist[bin];
+      if (cum + h >= K) {
+        w.misc[u * 8 + 0] = bin;
+        w.misc[u * 8 + 1] = (int)(K - cum);
+        break;
+      }
+      cum += h;
+    }
+  }
+  __syncthreads();
+  for (int i = 0; i < 64; ++i) hist[64 * t + i] = 0;  // leave zeroed for the next call
+}
+
+__global__ void __launch_bounds__(256) compact_kernel(const int32_t *__restrict__ len, int n_local, int n_topk,
+                                                       SelWS w) {
+  const int u = blockIdx.y;
+  const int64_t n = *len;
+  if (select_all(n, n_local, n_topk)) return;
+  const int64_t ncand = n - n_local;
+  const uint32_t b1 = (uint32_t)w.misc[u * 8 + 0];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncand; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = w.keys[(size_t)u * w.cap + j];
+    const uint32_t bin = (uint32_t)(key >> 48);
+    if (bin > b1) {
+      atomicOr(&w.bitmap[(size_t)u * (w.cap / 32 + 1) + (j >> 5)], 1u << (j & 31));
+    } else if (bin == b1) {
+      const int pos = atomicAdd(&w.misc[u * 8 + 2], 1);
+      if (pos < CAND_CAP) {
+        w.cand_key[(size_t)u * CAND_CAP + pos] = key;
+        w.cand_idx[(size_t)u * CAND_CAP + pos] = (uint32_t)j;
+      }
+    }
+  }
+}
+
+// composite order: larger key first, then larger index (retriever.py:208-209)
+__device__ __forceinline__ bool beats(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+  return ka > kb || (ka == kb && ia > ib);
+}
+
+__global__ void __launch_bounds__(1024) finish_kernel(const int32_t *__restrict__ len, int n_local, int n_topk,
+                                                       SelWS w, int32_t *__restrict__ sel_idx, int sel_stride,
+                                                       int32_t *__restrict__ sel_count,
+                                                       int32_t *__restrict__ fetch_count) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  uint64_t *sk = reinterpret_cast<uint64_t *>(fsm);                 // [CAND_CAP]
+  uint32_t *si = reinterpret_cast<uint32_t *>(fsm + CAND_CAP * 8);  // [CAND_CAP]
+  __shared__ uint32_t scan[1024];
+  __shared__ uint32_t dhist[256];
+  __shared__ int sh_need, sh_digit;
+  const int u = blockIdx.x;
+  const int t = threadIdx.x;
+  const int64_t n = *len;
+  const int64_t bw = w.cap / 32 + 1;
+  uint32_t *bm = w.bitmap + (size_t)u * bw;
+  const bool all = select_all(n, n_local, n_topk);
+  const int64_t local_start = n > n_local ? n - n_local : 0;
+  if (all) {
+    for (int64_t j = t; j < n; j += blockDim.x) sel_idx[(size_t)u * sel_stride + j] = (int32_t)j;
+    if (t == 0) {
+      sel_count[u] = (int32_t)n;
+      if (fetch_count) fetch_count[u] = (int32_t)local_start;
+    }
+    return;
+  }
+  const uint32_t b1 = (uint32_t)w.misc[u * 8 + 0];
+  const int need0 = w.misc[u * 8 + 1];
+  const int m = w.misc[u * 8 + 2];
+  if (m <= CAND_CAP) {
+    // bitonic sort of the threshold-bin candidates, descending
+    int P = 1;
+    while (P < m) P <<= 1;
+    for (int i = t; i < P; i += blockDim.x) {
+      if (i < m) {
+        sk[i] = w.cand_key[(size_t)u * CAND_CAP + i];
+        si[i] = w.cand_idx[(size_t)u * CAND_CAP + i];
+      } else {
+        sk[i] = 0;
+        si[i] = 0;
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = t; i < P; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const bool desc = (i & k) == 0;
+            const bool swap = desc ? beats(sk[ixj], si[ixj], sk[i], si[i]) : beats(sk[i], si[i], sk[ixj], si[ixj]);
+            if (swap) {
+              const uint64_t tk = sk[i]; sk[i] = sk[ixj]; sk[ixj] = tk;
+              const uint32_t ti = si[i]; si[i] = si[ixj]; si[ixj] = ti;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = t; i < need0; i += blockDim.x) atomicOr(&bm[si[i] >> 5], 1u << (si[i] & 31));
+  } else {
+    // Degenerate inputs (many equal scores): exact radix select over the
+    // 80-bit remainder (key bits 47..0, then index bits 31..0) of every
+    // candidate in bin b1, reading the keys from global memory.
+    const int64_t ncand = n - n_local;
+    const uint64_t *keys = w.keys + (size_t)u * w.cap;
+    __shared__ uint32_t digits[10];
+    if (t == 0) sh_need = need0;
+    __syncthreads();
+    for (int lvl = 0; lvl < 10; ++lvl) {
+      for (int i = t; i < 256; i += blockDim.x) dhist[i] = 0;
+      __syncthreads();
+      for (int64_t j = t; j < ncand; j += blockDim.x) {
+        const uint64_t key = keys[j];
+        if ((uint32_t)(key >> 48) != b1) continue;
+        bool match = true;
+        for (int q = 0; q < lvl && match; ++q) {
+          const uint32_t dg = q < 6 ? (uint32_t)((key >> (40 - 8 * q)) & 255) : (uint32_t)((j >> (24 - 8 * (q - 6))) & 255);
+          match = dg == digits[q];
+        }
+        if (!match) continue;
+        const uint32_t dg = lvl < 6 ? (uint32_t)((key >> (40 - 8 * lvl)) & 255)
+                                    : (uint32_t)((j >> (24 - 8 * (lvl - 6))) & 255);
+        atomicAdd(&dhist[dg], 1u);
+      }
+      __syncthreads();
+      if (t == 0) {
+        int cum = 0, D = 0;
+        for (int dgt = 255; dgt >= 0; --dgt) {
+          if (cum + (int)dhist[dgt] >= sh_need) { D = dgt; break; }
+          cum += dhist[dgt];
+        }
+        sh_digit = D;
+        digits[lvl] = D;
+        sh_need -= cum;
+      }
+      __syncthreads();
+      const uint32_t D = (uint32_t)sh_digit;
+      for (int64_t j = t; j < ncand; j += blockDim.x) {
+        const uint64_t key = keys[j];
+        if ((uint32_t)(key >> 48) != b1) continue;
+        bool match = true;
+        for (int q = 0; q < lvl && match; ++q) {
+          const uint32_t dg = q < 6 ? (uint32_t)((key >> (40 - 8 * q)) & 255) : (uint32_t)((j >> (24 - 8 * (q - 6))) & 255);
+          match = dg == digits[q];
+        }
+        if (!match) continue;
+        const uint32_t dg = lvl < 6 ? (uint32_t)((key >> (40 - 8 * lvl)) & 255)
+                                    : (uint32_t)((j >> (24 - 8 * (lvl - 6))) & 255);
+        if (dg > D || (lvl == 9 && dg == D)) atomicOr(&bm[j >> 5], 1u << (j & 31));
+      }
+      __syncthreads();
+    }
+  }
+  // the local window is always kept (retriever.py:210)
+  for (int64_t j = local_start + t; j < n; j += blockDim.x) atomicOr(&bm[j >> 5], 1u << (j & 31));
+  __syncthreads();
+  // bitmap -> ascending index list; clear the bitmap for the next call
+  const int64_t words = (n + 31) / 32;
+  const int64_t per = (words + blockDim.x - 1) / blockDim.x;
+  const int64_t w0 = t * per, w1 = min(words, w0 + per);
+  uint32_t cnt = 0;
+  for (int64_t q = w0; q < w1; ++q) cnt += __popc(bm[q]);
+  scan[t] = cnt;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    uint32_t v = t >= off ? scan[t - off] : 0;
+    __syncthreads();
+    scan[t] += v;
+    __syncthreads();
+  }
+  uint32_t pos = scan[t] - cnt;
+  for (int64_t q = w0; q < w1; ++q) {
+    uint32_t bits = bm[q];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      sel_idx[(size_t)u * sel_stride + pos++] = (int32_t)(q * 32 + b);
+    }
+    bm[q] = 0;
+  }
+  if (t == 1023) {
+    sel_count[u] = (int32_t)scan[1023];
+    if (fetch_count) fetch_count[u] = n_topk;
+    w.misc[u * 8 + 2] = 0;
+  }
+}
+
+static int run_select(const int32_t *len, int units, int n_local, int n_topk, SelWS w, int32_t *sel_idx,
+                      int sel_stride, int32_t *sel_count, int32_t *fetch_count, cudaStream_t st) {
+  find_bin_kernel<<<units, 1024, 0, st>>>(len, n_local, n_topk, w);
+  const int blocks = (int)imin64(4096, (w.cap + 255) / 256);
+  compact_kernel<<<dim3(blocks, units), 256, 0, st>>>(len, n_local, n_topk, w);
+  const size_t sm = (size_t)CAND_CAP * 12;
+  cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  finish_kernel<<<units, 1024, sm, st>>>(len, n_local, n_topk, w, sel_idx, sel_stride, sel_count, fetch_count);
+  return check_launch("tkv_select");
+}
+
+int select_tokens(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
+                  int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, double *scores_out,
+                  void *ws, cudaStream_t st) {
+  SelWS w = carve(ws, s.units, s.capacity);
+  const int blocks = (int)imin64(2048, (s.capacity + 255) / 256);
+  score_hist_kernel<<<dim3(blocks, s.units), 256, 0, st>>>(s, queries, G, channels, d_s, n_local, n_topk, w,
+                                                            scores_out);
+  return run_select(s.len, s.units, n_local, n_topk, w, sel_idx, n_local + n_topk, sel_count, fetch_count, st);
+}
+
+int topk_from_scores(const double *scores, int units, int64_t n, int n_local, int n_topk, int32_t *sel_idx,
+                     int32_t *sel_count, void *ws, cudaStream_t st) {
+  SelWS w = carve(ws, units, n);
+  set_len32_kernel<<<1, 1, 0, st>>>(w.len, n);
+  const int blocks = (int)imin64(2048, (n + 255) / 256);
+  keys_from_scores_kernel<<<dim3(blocks, units), 256, 0, st>>>(scores, n, n_local, n_topk, w);
+  return run_select(w.len, units, n_local, n_topk, w, sel_idx, n_local + n_topk, sel_count, nullptr, st);
+}
+
+// ===========================================================================
+// Gather + sparse attention (memsim.py:228-252 + pipeline.py:364-376).
+// One CTA per (64 selected rows, unit); each warp streams 16 rows: rows
+// below the local window are read straight from the pinned host store over
+// PCIe (UVA zero-copy), the rest from the device local mirror.
+// ===========================================================================
+constexpr int SA_ROWS = 64;
+constexpr int SA_WARPS = 4;
+constexpr int SA_RPW = SA_ROWS / SA_WARPS;
+
+template <int D, int GMAX>
+__global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const uint16_t *__restrict__ queries, int G,
+                                                                     const int32_t *__restrict__ sel_idx,
+                                                                     const int32_t *__restrict__ sel_count,
+                                                                     int n_local, int sel_stride, int keys_from_device,
+                                                                     float *__restrict__ pm, float *__restrict__ pl,
+                                                                     float *__restrict__ pacc, int chunks) {
+  constexpr int CPL = D / 32;  // channels per lane
+  __shared__ float wm[SA_WARPS][GMAX], wl[SA_WARPS][GMAX];
+  __shared__ float wacc[SA_WARPS][GMAX][D];
+  const int u = blockIdx.y, chunk = blockIdx.x;
+  const int cnt = sel_count[u];
+  const int r0 = chunk * SA_ROWS;
+  if (r0 >= cnt) return;
+  const int64_t n = *s.len;
+  const int64_t local_start = n > n_local ? n - n_local : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float inv_sqrt_d = 1.0f / sqrtf((float)D);
+  float q[GMAX][CPL];
+#pragma unroll
+  for (int h = 0; h < GMAX; ++h)
+#pragma unroll
+    for (int e = 0; e < CPL; ++e)
+      q[h][e] = h < G ? h2f(queries[((size_t)u * G + h) * D + lane * CPL + e]) : 0.0f;
+  // issue every row load of this warp first (PCIe latency hiding)
+  constexpr int CPW = (CPL + 1) / 2;  // 32-bit words per lane per row
+  uint32_t kw[SA_RPW][CPW], vw[SA_RPW][CPW];
+  int valid[SA_RPW];
+#pragma unroll
+  for (int j = 0; j < SA_RPW; ++j) {
+    const int r = r0 + warp * SA_RPW + j;
+    valid[j] = r < cnt;
+#pragma unroll
+    for (int e = 0; e < CPW; ++e) { kw[j][e] = 0; vw[j][e] = 0; }
+    if (!valid[j]) continue;
+    const int64_t idx = sel_idx[(size_t)u * sel_stride + r];
+    const uint16_t *kp, *vp;
+    if (idx < local_start) {
+      const uint16_t *row = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
+      kp = keys_from_device ? s.kdev + ((size_t)u * s.capacity + idx) * D : row;
+      vp = row + D;
+    } else {
+      const int64_t lr = idx - s.local_offset;
+      kp = s.loc_k + ((size_t)u * s.local_capacity + lr) * D;
+      vp = s.loc_v + ((size_t)u * s.local_capacity + lr) * D;
+    }
+    if constexpr (CPL == 4) {
+      const uint2 a = *reinterpret_cast<const uint2 *>(kp + lane * 4);
+      const uint2 b = *reinterpret_cast<const uint2 *>(vp + lane * 4);
+      kw[j][0] = a.x; kw[j][1] = a.y;
+      vw[j][0] = b.x; vw[j][1] = b.y;
+    } else if constexpr (CPL == 8) {
+      const uint4 a = *reinterpret_cast<const uint4 *>(kp + lane * 8);
+      const uint4 b = *reinterpret_cast<const uint4 *>(vp + lane * 8);
+      kw[j][0] = a.x; kw[j][1] = a.y; kw[j][2] = a.z; kw[j][3] = a.w;
+      vw[j][0] = b.x; vw[j][1] = b.y; vw[j][2] = b.z; vw[j][3] = b.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) {
+        kw[j][e >> 1] |= (uint32_t)kp[lane * CPL + e] << (16 * (e & 1));
+        vw[j][e >> 1] |= (uint32_t)vp[lane * CPL + e] << (16 * (e & 1));
+      }
+    }
+  }
+  float m[GMAX], l[GMAX], acc[GMAX][CPL];
+#pragma unroll
+  for (int h = 0; h < GMAX; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.0f;
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) acc[h][e] = 0.0f;
+  }
+#pragma unroll
+  for (int j = 0; j < SA_RPW; ++j) {
+    if (!valid[j]) continue;
+    float kf[CPL], vf[CPL];
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) {
+      kf[e] = h2f((uint16_t)(kw[j][e >> 1] >> (16 * (e & 1))));
+      vf[e] = h2f((uint16_t)(vw[j][e >> 1] >> (16 * (e & 1))));
+    }
+#pragma unroll
+    for (int h = 0; h < GMAX; ++h) {
+      if (h >= G) continue;
+      float dp = 0.0f;
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) dp = fmaf(q[h][e], kf[e], dp);
+      const float z = warp_sum(dp) * inv_sqrt_d;
+      const float mn = fmaxf(m[h], z);
+      const float sc = __expf(m[h] - mn), p = __expf(z - mn);
+      l[h] = l[h] * sc + p;
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) acc[h][e] = acc[h][e] * sc + p * vf[e];
+      m[h] = mn;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < GMAX; ++h) {
+    if (lane == 0) {
+      wm[warp][h] = m[h];
+      wl[warp][h] = l[h];
+    }
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) wacc[warp][h][lane * CPL + e] = acc[h][e];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int h = i / D, c = i % D;
+    float M = -INFINITY;
+    for (int wv = 0; wv < SA_WARPS; ++wv) M = fmaxf(M, wm[wv][h]);
+    float L = 0.0f, A = 0.0f;
+    for (int wv = 0; wv < SA_WARPS; ++wv) {
+      if (wm[wv][h] == -INFINITY) continue;
+      const float sc = __expf(wm[wv][h] - M);
+      L += sc * wl[wv][h];
+      A += sc * wacc[wv][h][c];
+    }
+    const size_t base = ((size_t)u * chunks + chunk) * G + h;
+    pacc[base * D + c] = A;
+    if (c == 0) {
+      pm[base] = M;
+      pl[base] = L;
+    }
+  }
+}
+
+int64_t sparse_attn_workspace(int units, int G, int d, int max_rows) {
+  const int chunks = (max_rows + SA_ROWS - 1) / SA_ROWS;
+  return (int64_t)units * chunks * G * (2 + d) * 4 + 256;
+}
+
+int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t *sel_idx, const int32_t *sel_count,
+                     int n_local, int max_rows, int keys_from_device, float *out, void *ws, cudaStream_t st) {
+  const int chunks = (max_rows + SA_ROWS - 1) / SA_ROWS;
+  float *pm = reinterpret_cast<float *>(ws);
+  float *pl = pm + (size_t)s.units * chunks * G;
+  float *pacc = pl + (size_t)s.units * chunks * G;
+  dim3 grid(chunks, s.units);
+  const int stride = max_rows;
+#define TKV_SA(D, GM)                                                                                        \
+  sparse_attn_kernel<D, GM><<<grid, SA_WARPS * 32, 0, st>>>(s, queries, G, sel_idx, sel_count, n_local, stride, \
+                                                            keys_from_device, pm, pl, pacc, chunks)
+  if (s.d == 128 && G <= 4) TKV_SA(128, 4);
+  else if (s.d == 128 && G <= 8) TKV_SA(128, 8);
+  else if (s.d == 64 && G <= 8) TKV_SA(64, 8);
+  else if (s.d == 32 && G <= 8) TKV_SA(32, 8);
+  else if (s.d == 96 && G <= 8) TKV_SA(96, 8);
+  else if (s.d == 256 && G <= 4) TKV_SA(256, 4);
+  else return fail(TKV_ERR_PARAMETER, "sparse attention supports d in {32,64,96,128,256} with G<=8 (G<=4 at d=256)");
+#undef TKV_SA
+  launch_combine(pm, pl, pacc, s.units, chunks, G, s.d, sel_count, SA_ROWS, out, st);
+  return check_launch("tkv_sparse_attention");
+}
+
+// ===========================================================================
+// PCIe probe: UVA zero-copy reads of random rows (the gather's roofline).
+// ===========================================================================
+__global__ void uva_probe_kernel(const uint4 *__restrict__ host, int row_vec, const int32_t *__restrict__ rows,
+                                 int nrows, float *sink) {
+  uint32_t x = 0;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  for (int r = wid; r < nrows; r += warps) {
+    const uint4 *row = host + (size_t)rows[r] * row_vec;
+    for (int v = lane; v < row_vec; v += 32) {
+      const uint4 a = __ldcv(row + v);
+      x ^= a.x ^ a.y ^ a.z ^ a.w;
+    }
+  }
+  if (x == 0x9e3779b9u) sink[0] = (float)x;  // keep the loads alive
+}
+
+int uva_probe(const void *host, size_t bytes, int row_bytes, const int32_t *rows, int nrows, float *sink,
+              cudaStream_t st) {
+  (void)bytes;
+  uva_probe_kernel<<<296, 256, 0, st>>>(reinterpret_cast<const uint4 *>(host), row_bytes / 16, rows, nrows, sink);
+  return check_launch("tkv_uva_read_probe");
+}
+
+}  // namespace tkv

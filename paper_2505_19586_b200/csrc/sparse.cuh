@@ -1,0 +1,24 @@
+#pragma once
+#include "qcache.cuh"
+
+namespace tkv {
+int sparse_prefill(const SL &s, const uint16_t *keys, const uint16_t *values, int64_t n, cudaStream_t st);
+int sparse_append(const SL &s, const uint16_t *nk, const uint16_t *nv, cudaStream_t st);
+int64_t stage1_workspace(int B, int hq, int H, int d);
+int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, int d, int G, const float *chmax,
+           int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st);
+int64_t select_workspace(int units, int64_t cap);
+int select_tokens(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
+                  int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, double *scores_out,
+                  void *ws, cudaStream_t st);
+int topk_from_scores(const double *scores, int units, int64_t n, int n_local, int n_topk, int32_t *sel_idx,
+                     int32_t *sel_count, void *ws, cudaStream_t st);
+int64_t sparse_attn_workspace(int units, int G, int d, int max_rows);
+int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t *sel_idx, const int32_t *sel_count,
+                     int n_local, int max_rows, int keys_from_device, float *out, void *ws, cudaStream_t st);
+int uva_probe(const void *host, size_t bytes, int row_bytes, const int32_t *rows, int nrows, float *sink,
+              cudaStream_t st);
+int64_t calibrate_workspace(int hq, int n_q, int64_t n);
+int dense_preference(const uint16_t *queries, const uint16_t *keys, int hq, int h, int n_q, int64_t n, int d,
+                     int64_t k, double *head_scores, void *ws, cudaStream_t st);
+}  // namespace tkv

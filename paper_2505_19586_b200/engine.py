@@ -1,0 +1,340 @@
+"""Hybrid decode engine: the per-layer decode-attention calls of
+hybridkv/pipeline.py:303-413 run as one stream-ordered (optionally CUDA-graph
+captured) decode step on one GPU, with KV heads sharded across ranks.
+
+Per step and layer l (pipeline.py order, attend-before-append):
+
+* quantization-friendly: ``QuantizedLayerKV.decode`` then ``append_token``;
+* sparsity-friendly: stage 1 (query estimate from hidden[l-1] + critical
+  channels) runs on a side stream as soon as layer l-1 starts, like the
+  reference's 1-worker prefetch executor (pipeline.py:288-313); then proxy
+  scores + exact top-k, PCIe gather + sparse attention, append;
+* with ``world_size > 1`` the head outputs of the layer are all-gathered
+  (one NCCL all-gather per layer over NVLink).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from .errors import ConfigError, ShapeError
+from .hoststore import OffloadedLayerKV
+from .identifier import LayerKind
+from .kv_model import ModelConfig
+from .quantizer import QuantizedLayerKV, as_f16
+from .retriever import WORKSPACES, RetrievalConfig, stage1_select
+from . import _lib
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """Decode-path knobs (the subset of PipelineConfig, pipeline.py:66-111,
+    that acts on the hot path) plus B200 placement options."""
+
+    bits: int = 1
+    group_size: int = 64
+    n_local: int = 64
+    n_topk: int = 128
+    critical_channels: int = 8
+    keys_on_device: bool = False   # gather K rows from HBM, only V crosses PCIe
+    quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
+
+    def validate(self) -> None:
+        if self.bits not in (1, 2):
+            raise ConfigError(f"bits must be 1 or 2 on the engine path, got {self.bits}")
+        if self.n_local < 0 or self.n_topk < 1 or self.critical_channels < 1:
+            raise ConfigError("token/channel budgets out of range")
+
+
+@dataclass(frozen=True)
+class ShardSlice:
+    """The (sequence, KV head) block one rank owns."""
+
+    b0: int
+    batch: int
+    k0: int
+    kv_heads: int
+
+
+def shard_plan(batch: int, num_kv_heads: int, world_size: int) -> list[ShardSlice]:
+    """Split the batch x kv-head units evenly over ranks:
+    heads are split inside a sequence when a rank owns fewer units than a
+    sequence has heads, otherwise whole sequences are assigned."""
+    units = batch * num_kv_heads
+    if units % world_size:
+        raise ConfigError(f"{units} (batch x kv heads) units do not split over {world_size} ranks")
+    per = units // world_size
+    plan = []
+    for r in range(world_size):
+        if per <= num_kv_heads:
+            if num_kv_heads % per:
+                raise ConfigError(f"{per} units per rank do not tile {num_kv_heads} kv heads")
+            plan.append(ShardSlice(b0=(r * per) // num_kv_heads, batch=1, k0=(r * per) % num_kv_heads, kv_heads=per))
+        else:
+            if per % num_kv_heads:
+                raise ConfigError(f"{per} units per rank are not whole sequences of {num_kv_heads} heads")
+            nb = per // num_kv_heads
+            plan.append(ShardSlice(b0=r * nb, batch=nb, k0=0, kv_heads=num_kv_heads))
+    return plan
+
+
+def assemble(gathered: list[torch.Tensor], plan: list[ShardSlice], batch: int, num_kv_heads: int) -> torch.Tensor:
+    """Per-rank outputs [B_r, h_r*G, d] -> full [batch, hq, d]."""
+    G = gathered[0].shape[1] // plan[0].kv_heads
+    d = gathered[0].shape[2]
+    out = gathered[0].new_empty((batch, num_kv_heads * G, d))
+    for s, t in zip(plan, gathered):
+        out[s.b0:s.b0 + s.batch, s.k0 * G:(s.k0 + s.kv_heads) * G] = t.reshape(s.batch, s.kv_heads * G, d)
+    return out
+
+
+def _label(x) -> str:
+    v = x.value if isinstance(x, LayerKind) else str(x)
+    if v in ("q", LayerKind.QUANTIZATION_FRIENDLY.value):
+        return "q"
+    if v in ("s", LayerKind.SPARSITY_FRIENDLY.value):
+        return "s"
+    raise ConfigError(f"unknown layer label {x!r}")
+
+
+@dataclass
+class _SparseState:
+    layer: OffloadedLayerKV
+    w_q: torch.Tensor          # [hq_r, hidden, d] fp16
+    channels: torch.Tensor     # [units, d_s] int32
+    s1_ws: torch.Tensor
+    s1_done: torch.cuda.Event = field(default_factory=lambda: torch.cuda.Event())
+
+
+class DecodeEngine:
+    """All layers of one model replica shard on one GPU."""
+
+    def __init__(self, model: ModelConfig, labels, config: EngineConfig, batch: int = 1, max_steps: int = 64,
+                 rank: int = 0, world_size: int = 1, process_group=None, device=None):
+        _lib.require_cuda()
+        config.validate()
+        self.model, self.cfg = model, config
+        self.labels = [_label(x) for x in labels]
+        if len(self.labels) != model.num_layers:
+            raise ConfigError("one label per layer is required")
+        self.batch, self.max_steps = batch, max_steps
+        self.rank, self.world = rank, world_size
+        self.group = process_group
+        self.plan = shard_plan(batch, model.num_kv_heads, world_size)
+        self.shard = self.plan[rank]
+        self.G = model.queries_per_kv_head
+        self.units = self.shard.batch * self.shard.kv_heads
+        self.hq_r = self.shard.kv_heads * self.G
+        self.d = model.head_dim
+        self.device = torch.device(device or "cuda")
+        self.retrieval = RetrievalConfig(config.n_local, config.n_topk, min(config.critical_channels, self.d))
+        self.layers: list = [None] * model.num_layers
+        self.sparse: dict[int, _SparseState] = {}
+        self.prefill_len = None
+        self.side = torch.cuda.Stream(device=self.device)
+        L, U, d = model.num_layers, self.units, self.d
+        kmax = self.retrieval.n_local + self.retrieval.n_topk
+        dev = self.device
+        # static per-step buffers (graph inputs/outputs)
+        self.hidden = torch.zeros((L, self.shard.batch, model.hidden_dim), dtype=torch.float16, device=dev)
+        self.queries = torch.zeros((L, U * self.G, d), dtype=torch.float16, device=dev)
+        self.new_keys = torch.zeros((L, U, d), dtype=torch.float16, device=dev)
+        self.new_values = torch.zeros((L, U, d), dtype=torch.float16, device=dev)
+        self.out = torch.zeros((L, U * self.G, d), dtype=torch.float32, device=dev)
+        self.gathered = (torch.zeros((L, world_size, U * self.G, d), dtype=torch.float32, device=dev)
+                         if world_size > 1 else None)
+        self.sel_idx = torch.zeros((U, kmax), dtype=torch.int32, device=dev)
+        self.sel_count = torch.zeros(U, dtype=torch.int32, device=dev)
+        self.fetch_count = torch.zeros(U, dtype=torch.int32, device=dev)
+        lib = _lib.load()
+        self.attn_ws = torch.zeros(int(lib.tkv_sparse_attn_workspace(U, self.G, d, kmax)), dtype=torch.uint8, device=dev)
+        self.sel_ws = None
+        self.graph = None
+        self.steps_done = 0
+        self.record_selection = False
+        self.profile = None  # list of (name, layer, start_event, end_event) when profiling
+        self.last_channels: dict[int, torch.Tensor] = {}
+        self.last_selection: dict[int, tuple] = {}
+
+    # -- prefill ---------------------------------------------------------------
+    def _slice_kv(self, x):
+        """[B, h, n, d] (full) or [B_r, h_r, n, d] (already sharded) -> units."""
+        x = as_f16(x, self.device)
+        s = self.shard
+        if x.dim() == 3:
+            x = x[None]
+        if x.shape[0] == self.batch and x.shape[1] == self.model.num_kv_heads and (self.world > 1):
+            x = x[s.b0:s.b0 + s.batch, s.k0:s.k0 + s.kv_heads]
+        if x.shape[0] != s.batch or x.shape[1] != s.kv_heads:
+            raise ShapeError(f"prefill K/V must be [{self.batch}, {self.model.num_kv_heads}, n, d]")
+        return x.reshape(self.units, x.shape[2], x.shape[3]).contiguous()
+
+    def prefill(self, layer: int, keys, values, w_q=None) -> None:
+        """Compress (Q layer, quantize_layer_kv) or offload (S layer,
+        HostPool.offload_layer) one layer's prefill cache."""
+        k, v = self._slice_kv(keys), self._slice_kv(values)
+        n = k.shape[1]
+        if self.prefill_len is None:
+            self.prefill_len = n
+        cap = n + self.max_steps
+        if self.labels[layer] == "q":
+            self.layers[layer] = QuantizedLayerKV.from_kv(k, v, self.cfg.bits, self.cfg.group_size, capacity=cap)
+            self.layers[layer].workspace(self.G)  # allocate before any graph capture
+        else:
+            if w_q is None:
+                raise ConfigError(f"sparsity-friendly layer {layer} needs its W_q for stage 1")
+            lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local,
+                                   keys_on_device=self.cfg.keys_on_device, device=self.device)
+            lay.offload(k, v)
+            w = as_f16(w_q, self.device)
+            if w.shape[0] == self.model.num_query_heads:
+                w = w[self.shard.k0 * self.G:(self.shard.k0 + self.shard.kv_heads) * self.G]
+            w = w.contiguous()
+            lib = _lib.load()
+            ws = torch.zeros(int(lib.tkv_stage1_workspace(self.shard.batch, self.hq_r, w.shape[1], self.d)),
+                             dtype=torch.uint8, device=self.device)
+            chans = torch.zeros((self.units, self.retrieval.d_s), dtype=torch.int32, device=self.device)
+            self.sparse[layer] = _SparseState(lay, w, chans, ws)
+            self.layers[layer] = lay
+            if self.sel_ws is None:
+                self.sel_ws = torch.zeros(int(lib.tkv_select_workspace(self.units, cap)), dtype=torch.uint8,
+                                          device=self.device)
+
+    # -- one step --------------------------------------------------------------
+    def load_step(self, hidden, queries, new_keys, new_values, non_blocking: bool = True) -> None:
+        """Copy one step's inputs into the static buffers.  Shapes (full or
+        rank slice): hidden [L, B, hidden], queries [L, B, hq, d],
+        new_keys/new_values [L, B, h, d]."""
+        s = self.shard
+
+        def sl(x, heads_per_unit):
+            if x.shape[1] == self.batch and self.world > 1:
+                x = x[:, s.b0:s.b0 + s.batch]
+                if heads_per_unit:
+                    x = x[:, :, s.k0 * heads_per_unit:(s.k0 + s.kv_heads) * heads_per_unit]
+            return x
+
+        self.hidden.copy_(sl(hidden, 0).reshape(self.hidden.shape), non_blocking=non_blocking)
+        self.queries.copy_(sl(queries, self.G).reshape(self.queries.shape), non_blocking=non_blocking)
+        self.new_keys.copy_(sl(new_keys, 1).reshape(self.new_keys.shape), non_blocking=non_blocking)
+        self.new_values.copy_(sl(new_values, 1).reshape(self.new_values.shape), non_blocking=non_blocking)
+
+    def _stage1(self, l: int) -> None:
+        st = self.sparse[l]
+        src = l - 1 if l >= 1 else 0  # pipeline.py:273
+        t0 = self._mark(self.side)
+        stage1_select(self.hidden[src], st.w_q, st.layer.chmax, self.G, self.retrieval.d_s,
+                      channels=st.channels, workspace=st.s1_ws, stream=self.side)
+        self._span("stage1", l, t0, self.side)
+        st.s1_done.record(self.side)
+
+    def _mark(self, stream):
+        if self.profile is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return ev
+
+    def _span(self, name, layer, start, stream):
+        if self.profile is not None:
+            self.profile.append((name, layer, start, self._mark(stream)))
+
+    def kernels_per_step(self) -> int:
+        """Launches of this library per decode step."""
+        q = sum(1 for x in self.labels if x == "q")
+        s = len(self.labels) - q
+        return q * 3 + s * 9
+
+    def _run_step(self) -> None:
+        main = torch.cuda.current_stream(self.device)
+        L = self.model.num_layers
+        begin = [torch.cuda.Event() for _ in range(L)]
+        for l in range(L):
+            begin[l].record(main)
+            nxt = [j for j in ((0, 1) if l == 0 else (l + 1,)) if j < L and self.labels[j] == "s"]
+            for j in nxt:
+                self.side.wait_event(begin[l])
+                with torch.cuda.stream(self.side):
+                    self._stage1(j)
+            lay = self.layers[l]
+            if self.labels[l] == "q":
+                t0 = self._mark(main)
+                lay.decode(self.queries[l], out=self.out[l], impl=self.cfg.quant_impl)
+                self._span("quant_decode", l, t0, main)
+                t0 = self._mark(main)
+                lay.append_token(self.new_keys[l], self.new_values[l])
+                self._span("quant_append", l, t0, main)
+            else:
+                st = self.sparse[l]
+                main.wait_event(st.s1_done)
+                t0 = self._mark(main)
+                lay.select(self.queries[l], st.channels, self.G, self.retrieval, self.sel_idx, self.sel_count,
+                           self.fetch_count, self.sel_ws)
+                self._span("select", l, t0, main)
+                if self.record_selection:
+                    self.last_channels[l] = st.channels.clone()
+                    self.last_selection[l] = (self.sel_idx.clone(), self.sel_count.clone(), self.fetch_count.clone())
+                t0 = self._mark(main)
+                lay.attend(self.queries[l], self.G, self.retrieval, self.sel_idx, self.sel_count, self.out[l],
+                           self.attn_ws, keys_from_device=self.cfg.keys_on_device)
+                self._span("gather_attend", l, t0, main)
+                t0 = self._mark(main)
+                lay.append(self.new_keys[l], self.new_values[l])
+                self._span("sparse_append", l, t0, main)
+            if self.world > 1:
+                torch.distributed.all_gather_into_tensor(self.gathered[l], self.out[l], group=self.group)
+        main.wait_stream(self.side)
+
+    def step(self, hidden=None, queries=None, new_keys=None, new_values=None) -> torch.Tensor:
+        """Run one decode step; returns this rank's outputs [L, units*G, d]
+        (fp32, device).  With inputs None the static buffers are used."""
+        if hidden is not None:
+            self.load_step(hidden, queries, new_keys, new_values)
+        if self.steps_done >= self.max_steps:
+            raise ConfigError("engine max_steps exhausted")
+        if self.graph is not None:
+            self.graph.replay()
+            for lay in self.layers:
+                lay.n += 1
+            self.steps_done += 1
+        else:
+            self._run_step()
+            self.steps_done += 1
+        return self.out
+
+    def step_profiled(self, hidden=None, queries=None, new_keys=None, new_values=None) -> dict:
+        """One eager step with CUDA events around every kernel group; returns
+        {name: [ms per launch]} (used by bench.py for the roofline)."""
+        if hidden is not None:
+            self.load_step(hidden, queries, new_keys, new_values)
+        self.profile = []
+        self._run_step()
+        self.steps_done += 1
+        torch.cuda.synchronize()
+        res: dict = {}
+        for name, layer, a, b in self.profile:
+            res.setdefault(name, []).append(a.elapsed_time(b))
+        self.profile = None
+        return res
+
+    def capture(self) -> None:
+        """Capture one decode step in a CUDA graph; ``step`` then replays it.
+        Capturing executes nothing, so the caches do not advance; the host
+        mirrors of the token counts are restored afterwards."""
+        saved = [lay.n for lay in self.layers]
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._run_step()
+        for lay, n in zip(self.layers, saved):
+            lay.n = n
+        self.graph = g
+
+    def full_output(self, l: int) -> torch.Tensor:
+        """Layer output [batch, hq, d] (all ranks' heads)."""
+        if self.world == 1:
+            return self.out[l].reshape(self.batch, self.model.num_query_heads, self.d)
+        parts = [self.gathered[l][r].reshape(s.batch, s.kv_heads * self.G, self.d) for r, s in enumerate(self.plan)]
+        return assemble(parts, self.plan, self.batch, self.model.num_kv_heads)

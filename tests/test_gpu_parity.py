@@ -1,0 +1,333 @@
+"""GPU parity: every CUDA path against the reference golden vectors and the
+CPU oracle on identical fp16 inputs.
+
+Tolerances (BASELINE.json north_star): packed bit-planes / GQT1 blobs
+bit-exact; top-k and channel index sets exact (no exact score ties are
+resolved differently: ties use the reference's index rule); attention
+outputs within relative error 2e-3, where
+    rel_err = max over query heads of ||out - ref||_2 / ||ref||_2.
+"""
+
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import tailorkv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+META = json.loads((GOLD / "golden.json").read_text())
+KER = np.load(GOLD / "kernels.npz")
+REL_TOL = 2e-3
+
+
+def rel_err(out, ref):
+    out = np.asarray(out, np.float64).reshape(ref.shape[0], -1)
+    ref = np.asarray(ref, np.float64).reshape(ref.shape[0], -1)
+    return float(max(np.linalg.norm(o - r) / max(np.linalg.norm(r), 1e-30) for o, r in zip(out, ref)))
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def tkv():
+    import paper_2505_19586_b200 as P
+
+    return P
+
+
+# ---------------------------------------------------------------------------
+# K1/K2 pack + GQT1 export: bit-exact against the reference
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case", [c for c in cases.PACK_CASES if c["gpu"]], ids=lambda c: c["name"])
+def test_pack_gqt1_bit_exact(tkv, case):
+    k, v = cases.pack_inputs(case)
+    q = tkv.quantize_layer_kv(k[None], v[None], case["bits"], case["g"])
+    gold = META["pack"][case["name"]]
+    kb, vb = q.to_bytes(0, "keys"), q.to_bytes(0, "values")
+    assert len(kb) == gold["keys_len"] and sha(kb) == gold["keys_sha256"]
+    assert len(vb) == gold["values_len"] and sha(vb) == gold["values_sha256"]
+
+
+def test_pack_multi_unit_each_head_exact(tkv):
+    rng = np.random.default_rng(3)
+    keys = cases.f16(rng.normal(size=(5, 700, 128)))
+    values = cases.f16(rng.normal(size=(5, 700, 128)))
+    for bits in (1, 2):
+        q = tkv.quantize_layer_kv(keys, values, bits, 64)
+        for u in range(5):
+            with np.errstate(over="ignore"):
+                assert q.to_bytes(u, "keys") == O.quantize_keys(keys[u], bits, 64).to_bytes()
+                assert q.to_bytes(u, "values") == O.quantize_values(values[u], bits, 64).to_bytes()
+
+
+@pytest.mark.parametrize("bits", [1, 2])
+def test_append_matches_batch_quantization(tkv, bits):
+    # quantizer.py:445-451 + test_quantizer.py:204-222: incremental == batch
+    rng = np.random.default_rng(4 + bits)
+    n0, T = 250, 80  # crosses two key-group boundaries (256, 320)
+    keys = cases.f16(rng.normal(size=(3, n0 + T, 128)))
+    values = cases.f16(rng.normal(size=(3, n0 + T, 128)))
+    q = tkv.QuantizedLayerKV.from_kv(keys[:, :n0], values[:, :n0], bits, 64, capacity=n0 + T)
+    for t in range(T):
+        q.append_token(keys[:, n0 + t], values[:, n0 + t])
+    for u in range(3):
+        assert q.to_bytes(u, "keys") == O.quantize_keys(keys[u], bits, 64).to_bytes()
+        assert q.to_bytes(u, "values") == O.quantize_values(values[u], bits, 64).to_bytes()
+
+
+def test_dequantize_bound(tkv):
+    rng = np.random.default_rng(8)
+    keys = cases.f16(rng.normal(size=(1, 513, 128)))
+    values = cases.f16(rng.normal(size=(1, 513, 128)))
+    q = tkv.quantize_layer_kv(keys, values, 2, 64)
+    kt = O.quantize_keys(keys[0], 2, 64)
+    np.testing.assert_allclose(q.dequantize(0, "keys").cpu().numpy(), kt.dequantize(), rtol=1e-6, atol=1e-6)
+
+
+def test_error_mapping(tkv):
+    with pytest.raises(tkv.EmptyCacheError):
+        tkv.quantize_layer_kv(np.zeros((1, 0, 128)), np.zeros((1, 0, 128)), 1, 64)
+    with pytest.raises(tkv.ParameterError):
+        tkv.quantize_layer_kv(np.zeros((1, 64, 128)), np.zeros((1, 64, 128)), 3, 64)
+    with pytest.raises(tkv.ShapeError):
+        tkv.quantize_layer_kv(np.zeros((1, 64, 128)), np.zeros((1, 65, 128)), 1, 64)
+    bad = np.zeros((1, 64, 128))
+    bad[0, 3, 4] = np.inf
+    with pytest.raises(tkv.NumericError):
+        tkv.quantize_layer_kv(bad, np.zeros((1, 64, 128)), 1, 64)
+
+
+# ---------------------------------------------------------------------------
+# K4 quantized decode attention
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("impl", [1, 0])
+@pytest.mark.parametrize("case", cases.DECODE_CASES, ids=lambda c: c["name"])
+def test_quant_decode_matches_reference(tkv, case, impl):
+    keys, values, queries = cases.decode_inputs(case)
+    q = tkv.quantize_layer_kv(keys, values, case["bits"], case["g"])
+    out = q.decode(queries, impl=impl).cpu().numpy()
+    ref = KER[case["name"] + "/out"]
+    assert rel_err(out, ref) <= REL_TOL
+
+
+def test_qgemv_raw_ops(tkv):
+    keys, values, queries = cases.decode_inputs(cases.DECODE_CASES[0])
+    q = tkv.quantize_layer_kv(keys, values, 1, 64)
+    logits = tkv.qgemv_scores(queries[0], q, 0).cpu().numpy()
+    np.testing.assert_allclose(logits, KER["dec_b1_ragged/logits0"], rtol=1e-5, atol=1e-4)
+    kq, vq = O.quantize_layer(keys, values, 1, 64)
+    w = O.stable_softmax(logits.astype(np.float64) / np.sqrt(128))
+    ref = O.qgemv_output(w, vq[0])
+    np.testing.assert_allclose(tkv.qgemv_output(w, q, 0).cpu().numpy(), ref, rtol=1e-5, atol=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# K5-K7 retrieval
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case", cases.TOPK_CASES, ids=lambda c: c["name"])
+def test_topk_exact(tkv, case):
+    scores = cases.topk_scores(case)
+    sel = tkv.select_topk_tokens(scores, tkv.RetrievalConfig(case["n_local"], case["n_topk"]))
+    assert np.array_equal(sel, KER[case["name"]])
+
+
+def test_topk_batched_units(tkv):
+    rng = np.random.default_rng(9)
+    s = rng.normal(size=(6, 9000))
+    s[3] = np.round(s[3])  # heavy ties in one unit
+    sel = tkv.select_topk_tokens(s, tkv.RetrievalConfig(32, 300))
+    for u in range(6):
+        assert np.array_equal(sel[u], O.select_tokens(s[u], 32, 300))
+
+
+@pytest.mark.parametrize("case", cases.CHANNEL_CASES, ids=lambda c: c["name"])
+def test_stage1_channels_exact(tkv, case):
+    qhat, chmax = cases.channel_inputs(case)
+    G, d = qhat.shape
+    # hidden = concat(q_hat heads), W_q[h] selects its slice -> q_hat exactly
+    hidden = torch.tensor(qhat.reshape(1, -1), dtype=torch.float16, device="cuda")
+    W = torch.zeros((G, G * d, d), dtype=torch.float16, device="cuda")
+    for h in range(G):
+        W[h, h * d:(h + 1) * d] = torch.eye(d)
+    cm = torch.tensor(chmax[None], dtype=torch.float32, device="cuda")
+    ch = tkv.stage1_select(hidden, W, cm, G, case["d_s"]).cpu().numpy()[0]
+    ref = O.select_channels(O.group_channel_scores(cases.f16(qhat), chmax.astype(np.float32)), case["d_s"])
+    assert np.array_equal(ch, ref)
+
+
+def test_stage1_estimate_matches_oracle(tkv):
+    rng = np.random.default_rng(10)
+    hq, H, d, G = 8, 1024, 128, 4
+    w_q = cases.f16(rng.normal(size=(hq, H, d)) / np.sqrt(H))
+    hid = cases.f16(rng.normal(size=(2, H)))
+    chmax = cases.f16(np.abs(rng.normal(size=(2 * hq // G, d))) + 0.1)
+    qhat = torch.empty((2, hq, d), dtype=torch.float64, device="cuda")
+    ch = tkv.stage1_select(torch.tensor(hid, dtype=torch.float16, device="cuda"),
+                           torch.tensor(w_q, dtype=torch.float16, device="cuda"),
+                           torch.tensor(chmax, dtype=torch.float32, device="cuda"), G, 8, q_hat=qhat).cpu().numpy()
+    for b in range(2):
+        ref_q = O.estimate_query(w_q, hid[b])
+        np.testing.assert_allclose(qhat[b].cpu().numpy(), ref_q, rtol=1e-10, atol=1e-12)
+        for kvh in range(hq // G):
+            ref = O.select_channels(O.group_channel_scores(ref_q[kvh * G:(kvh + 1) * G], chmax[b * 2 + kvh]), 8)
+            assert np.array_equal(ch[b * 2 + kvh], ref)
+
+
+def _sparse_layer(tkv, keys, values, n_local, steps=4, keys_on_device=False):
+    units, n, d = keys.shape
+    lay = tkv.OffloadedLayerKV(units, d, n + steps, n, n_local, keys_on_device=keys_on_device)
+    lay.offload(keys, values)
+    return lay
+
+
+@pytest.mark.parametrize("kod", [False, True])
+def test_select_and_sparse_attention_match_oracle(tkv, kod):
+    rng = np.random.default_rng(11)
+    units, n, d, G, d_s = 3, 5000, 128, 4, 8
+    keys = cases.f16(rng.normal(size=(units, n, d)))
+    values = cases.f16(rng.normal(size=(units, n, d)))
+    queries = cases.f16(rng.normal(size=(units * G, d)))
+    cfg = tkv.RetrievalConfig(64, 200, d_s)
+    lay = _sparse_layer(tkv, keys, values, cfg.n_local, keys_on_device=kod)
+    chans = np.stack([np.sort(rng.choice(d, d_s, replace=False)) for _ in range(units)]).astype(np.int32)
+    qdev = torch.tensor(queries, dtype=torch.float16, device="cuda")
+    cdev = torch.tensor(chans, device="cuda")
+    import paper_2505_19586_b200._lib as L
+    ws = torch.zeros(int(L.load().tkv_select_workspace(units, lay.capacity)), dtype=torch.uint8, device="cuda")
+    kmax = cfg.n_local + cfg.n_topk
+    idx = torch.zeros((units, kmax), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(units, dtype=torch.int32, device="cuda")
+    fc = torch.zeros(units, dtype=torch.int32, device="cuda")
+    scores = torch.zeros((units, lay.capacity), dtype=torch.float64, device="cuda")
+    lay.select(qdev, cdev, G, cfg, idx, cnt, fc, ws, scores_out=scores)
+    out = torch.zeros((units * G, d), dtype=torch.float32, device="cuda")
+    aws = torch.zeros(int(L.load().tkv_sparse_attn_workspace(units, G, d, kmax)), dtype=torch.uint8, device="cuda")
+    lay.attend(qdev, G, cfg, idx, cnt, out, aws, keys_from_device=kod)
+    idx, cnt, fc = idx.cpu().numpy(), cnt.cpu().numpy(), fc.cpu().numpy()
+    ref_out = np.empty((units * G, d))
+    for u in range(units):
+        qg = queries[u * G:(u + 1) * G]
+        sc = O.approx_scores(qg[:, chans[u]], keys[u][:, chans[u]])
+        np.testing.assert_allclose(scores[u, :n - cfg.n_local].cpu().numpy(), sc[:n - cfg.n_local], rtol=1e-12)
+        sel = O.select_tokens(sc, cfg.n_local, cfg.n_topk)
+        assert np.array_equal(idx[u, :cnt[u]], sel)
+        assert fc[u] == int((sel < n - cfg.n_local).sum())
+        for j in range(G):
+            ref_out[u * G + j] = O.sparse_attention(qg[j], keys[u], values[u], sel)
+    assert rel_err(out.cpu().numpy(), ref_out) <= 1e-5
+
+
+def test_host_store_gather_roundtrip(tkv):
+    rng = np.random.default_rng(12)
+    keys = cases.f16(rng.normal(size=(2, 300, 64)))
+    values = cases.f16(rng.normal(size=(2, 300, 64)))
+    lay = _sparse_layer(tkv, keys, values, 16)
+    idx = np.array([5, 0, 299, 17])
+    k, v = lay.gather(1, idx)
+    assert np.array_equal(k, keys[1][idx]) and np.array_equal(v, values[1][idx])
+    np.testing.assert_array_equal(lay.channel_abs_max().cpu().numpy(), np.abs(keys).max(axis=1))
+
+
+# ---------------------------------------------------------------------------
+# Layer classification (identifier.py) against the reference
+# ---------------------------------------------------------------------------
+def test_calibrate_matches_reference(tkv):
+    for c in cases.CALIB_CASES:
+        pq, pk = cases.calib_inputs(c)
+        g = META["calibrate"][c["name"]]
+        probe = tkv.SparsityProbe(k=g["k"], n_q=c["n_q"], tau=c["tau"])
+        prof = tkv.calibrate(list(pq), list(pk), probe)
+        for p, ref in zip(prof, g["layers"]):
+            np.testing.assert_allclose(p.per_head_scores, ref["scores"], rtol=1e-5, atol=1e-6)
+            assert p.label.value == ref["label"]
+
+
+# ---------------------------------------------------------------------------
+# Whole decode replay vs the reference pipeline (selections) and the oracle
+# (outputs), eager and CUDA-graph
+# ---------------------------------------------------------------------------
+def _golden_trace():
+    z = np.load(GOLD / "pipeline_trace.npz")
+    return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("run", list(cases.PIPELINE_CONFIGS), ids=str)
+def test_engine_replays_reference_pipeline(tkv, run, graph):
+    z = _golden_trace()
+    ref = META["pipeline"]["runs"][run]
+    rc = ref["config"]
+    L, h, n0, d = z["prefill_keys"].shape
+    hq = z["w_q"].shape[1]
+    T = z["queries"].shape[0]
+    labels = ["q" if lab == "quantization_friendly" else "s" for lab in ref["labels"]]
+    cfg = tkv.EngineConfig(bits=rc.get("bits", 1), n_local=rc.get("n_local", 64), n_topk=rc.get("n_topk", 128),
+                           critical_channels=rc.get("critical_channels", 8))
+    model = tkv.ModelConfig(L, hq, h, d, hq * d)
+    eng = tkv.DecodeEngine(model, labels, cfg, batch=1, max_steps=T)
+    for l in range(L):
+        eng.prefill(l, z["prefill_keys"][l][None], z["prefill_values"][l][None], z["w_q"][l])
+    eng.record_selection = not graph
+    if graph:
+        eng.capture()
+    steps = [{"hidden": z["hidden"][t].astype(np.float64), "queries": z["queries"][t].astype(np.float64),
+              "new_keys": z["new_keys"][t].astype(np.float64), "new_values": z["new_values"][t].astype(np.float64)}
+             for t in range(T)]
+    orc = O.replay(list(z["prefill_keys"].astype(np.float64)), list(z["prefill_values"].astype(np.float64)),
+                   list(z["w_q"].astype(np.float64)), steps, labels, bits=cfg.bits, n_local=cfg.n_local,
+                   n_topk=cfg.n_topk, d_s=cfg.critical_channels, compute_exact=False)
+    recs = {(r["layer"], r["step"]): r for r in ref["retrieval"]}
+    worst = 0.0
+    for t in range(T):
+        dev = lambda a: torch.tensor(a[:, None], dtype=torch.float16, device="cuda")  # noqa: E731
+        out = eng.step(dev(z["hidden"][t]), dev(z["queries"][t]), dev(z["new_keys"][t]), dev(z["new_values"][t]))
+        out = out.cpu().numpy()
+        for l in range(L):
+            worst = max(worst, rel_err(out[l], orc.outputs[t][l]))
+            if not graph and labels[l] == "s":
+                idx, cnt, fc = (x.cpu().numpy() for x in eng.last_selection[l])
+                chans = eng.last_channels[l].cpu().numpy()
+                for kvh, ph in enumerate(recs[(l, t)]["per_head"]):
+                    assert chans[kvh].tolist() == ph["channels"], (l, t, kvh)
+                    assert np.array_equal(idx[kvh, :cnt[kvh]], cases.hex_to_indices(ph["selected_hex"])), (l, t, kvh)
+                    assert fc[kvh] == ph["fetched"]
+    assert worst <= REL_TOL, worst
+
+
+def test_engine_config1_shapes(tkv):
+    """BASELINE config 1 shapes (Llama-8B heads, 4k, 1 Q 1-bit + 1 S layer,
+    n_topk=128) on synthetic inputs against the oracle replay."""
+    from paper_2505_19586_b200.synth import make_workload
+
+    w = make_workload(2, (0,), 32, 8, 128, 4096, 4, seed=7)
+    cfg = tkv.EngineConfig(bits=1, n_local=64, n_topk=128, critical_channels=8)
+    model = tkv.ModelConfig(2, 32, 8, 128, 4096)
+    eng = tkv.DecodeEngine(model, w.labels, cfg, max_steps=4)
+    w_q_np = []
+    for l in range(2):
+        wq = w.w_q[l] if w.w_q[l] is not None else torch.zeros(32, 4096, 128, dtype=torch.float16, device="cuda")
+        eng.prefill(l, w.prefill_keys[l], w.prefill_values[l], wq)
+        w_q_np.append(wq.double().cpu().numpy())
+    steps = [{"hidden": w.hidden[t, :, 0].double().cpu().numpy(), "queries": w.queries[t, :, 0].double().cpu().numpy(),
+              "new_keys": w.new_keys[t, :, 0].double().cpu().numpy(),
+              "new_values": w.new_values[t, :, 0].double().cpu().numpy()} for t in range(4)]
+    orc = O.replay([k[0].double().cpu().numpy() for k in w.prefill_keys],
+                   [v[0].double().cpu().numpy() for v in w.prefill_values], w_q_np, steps, w.labels,
+                   compute_exact=False)
+    eng.record_selection = True
+    for t in range(4):
+        out = eng.step(w.hidden[t], w.queries[t], w.new_keys[t], w.new_values[t]).cpu().numpy()
+        for l in range(2):
+            assert rel_err(out[l], orc.outputs[t][l]) <= REL_TOL
+        idx, cnt, _ = (x.cpu().numpy() for x in eng.last_selection[1])
+        for kvh in range(8):
+            assert np.array_equal(idx[kvh, :cnt[kvh]], orc.selected[(1, t)][kvh])
