@@ -28,6 +28,25 @@ __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { retur
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 __device__ __forceinline__ double h2d(uint16_t h) { return (double)__half2float(__ushort_as_half(h)); }
 
+// float64 -> fp16 bits, round to nearest even (numpy's astype(float16) of a
+// float64); written out because __double2half is not a direct conversion.
+__device__ __forceinline__ uint16_t f64_to_f16_bits(double x) {
+  const uint64_t b = (uint64_t)__double_as_longlong(x);
+  const uint16_t sign = (uint16_t)((b >> 48) & 0x8000u);
+  const int ex = (int)((b >> 52) & 0x7ff);
+  if (ex == 0x7ff) return sign | ((b & 0xfffffffffffffull) ? 0x7e00u : 0x7c00u);
+  const double a = fabs(x);
+  if (a < 6.103515625e-05) {  // below 2^-14: subnormal grid of 2^-24
+    const double q = rint(a * 16777216.0);
+    return sign | (uint16_t)q;  // q == 1024 is the smallest normal
+  }
+  int e = ex - 1023;
+  double q = rint(ldexp(a, 10 - e));  // in [1024, 2048]
+  if (q >= 2048.0) { q = 1024.0; ++e; }
+  if (e > 15) return sign | 0x7c00u;
+  return sign | (uint16_t)(((e + 15) << 10) | ((int)q - 1024));
+}
+
 __device__ __forceinline__ uint32_t pack_lohi(uint16_t lo, uint16_t hi) {
   return (uint32_t)lo | ((uint32_t)hi << 16);
 }

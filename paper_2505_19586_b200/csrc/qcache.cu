@@ -344,7 +344,7 @@ __device__ __forceinline__ uint16_t scale_f16(uint32_t lohi, int bits) {
   const double lo = h2d(lohi & 0xffff), hi = h2d(lohi >> 16);
   double s = __ddiv_rn(__dsub_rn(hi, lo), (double)((1 << bits) - 1));
   if (s == 0.0) s = 1.0;
-  return __half_as_ushort(__double2half(s));
+  return f64_to_f16_bits(s);
 }
 
 __global__ void export_kernel(QC c, int u, int which, int64_t n, uint8_t *out, int64_t packed_len,
