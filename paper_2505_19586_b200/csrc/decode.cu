@@ -14,39 +14,63 @@ constexpr int SIMT_CHUNK = 256;  // tokens per CTA in the SIMT kernel
 // Fixed chunk order -> bit-identical repeated runs (pipeline determinism,
 // test_pipeline.py:189-195).
 // ---------------------------------------------------------------------------
-__global__ void combine_kernel(const float *__restrict__ pm, const float *__restrict__ pl,
-                               const float *__restrict__ pacc, int chunks, int G, int d,
-                               const int32_t *__restrict__ rows, int rows_stride, int rows_per_chunk,
-                               float *__restrict__ out) {
+__global__ void __launch_bounds__(256) combine_kernel(const float *__restrict__ pm, const float *__restrict__ pl,
+                                                       const float *__restrict__ pacc, int chunks, int G, int d,
+                                                       const int32_t *__restrict__ rows, int rows_stride,
+                                                       int rows_per_chunk, float *__restrict__ out) {
+  __shared__ float red_m[8];
+  __shared__ float part_acc[256];
+  __shared__ float part_l[256];
   const int u = blockIdx.x / G, h = blockIdx.x % G;
   const int nrows = rows ? rows[(size_t)u * rows_stride] : chunks * rows_per_chunk;
   const int valid = min(chunks, (nrows + rows_per_chunk - 1) / rows_per_chunk);
+  const size_t base0 = (size_t)u * chunks * G + h;
+  // global max over the valid chunks
   float M = -INFINITY;
-  for (int ci = 0; ci < valid; ++ci) M = fmaxf(M, pm[((size_t)u * chunks + ci) * G + h]);
-  for (int ch = threadIdx.x; ch < d; ch += blockDim.x) {
-    float L = 0.0f, acc = 0.0f;
-    for (int ci = 0; ci < valid; ++ci) {
-      const size_t base = ((size_t)u * chunks + ci) * G + h;
+  for (int ci = threadIdx.x; ci < valid; ci += blockDim.x) M = fmaxf(M, pm[base0 + (size_t)ci * G]);
+  M = warp_max(M);
+  if ((threadIdx.x & 31) == 0) red_m[threadIdx.x >> 5] = M;
+  __syncthreads();
+  M = -INFINITY;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) M = fmaxf(M, red_m[i]);
+  // thread = (chunk slice, channel); fixed summation order per slice
+  const int slices = max(1, (int)blockDim.x / d);
+  const int ch = threadIdx.x % d, sl = threadIdx.x / d;
+  float L = 0.0f, acc = 0.0f;
+  if (sl < slices) {
+#pragma unroll 4
+    for (int ci = sl; ci < valid; ci += slices) {
+      const size_t base = base0 + (size_t)ci * G;
       const float m = pm[base];
-      if (m == -INFINITY) continue;
-      const float sc = __expf(m - M);
+      const float sc = m == -INFINITY ? 0.0f : __expf(m - M);
       L += sc * pl[base];
       acc += sc * pacc[base * d + ch];
     }
-    out[((size_t)u * G + h) * d + ch] = acc / L;
+  }
+  if (sl < slices) {
+    part_acc[threadIdx.x] = acc;
+    part_l[threadIdx.x] = L;
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    float a = 0.0f, l = 0.0f;
+    for (int j = 0; j < slices; ++j) {
+      a += part_acc[j * d + threadIdx.x];
+      l += part_l[j * d + threadIdx.x];
+    }
+    out[((size_t)u * G + h) * d + threadIdx.x] = a / l;
   }
 }
 
 void launch_combine(const float *pm, const float *pl, const float *pacc, int units, int chunks, int G, int d,
                     const int32_t *rows, int rows_per_chunk, float *out, cudaStream_t st) {
-  combine_kernel<<<units * G, min(d, 256), 0, st>>>(pm, pl, pacc, chunks, G, d, rows, rows ? 1 : 0,
-                                                    rows_per_chunk, out);
+  combine_kernel<<<units * G, 256, 0, st>>>(pm, pl, pacc, chunks, G, d, rows, rows ? 1 : 0, rows_per_chunk, out);
 }
 
 // variant where every unit shares one device row count (quantized layers)
 static void launch_combine_scalar(const float *pm, const float *pl, const float *pacc, int units, int chunks, int G,
                                   int d, const int32_t *len, int rows_per_chunk, float *out, cudaStream_t st) {
-  combine_kernel<<<units * G, min(d, 256), 0, st>>>(pm, pl, pacc, chunks, G, d, len, 0, rows_per_chunk, out);
+  combine_kernel<<<units * G, 256, 0, st>>>(pm, pl, pacc, chunks, G, d, len, 0, rows_per_chunk, out);
 }
 
 // ---------------------------------------------------------------------------

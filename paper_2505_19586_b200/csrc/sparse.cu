@@ -3,6 +3,7 @@
 // attention.  Reference: retriever.py:84-226, memsim.py:76-252,
 // pipeline.py:271-286, 340-376, 405-413.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "qcache.cuh"
@@ -132,88 +133,97 @@ int sparse_append(const SL &s, const uint16_t *nk, const uint16_t *nv, cudaStrea
 // the top-d_s channels, ties to the lower index, ascending
 // (retriever.py:138-163).  float64 accumulation like the reference einsum.
 // ===========================================================================
-constexpr int S1_ROWS_PER_CTA = 128;
-constexpr int S1_MAXB = 16;
+constexpr int S1_ROWS_PER_CTA = 256;
+constexpr int S1_BG = 4;  // sequences per CTA
 
+// grid (splits, hq, ceil(B/4)); each thread owns 8 channels (one 16-byte load
+// per W_q row) of 16 rows in flight; float64 accumulation.
 __global__ void __launch_bounds__(256) stage1_gemv_kernel(const uint16_t *__restrict__ hidden,
                                                            const uint16_t *__restrict__ w_q, int B, int H, int d,
                                                            double *__restrict__ part) {
-  // grid (splits, hq); block 256 = (d/2 column pairs) x rows-in-flight
-  extern __shared__ __align__(16) double s1sm[];
-  const int qh = blockIdx.y, split = blockIdx.x, splits = gridDim.x;
+  __shared__ double red[256 * 8];
+  const int qh = blockIdx.y, split = blockIdx.x, bg = blockIdx.z;
   const int hq = gridDim.y;
-  const int pairs = d / 2;
-  const int rgroups = blockDim.x / pairs;
-  const int cp = threadIdx.x % pairs, rg = threadIdx.x / pairs;
+  const int tpr = d / 8;                 // threads per row
+  const int rgroups = blockDim.x / tpr;  // rows in flight
+  const int cg8 = threadIdx.x % tpr, rg = threadIdx.x / tpr;
   const int i0 = split * S1_ROWS_PER_CTA, i1 = min(H, i0 + S1_ROWS_PER_CTA);
-  double acc0[S1_MAXB], acc1[S1_MAXB];
+  const int b0 = bg * S1_BG, nb = min(S1_BG, B - b0);
+  double acc[S1_BG][8];
 #pragma unroll
-  for (int b = 0; b < S1_MAXB; ++b) { acc0[b] = 0.0; acc1[b] = 0.0; }
-  if (rg < rgroups) {
-    const uint32_t *w = reinterpret_cast<const uint32_t *>(w_q + ((size_t)qh * H) * d);
-    for (int i = i0 + rg; i < i1; i += rgroups) {
-      const uint32_t pr = __ldg(&w[(size_t)i * pairs + cp]);
-      const double w0 = h2d(pr & 0xffff), w1 = h2d(pr >> 16);
+  for (int b = 0; b < S1_BG; ++b)
 #pragma unroll
-      for (int b = 0; b < S1_MAXB; ++b) {
-        if (b < B) {
-          const double hv = h2d(hidden[(size_t)b * H + i]);
-          acc0[b] = fma(hv, w0, acc0[b]);
-          acc1[b] = fma(hv, w1, acc1[b]);
-        }
+    for (int e = 0; e < 8; ++e) acc[b][e] = 0.0;
+  const uint4 *w = reinterpret_cast<const uint4 *>(w_q + (size_t)qh * H * d);
+#pragma unroll 4
+  for (int i = i0 + rg; i < i1; i += rgroups) {
+    const uint4 v = __ldg(&w[(size_t)i * tpr + cg8]);
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+    double wd[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) wd[e] = h2d((uint16_t)(wv[e >> 1] >> (16 * (e & 1))));
+#pragma unroll
+    for (int b = 0; b < S1_BG; ++b) {
+      if (b < nb) {
+        const double hv = h2d(hidden[(size_t)(b0 + b) * H + i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[b][e] = fma(hv, wd[e], acc[b][e]);
       }
     }
   }
-  // reduce row groups in a fixed order
-  for (int b = 0; b < B; ++b) {
-    if (rg < rgroups) {
-      s1sm[(rg * pairs + cp) * 2 + 0] = acc0[b];
-      s1sm[(rg * pairs + cp) * 2 + 1] = acc1[b];
-    }
+  for (int b = 0; b < nb; ++b) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[(rg * tpr + cg8) * 8 + e] = acc[b][e];
     __syncthreads();
-    if (rg == 0) {
-      double a0 = 0.0, a1 = 0.0;
-      for (int r = 0; r < rgroups; ++r) {
-        a0 += s1sm[(r * pairs + cp) * 2 + 0];
-        a1 += s1sm[(r * pairs + cp) * 2 + 1];
-      }
-      double *o = part + (((size_t)split * B + b) * hq + qh) * d;
-      o[2 * cp] = a0;
-      o[2 * cp + 1] = a1;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      double a = 0.0;
+      for (int r = 0; r < rgroups; ++r) a += red[(r * tpr + c / 8) * 8 + (c & 7)];
+      part[(((size_t)split * B + b0 + b) * hq + qh) * d + c] = a;
     }
     __syncthreads();
   }
 }
 
-__global__ void stage1_select_kernel(const double *__restrict__ part, int splits, int B, int hq, int d, int G,
-                                     const float *__restrict__ chmax, int d_s, double *__restrict__ q_hat,
-                                     int32_t *__restrict__ channels) {
-  // one CTA per unit (b, kvh); blockDim == d
+__global__ void __launch_bounds__(256) stage1_select_kernel(const double *__restrict__ part, int splits, int B, int hq,
+                                                             int d, int G, const float *__restrict__ chmax, int d_s,
+                                                             double *__restrict__ q_hat,
+                                                             int32_t *__restrict__ channels) {
+  // one CTA per unit (b, kvh)
+  __shared__ double qs[16 * 256];
   __shared__ double score[256];
+  __shared__ int flags[256];
   const int u = blockIdx.x;
   const int hkv = hq / G;
   const int b = u / hkv, kvh = u % hkv;
-  const int c = threadIdx.x;
-  double sabs = 0.0;
-  for (int j = 0; j < G; ++j) {
+  for (int p = threadIdx.x; p < G * d; p += blockDim.x) {
+    const int j = p / d, c = p % d;
     const int qh = kvh * G + j;
     double q = 0.0;
+#pragma unroll 8
     for (int sp = 0; sp < splits; ++sp) q += part[(((size_t)sp * B + b) * hq + qh) * d + c];
+    qs[p] = q;
     if (q_hat) q_hat[((size_t)b * hq + qh) * d + c] = q;
-    sabs += fabs(q);
   }
-  const double sc = sabs * (double)chmax[(size_t)u * d + c];
-  score[c] = sc;
   __syncthreads();
-  int rank = 0;
-  for (int j = 0; j < d; ++j) {
-    const double o = score[j];
-    rank += (o > sc) || (o == sc && j < c);
+  const int c = threadIdx.x;
+  double sc = 0.0;
+  if (c < d) {
+    double sabs = 0.0;
+    for (int j = 0; j < G; ++j) sabs += fabs(qs[j * d + c]);  // retriever.py:148
+    sc = sabs * (double)chmax[(size_t)u * d + c];
+    score[c] = sc;
   }
-  const bool sel = rank < d_s;
-  // ascending position among the selected channels
-  __shared__ int flags[256];
-  flags[c] = sel ? 1 : 0;
+  __syncthreads();
+  bool sel = false;
+  if (c < d) {
+    int rank = 0;
+    for (int j = 0; j < d; ++j) {
+      const double o = score[j];
+      rank += (o > sc) || (o == sc && j < c);  // ties -> lower index (retriever.py:161)
+    }
+    sel = rank < d_s;
+    flags[c] = sel ? 1 : 0;
+  }
   __syncthreads();
   if (sel) {
     int pos = 0;
@@ -229,11 +239,11 @@ int64_t stage1_workspace(int B, int hq, int H, int d) {
 
 int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, int d, int G, const float *chmax,
            int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st) {
+  if (G > 16) return fail(TKV_ERR_SHAPE, "stage 1 supports at most 16 query heads per KV head");
   const int splits = (H + S1_ROWS_PER_CTA - 1) / S1_ROWS_PER_CTA;
   double *part = reinterpret_cast<double *>(ws);
-  const size_t sm = (size_t)256 * 2 * sizeof(double);
-  stage1_gemv_kernel<<<dim3(splits, hq), 256, sm, st>>>(hidden, w_q, B, H, d, part);
-  stage1_select_kernel<<<B * (hq / G), d, 0, st>>>(part, splits, B, hq, d, G, chmax, d_s, q_hat, channels);
+  stage1_gemv_kernel<<<dim3(splits, hq, (B + S1_BG - 1) / S1_BG), 256, 0, st>>>(hidden, w_q, B, H, d, part);
+  stage1_select_kernel<<<B * (hq / G), 256, 0, st>>>(part, splits, B, hq, d, G, chmax, d_s, q_hat, channels);
   return check_launch("tkv_stage1");
 }
 
@@ -552,9 +562,17 @@ static int run_select(const int32_t *len, int units, int n_local, int n_topk, Se
   return check_launch("tkv_select");
 }
 
+bool select_cluster_ok(const SL &s, int n_local);
+int select_cluster(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
+                   int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, double *scores_out,
+                   cudaStream_t st);
+
 int select_tokens(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                   int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, double *scores_out,
                   void *ws, cudaStream_t st) {
+  if (select_cluster_ok(s, n_local) && !getenv("TKV_SELECT_MULTIKERNEL"))
+    return select_cluster(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
+                          scores_out, st);
   SelWS w = carve(ws, s.units, s.capacity);
   const int blocks = (int)imin64(2048, (s.capacity + 255) / 256);
   score_hist_kernel<<<dim3(blocks, s.units), 256, 0, st>>>(s, queries, G, channels, d_s, n_local, n_topk, w,

@@ -199,7 +199,7 @@ class DecodeEngine:
             self.sparse[layer] = _SparseState(lay, w, chans, ws)
             self.layers[layer] = lay
             if self.sel_ws is None:
-                self.sel_ws = torch.zeros(int(lib.tkv_select_workspace(self.units, cap)), dtype=torch.uint8,
+                self.sel_ws = torch.zeros(int(lib.tkv_select_workspace(self.units, lay.capacity)), dtype=torch.uint8,
                                           device=self.device)
 
     # -- one step --------------------------------------------------------------

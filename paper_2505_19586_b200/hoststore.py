@@ -75,7 +75,8 @@ class OffloadedLayerKV:
         _lib.require_cuda()
         dev = torch.device(device or "cuda")
         self.device = dev
-        self.units, self.head_dim, self.capacity = units, head_dim, int(capacity)
+        capacity = (int(capacity) + 63) // 64 * 64  # 16-byte aligned channel rows for the scorer
+        self.units, self.head_dim, self.capacity = units, head_dim, capacity
         self.local_offset = max(0, prefill_len - n_local)
         self.local_capacity = self.capacity - self.local_offset
         d = head_dim

@@ -189,8 +189,11 @@ def _sparse_layer(tkv, keys, values, n_local, steps=4, keys_on_device=False):
     return lay
 
 
+@pytest.mark.parametrize("path", ["cluster", "multikernel"])
 @pytest.mark.parametrize("kod", [False, True])
-def test_select_and_sparse_attention_match_oracle(tkv, kod):
+def test_select_and_sparse_attention_match_oracle(tkv, kod, path, monkeypatch):
+    if path == "multikernel":
+        monkeypatch.setenv("TKV_SELECT_MULTIKERNEL", "1")
     rng = np.random.default_rng(11)
     units, n, d, G, d_s = 3, 5000, 128, 4, 8
     keys = cases.f16(rng.normal(size=(units, n, d)))
@@ -224,6 +227,38 @@ def test_select_and_sparse_attention_match_oracle(tkv, kod):
         for j in range(G):
             ref_out[u * G + j] = O.sparse_attention(qg[j], keys[u], values[u], sel)
     assert rel_err(out.cpu().numpy(), ref_out) <= 1e-5
+
+
+@pytest.mark.parametrize("dist", ["ties", "zeros", "normal"])
+def test_cluster_select_ties_and_sizes(tkv, dist):
+    """Scorer + top-k on inputs with massive exact score ties (the cluster
+    radix select resolves them toward larger indices like lexsort)."""
+    rng = np.random.default_rng(21)
+    units, n, d, G = 2, 20000, 64, 2
+    if dist == "ties":
+        keys = np.round(rng.normal(size=(units, n, d)))
+    elif dist == "zeros":
+        keys = np.zeros((units, n, d))
+    else:
+        keys = rng.normal(size=(units, n, d))
+    keys = cases.f16(keys)
+    values = cases.f16(rng.normal(size=(units, n, d)))
+    cfg = tkv.RetrievalConfig(17, 777, 4)
+    lay = _sparse_layer(tkv, keys, values, cfg.n_local)
+    queries = cases.f16(np.round(rng.normal(size=(units * G, d))))
+    chans = np.stack([np.sort(rng.choice(d, 4, replace=False)) for _ in range(units)]).astype(np.int32)
+    import paper_2505_19586_b200._lib as L
+    ws = torch.zeros(int(L.load().tkv_select_workspace(units, lay.capacity)), dtype=torch.uint8, device="cuda")
+    kmax = cfg.n_local + cfg.n_topk
+    idx = torch.zeros((units, kmax), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(units, dtype=torch.int32, device="cuda")
+    fc = torch.zeros(units, dtype=torch.int32, device="cuda")
+    lay.select(torch.tensor(queries, dtype=torch.float16, device="cuda"), torch.tensor(chans, device="cuda"), G, cfg,
+               idx, cnt, fc, ws)
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for u in range(units):
+        sc = O.approx_scores(queries[u * G:(u + 1) * G][:, chans[u]], keys[u][:, chans[u]])
+        assert np.array_equal(idx[u, :cnt[u]], O.select_tokens(sc, cfg.n_local, cfg.n_topk))
 
 
 def test_host_store_gather_roundtrip(tkv):
