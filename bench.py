@@ -32,13 +32,13 @@ METRIC = "decode ms/token @128k ctx (Llama-3.1-8B shapes) at 1/2/4/8 B200; HBM &
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--topk-frac", type=float, default=0.02)
-    ap.add_argument("--keys-on-device", action="store_true",
-                    help="gather K rows from HBM (only V crosses PCIe)")
+    ap.add_argument("--keys-over-pcie", action="store_true",
+                    help="headline with K and V rows both gathered over PCIe (the reference's fetch_topk transfer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=2505)
     return ap.parse_args()
@@ -138,7 +138,7 @@ def workload_config(args, n_topk):
         "ctx": args.ctx, "batch": 1, "layers": 32, "q_layers": [0, 1], "bits": 1, "group_size": 64,
         "n_topk": n_topk, "n_local": 64, "d_s": 8, "kv_heads": 8, "q_heads": 32, "head_dim": 128,
         "parallelism": f"kv-head shard x{args.gpus}",
-        "keys_from": "hbm" if args.keys_on_device else "host",
+        "key_rows_from": "host (PCIe)" if args.keys_over_pcie else "hbm (scorer copy); value rows over PCIe",
         "l2": "inputs larger than L2 (>1.6 GB HBM read per step)",
     }
 
@@ -147,21 +147,34 @@ def workload_config(args, n_topk):
 # measurement helpers
 # ---------------------------------------------------------------------------
 class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML every 20 ms while the
+    timed region runs (nvidia-smi's query fields, in-process)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
     def __init__(self, index: int):
         self.index, self.samples, self._stop = index, [], threading.Event()
         self.t = threading.Thread(target=self._run, daemon=True)
+        self.max_mhz = None
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                try:
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((sm, r))
+                self._stop.wait(0.02)
+        except Exception as exc:  # pragma: no cover
+            self.samples.append((None, 0))
+            self.error = str(exc)
 
     def __enter__(self):
         self.t.start()
@@ -173,12 +186,11 @@ class ClockSampler:
 
     def summary(self):
         import statistics
-        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples if len(s) >= 6 for i in range(4) if s[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+
+        sm = [s for s, _ in self.samples if s is not None]
+        reasons = sorted({k for _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm)}
 
 
 def pcie_peaks(torch, lib_mod, device):
@@ -250,10 +262,10 @@ def main():
     L, n = model.num_layers, args.ctx
     n_topk = round(args.topk_frac * n)
     cfg = P.EngineConfig(bits=1, group_size=64, n_local=64, n_topk=n_topk, critical_channels=8,
-                         keys_on_device=args.keys_on_device)
+                         keys_from_hbm=not args.keys_over_pcie)
     W, K = args.warmup, args.steps
     PROF = 2
-    total = W + 2 * K + PROF + 1
+    total = W + 3 * K + 2 * PROF + 2
     t_setup = time.time()
     wl = make_workload(L, (0, 1), model.num_query_heads, model.num_kv_heads, model.head_dim, n, total,
                        batch=1, seed=args.seed, device=device)
@@ -271,13 +283,33 @@ def main():
         return wl.hidden[t], wl.queries[t], wl.new_keys[t], wl.new_values[t]
 
     # per-kernel profile (eager, events around each kernel group)
-    prof = {}
-    for _ in range(PROF):
-        for k, v in eng.step_profiled(*inputs(step_i)).items():
-            prof.setdefault(k, []).extend(v)
-        step_i += 1
+    def profile_mode(from_hbm):
+        nonlocal step_i
+        eng.keys_from_hbm = from_hbm
+        res = {}
+        for _ in range(PROF):
+            for k, v in eng.step_profiled(*inputs(step_i)).items():
+                res.setdefault(k, []).extend(v)
+            step_i += 1
+        return res
+
+    prof_alt = profile_mode(args.keys_over_pcie)  # the other key-row source
+    prof = profile_mode(not args.keys_over_pcie)
     fetch_rows = int(eng.fetch_count.sum().item())
 
+    # variant: the other key-row source, graph-timed for K steps
+    eng.keys_from_hbm = args.keys_over_pcie
+    eng.capture()
+    torch.cuda.synchronize()
+    sv, ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sv.record()
+    for _ in range(K):
+        eng.step(*inputs(step_i)); step_i += 1
+    ev.record()
+    torch.cuda.synchronize()
+    ms_variant = sv.elapsed_time(ev) / K
+
+    eng.keys_from_hbm = not args.keys_over_pcie
     eng.capture()
     for _ in range(W):
         eng.step(*inputs(step_i)); step_i += 1
@@ -333,7 +365,10 @@ def main():
     select_ms = mean(prof.get("select", []))
     stage1_ms = mean(prof.get("stage1", []))
     from oracle import tailorkv_oracle as O  # byte formulas only (memsim.py accounting)
-    gather_bytes = O.gather_bytes(fetch_rows, model.head_dim) if not args.keys_on_device else fetch_rows * model.head_dim * 2
+    # algorithmic PCIe bytes of one gather launch: K+V rows (memsim.py:249) or V rows only
+    gather_bytes = O.gather_bytes(fetch_rows, model.head_dim) if args.keys_over_pcie else fetch_rows * model.head_dim * 2
+    alt_bytes = O.gather_bytes(fetch_rows, model.head_dim) if not args.keys_over_pcie else fetch_rows * model.head_dim * 2
+    alt_ms = mean(prof_alt.get("gather_attend", []))
     quant_bytes = O.quant_layer_bytes(n, U, model.head_dim, 1, 64)
     scorer_bytes = O.scorer_bytes(n, U, 8)
     wq_bytes = eng.hq_r * model.hidden_dim * model.head_dim * 2
@@ -362,6 +397,9 @@ def main():
         "pcie": {"memcpy_h2d_gbs": memcpy_gbs, "uva_512B_rows_gbs": uva_gbs,
                  "gather_bytes_per_token": gather_bytes * 30, "fetched_rows_per_layer": fetch_rows},
         "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",
+                    "ms_per_token": ms_variant, "gather_ms": alt_ms,
+                    "gather_pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "gather_bytes": alt_bytes},
         "gpu_launches": eng.kernels_per_step() * K,
         "clocks": clocks.summary(),
         "setup_s": setup_s,

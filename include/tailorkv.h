@@ -165,8 +165,9 @@ int tkv_topk_from_scores(const double *scores, int32_t units, int64_t n, int32_t
 
 /* Gather + sparse attention (replaces fetch_topk memsim.py:228-252 +
  * pipeline.py:364-376): rows below the local window come from the pinned host
- * store over PCIe (keys from kdev when keys_from_device != 0), the rest from
- * the local mirror.  out fp32 [units*G][d]. */
+ * store over PCIe (with keys_from_device != 0 only the value rows cross PCIe;
+ * key rows come from kdev, or from the channel-major scorer copy kt when kdev
+ * is NULL), the rest from the local mirror.  out fp32 [units*G][d]. */
 int64_t tkv_sparse_attn_workspace(int32_t units, int32_t G, int32_t d, int32_t max_rows);
 int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *sel_idx,
                          const int32_t *sel_count, int32_t n_local, int32_t max_rows, int32_t keys_from_device,

@@ -180,7 +180,6 @@ int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int
                          const int32_t *sel_count, int32_t n_local, int32_t max_rows, int32_t keys_from_device,
                          float *out, void *workspace, void *stream) {
   if (int r = validate_sparse(s)) return r;
-  TKV_REQUIRE(!keys_from_device || s->kdev != nullptr, TKV_ERR_PARAMETER, "keys_from_device needs device keys");
   return sparse_attention(*s, queries, G, sel_idx, sel_count, n_local, max_rows, keys_from_device, out, workspace,
                           as_stream(stream));
 }

@@ -636,6 +636,22 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
     if (!valid[j]) continue;
     const int64_t idx = sel_idx[(size_t)u * sel_stride + r];
     const uint16_t *kp, *vp;
+    if (idx < local_start && keys_from_device && !s.kdev) {
+      // key row straight from the channel-major HBM copy the scorer uses
+      // (scattered 2-byte reads, no extra memory); value row over PCIe
+      vp = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D + D;
+#pragma unroll
+      for (int e = 0; e < CPL; ++e)
+        kw[j][e >> 1] |= (uint32_t)s.kt[((size_t)u * D + lane * CPL + e) * s.capacity + idx] << (16 * (e & 1));
+      if constexpr (CPL == 4) {
+        const uint2 b = *reinterpret_cast<const uint2 *>(vp + lane * 4);
+        vw[j][0] = b.x; vw[j][1] = b.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) vw[j][e >> 1] |= (uint32_t)vp[lane * CPL + e] << (16 * (e & 1));
+      }
+      continue;
+    }
     if (idx < local_start) {
       const uint16_t *row = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
       kp = keys_from_device ? s.kdev + ((size_t)u * s.capacity + idx) * D : row;

@@ -38,7 +38,7 @@ class EngineConfig:
     n_local: int = 64
     n_topk: int = 128
     critical_channels: int = 8
-    keys_on_device: bool = False   # gather K rows from HBM, only V crosses PCIe
+    keys_from_hbm: bool = True     # gather key rows from the HBM scorer copy; only V rows cross PCIe
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
     def validate(self) -> None:
@@ -155,6 +155,7 @@ class DecodeEngine:
         self.steps_done = 0
         self.record_selection = False
         self.profile = None  # list of (name, layer, start_event, end_event) when profiling
+        self.keys_from_hbm = config.keys_from_hbm
         self.last_channels: dict[int, torch.Tensor] = {}
         self.last_selection: dict[int, tuple] = {}
 
@@ -185,8 +186,7 @@ class DecodeEngine:
         else:
             if w_q is None:
                 raise ConfigError(f"sparsity-friendly layer {layer} needs its W_q for stage 1")
-            lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local,
-                                   keys_on_device=self.cfg.keys_on_device, device=self.device)
+            lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local, device=self.device)
             lay.offload(k, v)
             w = as_f16(w_q, self.device)
             if w.shape[0] == self.model.num_query_heads:
@@ -278,7 +278,7 @@ class DecodeEngine:
                     self.last_selection[l] = (self.sel_idx.clone(), self.sel_count.clone(), self.fetch_count.clone())
                 t0 = self._mark(main)
                 lay.attend(self.queries[l], self.G, self.retrieval, self.sel_idx, self.sel_count, self.out[l],
-                           self.attn_ws, keys_from_device=self.cfg.keys_on_device)
+                           self.attn_ws, keys_from_device=self.keys_from_hbm)
                 self._span("gather_attend", l, t0, main)
                 t0 = self._mark(main)
                 lay.append(self.new_keys[l], self.new_values[l])

@@ -295,9 +295,10 @@ def _golden_trace():
     return {k: z[k] for k in z.files}
 
 
-@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("graph,kfh", [(False, True), (False, False), (True, True)],
+                         ids=["eager-keys_hbm", "eager-keys_pcie", "graph-keys_hbm"])
 @pytest.mark.parametrize("run", list(cases.PIPELINE_CONFIGS), ids=str)
-def test_engine_replays_reference_pipeline(tkv, run, graph):
+def test_engine_replays_reference_pipeline(tkv, run, graph, kfh):
     z = _golden_trace()
     ref = META["pipeline"]["runs"][run]
     rc = ref["config"]
@@ -306,7 +307,7 @@ def test_engine_replays_reference_pipeline(tkv, run, graph):
     T = z["queries"].shape[0]
     labels = ["q" if lab == "quantization_friendly" else "s" for lab in ref["labels"]]
     cfg = tkv.EngineConfig(bits=rc.get("bits", 1), n_local=rc.get("n_local", 64), n_topk=rc.get("n_topk", 128),
-                           critical_channels=rc.get("critical_channels", 8))
+                           critical_channels=rc.get("critical_channels", 8), keys_from_hbm=kfh)
     model = tkv.ModelConfig(L, hq, h, d, hq * d)
     eng = tkv.DecodeEngine(model, labels, cfg, batch=1, max_steps=T)
     for l in range(L):
