@@ -60,7 +60,7 @@ typedef struct tkv_qcache {
   uint16_t *key_resid;   /* fp16 [units][g][d] */
   uint32_t *val_codes;   /* [units][capacity/32][sets][32][4] */
   uint32_t *val_lohi;    /* half2(lo,hi) [units][capacity][ceil(d/g)] */
-  float *val_smax;       /* [units] running max of value group scale */
+  float *val_smax;       /* [units][2] running max group scale: [0] values, [1] keys */
   int32_t *len;          /* device scalar: tokens held (all units) */
   uint32_t *ticket;      /* device scalar scratch for append */
 } tkv_qcache;

@@ -64,7 +64,7 @@ int tkv_qcache_sizes(int32_t units, int32_t d, int32_t bits, int32_t g, int64_t 
   sizes[2] = (int64_t)units * g * d * 2;
   sizes[3] = (int64_t)units * (capacity / 32) * val_sets(d, bits) * 128 * 4;
   sizes[4] = (int64_t)units * capacity * nb * 4;
-  sizes[5] = (int64_t)units * 4;
+  sizes[5] = (int64_t)units * 8;  // [units][2]: max value scale, max key scale
   return TKV_OK;
 }
 

@@ -68,7 +68,7 @@ void launch_combine(const float *pm, const float *pl, const float *pacc, int uni
 }
 
 // variant where every unit shares one device row count (quantized layers)
-static void launch_combine_scalar(const float *pm, const float *pl, const float *pacc, int units, int chunks, int G,
+void launch_combine_scalar(const float *pm, const float *pl, const float *pacc, int units, int chunks, int G,
                                   int d, const int32_t *len, int rows_per_chunk, float *out, cudaStream_t st) {
   combine_kernel<<<units * G, 256, 0, st>>>(pm, pl, pacc, chunks, G, d, len, 0, rows_per_chunk, out);
 }

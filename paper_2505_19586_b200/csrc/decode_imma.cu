@@ -1,14 +1,375 @@
-// Tensor-core (mma.sync IMMA u8 x s8) quantized decode -- see DESIGN.md 4.2.
+// Tensor-core quantized decode attention for d = 128,
+// g = 64, 1/2-bit codes, up to 4 query heads per KV head.
+//
+// Keys:   logits[t, h] = sum_c code[t,c] * (q[h,c] s[g,c]) + q[h] . lo[g]
+//         (quantizer.py:505-533).  MMA m16n8k32 u8 x s8 -> s32 with
+//         A = key codes (tokens x channels) taken straight from the packed
+//         bit-planes with ONE LOP3 per 4 codes: byte lanes of a code word hold
+//         the codes of 8/b different m-tiles at bit offset k*b, so
+//         (word & mask_k) is the u8 operand scaled by 2^(k b), undone on the
+//         int32 result.  B = q*s quantised to a 16-bit fixed point split into
+//         two s8 digits (hi, lo) that occupy the 8 N columns (4 heads x 2).
+// Values: out^T[c, h] = sum_t code[t,c] * (p[t,h] s[t,cb]) + sum_t p lo
+//         (quantizer.py:536-558), same operand trick with A = value codes
+//         (channels x tokens).  Integer accumulation is exact, so the split-K
+//         partial only carries the fixed-point rounding of B.
+// Softmax: online max/rescale per 64-token group (pipeline.py:153-156, 336).
+#include <cmath>
+
 #include "common.cuh"
 #include "qcache.cuh"
 
 namespace tkv {
 
-bool imma_supported(const QC &c, int G) { (void)c; (void)G; return false; }
+constexpr int IM_D = 128;
+constexpr int IM_G = 64;
+constexpr int IM_CHUNK = 1024;                 // tokens per CTA
+constexpr int IM_GROUPS = IM_CHUNK / IM_G;     // 16
+constexpr int IM_WARPS = 4;
+constexpr float IM_QMAX = 32512.0f;            // |x| bound of the 2-digit fixed point
+constexpr float IM_MAGIC = 12582912.0f + 128.0f;  // 1.5*2^23 + 128: RNE to int, +128 digit bias
+
+bool imma_supported(const QC &c, int G) {
+  return c.d == IM_D && c.g == IM_G && (c.bits == 1 || c.bits == 2) && G >= 1 && G <= 4;
+}
+
+__device__ __forceinline__ void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                     uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// pack the digit byte (sel: 0x1 hi = byte 1, 0x0 lo = byte 0) of four
+// fixed-point floats into one s8x4 register; lo digits are re-centred by ^0x80
+__device__ __forceinline__ uint32_t pack_digits(float x0, float x1, float x2, float x3, uint32_t sel2,
+                                                uint32_t sel4, uint32_t xr) {
+  const uint32_t a = __byte_perm(__float_as_uint(x0), __float_as_uint(x1), sel2);
+  const uint32_t b = __byte_perm(__float_as_uint(x2), __float_as_uint(x3), sel2);
+  return __byte_perm(a, b, 0x5410) ^ xr;
+  (void)sel4;
+}
+
+struct ImSmem {
+  float q[4][IM_D];             // query (h < G, else 0)
+  float qinv[4][IM_D];          // q * 32512 / bound_h
+  float kscale[4];              // bound_h / 32512
+  float off[IM_GROUPS][4];      // q_h . lo_g
+  uint32_t bfrag[IM_GROUPS][4][32][2];  // key B fragments per group, k-step, lane
+  union {
+    struct {
+      float s[IM_GROUPS][IM_D];  // key scales of the chunk's groups
+      float lo[IM_GROUPS][IM_D];
+    } k;
+    struct {
+      float sv[2][IM_CHUNK];     // value scale * 32512/Smax_v per (cb, token)
+      float lov[2][IM_CHUNK];    // value zero-point per (cb, token)
+    } v;
+  } u;
+  float p[IM_WARPS][4][IM_G];    // per-warp softmax numerators of the current group
+  float wm[IM_WARPS][4], wl[IM_WARPS][4];
+};
+
+template <int BITS>
+__global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC c, const uint16_t *__restrict__ queries,
+                                                                              int G, float *__restrict__ pm,
+                                                                              float *__restrict__ pl,
+                                                                              float *__restrict__ pacc, int chunks) {
+  constexpr int KT = 128 / BITS;           // key tile tokens
+  constexpr int GPT = KT / IM_G;           // groups per key tile
+  constexpr int VS = BITS;                 // value code sets (d = 128)
+  constexpr int SLOTS = 8 / BITS;
+  constexpr uint32_t CM = BITS == 1 ? 0x01010101u : 0x03030303u;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ImSmem &S = *reinterpret_cast<ImSmem *>(smraw);
+  const int u = blockIdx.y, chunk = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g8 = lane >> 2, tq = lane & 3;
+  const int64_t n = *c.len;
+  const int64_t t0 = (int64_t)chunk * IM_CHUNK;
+  if (t0 >= n) return;
+  const int64_t ncomp = (n / IM_G) * IM_G;
+  const float inv_sqrt_d = 0.08838834764831845f;  // 1/sqrt(128)
+  const float kmax_s = c.val_smax[2 * u + 1];
+  const float vmax_s = c.val_smax[2 * u];
+  const float vinv = vmax_s > 0.0f ? IM_QMAX / vmax_s : 0.0f;
+  const float vscale = vmax_s / IM_QMAX;
+
+  // ---- prologue: query, fixed-point scales, per-group key params ----
+  for (int i = tid; i < 4 * IM_D; i += blockDim.x) {
+    const int h = i / IM_D;
+    S.q[h][i % IM_D] = h < G ? h2f(queries[((size_t)u * G + h) * IM_D + i % IM_D]) : 0.0f;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int h = 0; h < 4; ++h) {
+      float m = 0.0f;
+      for (int i = lane; i < IM_D; i += 32) m = fmaxf(m, fabsf(S.q[h][i]));
+      m = warp_max(m);
+      const float bound = m * kmax_s;
+      if (lane == 0) S.kscale[h] = bound / IM_QMAX;
+      const float inv = bound > 0.0f ? IM_QMAX / bound : 0.0f;
+      for (int i = lane; i < IM_D; i += 32) S.qinv[h][i] = S.q[h][i] * inv;
+    }
+  }
+  const int ngroups = (int)imin64(IM_GROUPS, (n - t0 + IM_G - 1) / IM_G);
+  const int64_t g0 = t0 / IM_G;
+  const uint32_t *klohi = c.key_lohi + ((size_t)u * (c.capacity / IM_G) + g0) * IM_D;
+  for (int i = tid; i < IM_GROUPS * IM_D; i += blockDim.x) {
+    const int gi = i / IM_D, ch = i % IM_D;
+    float sc = 0.0f, lo = 0.0f;
+    if (gi < ngroups && (g0 + gi + 1) * IM_G <= ncomp) {
+      const uint32_t w = klohi[i];
+      lo = h2f(w & 0xffff);
+      const float hi = h2f(w >> 16);
+      sc = hi > lo ? (hi - lo) / (float)((1 << BITS) - 1) : 0.0f;  // degenerate groups have all-zero codes
+    }
+    S.u.k.s[gi][ch] = sc;
+    S.u.k.lo[gi][ch] = lo;
+  }
+  __syncthreads();
+  // offsets q_h . lo_g : 64 outputs, 2 threads each
+  {
+    const int o = tid >> 1, half = tid & 1;
+    const int gi = o >> 2, h = o & 3;
+    float a = 0.0f;
+    for (int ch = half * 64; ch < half * 64 + 64; ++ch) a = fmaf(S.q[h][ch], S.u.k.lo[gi][ch], a);
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    if (half == 0) S.off[gi][h] = a;
+  }
+  // key B fragments: item = (gi, ks, j, tq, h); 4 channels each -> hi & lo digit words
+  for (int it = tid; it < IM_GROUPS * 4 * 2 * 4 * 4; it += blockDim.x) {
+    const int h = it & 3, tqq = (it >> 2) & 3, j = (it >> 4) & 1, ks = (it >> 5) & 3, gi = it >> 7;
+    const int ch = 32 * ks + 16 * j + 4 * tqq;
+    float x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = fmaf(S.u.k.s[gi][ch + i], S.qinv[h][ch + i], IM_MAGIC);
+    const uint32_t hiw = pack_digits(x[0], x[1], x[2], x[3], 0x0051, 0, 0u);  // bytes 1
+    const uint32_t low = pack_digits(x[0], x[1], x[2], x[3], 0x0040, 0, 0x80808080u);  // bytes 0
+    S.bfrag[gi][ks][(2 * h) * 4 + tqq][j] = hiw;
+    S.bfrag[gi][ks][(2 * h + 1) * 4 + tqq][j] = low;
+  }
+  __syncthreads();
+  // value params of the chunk's tokens (reuses the key-param space)
+  const uint32_t *vlohi = c.val_lohi + ((size_t)u * c.capacity + t0) * 2;
+  for (int i = tid; i < IM_CHUNK * 2; i += blockDim.x) {
+    const int t = i >> 1, cb = i & 1;
+    float sv = 0.0f, lo = 0.0f;
+    if (t0 + t < n) {
+      const uint32_t w = vlohi[i];
+      lo = h2f(w & 0xffff);
+      const float hi = h2f(w >> 16);
+      sv = group_scale_f(lo, hi, BITS) * vinv;
+    }
+    S.u.v.sv[cb][t] = sv;
+    S.u.v.lov[cb][t] = lo;
+  }
+  __syncthreads();
+
+  // ---- main loop: each warp walks whole key tiles of its chunk ----
+  const uint4 *kcodes = reinterpret_cast<const uint4 *>(c.key_codes) + (size_t)u * (c.capacity / KT) * 4 * 32;
+  const uint4 *vcodes = reinterpret_cast<const uint4 *>(c.val_codes) + (size_t)u * (c.capacity / 32) * VS * 32;
+  const uint16_t *kres = c.key_resid + (size_t)u * IM_G * IM_D;
+  const uint32_t dsel = (g8 & 1) ? 0x0040u : 0x0051u;  // this lane's B column digit
+  const uint32_t dxor = (g8 & 1) ? 0x80808080u : 0u;
+  const int hB = g8 >> 1;                              // head of this lane's B column
+  float m_run = -INFINITY, l_run = 0.0f, zsum[2] = {0.0f, 0.0f};
+  float acc[8][2];
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) { acc[mt][0] = 0.0f; acc[mt][1] = 0.0f; }
+  const float ks_h = S.kscale[tq];
+
+  for (int kt = warp; kt < IM_CHUNK / KT; kt += IM_WARPS) {
+    const int64_t tile_t0 = t0 + (int64_t)kt * KT;
+    if (tile_t0 >= n) break;
+    uint4 X[4];
+    const bool any_complete = tile_t0 + IM_G <= ncomp;
+    if (any_complete) {
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) X[ks] = __ldg(&kcodes[((tile_t0 / KT) * 4 + ks) * 32 + lane]);
+    }
+#pragma unroll
+    for (int gl = 0; gl < GPT; ++gl) {
+      const int64_t gt0 = tile_t0 + gl * IM_G;  // group's first token
+      if (gt0 >= n) break;
+      const int gi = kt * GPT + gl;            // group index within the chunk
+      float z[4][2];
+      if (gt0 + IM_G <= ncomp) {
+        uint32_t b[4][2];
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint2 bb = *reinterpret_cast<const uint2 *>(&S.bfrag[gi][ks][lane][0]);
+          b[ks][0] = bb.x;
+          b[ks][1] = bb.y;
+        }
+        const float off = S.off[gi][tq];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          const int k = gl * 4 + mt;
+          const uint32_t msk = CM << (k * BITS);
+          int C[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            imma(C, X[ks].x & msk, X[ks].y & msk, X[ks].z & msk, X[ks].w & msk, b[ks][0], b[ks][1]);
+          const float sc = ks_h * __int_as_float((127 - k * BITS) << 23);  // * 2^-(k b)
+          z[mt][0] = fmaf(fmaf((float)C[0], 256.0f, (float)C[1]), sc, off) * inv_sqrt_d;
+          z[mt][1] = fmaf(fmaf((float)C[2], 256.0f, (float)C[3]), sc, off) * inv_sqrt_d;
+        }
+      } else {
+        // the fp16 residual group (< g rows, quantizer.py:529-530): plain FMAs
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int tl = mt * 16 + g8 + 8 * r;
+            const int64_t T = gt0 + tl;
+            float a = -INFINITY;
+            if (T < n) {
+              const uint16_t *kr = kres + (size_t)(T - ncomp) * IM_D;
+              a = 0.0f;
+              for (int ch = 0; ch < IM_D; ch += 2) {
+                const uint32_t pr = *reinterpret_cast<const uint32_t *>(kr + ch);
+                a = fmaf(h2f(pr & 0xffff), S.q[tq][ch], a);
+                a = fmaf(h2f(pr >> 16), S.q[tq][ch + 1], a);
+              }
+              a *= inv_sqrt_d;
+            }
+            z[mt][r] = a;
+          }
+      }
+      // mask tokens beyond n (complete groups never straddle n)
+      if (gt0 + IM_G > n) {
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+            if (gt0 + mt * 16 + g8 + 8 * r >= n) z[mt][r] = -INFINITY;
+      }
+      // ---- online softmax over this group (head tq) ----
+      float gmax = -INFINITY;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) gmax = fmaxf(gmax, fmaxf(z[mt][0], z[mt][1]));
+      gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, 4));
+      gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, 8));
+      gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, 16));
+      const float m_new = fmaxf(m_run, gmax);
+      const float alpha = __expf(m_run - m_new);
+      m_run = m_new;
+      float psum = 0.0f, zl0 = 0.0f, zl1 = 0.0f;
+      const int tl0 = (int)(gt0 - t0);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int tl = mt * 16 + g8 + 8 * r;
+          const float p = __expf(z[mt][r] - m_new);
+          S.p[warp][tq][tl] = p;
+          psum += p;
+          zl0 = fmaf(p, S.u.v.lov[0][tl0 + tl], zl0);
+          zl1 = fmaf(p, S.u.v.lov[1][tl0 + tl], zl1);
+        }
+      l_run = fmaf(l_run, alpha, psum);
+      zsum[0] = fmaf(zsum[0], alpha, zl0);
+      zsum[1] = fmaf(zsum[1], alpha, zl1);
+      __syncwarp();
+      // ---- value MMA over the group's two 32-token k-steps ----
+      int V[8][4];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) { V[mt][0] = 0; V[mt][1] = 0; V[mt][2] = 0; V[mt][3] = 0; }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int64_t vt = (gt0 >> 5) + v;
+        uint4 A[VS];
+#pragma unroll
+        for (int st = 0; st < VS; ++st) A[st] = __ldg(&vcodes[(vt * VS + st) * 32 + lane]);
+        const int tb = v * 32 + 4 * tq;  // token (within group) of byte 0, b0 half
+        const float4 p0 = *reinterpret_cast<const float4 *>(&S.p[warp][hB][tb]);
+        const float4 p1 = *reinterpret_cast<const float4 *>(&S.p[warp][hB][tb + 16]);
+        uint32_t B[2][2];
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          const float4 s0 = *reinterpret_cast<const float4 *>(&S.u.v.sv[cb][tl0 + tb]);
+          const float4 s1 = *reinterpret_cast<const float4 *>(&S.u.v.sv[cb][tl0 + tb + 16]);
+          B[cb][0] = pack_digits(fmaf(p0.x, s0.x, IM_MAGIC), fmaf(p0.y, s0.y, IM_MAGIC), fmaf(p0.z, s0.z, IM_MAGIC),
+                                 fmaf(p0.w, s0.w, IM_MAGIC), dsel, 0, dxor);
+          B[cb][1] = pack_digits(fmaf(p1.x, s1.x, IM_MAGIC), fmaf(p1.y, s1.y, IM_MAGIC), fmaf(p1.z, s1.z, IM_MAGIC),
+                                 fmaf(p1.w, s1.w, IM_MAGIC), dsel, 0, dxor);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          const int st = mt / SLOTS, slot = mt % SLOTS;
+          const uint32_t msk = CM << (slot * BITS);
+          const uint4 a = A[st];
+          imma(V[mt], a.x & msk, a.y & msk, a.z & msk, a.w & msk, B[mt / 4][0], B[mt / 4][1]);
+        }
+      }
+      // ---- flush the exact integer partials into the float accumulators ----
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        const int slot = mt % SLOTS;
+        const float sc = vscale * __int_as_float((127 - slot * BITS) << 23);
+        acc[mt][0] = fmaf(acc[mt][0], alpha, fmaf((float)V[mt][0], 256.0f, (float)V[mt][1]) * sc);
+        acc[mt][1] = fmaf(acc[mt][1], alpha, fmaf((float)V[mt][2], 256.0f, (float)V[mt][3]) * sc);
+      }
+      __syncwarp();
+    }
+  }
+  // ---- reduce the warp: l and z-sums over the 8 lanes sharing head tq ----
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, o);
+    zsum[0] += __shfl_xor_sync(0xffffffffu, zsum[0], o);
+    zsum[1] += __shfl_xor_sync(0xffffffffu, zsum[1], o);
+  }
+  __syncthreads();  // the chunk's value params are no longer needed: reuse as warp partials
+  float *wacc = &S.u.v.sv[0][0];  // [warps][4][128]
+  if (g8 == 0) {
+    S.wm[warp][tq] = m_run;
+    S.wl[warp][tq] = l_run;
+  }
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) wacc[(warp * 4 + tq) * IM_D + mt * 16 + g8 + 8 * r] = acc[mt][r] + zsum[mt >> 2];
+  __syncthreads();
+  for (int i = tid; i < G * IM_D; i += blockDim.x) {
+    const int h = i / IM_D, ch = i % IM_D;
+    float M = -INFINITY;
+    for (int w = 0; w < IM_WARPS; ++w) M = fmaxf(M, S.wm[w][h]);
+    float L = 0.0f, A = 0.0f;
+    for (int w = 0; w < IM_WARPS; ++w) {
+      if (S.wm[w][h] == -INFINITY) continue;
+      const float sc = __expf(S.wm[w][h] - M);
+      L = fmaf(sc, S.wl[w][h], L);
+      A = fmaf(sc, wacc[(w * 4 + h) * IM_D + ch], A);
+    }
+    const size_t base = ((size_t)u * chunks + chunk) * G + h;
+    pacc[base * IM_D + ch] = A;
+    if (ch == 0) {
+      pm[base] = M;
+      pl[base] = L;
+    }
+  }
+}
 
 int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st) {
-  (void)c; (void)q; (void)G; (void)out; (void)ws; (void)st;
-  return fail(TKV_ERR_PARAMETER, "tensor-core decode not built");
+  const int chunks = (int)((c.capacity + IM_CHUNK - 1) / IM_CHUNK);
+  float *pm = reinterpret_cast<float *>(ws);
+  float *pl = pm + (size_t)c.units * chunks * G;
+  float *pacc = pl + (size_t)c.units * chunks * G;
+  const size_t sm = sizeof(ImSmem);
+  dim3 grid(chunks, c.units);
+  if (c.bits == 1) {
+    cudaFuncSetAttribute(quant_decode_imma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    quant_decode_imma_kernel<1><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks);
+  } else {
+    cudaFuncSetAttribute(quant_decode_imma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    quant_decode_imma_kernel<2><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks);
+  }
+  launch_combine_scalar(pm, pl, pacc, c.units, chunks, G, c.d, c.len, IM_CHUNK, out, st);
+  return check_launch("tkv_quant_decode(imma)");
 }
 
 }  // namespace tkv

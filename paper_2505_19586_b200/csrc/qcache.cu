@@ -8,6 +8,10 @@
 
 namespace tkv {
 
+__device__ __forceinline__ void atomic_max_pos(float *addr, float v) {
+  atomicMax(reinterpret_cast<int *>(addr), __float_as_int(v));  // v >= 0
+}
+
 // ---------------------------------------------------------------------------
 // Pack keys: one CTA per (key tile, unit).  quantizer.py:277-293.
 // ---------------------------------------------------------------------------
@@ -47,6 +51,7 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
     const uint32_t w = pack_lohi(lob, hib);
     lohi[p] = w;
     c.key_lohi[((size_t)u * (c.capacity / g) + (t0 / g) + grp) * d + ch] = w;
+    atomic_max_pos(&c.val_smax[2 * u + 1], hi > lo ? (hi - lo) / (float)((1 << bits) - 1) : 0.0f);
   }
   __syncthreads();
   for (int p = threadIdx.x; p < Tk * d; p += blockDim.x) {
@@ -82,10 +87,6 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
 // ---------------------------------------------------------------------------
 // Pack values: one CTA per (32-token tile, unit).  quantizer.py:252-275.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void atomic_max_pos(float *addr, float v) {
-  atomicMax(reinterpret_cast<int *>(addr), __float_as_int(v));  // v >= 0
-}
-
 __global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *__restrict__ values, int64_t n,
                                                            int64_t row0, int64_t src_rows) {
   // row0: first token index of this call (prefill: 0).  src holds rows [row0, row0+src_rows).
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *
     if (row0 > t0) word |= dst[wi];
     dst[wi] = word;
   }
-  if (threadIdx.x == 0) atomic_max_pos(&c.val_smax[u], smax);
+  if (threadIdx.x == 0) atomic_max_pos(&c.val_smax[2 * u], smax);
 }
 
 __global__ void copy_residual_kernel(QC c, const uint16_t *__restrict__ keys, int64_t n, int64_t n_complete) {
@@ -192,7 +193,7 @@ int pack(const QC &c, const uint16_t *keys, const uint16_t *values, int64_t n, i
   }
   const int Tk = key_tile_tokens(c.bits);
   const int64_t n_complete = (n / c.g) * c.g;
-  cudaMemsetAsync(c.val_smax, 0, sizeof(float) * c.units, st);
+  cudaMemsetAsync(c.val_smax, 0, sizeof(float) * 2 * c.units, st);
   if (n_complete > 0) {
     const size_t sm = (size_t)Tk * c.d * 3 + (size_t)(Tk / c.g) * c.d * 4;
     cudaFuncSetAttribute(pack_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(256) append_kernel(QC c, const uint16_t *__res
     float m = 0.0f;
     for (int b = 0; b < nb; ++b)
       m = fmaxf(m, group_scale_f(h2f(vlohi[b] & 0xffff), h2f(vlohi[b] >> 16), bits));
-    atomic_max_pos(&c.val_smax[u], m);
+    atomic_max_pos(&c.val_smax[2 * u], m);
   }
   for (int ch = threadIdx.x; ch < d; ch += blockDim.x) {
     const uint32_t w = vlohi[ch / g];
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(256) append_kernel(QC c, const uint16_t *__res
       if (lo == 0.0f) lob = 0;
       if (hi == 0.0f) hib = 0;
       c.key_lohi[((size_t)u * (c.capacity / g) + grp) * d + ch] = pack_lohi(lob, hib);
+      atomic_max_pos(&c.val_smax[2 * u + 1], hi > lo ? (hi - lo) / (float)((1 << bits) - 1) : 0.0f);
       for (int rr = 0; rr < g; ++rr)
         kcodes[rr * d + ch] = (uint8_t)encode_code(h2f(res[rr * d + ch]), lo, hi, bits);
     }

@@ -23,4 +23,7 @@ int quant_decode(const QC &c, const uint16_t *q, int G, float *out, void *ws, in
 void launch_combine(const float *part_m, const float *part_l, const float *part_acc, int units, int chunks, int G,
                     int d, const int32_t *chunk_rows, int rows_per_chunk, float *out, cudaStream_t st);
 
+void launch_combine_scalar(const float *pm, const float *pl, const float *pacc, int units, int chunks, int G, int d,
+                           const int32_t *len, int rows_per_chunk, float *out, cudaStream_t st);
+
 }  // namespace tkv

@@ -119,6 +119,43 @@ def test_quant_decode_matches_reference(tkv, case, impl):
     assert rel_err(out, ref) <= REL_TOL
 
 
+@pytest.mark.parametrize("bits", [1, 2])
+@pytest.mark.parametrize("n,kscale", [(32768 + 17, 0.05), (5000, 0.5), (64 * 17, 0.2)])
+def test_quant_decode_tensor_core_vs_oracle(tkv, bits, n, kscale):
+    """The IMMA kernel (impl=2) at long context, dense (near-uniform) and
+    peaky attention, against the float64 oracle and the SIMT kernel."""
+    rng = np.random.default_rng(n + bits)
+    h, G, d = 2, 4, 128
+    keys = cases.f16(rng.normal(0, kscale, size=(h, n, d)))
+    keys[:, ::97] += cases.f16(rng.normal(0, 3 * kscale, size=(h, 1, d)))  # a few louder tokens
+    keys = cases.f16(keys)
+    values = cases.f16(rng.normal(size=(h, n, d)))
+    queries = cases.f16(rng.normal(size=(h * G, d)))
+    q = tkv.quantize_layer_kv(keys, values, bits, 64)
+    kq, vq = O.quantize_layer(keys, values, bits, 64)
+    ref = O.quant_layer_decode(queries, kq, vq)
+    out2 = q.decode(queries, impl=2).cpu().numpy()
+    assert rel_err(out2, ref) <= REL_TOL
+    assert rel_err(out2, ref) <= 2e-4  # typical margin of the exact-integer design
+
+
+@pytest.mark.parametrize("bits", [1, 2])
+def test_quant_decode_after_appends(tkv, bits):
+    rng = np.random.default_rng(77 + bits)
+    h, G, d, n0, T = 2, 4, 128, 1000, 90
+    keys = cases.f16(rng.normal(0, 0.3, size=(h, n0 + T, d)))
+    values = cases.f16(rng.normal(size=(h, n0 + T, d)))
+    queries = cases.f16(rng.normal(size=(h * G, d)))
+    q = tkv.QuantizedLayerKV.from_kv(keys[:, :n0], values[:, :n0], bits, 64, capacity=n0 + T)
+    for t in range(T):
+        q.append_token(keys[:, n0 + t], values[:, n0 + t])
+        if t % 29 == 0 or t == T - 1:
+            kq, vq = O.quantize_layer(keys[:, :n0 + t + 1], values[:, :n0 + t + 1], bits, 64)
+            ref = O.quant_layer_decode(queries, kq, vq)
+            for impl in (1, 2):
+                assert rel_err(q.decode(queries, impl=impl).cpu().numpy(), ref) <= REL_TOL
+
+
 def test_qgemv_raw_ops(tkv):
     keys, values, queries = cases.decode_inputs(cases.DECODE_CASES[0])
     q = tkv.quantize_layer_kv(keys, values, 1, 64)
