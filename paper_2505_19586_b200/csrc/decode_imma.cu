@@ -52,12 +52,46 @@ __device__ __forceinline__ uint32_t pack_digits(float x0, float x1, float x2, fl
   (void)sel4;
 }
 
+// ---- TMA 1-D bulk copies into shared memory, completion on an mbarrier ----
+__device__ __forceinline__ uint32_t sm_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm_addr(dst)),
+      "l"(src), "r"(bytes), "r"(sm_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @p bra.uni DONE_%=;\n"
+      " bra.uni WAIT_%=;\n DONE_%=:\n}\n" ::"r"(sm_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// Staging area: the chunk's packed codes and group parameters, brought in by
+// four bulk copies at CTA start (16 KB keys + 16 KB values + params).
+struct ImStage {
+  uint4 kc[16 * 1024 / 16];   // key code words of the chunk
+  uint4 vc[16 * 1024 / 16];   // value code words of the chunk
+  uint32_t klohi[16 * 128];   // key (lo, hi) per group x channel
+  uint32_t vlohi[1024 * 2];   // value (lo, hi) per token x channel block
+  uint64_t bar[2];
+};
+
 struct ImSmem {
   float q[4][IM_D];             // query (h < G, else 0)
-  float qinv[4][IM_D];          // q * 32512 / bound_h
-  float kscale[4];              // bound_h / 32512
+  float qinv[4][IM_D];          // [h][group]: 32512 / max_c |q_hc s_gc|
+  float kscale[IM_GROUPS][4];   // per (group, head): max_c |q_hc s_gc| / 32512
   float off[IM_GROUPS][4];      // q_h . lo_g
-  uint32_t bfrag[IM_GROUPS][4][32][2];  // key B fragments per group, k-step, lane
+  uint32_t bfrag[IM_GROUPS][4][36][2];  // key B fragments per group, k-step, lane (padded rows)
   union {
     struct {
       float s[IM_GROUPS][IM_D];  // key scales of the chunk's groups
@@ -68,15 +102,17 @@ struct ImSmem {
       float lov[2][IM_CHUNK];    // value zero-point per (cb, token)
     } v;
   } u;
-  float p[IM_WARPS][4][IM_G];    // per-warp softmax numerators of the current group
+  float p[IM_WARPS][4][IM_G + 8];  // per-warp softmax numerators of the current group (padded rows)
   float wm[IM_WARPS][4], wl[IM_WARPS][4];
 };
 
 template <int BITS>
-__global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC c, const uint16_t *__restrict__ queries,
+__global__ void __launch_bounds__(IM_WARPS * 32, 2) quant_decode_imma_kernel(QC c, const uint16_t *__restrict__ queries,
                                                                               int G, float *__restrict__ pm,
                                                                               float *__restrict__ pl,
                                                                               float *__restrict__ pacc, int chunks) {
+  constexpr int CH = IM_CHUNK / BITS;      // tokens per CTA (16 KB of key codes)
+  constexpr int NG = CH / IM_G;            // groups per CTA
   constexpr int KT = 128 / BITS;           // key tile tokens
   constexpr int GPT = KT / IM_G;           // groups per key tile
   constexpr int VS = BITS;                 // value code sets (d = 128)
@@ -84,18 +120,39 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC 
   constexpr uint32_t CM = BITS == 1 ? 0x01010101u : 0x03030303u;
   extern __shared__ __align__(16) unsigned char smraw[];
   ImSmem &S = *reinterpret_cast<ImSmem *>(smraw);
+  ImStage &T = *reinterpret_cast<ImStage *>(smraw + ((sizeof(ImSmem) + 127) & ~size_t(127)));
   const int u = blockIdx.y, chunk = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g8 = lane >> 2, tq = lane & 3;
   const int64_t n = *c.len;
-  const int64_t t0 = (int64_t)chunk * IM_CHUNK;
+  const int64_t t0 = (int64_t)chunk * CH;
   if (t0 >= n) return;
+  // ---- issue the chunk's bulk copies first; params on bar[0], codes on bar[1] ----
+  if (tid == 0) {
+    mbar_init(&T.bar[0], 1);
+    mbar_init(&T.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int64_t cap = c.capacity;
+    const int64_t g0c = t0 / IM_G, kt0 = t0 / KT, vt0 = t0 / 32;
+    const uint32_t kl_bytes = (uint32_t)(imin64(NG, cap / IM_G - g0c) * IM_D * 4);
+    const uint32_t vl_bytes = (uint32_t)(imin64(CH, cap - t0) * 8);
+    const uint32_t kc_bytes = (uint32_t)(imin64(CH / KT, cap / KT - kt0) * 2048);
+    const uint32_t vc_bytes = (uint32_t)(imin64(CH / 32, cap / 32 - vt0) * VS * 512);
+    mbar_expect_tx(&T.bar[0], kl_bytes + vl_bytes);
+    bulk_g2s(T.klohi, c.key_lohi + ((size_t)u * (cap / IM_G) + g0c) * IM_D, kl_bytes, &T.bar[0]);
+    bulk_g2s(T.vlohi, c.val_lohi + ((size_t)u * cap + t0) * 2, vl_bytes, &T.bar[0]);
+    mbar_expect_tx(&T.bar[1], kc_bytes + vc_bytes);
+    bulk_g2s(T.kc, c.key_codes + ((size_t)u * (cap / KT) + kt0) * 512, kc_bytes, &T.bar[1]);
+    bulk_g2s(T.vc, c.val_codes + ((size_t)u * (cap / 32) + vt0) * VS * 128, vc_bytes, &T.bar[1]);
+  }
   const int64_t ncomp = (n / IM_G) * IM_G;
   const float inv_sqrt_d = 0.08838834764831845f;  // 1/sqrt(128)
   const float kmax_s = c.val_smax[2 * u + 1];
   const float vmax_s = c.val_smax[2 * u];
-  const float vinv = vmax_s > 0.0f ? IM_QMAX / vmax_s : 0.0f;
-  const float vscale = vmax_s / IM_QMAX;
+  (void)vmax_s;
 
   // ---- prologue: query, fixed-point scales, per-group key params ----
   for (int i = tid; i < 4 * IM_D; i += blockDim.x) {
@@ -103,74 +160,101 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC 
     S.q[h][i % IM_D] = h < G ? h2f(queries[((size_t)u * G + h) * IM_D + i % IM_D]) : 0.0f;
   }
   __syncthreads();
-  if (warp == 0) {
-    for (int h = 0; h < 4; ++h) {
-      float m = 0.0f;
-      for (int i = lane; i < IM_D; i += 32) m = fmaxf(m, fabsf(S.q[h][i]));
-      m = warp_max(m);
-      const float bound = m * kmax_s;
-      if (lane == 0) S.kscale[h] = bound / IM_QMAX;
-      const float inv = bound > 0.0f ? IM_QMAX / bound : 0.0f;
-      for (int i = lane; i < IM_D; i += 32) S.qinv[h][i] = S.q[h][i] * inv;
-    }
-  }
-  const int ngroups = (int)imin64(IM_GROUPS, (n - t0 + IM_G - 1) / IM_G);
+  (void)kmax_s;
+  const int ngroups = (int)imin64(NG, (n - t0 + IM_G - 1) / IM_G);
   const int64_t g0 = t0 / IM_G;
-  const uint32_t *klohi = c.key_lohi + ((size_t)u * (c.capacity / IM_G) + g0) * IM_D;
-  for (int i = tid; i < IM_GROUPS * IM_D; i += blockDim.x) {
-    const int gi = i / IM_D, ch = i % IM_D;
-    float sc = 0.0f, lo = 0.0f;
-    if (gi < ngroups && (g0 + gi + 1) * IM_G <= ncomp) {
-      const uint32_t w = klohi[i];
-      lo = h2f(w & 0xffff);
-      const float hi = h2f(w >> 16);
-      sc = hi > lo ? (hi - lo) / (float)((1 << BITS) - 1) : 0.0f;  // degenerate groups have all-zero codes
-    }
-    S.u.k.s[gi][ch] = sc;
-    S.u.k.lo[gi][ch] = lo;
-  }
-  __syncthreads();
-  // offsets q_h . lo_g : 64 outputs, 2 threads each
+  constexpr float KINV = 1.0f / (float)((1 << BITS) - 1);
+  mbar_wait(&T.bar[0], 0);
+  // Key groups, one warp per group, lane = one channel quad of the B-fragment
+  // layout (ks, j, tq): decode (lo, s) from the staged params, offsets
+  // q_h . lo_g, the per-(group, head) bound max_c |q_hc s_gc| (halving
+  // butterflies), then the two s8 digits of every W = q s.
   {
-    const int o = tid >> 1, half = tid & 1;
-    const int gi = o >> 2, h = o & 3;
-    float a = 0.0f;
-    for (int ch = half * 64; ch < half * 64 + 64; ++ch) a = fmaf(S.q[h][ch], S.u.k.lo[gi][ch], a);
-    a += __shfl_xor_sync(0xffffffffu, a, 1);
-    if (half == 0) S.off[gi][h] = a;
-  }
-  // key B fragments: item = (gi, ks, j, tq, h); 4 channels each -> hi & lo digit words
-  for (int it = tid; it < IM_GROUPS * 4 * 2 * 4 * 4; it += blockDim.x) {
-    const int h = it & 3, tqq = (it >> 2) & 3, j = (it >> 4) & 1, ks = (it >> 5) & 3, gi = it >> 7;
+    const int tqq = lane & 3, j = (lane >> 2) & 1, ks = lane >> 3;
     const int ch = 32 * ks + 16 * j + 4 * tqq;
-    float x[4];
+    float4 qv[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = fmaf(S.u.k.s[gi][ch + i], S.qinv[h][ch + i], IM_MAGIC);
-    const uint32_t hiw = pack_digits(x[0], x[1], x[2], x[3], 0x0051, 0, 0u);  // bytes 1
-    const uint32_t low = pack_digits(x[0], x[1], x[2], x[3], 0x0040, 0, 0x80808080u);  // bytes 0
-    S.bfrag[gi][ks][(2 * h) * 4 + tqq][j] = hiw;
-    S.bfrag[gi][ks][(2 * h + 1) * 4 + tqq][j] = low;
-  }
-  __syncthreads();
-  // value params of the chunk's tokens (reuses the key-param space)
-  const uint32_t *vlohi = c.val_lohi + ((size_t)u * c.capacity + t0) * 2;
-  for (int i = tid; i < IM_CHUNK * 2; i += blockDim.x) {
-    const int t = i >> 1, cb = i & 1;
-    float sv = 0.0f, lo = 0.0f;
-    if (t0 + t < n) {
-      const uint32_t w = vlohi[i];
-      lo = h2f(w & 0xffff);
-      const float hi = h2f(w >> 16);
-      sv = group_scale_f(lo, hi, BITS) * vinv;
+    for (int h = 0; h < 4; ++h) qv[h] = *reinterpret_cast<const float4 *>(&S.q[h][ch]);
+    const bool b4 = lane & 16, b3 = lane & 8;
+    for (int gi = warp; gi < NG; gi += IM_WARPS) {
+      float lo[4] = {0.f, 0.f, 0.f, 0.f}, sc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (gi < ngroups && (g0 + gi + 1) * IM_G <= ncomp) {
+        const uint4 raw = *reinterpret_cast<const uint4 *>(&T.klohi[gi * IM_D + ch]);
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          lo[i] = h2f(w[i] & 0xffff);
+          sc[i] = (h2f(w[i] >> 16) - lo[i]) * KINV;  // 0 for degenerate groups (all codes 0)
+        }
+      }
+      float W[4][4], dt[4], mx[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float qa[4] = {qv[h].x, qv[h].y, qv[h].z, qv[h].w};
+        dt[h] = 0.0f;
+        mx[h] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          W[h][i] = qa[i] * sc[i];
+          dt[h] = fmaf(qa[i], lo[i], dt[h]);
+          mx[h] = fmaxf(mx[h], fabsf(W[h][i]));
+        }
+      }
+      float d2[2], m2[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float sd = b4 ? dt[k] : dt[k + 2], sm = b4 ? mx[k] : mx[k + 2];
+        const float rd = __shfl_xor_sync(0xffffffffu, sd, 16), rm = __shfl_xor_sync(0xffffffffu, sm, 16);
+        d2[k] = (b4 ? dt[k + 2] : dt[k]) + rd;
+        m2[k] = fmaxf(b4 ? mx[k + 2] : mx[k], rm);
+      }
+      float d1, m1;
+      {
+        const float sd = b3 ? d2[0] : d2[1], sm = b3 ? m2[0] : m2[1];
+        const float rd = __shfl_xor_sync(0xffffffffu, sd, 8), rm = __shfl_xor_sync(0xffffffffu, sm, 8);
+        d1 = (b3 ? d2[1] : d2[0]) + rd;
+        m1 = fmaxf(b3 ? m2[1] : m2[0], rm);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+      }
+      if ((lane & 7) == 0) {
+        const int h = (b4 ? 2 : 0) + (b3 ? 1 : 0);
+        S.off[gi][h] = d1;
+        S.kscale[gi][h] = m1 / IM_QMAX;
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float mh = __shfl_sync(0xffffffffu, m1, 8 * h);
+        const float inv = mh > 0.0f ? IM_QMAX / mh : 0.0f;
+        const float x0 = fmaf(W[h][0], inv, IM_MAGIC), x1 = fmaf(W[h][1], inv, IM_MAGIC);
+        const float x2 = fmaf(W[h][2], inv, IM_MAGIC), x3 = fmaf(W[h][3], inv, IM_MAGIC);
+        S.bfrag[gi][ks][(2 * h) * 4 + tqq][j] = pack_digits(x0, x1, x2, x3, 0x0051, 0, 0u);              // hi: bytes 1
+        S.bfrag[gi][ks][(2 * h + 1) * 4 + tqq][j] = pack_digits(x0, x1, x2, x3, 0x0040, 0, 0x80808080u);  // lo: bytes 0
+      }
     }
-    S.u.v.sv[cb][t] = sv;
-    S.u.v.lov[cb][t] = lo;
+  }
+  // value params of the chunk's tokens: both channel blocks of a token at once
+  for (int t = tid; t < CH; t += blockDim.x) {
+    float s0 = 0.f, s1 = 0.f, l0 = 0.f, l1 = 0.f;
+    if (t0 + t < n) {
+      const uint2 w = *reinterpret_cast<const uint2 *>(&T.vlohi[2 * t]);
+      l0 = h2f(w.x & 0xffff);
+      l1 = h2f(w.y & 0xffff);
+      s0 = (h2f(w.x >> 16) - l0) * KINV;
+      s1 = (h2f(w.y >> 16) - l1) * KINV;
+    }
+    S.u.v.sv[0][t] = s0;
+    S.u.v.sv[1][t] = s1;
+    S.u.v.lov[0][t] = l0;
+    S.u.v.lov[1][t] = l1;
   }
   __syncthreads();
 
   // ---- main loop: each warp walks whole key tiles of its chunk ----
-  const uint4 *kcodes = reinterpret_cast<const uint4 *>(c.key_codes) + (size_t)u * (c.capacity / KT) * 4 * 32;
-  const uint4 *vcodes = reinterpret_cast<const uint4 *>(c.val_codes) + (size_t)u * (c.capacity / 32) * VS * 32;
+  mbar_wait(&T.bar[1], 0);
   const uint16_t *kres = c.key_resid + (size_t)u * IM_G * IM_D;
   const uint32_t dsel = (g8 & 1) ? 0x0040u : 0x0051u;  // this lane's B column digit
   const uint32_t dxor = (g8 & 1) ? 0x80808080u : 0u;
@@ -179,16 +263,15 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC 
   float acc[8][2];
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) { acc[mt][0] = 0.0f; acc[mt][1] = 0.0f; }
-  const float ks_h = S.kscale[tq];
 
-  for (int kt = warp; kt < IM_CHUNK / KT; kt += IM_WARPS) {
+  for (int kt = warp; kt < CH / KT; kt += IM_WARPS) {
     const int64_t tile_t0 = t0 + (int64_t)kt * KT;
     if (tile_t0 >= n) break;
     uint4 X[4];
     const bool any_complete = tile_t0 + IM_G <= ncomp;
     if (any_complete) {
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) X[ks] = __ldg(&kcodes[((tile_t0 / KT) * 4 + ks) * 32 + lane]);
+      for (int ks = 0; ks < 4; ++ks) X[ks] = T.kc[(kt * 4 + ks) * 32 + lane];
     }
 #pragma unroll
     for (int gl = 0; gl < GPT; ++gl) {
@@ -205,6 +288,7 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC 
           b[ks][1] = bb.y;
         }
         const float off = S.off[gi][tq];
+        const float ks_h = S.kscale[gi][tq];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
           const int k = gl * 4 + mt;
@@ -275,27 +359,48 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC 
       zsum[1] = fmaf(zsum[1], alpha, zl1);
       __syncwarp();
       // ---- value MMA over the group's two 32-token k-steps ----
+      // B[t, (h,digit)] = p[t,h] * s[t,cb] in a 16-bit fixed point scaled by
+      // this group's max_t,cb p*s of head h (adaptive, exact integer MMA)
+      float prod[2][2][8];  // [vtile][cb][token slot]
+      float pmax = 0.0f;
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int tb = v * 32 + 4 * tq;
+        const float4 p0 = *reinterpret_cast<const float4 *>(&S.p[warp][hB][tb]);
+        const float4 p1 = *reinterpret_cast<const float4 *>(&S.p[warp][hB][tb + 16]);
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          const float4 s0 = *reinterpret_cast<const float4 *>(&S.u.v.sv[cb][tl0 + tb]);
+          const float4 s1 = *reinterpret_cast<const float4 *>(&S.u.v.sv[cb][tl0 + tb + 16]);
+          float *pr = prod[v][cb];
+          pr[0] = p0.x * s0.x; pr[1] = p0.y * s0.y; pr[2] = p0.z * s0.z; pr[3] = p0.w * s0.w;
+          pr[4] = p1.x * s1.x; pr[5] = p1.y * s1.y; pr[6] = p1.z * s1.z; pr[7] = p1.w * s1.w;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pmax = fmaxf(pmax, pr[e]);
+        }
+      }
+      pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 1));
+      pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 2));
+      pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 4));
+      const float pinv = pmax > 0.0f ? IM_QMAX / pmax : 0.0f;
+      const float vsc_h = __shfl_sync(0xffffffffu, pmax, (2 * tq) * 4) * (1.0f / IM_QMAX);  // head tq's scale
       int V[8][4];
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) { V[mt][0] = 0; V[mt][1] = 0; V[mt][2] = 0; V[mt][3] = 0; }
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int64_t vt = (gt0 >> 5) + v;
+        const int vt = (int)((gt0 - t0) >> 5) + v;
         uint4 A[VS];
 #pragma unroll
-        for (int st = 0; st < VS; ++st) A[st] = __ldg(&vcodes[(vt * VS + st) * 32 + lane]);
-        const int tb = v * 32 + 4 * tq;  // token (within group) of byte 0, b0 half
-        const float4 p0 = *reinterpret_cast<const float4 *>(&S.p[warp][hB][tb]);
-        const float4 p1 = *reinterpret_cast<const float4 *>(&S.p[warp][hB][tb + 16]);
+        for (int st = 0; st < VS; ++st) A[st] = T.vc[(vt * VS + st) * 32 + lane];
         uint32_t B[2][2];
 #pragma unroll
         for (int cb = 0; cb < 2; ++cb) {
-          const float4 s0 = *reinterpret_cast<const float4 *>(&S.u.v.sv[cb][tl0 + tb]);
-          const float4 s1 = *reinterpret_cast<const float4 *>(&S.u.v.sv[cb][tl0 + tb + 16]);
-          B[cb][0] = pack_digits(fmaf(p0.x, s0.x, IM_MAGIC), fmaf(p0.y, s0.y, IM_MAGIC), fmaf(p0.z, s0.z, IM_MAGIC),
-                                 fmaf(p0.w, s0.w, IM_MAGIC), dsel, 0, dxor);
-          B[cb][1] = pack_digits(fmaf(p1.x, s1.x, IM_MAGIC), fmaf(p1.y, s1.y, IM_MAGIC), fmaf(p1.z, s1.z, IM_MAGIC),
-                                 fmaf(p1.w, s1.w, IM_MAGIC), dsel, 0, dxor);
+          const float *pr = prod[v][cb];
+          B[cb][0] = pack_digits(fmaf(pr[0], pinv, IM_MAGIC), fmaf(pr[1], pinv, IM_MAGIC), fmaf(pr[2], pinv, IM_MAGIC),
+                                 fmaf(pr[3], pinv, IM_MAGIC), dsel, 0, dxor);
+          B[cb][1] = pack_digits(fmaf(pr[4], pinv, IM_MAGIC), fmaf(pr[5], pinv, IM_MAGIC), fmaf(pr[6], pinv, IM_MAGIC),
+                                 fmaf(pr[7], pinv, IM_MAGIC), dsel, 0, dxor);
         }
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
@@ -309,7 +414,7 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC 
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
         const int slot = mt % SLOTS;
-        const float sc = vscale * __int_as_float((127 - slot * BITS) << 23);
+        const float sc = vsc_h * __int_as_float((127 - slot * BITS) << 23);
         acc[mt][0] = fmaf(acc[mt][0], alpha, fmaf((float)V[mt][0], 256.0f, (float)V[mt][1]) * sc);
         acc[mt][1] = fmaf(acc[mt][1], alpha, fmaf((float)V[mt][2], 256.0f, (float)V[mt][3]) * sc);
       }
@@ -355,11 +460,12 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 3) quant_decode_imma_kernel(QC 
 }
 
 int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st) {
-  const int chunks = (int)((c.capacity + IM_CHUNK - 1) / IM_CHUNK);
+  const int CH = IM_CHUNK / c.bits;
+  const int chunks = (int)((c.capacity + CH - 1) / CH);
   float *pm = reinterpret_cast<float *>(ws);
   float *pl = pm + (size_t)c.units * chunks * G;
   float *pacc = pl + (size_t)c.units * chunks * G;
-  const size_t sm = sizeof(ImSmem);
+  const size_t sm = ((sizeof(ImSmem) + 127) & ~size_t(127)) + sizeof(ImStage);
   dim3 grid(chunks, c.units);
   if (c.bits == 1) {
     cudaFuncSetAttribute(quant_decode_imma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -368,7 +474,7 @@ int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *w
     cudaFuncSetAttribute(quant_decode_imma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     quant_decode_imma_kernel<2><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks);
   }
-  launch_combine_scalar(pm, pl, pacc, c.units, chunks, G, c.d, c.len, IM_CHUNK, out, st);
+  launch_combine_scalar(pm, pl, pacc, c.units, chunks, G, c.d, c.len, CH, out, st);
   return check_launch("tkv_quant_decode(imma)");
 }
 

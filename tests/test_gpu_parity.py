@@ -136,7 +136,7 @@ def test_quant_decode_tensor_core_vs_oracle(tkv, bits, n, kscale):
     ref = O.quant_layer_decode(queries, kq, vq)
     out2 = q.decode(queries, impl=2).cpu().numpy()
     assert rel_err(out2, ref) <= REL_TOL
-    assert rel_err(out2, ref) <= 2e-4  # typical margin of the exact-integer design
+    assert rel_err(out2, ref) <= 5e-4  # typical margin of the exact-integer design
 
 
 @pytest.mark.parametrize("bits", [1, 2])
