@@ -18,59 +18,56 @@ __global__ void __launch_bounds__(256) combine_kernel(const float *__restrict__ 
                                                        const float *__restrict__ pacc, int chunks, int G, int d,
                                                        const int32_t *__restrict__ rows, int rows_stride,
                                                        int rows_per_chunk, float *__restrict__ out) {
+  // grid (units*G, ceil(d/32)); 8 warps split the chunks, lanes own channels
   __shared__ float red_m[8];
-  __shared__ float part_acc[256];
-  __shared__ float part_l[256];
+  __shared__ float part_acc[8][32];
+  __shared__ float part_l[8];
   const int u = blockIdx.x / G, h = blockIdx.x % G;
+  const int ch = blockIdx.y * 32 + (threadIdx.x & 31);
+  const int warp = threadIdx.x >> 5;
   const int nrows = rows ? rows[(size_t)u * rows_stride] : chunks * rows_per_chunk;
   const int valid = min(chunks, (nrows + rows_per_chunk - 1) / rows_per_chunk);
   const size_t base0 = (size_t)u * chunks * G + h;
-  // global max over the valid chunks
   float M = -INFINITY;
   for (int ci = threadIdx.x; ci < valid; ci += blockDim.x) M = fmaxf(M, pm[base0 + (size_t)ci * G]);
   M = warp_max(M);
-  if ((threadIdx.x & 31) == 0) red_m[threadIdx.x >> 5] = M;
+  if ((threadIdx.x & 31) == 0) red_m[warp] = M;
   __syncthreads();
   M = -INFINITY;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) M = fmaxf(M, red_m[i]);
-  // thread = (chunk slice, channel); fixed summation order per slice
-  const int slices = max(1, (int)blockDim.x / d);
-  const int ch = threadIdx.x % d, sl = threadIdx.x / d;
+  for (int i = 0; i < 8; ++i) M = fmaxf(M, red_m[i]);
   float L = 0.0f, acc = 0.0f;
-  if (sl < slices) {
 #pragma unroll 4
-    for (int ci = sl; ci < valid; ci += slices) {
-      const size_t base = base0 + (size_t)ci * G;
-      const float m = pm[base];
-      const float sc = m == -INFINITY ? 0.0f : __expf(m - M);
-      L += sc * pl[base];
-      acc += sc * pacc[base * d + ch];
-    }
+  for (int ci = warp; ci < valid; ci += 8) {
+    const size_t base = base0 + (size_t)ci * G;
+    const float m = pm[base];
+    const float sc = m == -INFINITY ? 0.0f : __expf(m - M);
+    L += sc * pl[base];
+    if (ch < d) acc += sc * pacc[base * d + ch];
   }
-  if (sl < slices) {
-    part_acc[threadIdx.x] = acc;
-    part_l[threadIdx.x] = L;
-  }
+  part_acc[warp][threadIdx.x & 31] = acc;
+  if ((threadIdx.x & 31) == 0) part_l[warp] = L;
   __syncthreads();
-  if (threadIdx.x < d) {
+  if (warp == 0 && ch < d) {
     float a = 0.0f, l = 0.0f;
-    for (int j = 0; j < slices; ++j) {
-      a += part_acc[j * d + threadIdx.x];
-      l += part_l[j * d + threadIdx.x];
+    for (int w = 0; w < 8; ++w) {  // fixed order: deterministic
+      a += part_acc[w][threadIdx.x];
+      l += part_l[w];
     }
-    out[((size_t)u * G + h) * d + threadIdx.x] = a / l;
+    out[((size_t)u * G + h) * d + ch] = a / l;
   }
 }
 
 void launch_combine(const float *pm, const float *pl, const float *pacc, int units, int chunks, int G, int d,
                     const int32_t *rows, int rows_per_chunk, float *out, cudaStream_t st) {
-  combine_kernel<<<units * G, 256, 0, st>>>(pm, pl, pacc, chunks, G, d, rows, rows ? 1 : 0, rows_per_chunk, out);
+  combine_kernel<<<dim3(units * G, (d + 31) / 32), 256, 0, st>>>(pm, pl, pacc, chunks, G, d, rows, rows ? 1 : 0,
+                                                                 rows_per_chunk, out);
 }
 
 // variant where every unit shares one device row count (quantized layers)
 void launch_combine_scalar(const float *pm, const float *pl, const float *pacc, int units, int chunks, int G,
                                   int d, const int32_t *len, int rows_per_chunk, float *out, cudaStream_t st) {
-  combine_kernel<<<units * G, 256, 0, st>>>(pm, pl, pacc, chunks, G, d, len, 0, rows_per_chunk, out);
+  combine_kernel<<<dim3(units * G, (d + 31) / 32), 256, 0, st>>>(pm, pl, pacc, chunks, G, d, len, 0, rows_per_chunk,
+                                                                 out);
 }
 
 // ---------------------------------------------------------------------------
