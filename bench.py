@@ -232,9 +232,17 @@ def pcie_peaks(torch, lib_mod, device):
     b.record()
     torch.cuda.synchronize()
     uva_gbs = 5 * nrows * 512 / (a.elapsed_time(b) * 1e-3) / 1e9
+    rows256 = rows * 2
+    a.record()
+    for _ in range(5):
+        lib.tkv_uva_read_probe(arena.addr, 1 << 30, 256, rows256.data_ptr(), nrows, sink.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    b.record()
+    torch.cuda.synchronize()
+    uva256_gbs = 5 * nrows * 256 / (a.elapsed_time(b) * 1e-3) / 1e9
     arena.close()
     del host, dev
-    return memcpy_gbs, uva_gbs
+    return memcpy_gbs, uva_gbs, uva256_gbs
 
 
 def main():
@@ -354,7 +362,7 @@ def main():
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    memcpy_gbs, uva_gbs = pcie_peaks(torch, _lib, device)
+    memcpy_gbs, uva_gbs, uva256_gbs = pcie_peaks(torch, _lib, device)
 
     def mean(x):
         return sum(x) / len(x) if x else float("nan")
@@ -394,7 +402,7 @@ def main():
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
                      "frac": dom["frac"], "traffic": None, "kernel": "sparse_attn_kernel (UVA gather + attention)"},
         "rooflines": rooflines,
-        "pcie": {"memcpy_h2d_gbs": memcpy_gbs, "uva_512B_rows_gbs": uva_gbs,
+        "pcie": {"memcpy_h2d_gbs": memcpy_gbs, "uva_512B_rows_gbs": uva_gbs, "uva_256B_rows_gbs": uva256_gbs,
                  "gather_bytes_per_token": gather_bytes * 30, "fetched_rows_per_layer": fetch_rows},
         "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",

@@ -146,16 +146,35 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
       tot[tid] = t;
     }
     __syncthreads();
-    if (tid == 0) {
-      int cum = 0, D = 0;
-      for (int dg = 255; dg >= 0; --dg) {
-        if (cum + (int)tot[dg] >= need) { D = dg; break; }
-        cum += (int)tot[dg];
+    if (tid < 32) {
+      // warp-parallel descending scan: lane l owns bins 255-8l-7 .. 255-8l
+      uint32_t v[8];
+      int sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = tot[255 - 8 * tid - i];
+        sum += (int)v[i];
       }
-      sh_need = need - cum;
-      sh_prefix = prefix | ((uint64_t)D << shift);
-      sh_mask = mask | (255ull << shift);
-      sh_done = (int)tot[D] == need - cum;
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
+      const int L = __ffs(hit) - 1;
+      if (tid == L) {
+        int cum = incl - sum, D = 255 - 8 * L;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (cum + (int)v[i] >= need) { D = 255 - 8 * L - i; break; }
+          cum += (int)v[i];
+        }
+        sh_need = need - cum;
+        sh_prefix = prefix | ((uint64_t)D << shift);
+        sh_mask = mask | (255ull << shift);
+        sh_done = (int)tot[D] == need - cum;
+      }
     }
     __syncthreads();
     prefix = sh_prefix;

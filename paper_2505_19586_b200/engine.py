@@ -38,7 +38,9 @@ class EngineConfig:
     n_local: int = 64
     n_topk: int = 128
     critical_channels: int = 8
-    keys_from_hbm: bool = True     # gather key rows from the HBM scorer copy; only V rows cross PCIe
+    keys_from_hbm: bool = True     # gather key rows from HBM; only V rows cross PCIe
+    token_major_keys: bool = True  # keep a token-major HBM key copy for that gather (else read the scorer's
+                                   # channel-major copy: no extra memory, 32x more DRAM sectors)
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
     def validate(self) -> None:
@@ -186,7 +188,9 @@ class DecodeEngine:
         else:
             if w_q is None:
                 raise ConfigError(f"sparsity-friendly layer {layer} needs its W_q for stage 1")
-            lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local, device=self.device)
+            lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local,
+                                   keys_on_device=self.cfg.keys_from_hbm and self.cfg.token_major_keys,
+                                   device=self.device)
             lay.offload(k, v)
             w = as_f16(w_q, self.device)
             if w.shape[0] == self.model.num_query_heads:
