@@ -302,8 +302,13 @@ def main():
         return res
 
     prof_alt = profile_mode(args.keys_over_pcie)  # the other key-row source
+    h0, m0 = eng.cache_counters()
     prof = profile_mode(not args.keys_over_pcie)
+    h1, m1 = eng.cache_counters()
+    n_sparse = sum(1 for x in wl.labels if x == "s")
     fetch_rows = int(eng.fetch_count.sum().item())
+    cached_rows = (h1 - h0) / (PROF * n_sparse)   # per gather launch, served from the HBM row cache
+    pcie_rows = (m1 - m0) / (PROF * n_sparse)      # per gather launch, fetched over PCIe
 
     # variant: the other key-row source, graph-timed for K steps
     eng.keys_from_hbm = args.keys_over_pcie
@@ -373,8 +378,10 @@ def main():
     select_ms = mean(prof.get("select", []))
     stage1_ms = mean(prof.get("stage1", []))
     from oracle import tailorkv_oracle as O  # byte formulas only (memsim.py accounting)
-    # algorithmic PCIe bytes of one gather launch: K+V rows (memsim.py:249) or V rows only
-    gather_bytes = O.gather_bytes(fetch_rows, model.head_dim) if args.keys_over_pcie else fetch_rows * model.head_dim * 2
+    # PCIe bytes of one gather launch: K+V rows (memsim.py:249, no row cache) or, in the
+    # default mode, the value rows that missed the HBM row cache (counted by the kernel)
+    gather_bytes = (O.gather_bytes(fetch_rows, model.head_dim) if args.keys_over_pcie
+                    else int(pcie_rows * model.head_dim * 2))
     alt_bytes = O.gather_bytes(fetch_rows, model.head_dim) if not args.keys_over_pcie else fetch_rows * model.head_dim * 2
     alt_ms = mean(prof_alt.get("gather_attend", []))
     quant_bytes = O.quant_layer_bytes(n, U, model.head_dim, 1, 64)
@@ -402,8 +409,12 @@ def main():
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
                      "frac": dom["frac"], "traffic": None, "kernel": "sparse_attn_kernel (UVA gather + attention)"},
         "rooflines": rooflines,
+        "row_cache": {"rows_per_gather_from_hbm_cache": cached_rows, "rows_per_gather_over_pcie": pcie_rows,
+                      "hit_rate": cached_rows / max(1.0, cached_rows + pcie_rows),
+                      "note": "value rows fetched at step t-1 stay in HBM; exact (rows never change)"},
         "pcie": {"memcpy_h2d_gbs": memcpy_gbs, "uva_512B_rows_gbs": uva_gbs, "uva_256B_rows_gbs": uva256_gbs,
-                 "gather_bytes_per_token": gather_bytes * 30, "fetched_rows_per_layer": fetch_rows},
+                 "gather_bytes_per_token": gather_bytes * n_sparse, "fetched_rows_per_layer": fetch_rows,
+                 "reference_fetch_topk_bytes_per_token": O.gather_bytes(fetch_rows, model.head_dim) * n_sparse},
         "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",
                     "ms_per_token": ms_variant, "gather_ms": alt_ms,

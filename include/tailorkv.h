@@ -126,6 +126,16 @@ typedef struct tkv_sparse_layer {
   uint16_t *host_kv;      /* pinned host store [units][capacity][2][d] (K row | V row) */
   int32_t *len;           /* device scalar */
   uint32_t *ticket;       /* device scalar scratch */
+  /* Optional step-to-step value-row cache (NULL cache_v disables it): the
+   * value rows fetched over PCIe at the previous step stay in HBM; a row
+   * selected again is read from there.  Rows never change once written, so
+   * any cached (index, row) pair stays valid. */
+  int32_t cache_rows;     /* rows per unit and buffer (>= n_local + n_topk) */
+  int32_t *cache_idx;     /* [2][units][cache_rows] ascending token indices */
+  int32_t *cache_cnt;     /* [2][units] */
+  uint16_t *cache_v;      /* [2][units][cache_rows][d] */
+  int32_t *cache_cur;     /* device scalar: buffer holding the previous step */
+  unsigned long long *cache_stats; /* [2]: rows served from HBM, rows fetched over PCIe */
 } tkv_sparse_layer;
 
 /* Prefill/offload (replaces HostPool.offload_layer memsim.py:88-93 and the

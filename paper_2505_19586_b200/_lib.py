@@ -57,6 +57,8 @@ class SparseLayer(C.Structure):
         ("capacity", C.c_int64), ("local_offset", C.c_int64), ("local_capacity", C.c_int64),
         ("kt", C.c_void_p), ("chmax", C.c_void_p), ("loc_k", C.c_void_p), ("loc_v", C.c_void_p),
         ("kdev", C.c_void_p), ("host_kv", C.c_void_p), ("len", C.c_void_p), ("ticket", C.c_void_p),
+        ("cache_rows", C.c_int32), ("cache_idx", C.c_void_p), ("cache_cnt", C.c_void_p), ("cache_v", C.c_void_p),
+        ("cache_cur", C.c_void_p), ("cache_stats", C.c_void_p),
     ]
 
 

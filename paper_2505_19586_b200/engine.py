@@ -41,6 +41,7 @@ class EngineConfig:
     keys_from_hbm: bool = True     # gather key rows from HBM; only V rows cross PCIe
     token_major_keys: bool = True  # keep a token-major HBM key copy for that gather (else read the scorer's
                                    # channel-major copy: no extra memory, 32x more DRAM sectors)
+    row_cache: bool = True         # keep the previous step's fetched value rows in HBM (exact; rows are immutable)
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
     def validate(self) -> None:
@@ -190,7 +191,8 @@ class DecodeEngine:
                 raise ConfigError(f"sparsity-friendly layer {layer} needs its W_q for stage 1")
             lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local,
                                    keys_on_device=self.cfg.keys_from_hbm and self.cfg.token_major_keys,
-                                   device=self.device)
+                                   device=self.device,
+                                   cache_rows=(self.retrieval.n_local + self.retrieval.n_topk) if self.cfg.row_cache else 0)
             lay.offload(k, v)
             w = as_f16(w_q, self.device)
             if w.shape[0] == self.model.num_query_heads:
@@ -335,6 +337,15 @@ class DecodeEngine:
         for lay, n in zip(self.layers, saved):
             lay.n = n
         self.graph = g
+
+    def cache_counters(self) -> tuple[int, int]:
+        """Summed (HBM-cache hits, PCIe-fetched rows) over the sparse layers."""
+        h = m = 0
+        for st in self.sparse.values():
+            a, b = st.layer.cache_counters()
+            h += a
+            m += b
+        return h, m
 
     def full_output(self, l: int) -> torch.Tensor:
         """Layer output [batch, hq, d] (all ranks' heads)."""

@@ -71,7 +71,7 @@ class OffloadedLayerKV:
     """One sparsity-friendly layer for ``units`` KV heads (batch x heads)."""
 
     def __init__(self, units: int, head_dim: int, capacity: int, prefill_len: int, n_local: int,
-                 keys_on_device: bool = False, numa_node: int | None = None, device=None):
+                 keys_on_device: bool = False, numa_node: int | None = None, device=None, cache_rows: int = 0):
         _lib.require_cuda()
         dev = torch.device(device or "cuda")
         self.device = dev
@@ -91,10 +91,22 @@ class OffloadedLayerKV:
         self.host_kv = self.arena.as_tensor(units * self.capacity * 2 * d).view(units, self.capacity, 2, d)
         self._len = torch.zeros(2, dtype=torch.int32, device=dev)
         self.n = 0
+        # step-to-step value-row cache (rows fetched at the previous step stay in HBM)
+        self.cache_rows = int(cache_rows)
+        if self.cache_rows:
+            self.cache_idx = torch.zeros((2, units, self.cache_rows), dtype=torch.int32, device=dev)
+            self.cache_cnt = torch.zeros((2, units), dtype=torch.int32, device=dev)
+            self.cache_v = torch.zeros((2, units, self.cache_rows, d), dtype=torch.float16, device=dev)
+            self.cache_cur = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.cache_stats = torch.zeros(2, dtype=torch.int64, device=dev)
+        else:
+            self.cache_idx = self.cache_cnt = self.cache_v = self.cache_cur = self.cache_stats = None
         self.struct = SparseLayer(units, d, self.capacity, self.local_offset, self.local_capacity,
                                   self.kt.data_ptr(), self.chmax.data_ptr(), self.loc_k.data_ptr(),
                                   self.loc_v.data_ptr(), ptr(self.kdev), self.arena.addr,
-                                  self._len.data_ptr(), self._len.data_ptr() + 4)
+                                  self._len.data_ptr(), self._len.data_ptr() + 4,
+                                  self.cache_rows, ptr(self.cache_idx), ptr(self.cache_cnt), ptr(self.cache_v),
+                                  ptr(self.cache_cur), ptr(self.cache_stats))
 
     @property
     def keys_on_device(self) -> bool:
@@ -125,6 +137,13 @@ class OffloadedLayerKV:
             raise ParameterError("layer capacity exhausted")
         check(_lib.load().tkv_sparse_append(C.byref(self.struct), ptr(k), ptr(v), stream_ptr(stream)))
         self.n += 1
+
+    def cache_counters(self) -> tuple[int, int]:
+        """(rows served from the HBM row cache, rows fetched over PCIe) so far."""
+        if self.cache_stats is None:
+            return 0, 0
+        a, b = self.cache_stats.tolist()
+        return int(a), int(b)
 
     def channel_abs_max(self) -> torch.Tensor:
         """Running max|K| per (unit, channel) (memsim.py:113-116)."""

@@ -374,6 +374,9 @@ def test_engine_replays_reference_pipeline(tkv, run, graph, kfh):
                     assert np.array_equal(idx[kvh, :cnt[kvh]], cases.hex_to_indices(ph["selected_hex"])), (l, t, kvh)
                     assert fc[kvh] == ph["fetched"]
     assert worst <= REL_TOL, worst
+    if kfh and not graph and labels.count("s"):
+        hits, misses = eng.cache_counters()
+        assert misses > 0 and hits + misses > 0  # the HBM row cache was exercised
 
 
 def test_engine_config1_shapes(tkv):
