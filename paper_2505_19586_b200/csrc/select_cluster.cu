@@ -2,16 +2,19 @@
 // (retriever.py:166-189) + exact top-k by (score desc, index desc) plus the
 // local window, sorted ascending (retriever.py:192-211) -- one launch.
 //
-// One 8-CTA thread-block cluster per unit (KV head).  Each CTA scores a
-// contiguous slice of the candidate tokens into shared memory (8-byte
-// order-preserving keys of the float64 scores), then the cluster runs an
-// 8-bit-digit radix select over the 64-bit keys with the per-CTA histograms
-// exchanged through distributed shared memory (DSMEM), so the 1 MB of keys of
-// a 128k-token head never round-trips through HBM.  Exact score ties at the
-// threshold are resolved toward the larger index, as the reference's
-// lexsort does.  Output order is ascending because every CTA owns a
-// contiguous index range and writes at its cluster-prefix offset.
+// One thread-block cluster per unit (KV head): 16 CTAs when the GPU can
+// co-schedule them (non-portable size), else 8.  Each CTA scores a contiguous
+// slice of the candidate tokens into shared memory as 8-byte
+// order-preserving keys of the float64 scores; the cluster then runs a radix
+// select with 11-bit digits over the bits below the keys' common prefix,
+// exchanging the per-CTA histograms through distributed shared memory (DSMEM),
+// so the 1 MB of keys of a 128k-token head never round-trips through HBM.
+// Exact score ties at the threshold go to the larger index, as the
+// reference's lexsort does.  Output order is ascending because every CTA owns
+// a contiguous index range and writes at its cluster-prefix offset.
 #include <cooperative_groups.h>
+
+#include <string>
 
 #include "common.cuh"
 #include "sparse.cuh"
@@ -20,9 +23,10 @@ namespace cg = cooperative_groups;
 
 namespace tkv {
 
-constexpr int SC_CTAS = 8;
 constexpr int SC_THREADS = 1024;
-constexpr int SC_CHUNK_CAP = 24576;  // keys per CTA (8 B each) -> 196608 candidates per unit
+constexpr int SC_CHUNK_CAP = 16384;  // keys per CTA (8 B each)
+constexpr int SC_BITS = 11;
+constexpr int SC_BINS = 1 << SC_BITS;
 
 __device__ __forceinline__ int block_excl_scan(int v, int *sh, int *total) {
   // sh: >= 33 ints
@@ -51,24 +55,32 @@ __device__ __forceinline__ int block_excl_scan(int v, int *sh, int *total) {
   return before;
 }
 
-__global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
+struct SelShared {
+  uint64_t keys[SC_CHUNK_CAP];
+  uint8_t flags[SC_CHUNK_CAP];
+  uint32_t hist[2][SC_BINS];
+  uint32_t tot[SC_BINS];
+};
+
+template <int CTAS>
+__global__ void __launch_bounds__(SC_THREADS, 1)
     select_cluster_kernel(SL s, const uint16_t *__restrict__ queries, int G, const int32_t *__restrict__ channels,
                           int d_s, int n_local, int n_topk, int32_t *__restrict__ sel_idx, int sel_stride,
                           int32_t *__restrict__ sel_count, int32_t *__restrict__ fetch_count,
                           double *__restrict__ scores_out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t hist[2][256];
-  __shared__ uint32_t tot[256];
+  SelShared &S = *reinterpret_cast<SelShared *>(smem);
   __shared__ double qsum[128];
   __shared__ int chs[128];
   __shared__ int scan_sh[40];
   __shared__ int cta_count;
-  __shared__ unsigned long long sh_prefix, sh_mask;
+  __shared__ unsigned long long kmin_sh[32], kmax_sh[32], ck[2];
+  __shared__ unsigned long long sh_prefix;
   __shared__ int sh_need, sh_done;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int u = blockIdx.y;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane_id = tid & 31;
   const int64_t n = *s.len;
   int32_t *out_idx = sel_idx + (size_t)u * sel_stride;
   if (n <= (int64_t)n_local + n_topk) {  // select everything (retriever.py:204-205)
@@ -82,11 +94,11 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
     return;  // uniform across the cluster
   }
   const int64_t ncand = n - n_local;
-  const int64_t chunk = ((ncand + SC_CTAS - 1) / SC_CTAS + 7) & ~int64_t(7);
+  const int64_t chunk = ((ncand + CTAS - 1) / CTAS + 7) & ~int64_t(7);
   const int64_t j0 = rank * chunk;
   const int m = (int)(j0 < ncand ? imin64(chunk, ncand - j0) : 0);
-  uint64_t *keys = reinterpret_cast<uint64_t *>(smem);
-  uint8_t *flags = smem + (size_t)SC_CHUNK_CAP * 8;
+  uint64_t *keys = S.keys;
+  uint8_t *flags = S.flags;
 
   for (int i = tid; i < d_s; i += blockDim.x) {
     const int ch = channels[(size_t)u * d_s + i];
@@ -98,6 +110,7 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
   __syncthreads();
   // ---- scores: 8 consecutive tokens per thread, 16-byte loads per channel row ----
   const uint16_t *kt = s.kt + (size_t)u * s.d * s.capacity;
+  unsigned long long lo = ~0ull, hi = 0ull;
   for (int e0 = tid * 8; e0 < m; e0 += SC_THREADS * 8) {
     const int64_t j = j0 + e0;
     double acc[8];
@@ -119,73 +132,98 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       if (e0 + e < m) {
-        keys[e0 + e] = orderable(acc[e]);
+        const unsigned long long k = orderable(acc[e]);
+        keys[e0 + e] = k;
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
         if (scores_out) scores_out[(size_t)u * s.capacity + j + e] = acc[e];
       }
     }
   }
-  if (tid == 0) { sh_prefix = 0; sh_mask = 0; sh_need = n_topk; sh_done = 0; }
+  // ---- the keys' common leading bits (cluster min/max) need no passes ----
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if (lane_id == 0) {
+    kmin_sh[tid >> 5] = lo;
+    kmax_sh[tid >> 5] = hi;
+  }
   __syncthreads();
-  // ---- cluster radix select over the 64-bit keys ----
-  uint64_t prefix = 0, mask = 0;
+  if (tid == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = kmin_sh[w] < lo ? kmin_sh[w] : lo;
+      hi = kmax_sh[w] > hi ? kmax_sh[w] : hi;
+    }
+    ck[0] = lo;
+    ck[1] = hi;
+  }
+  cluster.sync();
+  lo = ~0ull;
+  hi = 0ull;
+  for (int r = 0; r < CTAS; ++r) {
+    const unsigned long long *rk = cluster.map_shared_rank(ck, r);
+    lo = rk[0] < lo ? rk[0] : lo;
+    hi = rk[1] > hi ? rk[1] : hi;
+  }
+  int top = 64 - (lo == hi ? 64 : __clzll((long long)(lo ^ hi)));  // bits [0, top) still undecided
+  uint64_t prefix = top >= 64 ? 0ull : (lo >> top) << top;
   int need = n_topk;
   bool done = false;
-  for (int pass = 0; pass < 8 && !done; ++pass) {
-    const int shift = 56 - 8 * pass;
-    uint32_t *H = hist[pass & 1];
-    if (tid < 256) H[tid] = 0;
+  // ---- cluster radix select with 11-bit digits ----
+  for (int pass = 0; top > 0 && !done; ++pass) {
+    const int w = top < SC_BITS ? top : SC_BITS;
+    const int shift = top - w;
+    const uint64_t mask = top >= 64 ? 0ull : ~0ull << top;
+    const int nb = 1 << w;
+    uint32_t *H = S.hist[pass & 1];
+    for (int i = tid; i < nb; i += blockDim.x) H[i] = 0;
     __syncthreads();
+    const uint32_t dmask = (uint32_t)nb - 1u;
     for (int e = tid; e < m; e += blockDim.x) {
       const uint64_t k = keys[e];
-      if ((k & mask) == prefix) atomicAdd(&H[(uint32_t)(k >> shift) & 255u], 1u);
+      if ((k & mask) == prefix) atomicAdd(&H[(uint32_t)(k >> shift) & dmask], 1u);
     }
     cluster.sync();
-    if (tid < 256) {
+    // totals over the cluster, stored in descending-bin order
+    for (int b = tid; b < nb; b += blockDim.x) {
       uint32_t t = 0;
-      for (int r = 0; r < SC_CTAS; ++r) t += cluster.map_shared_rank(H, r)[tid];
-      tot[tid] = t;
+      for (int r = 0; r < CTAS; ++r) t += cluster.map_shared_rank(H, r)[b];
+      S.tot[nb - 1 - b] = t;
     }
     __syncthreads();
-    if (tid < 32) {
-      // warp-parallel descending scan: lane l owns bins 255-8l-7 .. 255-8l
-      uint32_t v[8];
-      int sum = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i] = tot[255 - 8 * tid - i];
-        sum += (int)v[i];
-      }
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tid >= o) incl += y;
-      }
-      const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
-      const int L = __ffs(hit) - 1;
-      if (tid == L) {
-        int cum = incl - sum, D = 255 - 8 * L;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (cum + (int)v[i] >= need) { D = 255 - 8 * L - i; break; }
-          cum += (int)v[i];
+    // each thread scans two consecutive (descending) bins; block scan finds the crossing
+    int v = 0;
+    for (int p = tid * 2; p < tid * 2 + 2 && p < nb; ++p) v += (int)S.tot[p];
+    int total;
+    const int before = block_excl_scan(v, scan_sh, &total);
+    if (before < need && before + v >= need) {
+      int cum = before;
+      for (int p = tid * 2; p < tid * 2 + 2 && p < nb; ++p) {
+        const int c = (int)S.tot[p];
+        if (cum + c >= need) {
+          const int bin = nb - 1 - p;
+          sh_need = need - cum;
+          sh_prefix = prefix | ((uint64_t)bin << shift);
+          sh_done = c == need - cum;
+          break;
         }
-        sh_need = need - cum;
-        sh_prefix = prefix | ((uint64_t)D << shift);
-        sh_mask = mask | (255ull << shift);
-        sh_done = (int)tot[D] == need - cum;
+        cum += c;
       }
     }
     __syncthreads();
     prefix = sh_prefix;
-    mask = sh_mask;
     need = sh_need;
     done = sh_done;
+    top = shift;
   }
-  // ---- selection flags ----
+  const uint64_t fmask = top >= 64 ? 0ull : ~0ull << top;
+  // ---- selection flags (prefix is the threshold key restricted to fmask) ----
   int ties = 0;
   for (int e = tid; e < m; e += blockDim.x) {
-    const uint64_t k = keys[e] & mask;
+    const uint64_t k = keys[e] & fmask;
     uint8_t f = k > prefix ? 1 : 0;
     if (k == prefix) {
       if (done) f = 1;
@@ -200,7 +238,7 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
     if (tid == 0) cta_count = tot_ties;
     cluster.sync();
     int above = 0;
-    for (int r = rank + 1; r < SC_CTAS; ++r) above += *cluster.map_shared_rank(&cta_count, r);
+    for (int r = rank + 1; r < CTAS; ++r) above += *cluster.map_shared_rank(&cta_count, r);
     const int allowed = max(0, min(tot_ties, need - above));
     // rank of a tie inside this CTA counted from the highest index
     const int per = (m + SC_THREADS - 1) / SC_THREADS;
@@ -232,7 +270,7 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
   for (int r = 0; r < rank; ++r) offset += *cluster.map_shared_rank(&cta_count, r);
   for (int e = b0; e < b1; ++e)
     if (flags[e]) out_idx[offset + pos++] = (int32_t)(j0 + e);
-  if (rank == SC_CTAS - 1) {
+  if (rank == CTAS - 1) {
     for (int i = tid; i < n_local; i += blockDim.x) out_idx[n_topk + i] = (int32_t)(ncand + i);
     if (tid == 0) {
       sel_count[u] = n_topk + n_local;
@@ -242,20 +280,69 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 1)
   cluster.sync();  // no CTA leaves while its shared memory may still be read
 }
 
+static int cluster_ctas() {
+  // 16-CTA clusters when the hardware co-schedules them, else 8 (portable)
+  static int cached = 0;
+  if (cached) return cached;
+  const size_t sm = sizeof(SelShared);
+  cudaFuncSetAttribute(select_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(select_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(select_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16, 1);
+  cfg.blockDim = dim3(SC_THREADS);
+  cfg.dynamicSmemBytes = sm;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 16;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  const char *env = getenv("TKV_SELECT_CLUSTER");
+  if (env && atoi(env) == 8)
+    cached = 8;
+  else if (cudaOccupancyMaxActiveClusters(&nclusters, select_cluster_kernel<16>, &cfg) == cudaSuccess && nclusters > 0)
+    cached = 16;
+  else
+    cached = 8;
+  cudaGetLastError();
+  return cached;
+}
+
 bool select_cluster_ok(const SL &s, int n_local) {
   const int64_t ncand = s.capacity - n_local;
-  const int64_t chunk = ((ncand + SC_CTAS - 1) / SC_CTAS + 7) & ~int64_t(7);
+  const int ctas = cluster_ctas();
+  const int64_t chunk = ((ncand + ctas - 1) / ctas + 7) & ~int64_t(7);
   return chunk <= SC_CHUNK_CAP && s.capacity % 8 == 0;
 }
 
 int select_cluster(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                    int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, double *scores_out,
                    cudaStream_t st) {
-  const size_t sm = (size_t)SC_CHUNK_CAP * 9;
-  cudaFuncSetAttribute(select_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid(SC_CTAS, s.units);
-  select_cluster_kernel<<<grid, SC_THREADS, sm, st>>>(s, queries, G, channels, d_s, n_local, n_topk, sel_idx,
-                                                       n_local + n_topk, sel_count, fetch_count, scores_out);
+  const int ctas = cluster_ctas();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas, s.units);
+  cfg.blockDim = dim3(SC_THREADS);
+  cfg.dynamicSmemBytes = sizeof(SelShared);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ctas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int stride = n_local + n_topk;
+  cudaError_t e;
+  if (ctas == 16)
+    e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<16>, s, queries, G, channels, d_s, n_local, n_topk, sel_idx,
+                           stride, sel_count, fetch_count, scores_out);
+  else
+    e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<8>, s, queries, G, channels, d_s, n_local, n_topk, sel_idx,
+                           stride, sel_count, fetch_count, scores_out);
+  if (e != cudaSuccess) return fail(TKV_ERR_CUDA, std::string("tkv_select_tokens(cluster): ") + cudaGetErrorString(e));
   return check_launch("tkv_select_tokens(cluster)");
 }
 
