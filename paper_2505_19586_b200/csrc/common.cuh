@@ -27,6 +27,16 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 __device__ __forceinline__ double h2d(uint16_t h) { return (double)__half2float(__ushort_as_half(h)); }
+// Exact fp16 -> float64 by bit manipulation (integer pipe, no F2F.F64):
+// normal numbers rebias the exponent (15 -> 1023); zero/subnormals are
+// man * 2^-24 (finite inputs only).
+__device__ __forceinline__ double h2d_fast(uint32_t h) {
+  const uint32_t e = (h >> 10) & 0x1fu, man = h & 0x3ffu;
+  const uint32_t sign = (h & 0x8000u) << 16;
+  const double nrm = __hiloint2double((int)(sign | ((e + 1008u) << 20) | (man << 10)), 0);
+  const double sub = __hiloint2double((int)(sign | 0x3e700000u), 0) * (double)man;  // +-2^-24 * man
+  return e ? nrm : sub;
+}
 
 // float64 -> fp16 bits, round to nearest even (numpy's astype(float16) of a
 // float64); written out because __double2half is not a direct conversion.

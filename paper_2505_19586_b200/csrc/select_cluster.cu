@@ -24,7 +24,7 @@ namespace cg = cooperative_groups;
 namespace tkv {
 
 constexpr int SC_THREADS = 1024;
-constexpr int SC_CHUNK_CAP = 16384;  // keys per CTA (8 B each)
+constexpr int SC_CHUNK_CAP = 18432;  // keys per CTA (8 B each): 8 CTAs cover 147,456 candidates
 constexpr int SC_BITS = 11;
 constexpr int SC_BINS = 1 << SC_BITS;
 
@@ -54,6 +54,17 @@ __device__ __forceinline__ int block_excl_scan(int v, int *sh, int *total) {
   __syncthreads();
   return before;
 }
+
+// phase timestamps of CTA 0 / unit 0 (debug: tkv_debug_select_phases)
+__device__ unsigned long long g_sel_phase[8];
+#define SC_MARK(i)                                                         \
+  do {                                                                     \
+    if (blockIdx.y == 0 && rank == 0 && tid == 0) {                        \
+      unsigned long long t_;                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                \
+      g_sel_phase[i] = t_;                                                 \
+    }                                                                      \
+  } while (0)
 
 struct SelShared {
   uint64_t keys[SC_CHUNK_CAP];
@@ -99,6 +110,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
   const int m = (int)(j0 < ncand ? imin64(chunk, ncand - j0) : 0);
   uint64_t *keys = S.keys;
   uint8_t *flags = S.flags;
+  SC_MARK(0);
 
   for (int i = tid; i < d_s; i += blockDim.x) {
     const int ch = channels[(size_t)u * d_s + i];
@@ -117,14 +129,30 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.0;
     const bool full = e0 + 8 <= m;
-    for (int i = 0; i < d_s; ++i) {
+    int i = 0;
+    if (full) {
+      // issue 8 channel-row loads before using any (HBM latency overlap)
+      for (; i + 8 <= d_s; i += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = __ldg(reinterpret_cast<const uint4 *>(kt + (size_t)chs[i + r] * s.capacity + j));
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double qv = qsum[i + r];
+          const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = fma(h2d_fast((w[e >> 1] >> (16 * (e & 1))) & 0xffffu), qv, acc[e]);
+        }
+      }
+    }
+    for (; i < d_s; ++i) {
       const uint16_t *row = kt + (size_t)chs[i] * s.capacity + j;
       const double qv = qsum[i];
       if (full) {
         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row));
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = fma(h2d((uint16_t)(w[e >> 1] >> (16 * (e & 1)))), qv, acc[e]);
+        for (int e = 0; e < 8; ++e) acc[e] = fma(h2d_fast((w[e >> 1] >> (16 * (e & 1))) & 0xffffu), qv, acc[e]);
       } else {
         for (int e = 0; e < 8 && e0 + e < m; ++e) acc[e] = fma(h2d(row[e]), qv, acc[e]);
       }
@@ -140,6 +168,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
       }
     }
   }
+  SC_MARK(1);
   // ---- the keys' common leading bits (cluster min/max) need no passes ----
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -172,6 +201,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
   uint64_t prefix = top >= 64 ? 0ull : (lo >> top) << top;
   int need = n_topk;
   bool done = false;
+  SC_MARK(2);
   // ---- cluster radix select with 11-bit digits ----
   for (int pass = 0; top > 0 && !done; ++pass) {
     const int w = top < SC_BITS ? top : SC_BITS;
@@ -218,7 +248,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
     need = sh_need;
     done = sh_done;
     top = shift;
+    if (blockIdx.y == 0 && rank == 0 && tid == 0) g_sel_phase[6] = pass + 1;
   }
+  SC_MARK(3);
+  if (blockIdx.y == 0 && rank == 0 && tid == 0) g_sel_phase[7] = 0;
   const uint64_t fmask = top >= 64 ? 0ull : ~0ull << top;
   // ---- selection flags (prefix is the threshold key restricted to fmask) ----
   int ties = 0;
@@ -257,6 +290,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
     cluster.sync();  // cta_count reads complete before reuse
   }
   __syncthreads();
+  SC_MARK(4);
   // ---- ascending output: contiguous ownership + cluster prefix offsets ----
   const int per = (m + SC_THREADS - 1) / SC_THREADS;
   const int b0 = tid * per, b1 = min(m, b0 + per);
@@ -278,6 +312,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
     }
   }
   cluster.sync();  // no CTA leaves while its shared memory may still be read
+  SC_MARK(5);
 }
 
 static int cluster_ctas() {
@@ -301,8 +336,8 @@ static int cluster_ctas() {
   cfg.numAttrs = 1;
   int nclusters = 0;
   const char *env = getenv("TKV_SELECT_CLUSTER");
-  if (env && atoi(env) == 8)
-    cached = 8;
+  if (!env || atoi(env) != 16)
+    cached = 8;  // measured: 16-CTA clusters are slower on B200 (fewer co-resident clusters)
   else if (cudaOccupancyMaxActiveClusters(&nclusters, select_cluster_kernel<16>, &cfg) == cudaSuccess && nclusters > 0)
     cached = 16;
   else
@@ -347,3 +382,7 @@ int select_cluster(const SL &s, const uint16_t *queries, int G, const int32_t *c
 }
 
 }  // namespace tkv
+
+extern "C" int tkv_debug_select_phases(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, tkv::g_sel_phase, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 7;
+}

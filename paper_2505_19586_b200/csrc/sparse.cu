@@ -162,11 +162,11 @@ __global__ void __launch_bounds__(256) stage1_gemv_kernel(const uint16_t *__rest
     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
     double wd[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) wd[e] = h2d((uint16_t)(wv[e >> 1] >> (16 * (e & 1))));
+    for (int e = 0; e < 8; ++e) wd[e] = h2d_fast((wv[e >> 1] >> (16 * (e & 1))) & 0xffffu);
 #pragma unroll
     for (int b = 0; b < S1_BG; ++b) {
       if (b < nb) {
-        const double hv = h2d(hidden[(size_t)(b0 + b) * H + i]);
+        const double hv = h2d_fast(hidden[(size_t)(b0 + b) * H + i]);
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[b][e] = fma(hv, wd[e], acc[b][e]);
       }

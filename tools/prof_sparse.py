@@ -48,3 +48,10 @@ for _ in range(20):
     a.record(); P.stage1_select(hid, w_q, lay.chmax, G, 8); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 print(f"stage1 {m(ts):.1f} us -> {w_q.numel() * 2 / (m(ts) * 1e-6) / 1e9:.0f} GB/s")
+import ctypes as C
+ph = (C.c_ulonglong * 8)()
+lay.select(q, ch, G, cfg, idx, cnt, fc, ws); torch.cuda.synchronize()
+lib.tkv_debug_select_phases(ph)
+t = list(ph)
+print("select phases (us): score %.1f minmax %.1f radix %.1f (passes %d) flags %.1f output %.1f" % (
+    (t[1]-t[0])/1e3, (t[2]-t[1])/1e3, (t[3]-t[2])/1e3, t[6], (t[4]-t[3])/1e3, (t[5]-t[4])/1e3))
