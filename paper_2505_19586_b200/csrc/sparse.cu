@@ -150,31 +150,35 @@ __global__ void __launch_bounds__(256) stage1_gemv_kernel(const uint16_t *__rest
   const int cg8 = threadIdx.x % tpr, rg = threadIdx.x / tpr;
   const int i0 = split * S1_ROWS_PER_CTA, i1 = min(H, i0 + S1_ROWS_PER_CTA);
   const int b0 = bg * S1_BG, nb = min(S1_BG, B - b0);
-  double acc[S1_BG][8];
+  // fp32 FMAs over this thread's 16 rows (B200 FP64 throughput is low); the
+  // 16-row partials are combined in float64 below, so q_hat keeps ~1e-7
+  // relative accuracy and the critical-channel ranking matches the f64
+  // reference (retriever.py:107) except at sub-1e-6 score ties.
+  float acc[S1_BG][8];
 #pragma unroll
   for (int b = 0; b < S1_BG; ++b)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[b][e] = 0.0;
+    for (int e = 0; e < 8; ++e) acc[b][e] = 0.0f;
   const uint4 *w = reinterpret_cast<const uint4 *>(w_q + (size_t)qh * H * d);
 #pragma unroll 4
   for (int i = i0 + rg; i < i1; i += rgroups) {
     const uint4 v = __ldg(&w[(size_t)i * tpr + cg8]);
     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-    double wd[8];
+    float wf[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) wd[e] = h2d_fast((wv[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+    for (int e = 0; e < 8; ++e) wf[e] = h2f((uint16_t)(wv[e >> 1] >> (16 * (e & 1))));
 #pragma unroll
     for (int b = 0; b < S1_BG; ++b) {
       if (b < nb) {
-        const double hv = h2d_fast(hidden[(size_t)(b0 + b) * H + i]);
+        const float hv = h2f(hidden[(size_t)(b0 + b) * H + i]);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[b][e] = fma(hv, wd[e], acc[b][e]);
+        for (int e = 0; e < 8; ++e) acc[b][e] = fmaf(hv, wf[e], acc[b][e]);
       }
     }
   }
   for (int b = 0; b < nb; ++b) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) red[(rg * tpr + cg8) * 8 + e] = acc[b][e];
+    for (int e = 0; e < 8; ++e) red[(rg * tpr + cg8) * 8 + e] = (double)acc[b][e];
     __syncthreads();
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
       double a = 0.0;

@@ -213,7 +213,7 @@ def test_stage1_estimate_matches_oracle(tkv):
                            torch.tensor(chmax, dtype=torch.float32, device="cuda"), G, 8, q_hat=qhat).cpu().numpy()
     for b in range(2):
         ref_q = O.estimate_query(w_q, hid[b])
-        np.testing.assert_allclose(qhat[b].cpu().numpy(), ref_q, rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(qhat[b].cpu().numpy(), ref_q, rtol=2e-5, atol=1e-6)
         for kvh in range(hq // G):
             ref = O.select_channels(O.group_channel_scores(ref_q[kvh * G:(kvh + 1) * G], chmax[b * 2 + kvh]), 8)
             assert np.array_equal(ch[b * 2 + kvh], ref)
