@@ -610,7 +610,9 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
                                                                      const int32_t *__restrict__ sel_count,
                                                                      int n_local, int sel_stride, int keys_from_device,
                                                                      float *__restrict__ pm, float *__restrict__ pl,
-                                                                     float *__restrict__ pacc, int chunks) {
+                                                                     float *__restrict__ pacc, int chunks,
+                                                                     unsigned *__restrict__ arrive,
+                                                                     float *__restrict__ out) {
   constexpr int CPL = D / 32;  // channels per lane
   __shared__ float wm[SA_WARPS][GMAX], wl[SA_WARPS][GMAX];
   __shared__ float wacc[SA_WARPS][GMAX][D];
@@ -804,11 +806,41 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
       pl[base] = L;
     }
   }
+  // ---- the last CTA of this unit merges the split-K partials (fixed order) ----
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int nvalid = (cnt + SA_ROWS - 1) / SA_ROWS;
+    const unsigned prev = atomicAdd(&arrive[u], 1u);
+    last = prev == (unsigned)nvalid - 1;
+    if (last) arrive[u] = 0;  // re-armed for the next launch / graph replay
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nvalid = (cnt + SA_ROWS - 1) / SA_ROWS;
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int h = i / D, c = i % D;
+    const size_t b0 = (size_t)u * chunks * G + h;
+    float M = -INFINITY;
+    for (int ci = 0; ci < nvalid; ++ci) M = fmaxf(M, __ldcg(&pm[b0 + (size_t)ci * G]));
+    float L = 0.0f, A = 0.0f;
+    for (int ci = 0; ci < nvalid; ++ci) {
+      const size_t b = b0 + (size_t)ci * G;
+      const float mm = __ldcg(&pm[b]);
+      if (mm == -INFINITY) continue;
+      const float sc = __expf(mm - M);
+      L += sc * __ldcg(&pl[b]);
+      A += sc * __ldcg(&pacc[b * D + c]);
+    }
+    out[((size_t)u * G + h) * D + c] = A / L;
+  }
 }
 
 int64_t sparse_attn_workspace(int units, int G, int d, int max_rows) {
   const int chunks = (max_rows + SA_ROWS - 1) / SA_ROWS;
-  return (int64_t)units * chunks * G * (2 + d) * 4 + 256;
+  return (int64_t)units * chunks * G * (2 + d) * 4 + (int64_t)units * 4 + 512;
 }
 
 int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t *sel_idx, const int32_t *sel_count,
@@ -817,11 +849,12 @@ int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t 
   float *pm = reinterpret_cast<float *>(ws);
   float *pl = pm + (size_t)s.units * chunks * G;
   float *pacc = pl + (size_t)s.units * chunks * G;
+  unsigned *arrive = reinterpret_cast<unsigned *>(pacc + (size_t)s.units * chunks * G * s.d);
   dim3 grid(chunks, s.units);
   const int stride = max_rows;
 #define TKV_SA(D, GM)                                                                                        \
   sparse_attn_kernel<D, GM><<<grid, SA_WARPS * 32, 0, st>>>(s, queries, G, sel_idx, sel_count, n_local, stride, \
-                                                            keys_from_device, pm, pl, pacc, chunks)
+                                                            keys_from_device, pm, pl, pacc, chunks, arrive, out)
   if (s.d == 128 && G <= 4) TKV_SA(128, 4);
   else if (s.d == 128 && G <= 8) TKV_SA(128, 8);
   else if (s.d == 64 && G <= 8) TKV_SA(64, 8);
@@ -830,7 +863,6 @@ int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t 
   else if (s.d == 256 && G <= 4) TKV_SA(256, 4);
   else return fail(TKV_ERR_PARAMETER, "sparse attention supports d in {32,64,96,128,256} with G<=8 (G<=4 at d=256)");
 #undef TKV_SA
-  launch_combine(pm, pl, pacc, s.units, chunks, G, s.d, sel_count, SA_ROWS, out, st);
   return check_launch("tkv_sparse_attention");
 }
 

@@ -251,7 +251,7 @@ class DecodeEngine:
         """Launches of this library per decode step."""
         q = sum(1 for x in self.labels if x == "q")
         s = len(self.labels) - q
-        return q * 3 + s * 9
+        return q * 3 + s * 5  # q: decode+combine+append; s: 2 stage-1 + select + gather/attend + append
 
     def _run_step(self) -> None:
         main = torch.cuda.current_stream(self.device)
