@@ -160,4 +160,38 @@ __device__ __forceinline__ void val_code_pos(int64_t t, int c, int d, int bits, 
   *bit = 8 * i + k * bits;
 }
 
+// Merge split-K softmax partials of one unit, executed by one whole CTA
+// (the last to finish): m/l [chunk][G], acc [chunk][G][d].  sm must hold
+// 2*G*nvalid floats (G*nvalid <= 1024).  Fixed summation order.
+__device__ __forceinline__ void merge_partials(const float *pm, const float *pl, const float *pacc, int G, int d,
+                                               int nvalid, float *out, float *sm) {
+  float *sc = sm, *ll = sm + G * nvalid;
+  for (int i = threadIdx.x; i < G * nvalid; i += blockDim.x) {
+    sc[i] = __ldcg(&pm[i]);  // i = ci*G + h
+    ll[i] = __ldcg(&pl[i]);
+  }
+  __syncthreads();
+  if (threadIdx.x < G) {
+    const int h = threadIdx.x;
+    float M = -INFINITY;
+    for (int ci = 0; ci < nvalid; ++ci) M = fmaxf(M, sc[ci * G + h]);
+    float L = 0.0f;
+    for (int ci = 0; ci < nvalid; ++ci) {
+      const float m = sc[ci * G + h];
+      const float e = m == -INFINITY ? 0.0f : __expf(m - M);
+      sc[ci * G + h] = e;
+      L += e * ll[ci * G + h];
+    }
+    ll[h] = L;  // reuse slot h (chunk 0 entries are consumed above)
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * d; i += blockDim.x) {
+    const int h = i / d, c = i % d;
+    float A = 0.0f;
+#pragma unroll 8
+    for (int ci = 0; ci < nvalid; ++ci) A += sc[ci * G + h] * __ldcg(&pacc[((size_t)ci * G + h) * d + c]);
+    out[(size_t)h * d + c] = A / ll[h];
+  }
+}
+
 }  // namespace tkv

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(256) quant_decode_simt(QC c, const uint16_t *_
 
 int64_t quant_decode_workspace(const QC &c, int G) {
   const int64_t chunks = (c.capacity + SIMT_CHUNK - 1) / SIMT_CHUNK;
-  return (int64_t)c.units * chunks * G * (2 + c.d) * (int64_t)sizeof(float) + 256;
+  return (int64_t)c.units * chunks * G * (2 + c.d) * (int64_t)sizeof(float) + (int64_t)c.units * 4 + 512;
 }
 
 int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st);

@@ -110,7 +110,9 @@ template <int BITS>
 __global__ void __launch_bounds__(IM_WARPS * 32, 2) quant_decode_imma_kernel(QC c, const uint16_t *__restrict__ queries,
                                                                               int G, float *__restrict__ pm,
                                                                               float *__restrict__ pl,
-                                                                              float *__restrict__ pacc, int chunks) {
+                                                                              float *__restrict__ pacc, int chunks,
+                                                                              unsigned *__restrict__ arrive,
+                                                                              float *__restrict__ out) {
   constexpr int CH = IM_CHUNK / BITS;      // tokens per CTA (16 KB of key codes)
   constexpr int NG = CH / IM_G;            // groups per CTA
   constexpr int KT = 128 / BITS;           // key tile tokens
@@ -457,6 +459,23 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 2) quant_decode_imma_kernel(QC 
       pl[base] = L;
     }
   }
+  if (!arrive) return;  // separate combine kernel
+  // ---- the last CTA of this unit merges the chunk partials (fixed order) ----
+  __shared__ bool last;
+  __syncthreads();
+  const int nvalid = (int)((n + CH - 1) / CH);
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&arrive[u], 1u);
+    last = prev == (unsigned)nvalid - 1;
+    if (last) arrive[u] = 0;  // re-armed for the next launch / graph replay
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const size_t b0 = (size_t)u * chunks * G;
+  merge_partials(pm + b0, pl + b0, pacc + b0 * IM_D, G, IM_D, nvalid, out + (size_t)u * G * IM_D,
+                 &S.u.v.sv[0][0]);
 }
 
 int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st) {
@@ -467,14 +486,22 @@ int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *w
   float *pacc = pl + (size_t)c.units * chunks * G;
   const size_t sm = ((sizeof(ImSmem) + 127) & ~size_t(127)) + sizeof(ImStage);
   dim3 grid(chunks, c.units);
+  // fused last-CTA merge when the partials fit the merge buffer, else a combine kernel
+  const bool fused = (size_t)G * chunks <= 1024;
+  // arrival counters live at the fixed tail of the workspace (the SIMT kernel
+  // uses more partial space, so both implementations can share one workspace)
+  const int64_t ws_bytes = quant_decode_workspace(c, G);
+  unsigned *arrive = fused ? reinterpret_cast<unsigned *>(reinterpret_cast<char *>(ws) + ws_bytes - 512 -
+                                                          (((int64_t)c.units * 4 + 15) & ~int64_t(15)))
+                           : nullptr;
   if (c.bits == 1) {
     cudaFuncSetAttribute(quant_decode_imma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    quant_decode_imma_kernel<1><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks);
+    quant_decode_imma_kernel<1><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks, arrive, out);
   } else {
     cudaFuncSetAttribute(quant_decode_imma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    quant_decode_imma_kernel<2><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks);
+    quant_decode_imma_kernel<2><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks, arrive, out);
   }
-  launch_combine_scalar(pm, pl, pacc, c.units, chunks, G, c.d, c.len, CH, out, st);
+  if (!fused) launch_combine_scalar(pm, pl, pacc, c.units, chunks, G, c.d, c.len, CH, out, st);
   return check_launch("tkv_quant_decode(imma)");
 }
 

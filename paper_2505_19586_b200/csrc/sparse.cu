@@ -820,7 +820,13 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
   if (!last) return;
   __threadfence();
   const int nvalid = (cnt + SA_ROWS - 1) / SA_ROWS;
-  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+  __shared__ float msm[2 * 1024];
+  if (G * nvalid <= 1024) {
+    const size_t b0 = (size_t)u * chunks * G;
+    merge_partials(pm + b0, pl + b0, pacc + b0 * D, G, D, nvalid, out + (size_t)u * G * D, msm);
+    return;
+  }
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {  // very long selections: serial merge
     const int h = i / D, c = i % D;
     const size_t b0 = (size_t)u * chunks * G + h;
     float M = -INFINITY;

@@ -113,7 +113,7 @@ class QuantizedLayerKV:
     def workspace(self, G: int) -> torch.Tensor:
         if G not in self._ws:
             size = _lib.load().tkv_quant_decode_workspace(C.byref(self.struct), G)
-            self._ws[G] = torch.empty(int(size), dtype=torch.uint8, device=self.device)
+            self._ws[G] = torch.zeros(int(size), dtype=torch.uint8, device=self.device)  # arrival counters start at 0
         return self._ws[G]
 
     def decode(self, queries, out: torch.Tensor | None = None, impl: int = 0, stream=None) -> torch.Tensor:
