@@ -487,7 +487,9 @@ int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *w
   const size_t sm = ((sizeof(ImSmem) + 127) & ~size_t(127)) + sizeof(ImStage);
   dim3 grid(chunks, c.units);
   // fused last-CTA merge when the partials fit the merge buffer, else a combine kernel
-  const bool fused = (size_t)G * chunks <= 1024;
+  // measured: one CTA merging 128 chunk partials is slower than the parallel
+  // combine kernel, so the fused merge stays off for the quantized decode
+  const bool fused = false;
   // arrival counters live at the fixed tail of the workspace (the SIMT kernel
   // uses more partial space, so both implementations can share one workspace)
   const int64_t ws_bytes = quant_decode_workspace(c, G);
