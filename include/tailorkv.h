@@ -135,6 +135,7 @@ typedef struct tkv_sparse_layer {
   int32_t *cache_cnt;     /* [2][units] */
   uint16_t *cache_v;      /* [2][units][cache_rows][d] */
   int32_t *cache_cur;     /* device scalar: buffer holding the previous step */
+  int32_t *cache_map;     /* [units][capacity] token -> last cache position (verified on use) */
   unsigned long long *cache_stats; /* [2]: rows served from HBM, rows fetched over PCIe */
 } tkv_sparse_layer;
 

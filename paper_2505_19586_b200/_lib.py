@@ -58,7 +58,7 @@ class SparseLayer(C.Structure):
         ("kt", C.c_void_p), ("chmax", C.c_void_p), ("loc_k", C.c_void_p), ("loc_v", C.c_void_p),
         ("kdev", C.c_void_p), ("host_kv", C.c_void_p), ("len", C.c_void_p), ("ticket", C.c_void_p),
         ("cache_rows", C.c_int32), ("cache_idx", C.c_void_p), ("cache_cnt", C.c_void_p), ("cache_v", C.c_void_p),
-        ("cache_cur", C.c_void_p), ("cache_stats", C.c_void_p),
+        ("cache_cur", C.c_void_p), ("cache_map", C.c_void_p), ("cache_stats", C.c_void_p),
     ]
 
 

@@ -600,7 +600,7 @@ int topk_from_scores(const double *scores, int units, int64_t n, int n_local, in
 // below the local window are read straight from the pinned host store over
 // PCIe (UVA zero-copy), the rest from the device local mirror.
 // ===========================================================================
-constexpr int SA_ROWS = 64;
+constexpr int SA_ROWS = 32;  // rows per CTA (8 per warp): ~5k warps in flight at config 2
 constexpr int SA_WARPS = 4;
 constexpr int SA_RPW = SA_ROWS / SA_WARPS;
 
@@ -642,16 +642,14 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
   }
   int my_pos = -1;
   if (use_cache && lane < SA_RPW) {
+    // token -> cache-position table (no clearing needed: an entry is trusted
+    // only if the previous buffer really holds that token at that position)
     const int r = r0 + warp * SA_RPW + lane;
     if (r < cnt) {
       const int key = sel_idx[(size_t)u * sel_stride + r];
       if (key < local_start) {
-        int lo = 0, hi = pcnt;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (__ldg(&pidx[mid]) < key) lo = mid + 1; else hi = mid;
-        }
-        if (lo < pcnt && __ldg(&pidx[lo]) == key) my_pos = lo;
+        const int pos = s.cache_map[(size_t)u * s.capacity + key];
+        if (pos >= 0 && pos < pcnt && __ldcg(&pidx[pos]) == key) my_pos = pos;
       }
     }
   }
@@ -732,7 +730,10 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
       if (!valid[j] || !fetched[j]) continue;
       const int r = r0 + warp * SA_RPW + j;
       ++nf;
-      if (lane == 0) ci[r] = (int32_t)rowidx[j];
+      if (lane == 0) {
+        ci[r] = (int32_t)rowidx[j];
+        s.cache_map[(size_t)u * s.capacity + rowidx[j]] = r;
+      }
       if constexpr (CPL == 4) {
         *reinterpret_cast<uint2 *>(cv + (size_t)r * D + lane * 4) = make_uint2(vw[j][0], vw[j][1]);
       } else {

@@ -98,15 +98,17 @@ class OffloadedLayerKV:
             self.cache_cnt = torch.zeros((2, units), dtype=torch.int32, device=dev)
             self.cache_v = torch.zeros((2, units, self.cache_rows, d), dtype=torch.float16, device=dev)
             self.cache_cur = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.cache_map = torch.full((units, self.capacity), -1, dtype=torch.int32, device=dev)
             self.cache_stats = torch.zeros(2, dtype=torch.int64, device=dev)
         else:
             self.cache_idx = self.cache_cnt = self.cache_v = self.cache_cur = self.cache_stats = None
+            self.cache_map = None
         self.struct = SparseLayer(units, d, self.capacity, self.local_offset, self.local_capacity,
                                   self.kt.data_ptr(), self.chmax.data_ptr(), self.loc_k.data_ptr(),
                                   self.loc_v.data_ptr(), ptr(self.kdev), self.arena.addr,
                                   self._len.data_ptr(), self._len.data_ptr() + 4,
                                   self.cache_rows, ptr(self.cache_idx), ptr(self.cache_cnt), ptr(self.cache_v),
-                                  ptr(self.cache_cur), ptr(self.cache_stats))
+                                  ptr(self.cache_cur), ptr(self.cache_map), ptr(self.cache_stats))
 
     @property
     def keys_on_device(self) -> bool:
