@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--keys-over-pcie", action="store_true",
                     help="headline with K and V rows both gathered over PCIe (the reference's fetch_topk transfer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="sparse layers as two launches (select, gather+attend)")
     ap.add_argument("--seed", type=int, default=2505)
     return ap.parse_args()
 
@@ -270,7 +271,7 @@ def main():
     L, n = model.num_layers, args.ctx
     n_topk = round(args.topk_frac * n)
     cfg = P.EngineConfig(bits=1, group_size=64, n_local=64, n_topk=n_topk, critical_channels=8,
-                         keys_from_hbm=not args.keys_over_pcie)
+                         keys_from_hbm=not args.keys_over_pcie, fused_sparse=not args.unfused)
     W, K = args.warmup, args.steps
     PROF = 2
     total = W + 3 * K + 2 * PROF + 4
@@ -290,26 +291,29 @@ def main():
     def inputs(t):
         return wl.hidden[t], wl.queries[t], wl.new_keys[t], wl.new_values[t]
 
-    # per-kernel profile (eager, events around each kernel group)
+    # per-kernel profile: the step graph captured with an event-record node
+    # around every kernel group, replayed like the timed graph (no host gaps)
     def profile_mode(from_hbm):
         nonlocal step_i
         eng.keys_from_hbm = from_hbm
-        eng.step(*inputs(step_i)); step_i += 1  # settle the row cache in this mode
+        eng.capture_profiled()
+        eng.load_step(*inputs(step_i)); eng.replay_profiled(); step_i += 1  # settle the row cache in this mode
         res = {}
+        c0 = eng.cache_counters()
         for _ in range(PROF):
-            for k, v in eng.step_profiled(*inputs(step_i)).items():
+            eng.load_step(*inputs(step_i))
+            for k, v in eng.replay_profiled().items():
                 res.setdefault(k, []).extend(v)
             step_i += 1
-        return res
+        c1 = eng.cache_counters()
+        return res, c1[0] - c0[0], c1[1] - c0[1]
 
-    prof_alt = profile_mode(args.keys_over_pcie)  # the other key-row source
-    h0, m0 = eng.cache_counters()
-    prof = profile_mode(not args.keys_over_pcie)
-    h1, m1 = eng.cache_counters()
+    prof_alt, _, _ = profile_mode(args.keys_over_pcie)  # the other key-row source
+    prof, hits, misses = profile_mode(not args.keys_over_pcie)
     n_sparse = sum(1 for x in wl.labels if x == "s")
     fetch_rows = int(eng.fetch_count.sum().item())
-    cached_rows = (h1 - h0) / (PROF * n_sparse)   # per gather launch, served from the HBM row cache
-    pcie_rows = (m1 - m0) / (PROF * n_sparse)      # per gather launch, fetched over PCIe
+    cached_rows = hits / (PROF * n_sparse)     # per launch, served from the HBM row cache
+    pcie_rows = misses / (PROF * n_sparse)     # per launch, fetched over PCIe
 
     # variant: the other key-row source, graph-timed for K steps
     eng.keys_from_hbm = args.keys_over_pcie
@@ -367,48 +371,60 @@ def main():
         ms, ms_e2e = t.tolist()
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_key = next((k for k in peaks if "hbm" in k.lower() and isinstance(peaks[k], (int, float))), None)
+    hbm_peak = float(peaks[hbm_key]) if hbm_key else 6552.0
+    hbm_src = f"MEASURED_PEAKS.json:{hbm_key}" if hbm_key else "BASELINE.md measured copy peak (MEASURED_PEAKS.json absent)"
     memcpy_gbs, uva_gbs, uva256_gbs = pcie_peaks(torch, _lib, device)
 
     def mean(x):
         return sum(x) / len(x) if x else float("nan")
 
     U = eng.units
-    gather_ms = mean(prof.get("gather_attend", []))
     quant_ms = mean(prof.get("quant_decode", []))
-    select_ms = mean(prof.get("select", []))
     stage1_ms = mean(prof.get("stage1", []))
+    if args.unfused:
+        sparse_ms = mean(prof.get("select", [])) + mean(prof.get("gather_attend", []))
+        alt_ms = mean(prof_alt.get("select", [])) + mean(prof_alt.get("gather_attend", []))
+    else:
+        sparse_ms = mean(prof.get("sparse_decode", []))
+        alt_ms = mean(prof_alt.get("sparse_decode", []))
+    append_ms = mean(prof.get("sparse_append", []))
     from oracle import tailorkv_oracle as O  # byte formulas only (memsim.py accounting)
-    # PCIe bytes of one gather launch: K+V rows (memsim.py:249, no row cache) or, in the
+    d = model.head_dim
+    # PCIe bytes of one sparse-layer launch: K+V rows (memsim.py:249, no row cache) or, in the
     # default mode, the value rows that missed the HBM row cache (counted by the kernel)
-    gather_bytes = (O.gather_bytes(fetch_rows, model.head_dim) if args.keys_over_pcie
-                    else int(pcie_rows * model.head_dim * 2))
-    alt_bytes = O.gather_bytes(fetch_rows, model.head_dim) if not args.keys_over_pcie else fetch_rows * model.head_dim * 2
-    alt_ms = mean(prof_alt.get("gather_attend", []))
-    quant_bytes = O.quant_layer_bytes(n, U, model.head_dim, 1, 64)
+    gather_bytes = O.gather_bytes(fetch_rows, d) if args.keys_over_pcie else int(pcie_rows * d * 2)
+    alt_bytes = O.gather_bytes(fetch_rows, d) if not args.keys_over_pcie else fetch_rows * d * 2
+    quant_bytes = O.quant_layer_bytes(n, U, d, 1, 64)
     scorer_bytes = O.scorer_bytes(n, U, 8)
-    wq_bytes = eng.hq_r * model.hidden_dim * model.head_dim * 2
+    # HBM bytes of the same launch: scorer columns + key rows (+ cached value rows)
+    sparse_hbm = scorer_bytes + (0 if args.keys_over_pcie else int(fetch_rows * d * 2 + cached_rows * d * 2))
+    wq_bytes = eng.hq_r * model.hidden_dim * d * 2
     rooflines = {
-        "gather_attend": {"bound": "pcie", "achieved": gather_bytes / (gather_ms * 1e-3) / 1e9,
-                          "peak": memcpy_gbs, "unit": "GB/s", "ms": gather_ms, "bytes": gather_bytes,
-                          "peak_source": "measured pinned cudaMemcpyAsync H2D 256 MiB, this run"},
+        "sparse_decode": {"bound": "pcie", "achieved": gather_bytes / (sparse_ms * 1e-3) / 1e9,
+                          "peak": memcpy_gbs, "unit": "GB/s", "ms": sparse_ms, "bytes": gather_bytes,
+                          "hbm_bytes": sparse_hbm, "hbm_gbs": sparse_hbm / (sparse_ms * 1e-3) / 1e9,
+                          "peak_source": "measured pinned cudaMemcpyAsync H2D 256 MiB, this run",
+                          "kernel": "sparse_fused_kernel (scores + top-k + gather + attention)" if not args.unfused
+                          else "select + sparse_attn"},
         "quant_decode": {"bound": "hbm", "achieved": quant_bytes / (quant_ms * 1e-3) / 1e9, "peak": hbm_peak,
-                         "unit": "GB/s", "ms": quant_ms, "bytes": quant_bytes, "peak_source": "MEASURED_PEAKS.json"},
-        "select(scorer+topk)": {"bound": "hbm", "achieved": scorer_bytes / (select_ms * 1e-3) / 1e9, "peak": hbm_peak,
-                                "unit": "GB/s", "ms": select_ms, "bytes": scorer_bytes},
+                         "unit": "GB/s", "ms": quant_ms, "bytes": quant_bytes, "peak_source": hbm_src},
         "stage1": {"bound": "hbm", "achieved": wq_bytes / (stage1_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                   "ms": stage1_ms, "bytes": wq_bytes},
+                   "ms": stage1_ms, "bytes": wq_bytes, "peak_source": hbm_src},
+        "sparse_append": {"ms": append_ms},
     }
     for r in rooflines.values():
-        r["frac"] = r["achieved"] / r["peak"]
-    dom = rooflines["gather_attend"]
+        if "achieved" in r:
+            r["frac"] = r["achieved"] / r["peak"]
+    dom = rooflines["sparse_decode"]
     line = {
         "metric": METRIC, "value": ms, "unit": "ms/token", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "fp16 storage / 1-bit codes, fp32 accumulate", "data": "synthetic (gen_trace-shaped, GPU-generated)",
         "config": workload_config(args, n_topk),
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
-                     "frac": dom["frac"], "traffic": None, "kernel": "sparse_attn_kernel (UVA gather + attention)"},
+                     "frac": dom["frac"], "traffic": None, "kernel": dom["kernel"],
+                     "timing": "CUDA events recorded as graph nodes around the kernel inside the replayed step"},
         "rooflines": rooflines,
         "row_cache": {"rows_per_gather_from_hbm_cache": cached_rows, "rows_per_gather_over_pcie": pcie_rows,
                       "hit_rate": cached_rows / max(1.0, cached_rows + pcie_rows),
@@ -418,8 +434,8 @@ def main():
                  "reference_fetch_topk_bytes_per_token": O.gather_bytes(fetch_rows, model.head_dim) * n_sparse},
         "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",
-                    "ms_per_token": ms_variant, "gather_ms": alt_ms,
-                    "gather_pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "gather_bytes": alt_bytes},
+                    "ms_per_token": ms_variant, "sparse_decode_ms": alt_ms,
+                    "pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "pcie_bytes": alt_bytes},
         "gpu_launches": eng.kernels_per_step() * K,
         "clocks": clocks.summary(),
         "setup_s": setup_s,

@@ -41,6 +41,10 @@ enum {
 /* Last error message of the calling thread ("" when none). */
 const char *tkv_last_error(void);
 int tkv_abi_version(void);
+/* Record a CUDA event on a stream; external != 0 makes the record a node of a
+ * graph being captured on that stream (cudaEventRecordExternal), so kernels
+ * can be timed inside a replayed decode-step graph. */
+int tkv_event_record(void *event, void *stream, int32_t external);
 
 /* ------------------------------------------------------------------------
  * Quantized layer cache (quantizer.py:187-497)
@@ -184,6 +188,18 @@ int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int
                          const int32_t *sel_count, int32_t n_local, int32_t max_rows, int32_t keys_from_device,
                          float *out, void *workspace, void *stream);
 
+/* One decode step of a sparsity-friendly layer in ONE launch (replaces
+ * pipeline.py:351-376: approx_scores retriever.py:166-189 + select_topk_tokens
+ * :192-211 + fetch_topk memsim.py:228-252 + sparse attention): proxy scores,
+ * exact top-k plus the local window, gather (value rows over PCIe or from the
+ * HBM row cache, key rows from HBM when keys_from_device != 0) and exact
+ * softmax attention.  Outputs are those of tkv_select_tokens followed by
+ * tkv_sparse_attention; `workspace` >= tkv_sparse_decode_workspace bytes (used
+ * only by shapes outside the fused kernel). */
+int64_t tkv_sparse_decode_workspace(int32_t units, int64_t capacity, int32_t G, int32_t d, int32_t max_rows);
+int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
+                      int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
+                      int32_t *fetch_count, int32_t keys_from_device, float *out, void *workspace, void *stream);
 /* Pinned, NUMA-local host arena for the KV store (memsim.py:76-135).  numa_node
  * < 0 leaves placement to the OS.  Returns a host pointer usable by kernels
  * (UVA) or NULL. */

@@ -68,6 +68,7 @@ _I64 = C.c_int64
 _SIGS = {
     "tkv_last_error": (C.c_char_p, []),
     "tkv_abi_version": (C.c_int, []),
+    "tkv_event_record": (C.c_int, [_P, _P, _I32]),
     "tkv_qcache_sizes": (C.c_int, [_I32, _I32, _I32, _I32, _I64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "tkv_qcache_pack": (C.c_int, [C.POINTER(QCache), _P, _P, _I64, _I32, _P]),
     "tkv_qcache_append": (C.c_int, [C.POINTER(QCache), _P, _P, _P]),
@@ -87,6 +88,9 @@ _SIGS = {
     "tkv_topk_from_scores": (C.c_int, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P]),
     "tkv_sparse_attn_workspace": (C.c_int64, [_I32, _I32, _I32, _I32]),
     "tkv_sparse_attention": (C.c_int, [C.POINTER(SparseLayer), _P, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
+    "tkv_sparse_decode_workspace": (C.c_int64, [_I32, _I64, _I32, _I32, _I32]),
+    "tkv_sparse_decode": (C.c_int, [C.POINTER(SparseLayer), _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P,
+                                    _P]),
     "tkv_host_store_create": (C.c_void_p, [C.c_size_t, _I32]),
     "tkv_host_store_destroy": (C.c_int, [_P, C.c_size_t]),
     "tkv_uva_read_probe": (C.c_int, [_P, C.c_size_t, _I32, _P, _I32, _P, _P]),

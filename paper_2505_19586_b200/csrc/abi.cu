@@ -51,6 +51,14 @@ extern "C" {
 const char *tkv_last_error(void) { return g_err.c_str(); }
 int tkv_abi_version(void) { return 1; }
 
+int tkv_event_record(void *event, void *stream, int32_t external) {
+  const cudaError_t e = external ? cudaEventRecordWithFlags(static_cast<cudaEvent_t>(event), as_stream(stream),
+                                                            cudaEventRecordExternal)
+                                 : cudaEventRecord(static_cast<cudaEvent_t>(event), as_stream(stream));
+  if (e != cudaSuccess) return fail(TKV_ERR_CUDA, std::string("tkv_event_record: ") + cudaGetErrorString(e));
+  return TKV_OK;
+}
+
 int tkv_qcache_sizes(int32_t units, int32_t d, int32_t bits, int32_t g, int64_t capacity, int64_t sizes[6],
                      int32_t *tile) {
   tkv_qcache c{};
@@ -170,6 +178,31 @@ int tkv_topk_from_scores(const double *scores, int32_t units, int64_t n, int32_t
   TKV_REQUIRE(n >= 1, TKV_ERR_EMPTY_CACHE, "token selection over an empty cache");
   TKV_REQUIRE(n_local >= 0 && n_topk >= 1, TKV_ERR_PARAMETER, "token budgets out of range");
   return topk_from_scores(scores, units, n, n_local, n_topk, sel_idx, sel_count, workspace, as_stream(stream));
+}
+
+int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
+                      int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
+                      int32_t *fetch_count, int32_t keys_from_device, float *out, void *workspace, void *stream) {
+  if (int r = validate_sparse(s)) return r;
+  TKV_REQUIRE(n_local >= 0 && n_local <= 4096, TKV_ERR_PARAMETER, "n_local must lie in [0, 4096]");
+  TKV_REQUIRE(n_topk >= 1, TKV_ERR_PARAMETER, "n_topk must be >= 1");
+  TKV_REQUIRE(d_s >= 1 && d_s <= s->d && d_s <= 128, TKV_ERR_PARAMETER, "d_s must lie in [1, min(head_dim,128)]");
+  TKV_REQUIRE(G >= 1 && G <= 8, TKV_ERR_SHAPE, "group size must lie in [1, 8]");
+  if (sparse_decode_supported(*s, G, n_local))
+    return sparse_decode_fused(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
+                               keys_from_device, out, as_stream(stream));
+  // shapes outside the fused kernel: select, then gather + attention (two launches)
+  char *ws = static_cast<char *>(workspace);
+  const int64_t sel_ws = (select_workspace(s->units, s->capacity) + 255) / 256 * 256;
+  if (int r = select_tokens(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, nullptr,
+                            ws, as_stream(stream)))
+    return r;
+  return sparse_attention(*s, queries, G, sel_idx, sel_count, n_local, n_local + n_topk, keys_from_device, out,
+                          ws + sel_ws, as_stream(stream));
+}
+
+int64_t tkv_sparse_decode_workspace(int32_t units, int64_t capacity, int32_t G, int32_t d, int32_t max_rows) {
+  return (select_workspace(units, capacity) + 255) / 256 * 256 + sparse_attn_workspace(units, G, d, max_rows);
 }
 
 int64_t tkv_sparse_attn_workspace(int32_t units, int32_t G, int32_t d, int32_t max_rows) {

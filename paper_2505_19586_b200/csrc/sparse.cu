@@ -137,75 +137,21 @@ int sparse_append(const SL &s, const uint16_t *nk, const uint16_t *nv, cudaStrea
 constexpr int S1_ROWS_PER_CTA = 256;
 constexpr int S1_BG = 4;  // sequences per CTA
 
-// grid (splits, hq, ceil(B/4)); each thread owns 8 channels (one 16-byte load
-// per W_q row) of 16 rows in flight; float64 accumulation.
-__global__ void __launch_bounds__(256) stage1_gemv_kernel(const uint16_t *__restrict__ hidden,
-                                                           const uint16_t *__restrict__ w_q, int B, int H, int d,
-                                                           double *__restrict__ part) {
-  __shared__ double red[256 * 8];
-  const int qh = blockIdx.y, split = blockIdx.x, bg = blockIdx.z;
-  const int hq = gridDim.y;
-  const int tpr = d / 8;                 // threads per row
-  const int rgroups = blockDim.x / tpr;  // rows in flight
-  const int cg8 = threadIdx.x % tpr, rg = threadIdx.x / tpr;
-  const int i0 = split * S1_ROWS_PER_CTA, i1 = min(H, i0 + S1_ROWS_PER_CTA);
-  const int b0 = bg * S1_BG, nb = min(S1_BG, B - b0);
-  // fp32 FMAs over this thread's 16 rows (B200 FP64 throughput is low); the
-  // 16-row partials are combined in float64 below, so q_hat keeps ~1e-7
-  // relative accuracy and the critical-channel ranking matches the f64
-  // reference (retriever.py:107) except at sub-1e-6 score ties.
-  float acc[S1_BG][8];
-#pragma unroll
-  for (int b = 0; b < S1_BG; ++b)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[b][e] = 0.0f;
-  const uint4 *w = reinterpret_cast<const uint4 *>(w_q + (size_t)qh * H * d);
-#pragma unroll 4
-  for (int i = i0 + rg; i < i1; i += rgroups) {
-    const uint4 v = __ldg(&w[(size_t)i * tpr + cg8]);
-    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-    float wf[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) wf[e] = h2f((uint16_t)(wv[e >> 1] >> (16 * (e & 1))));
-#pragma unroll
-    for (int b = 0; b < S1_BG; ++b) {
-      if (b < nb) {
-        const float hv = h2f(hidden[(size_t)(b0 + b) * H + i]);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[b][e] = fmaf(hv, wf[e], acc[b][e]);
-      }
-    }
-  }
-  for (int b = 0; b < nb; ++b) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) red[(rg * tpr + cg8) * 8 + e] = (double)acc[b][e];
-    __syncthreads();
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-      double a = 0.0;
-      for (int r = 0; r < rgroups; ++r) a += red[(r * tpr + c / 8) * 8 + (c & 7)];
-      part[(((size_t)split * B + b0 + b) * hq + qh) * d + c] = a;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(256) stage1_select_kernel(const double *__restrict__ part, int splits, int B, int hq,
-                                                             int d, int G, const float *__restrict__ chmax, int d_s,
-                                                             double *__restrict__ q_hat,
-                                                             int32_t *__restrict__ channels) {
-  // one CTA per unit (b, kvh)
-  __shared__ double qs[16 * 256];
-  __shared__ double score[256];
-  __shared__ int flags[256];
-  const int u = blockIdx.x;
+// Channel selection of one unit (b, kvh) from the split partials:
+// q_hat = sum over splits (float64), s_c = (sum_group |q_hat_c|) * chmax_c,
+// top d_s with ties to the lower index, ascending (retriever.py:111-163).
+__device__ void stage1_select_unit(const double *__restrict__ part, int splits, int B, int hq, int d, int G,
+                                   const float *__restrict__ chmax, int d_s, double *__restrict__ q_hat,
+                                   int32_t *__restrict__ channels, int b, int kvh, double *qs, double *score,
+                                   int *flags) {
   const int hkv = hq / G;
-  const int b = u / hkv, kvh = u % hkv;
+  const int u = b * hkv + kvh;
   for (int p = threadIdx.x; p < G * d; p += blockDim.x) {
     const int j = p / d, c = p % d;
     const int qh = kvh * G + j;
     double q = 0.0;
 #pragma unroll 8
-    for (int sp = 0; sp < splits; ++sp) q += part[(((size_t)sp * B + b) * hq + qh) * d + c];
+    for (int sp = 0; sp < splits; ++sp) q += __ldcg(&part[(((size_t)sp * B + b) * hq + qh) * d + c]);
     qs[p] = q;
     if (q_hat) q_hat[((size_t)b * hq + qh) * d + c] = q;
   }
@@ -235,20 +181,159 @@ __global__ void __launch_bounds__(256) stage1_select_kernel(const double *__rest
     for (int j = 0; j < c; ++j) pos += flags[j];
     channels[(size_t)u * d_s + pos] = c;
   }
+  __syncthreads();
+}
+
+// 16-byte read-only load kept where it is written (issued before the
+// barrier that follows, so all of a thread's W_q loads are in flight at once)
+__device__ __forceinline__ uint4 s1_ld_nc_v4(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// grid (splits, hq, ceil(B/4)) sized to one wave (2 CTAs of 512 threads per
+// SM), D/8 threads per W_q row (8 channels = one 16-byte load each); every
+// thread issues its rows' loads in two batches of 8 before any use.  fp32
+// FMAs over a thread's rows, float64 from there on, so q_hat keeps ~1e-7
+// relative accuracy and the critical-channel ranking matches the float64
+// reference (retriever.py:107) except at sub-1e-6 score ties.  The last CTA
+// of each (sequence group, KV head) runs the channel selection (no second
+// launch).
+constexpr int S1_THREADS = 512;
+template <int D, int BG>
+__global__ void __launch_bounds__(S1_THREADS, 2) stage1_fused_kernel(const uint16_t *__restrict__ hidden,
+                                                                  const uint16_t *__restrict__ w_q, int B, int H,
+                                                                  int rows_per_cta, double *__restrict__ part,
+                                                                  unsigned *__restrict__ arrive, int G,
+                                                                  const float *__restrict__ chmax, int d_s,
+                                                                  double *__restrict__ q_hat,
+                                                                  int32_t *__restrict__ channels) {
+  constexpr int TPR = D / 8;               // threads per row
+  constexpr int RG = S1_THREADS / TPR;     // row groups
+  constexpr int BATCH = 8;                 // loads in flight per thread and batch
+  __shared__ float hs[BG][1024];
+  __shared__ float red[S1_THREADS * 8];
+  __shared__ bool last;
+  const int qh = blockIdx.y, split = blockIdx.x, bg = blockIdx.z;
+  const int hq = gridDim.y, splits = gridDim.x;
+  const int cg8 = threadIdx.x % TPR, rg = threadIdx.x / TPR;
+  const int i0 = split * rows_per_cta, nrow = min(rows_per_cta, H - i0);
+  const int b0 = bg * BG, nb = min(BG, B - b0);
+  const uint4 *w = reinterpret_cast<const uint4 *>(w_q + ((size_t)qh * H + i0) * D);
+  uint4 v[BATCH];
+#pragma unroll
+  for (int k = 0; k < BATCH; ++k) {
+    const int i = rg + RG * k;
+    if (i < nrow) v[k] = s1_ld_nc_v4(&w[(size_t)i * TPR + cg8]);
+  }
+  for (int t = threadIdx.x; t < BG * rows_per_cta; t += blockDim.x) {
+    const int b = t / rows_per_cta, i = t % rows_per_cta;
+    hs[b][i] = (b < nb && i < nrow) ? h2f(hidden[(size_t)(b0 + b) * H + i0 + i]) : 0.0f;
+  }
+  __syncthreads();
+  float acc[BG][8];
+#pragma unroll
+  for (int b = 0; b < BG; ++b)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[b][e] = 0.0f;
+  for (int k0 = 0; k0 * RG < nrow; k0 += BATCH) {
+    if (k0 > 0) {  // next batch (the first one was issued before the barrier)
+#pragma unroll
+      for (int k = 0; k < BATCH; ++k) {
+        const int i = rg + RG * (k0 + k);
+        if (i < nrow) v[k] = s1_ld_nc_v4(&w[(size_t)i * TPR + cg8]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < BATCH; ++k) {
+      const int i = rg + RG * (k0 + k);
+      if (i >= nrow) break;
+      const uint32_t wv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+      float wf[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) wf[e] = h2f((uint16_t)(wv[e >> 1] >> (16 * (e & 1))));
+#pragma unroll
+      for (int b = 0; b < BG; ++b) {
+        const float hv = hs[b][i];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[b][e] = fmaf(hv, wf[e], acc[b][e]);
+      }
+    }
+  }
+  for (int b = 0; b < nb; ++b) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[(rg * TPR + cg8) * 8 + e] = acc[b][e];
+    __syncthreads();
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      double a = 0.0;
+#pragma unroll 8
+      for (int r = 0; r < RG; ++r) a += (double)red[(r * TPR + c / 8) * 8 + (c & 7)];
+      part[(((size_t)split * B + b0 + b) * hq + qh) * D + c] = a;
+    }
+    __syncthreads();
+  }
+  // last arriving CTA of (sequence group, KV head) selects the channels
+  const int kvh = qh / G, hkv = hq / G;
+  unsigned *ctr = arrive + (size_t)bg * hkv + kvh;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(ctr, 1u);
+    last = prev == (unsigned)(splits * G) - 1;
+    if (last) *ctr = 0;  // re-armed for the next launch / graph replay
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double *qs = reinterpret_cast<double *>(red);  // G*D <= 2048 doubles
+  __shared__ double score[256];
+  __shared__ int flags[256];
+  for (int b = 0; b < nb; ++b)
+    stage1_select_unit(part, splits, B, hq, D, G, chmax, d_s, q_hat, channels, b0 + b, kvh, qs, score, flags);
+}
+
+static int stage1_splits(int hq, int H) {
+  // one wave: 2 CTAs per SM; splits a multiple of 8 rows, at most 1024 rows each
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int splits = (2 * sms) / hq;
+  splits = max(splits, (H + 1023) / 1024);
+  splits = max(1, min(splits, (H + 7) / 8));
+  return splits;
 }
 
 int64_t stage1_workspace(int B, int hq, int H, int d) {
-  const int splits = (H + S1_ROWS_PER_CTA - 1) / S1_ROWS_PER_CTA;
-  return (int64_t)splits * B * hq * d * 8 + 256;
+  const int splits = stage1_splits(hq, H);
+  const int64_t part = (int64_t)splits * B * hq * d * 8;
+  return (part + 255) / 256 * 256 + (int64_t)((B + S1_BG - 1) / S1_BG) * hq * 4 + 256;
 }
 
 int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, int d, int G, const float *chmax,
            int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st) {
-  if (G > 16) return fail(TKV_ERR_SHAPE, "stage 1 supports at most 16 query heads per KV head");
-  const int splits = (H + S1_ROWS_PER_CTA - 1) / S1_ROWS_PER_CTA;
+  if (G > 16 || G * d > 2048) return fail(TKV_ERR_SHAPE, "stage 1 supports G*head_dim <= 2048 (G <= 16)");
+  const int splits = stage1_splits(hq, H);
+  const int rows = ((H + splits - 1) / splits + 7) / 8 * 8;
+  if (rows > 1024) return fail(TKV_ERR_SHAPE, "stage 1: hidden size too large for the split plan");
   double *part = reinterpret_cast<double *>(ws);
-  stage1_gemv_kernel<<<dim3(splits, hq, (B + S1_BG - 1) / S1_BG), 256, 0, st>>>(hidden, w_q, B, H, d, part);
-  stage1_select_kernel<<<B * (hq / G), 256, 0, st>>>(part, splits, B, hq, d, G, chmax, d_s, q_hat, channels);
+  const int64_t pbytes = ((int64_t)splits * B * hq * d * 8 + 255) / 256 * 256;
+  unsigned *arrive = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + pbytes);
+  const int bg = B == 1 ? 1 : S1_BG;
+  const dim3 grid((H + rows - 1) / rows, hq, (B + bg - 1) / bg);
+#define TKV_S1(DD)                                                                                               \
+  (B == 1 ? stage1_fused_kernel<DD, 1><<<grid, S1_THREADS, 0, st>>>(hidden, w_q, B, H, rows, part, arrive, G, chmax, \
+                                                                   d_s, q_hat, channels)                         \
+          : stage1_fused_kernel<DD, S1_BG><<<grid, S1_THREADS, 0, st>>>(hidden, w_q, B, H, rows, part, arrive, G,   \
+                                                                       chmax, d_s, q_hat, channels))
+  switch (d) {
+    case 128: TKV_S1(128); break;
+    case 64: TKV_S1(64); break;
+    case 256: TKV_S1(256); break;
+    case 32: TKV_S1(32); break;
+    default: return fail(TKV_ERR_SHAPE, "stage 1 supports head_dim in {32, 64, 128, 256}");
+  }
+#undef TKV_S1
   return check_launch("tkv_stage1");
 }
 

@@ -1,0 +1,1237 @@
+// One launch per sparsity-friendly layer: proxy scores (retriever.py:166-189)
+// -> exact top-k by (score desc, index desc) plus the local window, sorted
+// ascending (retriever.py:192-211) -> gather of the selected rows (value rows
+// over PCIe from the pinned host store, memsim.py:228-252) -> exact softmax
+// attention over them (pipeline.py:364-376).
+//
+// One 8-CTA thread-block cluster per unit (batch x KV head), 1024 threads per
+// CTA.  Each CTA owns a contiguous slice of the candidate tokens:
+//
+// 1. score: fp32 proxy scores of the slice into shared memory as
+//    order-preserving 32-bit keys; min/max in registers;
+// 2. threshold: a 4096-bin linear histogram over [min, max] (no contention,
+//    one pass), per-bin totals reduced across the cluster through distributed
+//    shared memory, then the bin holding the n_topk-th largest score; crowded
+//    bins are refined with a second histogram over the bin's own range;
+// 3. exact band: fp32 scores differ from the reference's float64 scores by at
+//    most eps (a rigorous bound), so every key more than 2 eps
+//    above the threshold bin is selected, every key more than 2 eps below is
+//    not, and the few keys in between are rescored in float64 and ranked
+//    exactly with the reference's tie rule (larger index wins);
+//    degenerate inputs (huge exact-tie sets) take a float64 radix select;
+// 4. output: ascending indices via cluster prefix offsets (sel_idx, counts);
+// 5. (ATTEND) each CTA gathers its own selected rows -- keys from HBM, values
+//    from the step-to-step HBM row cache or over PCIe by zero-copy loads, all
+//    issued before any use -- runs an online softmax per warp, and the
+//    partials are merged in a fixed order: warps in shared memory, CTAs over
+//    DSMEM into rank 0, which writes the head outputs.
+//
+// No intermediate touches global memory except the selection outputs the API
+// returns; the 1 MB of keys of a 128k-token head stays on chip.
+#include <cooperative_groups.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "sparse.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tkv {
+
+constexpr int FZ_CTAS = 8;
+constexpr int FZ_THREADS = 512;
+constexpr int FZ_WARPS = FZ_THREADS / 32;
+constexpr int FZ_CAP = 18432;        // candidate keys per CTA: 8 CTAs cover 147,456 tokens
+constexpr int FZ_NB = 512;           // linear histogram bins per pass
+constexpr int FZ_REFINE = 96;        // refine the threshold bin while it holds more keys (cluster-wide)
+constexpr int FZ_BAND = 256;         // per-CTA cap of float64-rescored band members
+constexpr int FZ_XBITS = 11;         // exact fallback: radix digit
+constexpr int FZ_XBINS = 1 << FZ_XBITS;
+
+__device__ __forceinline__ int fz_block_excl_scan(int v, int *sh, int *total) {
+  // sh: >= 33 ints
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    sh[lane] = s;  // inclusive warp totals
+  }
+  __syncthreads();
+  const int before = (w ? sh[w - 1] : 0) + x - v;
+  if (total) *total = sh[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+// exclusive block scan of a 64-bit value (packed 16-bit fields; no field overflows)
+__device__ __forceinline__ unsigned long long fz_block_excl_scan64(unsigned long long v, unsigned long long *sh,
+                                                                   unsigned long long *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    sh[lane] = t;
+  }
+  __syncthreads();
+  const unsigned long long before = (w ? sh[w - 1] : 0ull) + x - v;
+  *total = sh[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+__device__ __forceinline__ uint32_t fz_orderable32(float x) {
+  if (x == 0.0f) x = 0.0f;
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fz_from_orderable32(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+struct FzCtl {
+  uint32_t kmin, kmax;          // this CTA's min/max orderable key
+  double ksum, ksq;             // this CTA's sum and sum of squares of the fp32 scores
+  int cta_count, band_count, overflow;
+  int bin, inbin, status;       // threshold bin and its keys (cluster-wide); status 0 ok, -1 below, 1 above
+  unsigned long long xprefix;   // exact path
+  int xneed, xdone;
+  unsigned long long xk[2];
+  unsigned long long wk[2][32];
+  double wsum[2][32];
+  int scan[40];
+  unsigned long long scan64[33];
+  int hits, misses;
+  unsigned long long bar;       // mbarrier of the value-row staging
+};
+
+// dynamic shared memory
+constexpr int FZ_UNION = FZ_CAP * 8;  // bytes of the phase-overlaid region (float64 keys of the exact path)
+struct FzShared {
+  union {
+    uint64_t keys64[FZ_CAP];  // exact fallback: order-preserving float64 score keys
+    struct {
+      uint32_t keys32[FZ_CAP];   // fp32 order-preserving keys
+      uint32_t hist[FZ_NB + 4];  // linear bins + [NB] keys above the range
+      uint32_t tot[FZ_NB + 4];   // cluster totals
+      unsigned long long band_key[FZ_BAND];
+      uint32_t band_idx[FZ_BAND];
+      unsigned long long all_key[FZ_BAND * FZ_CTAS];
+      uint32_t all_idx[FZ_BAND * FZ_CTAS];
+    } f;
+    unsigned char raw[FZ_UNION];  // attention phase: staged rows, logits, row list, partials
+  } k;
+  uint8_t flags[FZ_CAP];
+  uint32_t xhist[2][FZ_XBINS];
+  uint32_t xtot[FZ_XBINS];
+  float cta_m[8], cta_l[8];
+  float cta_acc[1024];  // this CTA's merged partial, read by rank 0 over DSMEM
+  float qs[1024];       // queries [G][D] * log2(e)/sqrt(d)
+};
+
+// ---------------------------------------------------------------------------
+// exact fallback (float64 keys): common prefix + 11-bit radix + tie flags
+// ---------------------------------------------------------------------------
+__device__ void fz_common_prefix(cg::cluster_group &cluster, const uint64_t *keys, int m, FzCtl &C, int &top,
+                                 unsigned long long &prefix) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int e = tid; e < m; e += blockDim.x) {
+    const unsigned long long k = keys[e];
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if (lane == 0) {
+    C.wk[0][tid >> 5] = lo;
+    C.wk[1][tid >> 5] = hi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = C.wk[0][w] < lo ? C.wk[0][w] : lo;
+      hi = C.wk[1][w] > hi ? C.wk[1][w] : hi;
+    }
+    C.xk[0] = lo;
+    C.xk[1] = hi;
+  }
+  cluster.sync();
+  lo = ~0ull;
+  hi = 0ull;
+  for (int r = 0; r < FZ_CTAS; ++r) {
+    const FzCtl *R = cluster.map_shared_rank(&C, r);
+    lo = R->xk[0] < lo ? R->xk[0] : lo;
+    hi = R->xk[1] > hi ? R->xk[1] : hi;
+  }
+  const int diff = lo == hi ? 0 : 64 - __clzll((long long)(lo ^ hi));
+  top = diff;
+  prefix = top >= 64 ? 0ull : (lo >> top) << top;
+}
+
+__device__ void fz_radix(cg::cluster_group &cluster, const uint64_t *keys, int m, FzShared &S, FzCtl &C, int &top,
+                         unsigned long long &prefix, int &need, bool &done) {
+  const int tid = threadIdx.x;
+  done = false;
+  for (int pass = 0; top > 0 && !done; ++pass) {
+    const int w = top < FZ_XBITS ? top : FZ_XBITS;
+    const int shift = top - w;
+    const unsigned long long mask = top >= 64 ? 0ull : ~0ull << top;
+    const int nb = 1 << w;
+    uint32_t *H = S.xhist[pass & 1];
+    for (int i = tid; i < nb; i += blockDim.x) H[i] = 0;
+    __syncthreads();
+    const uint32_t dmask = (uint32_t)nb - 1u;
+    for (int e = tid; e < m; e += blockDim.x) {
+      const unsigned long long k = keys[e];
+      if ((k & mask) == prefix) atomicAdd(&H[(uint32_t)(k >> shift) & dmask], 1u);
+    }
+    cluster.sync();
+    for (int b = tid; b < nb; b += blockDim.x) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int r = 0; r < FZ_CTAS; ++r) t += cluster.map_shared_rank(H, r)[b];
+      S.xtot[nb - 1 - b] = t;  // descending-bin order
+    }
+    __syncthreads();
+    const int bpt = (nb + (int)blockDim.x - 1) / (int)blockDim.x;  // bins per thread
+    int v = 0;
+    for (int p2 = tid * bpt; p2 < tid * bpt + bpt && p2 < nb; ++p2) v += (int)S.xtot[p2];
+    int total;
+    const int before = fz_block_excl_scan(v, C.scan, &total);
+    if (before < need && before + v >= need) {
+      int cum = before;
+      for (int p2 = tid * bpt; p2 < tid * bpt + bpt && p2 < nb; ++p2) {
+        const int c = (int)S.xtot[p2];
+        if (cum + c >= need) {
+          C.xneed = need - cum;
+          C.xprefix = prefix | ((unsigned long long)(nb - 1 - p2) << shift);
+          C.xdone = c == need - cum;
+          break;
+        }
+        cum += c;
+      }
+    }
+    __syncthreads();
+    prefix = C.xprefix;
+    need = C.xneed;
+    done = C.xdone;
+    top = shift;
+  }
+}
+
+__device__ void fz_exact_flags(cg::cluster_group &cluster, const uint64_t *keys, int m, uint8_t *flags, FzCtl &C,
+                               int top, unsigned long long prefix, int need, bool done) {
+  const int tid = threadIdx.x;
+  const int rank = (int)cluster.block_rank();
+  const unsigned long long fmask = top >= 64 ? 0ull : ~0ull << top;
+  int ties = 0;
+  for (int e = tid; e < m; e += blockDim.x) {
+    const unsigned long long k = (unsigned long long)keys[e] & fmask;
+    uint8_t f = k > prefix ? 1 : 0;
+    if (k == prefix) {
+      if (done) f = 1;
+      else { f = 2; ++ties; }
+    }
+    flags[e] = f;
+  }
+  if (done) return;
+  int tot_ties;
+  fz_block_excl_scan(ties, C.scan, &tot_ties);
+  if (tid == 0) C.cta_count = tot_ties;
+  cluster.sync();
+  int above = 0;
+  for (int r = rank + 1; r < FZ_CTAS; ++r) above += cluster.map_shared_rank(&C, r)->cta_count;
+  const int allowed = max(0, min(tot_ties, need - above));
+  const int per = (m + FZ_THREADS - 1) / FZ_THREADS;
+  const int b0 = tid * per, b1 = min(m, b0 + per);
+  int mine = 0;
+  for (int e = b0; e < b1; ++e) mine += flags[e] == 2;
+  int dummy;
+  const int before = fz_block_excl_scan(mine, C.scan, &dummy);
+  int higher = tot_ties - before - mine;  // ties at indices above this thread's range
+  for (int e = b1 - 1; e >= b0; --e) {
+    if (flags[e] == 2) {
+      flags[e] = higher < allowed ? 1 : 0;
+      ++higher;
+    }
+  }
+  cluster.sync();  // cta_count reads complete before reuse
+}
+
+__device__ __forceinline__ double fz_exact_score(const uint16_t *kt, int64_t cap, const int *chs, const double *qsum,
+                                                 int d_s, int64_t j) {
+  double sc = 0.0;
+  for (int i = 0; i < d_s; ++i) sc = fma(h2d(kt[(size_t)chs[i] * cap + j]), qsum[i], sc);
+  return sc;
+}
+
+// cluster-wide min/max (orderable keys) and sum / sum of squares of the scores
+__device__ __forceinline__ void fz_cluster_stats(cg::cluster_group &cluster, FzCtl &C, uint32_t lo, uint32_t hi,
+                                                 double sum, double sq, uint32_t &glo, uint32_t &ghi, double &gsum,
+                                                 double &gsq) {
+  const int tid = threadIdx.x, lane = tid & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  }
+  if (lane == 0) {
+    C.wk[0][tid >> 5] = lo;
+    C.wk[1][tid >> 5] = hi;
+    C.wsum[0][tid >> 5] = sum;
+    C.wsum[1][tid >> 5] = sq;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const bool ok = tid < (int)(blockDim.x >> 5);
+    uint32_t a = ok ? (uint32_t)C.wk[0][tid] : 0xffffffffu, b = ok ? (uint32_t)C.wk[1][tid] : 0u;
+    double x = ok ? C.wsum[0][tid] : 0.0, y = ok ? C.wsum[1][tid] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+      x += __shfl_xor_sync(0xffffffffu, x, o);
+      y += __shfl_xor_sync(0xffffffffu, y, o);
+    }
+    if (tid == 0) {
+      C.kmin = a;
+      C.kmax = b;
+      C.ksum = x;
+      C.ksq = y;
+    }
+  }
+  cluster.sync();
+  glo = 0xffffffffu;
+  ghi = 0u;
+  gsum = 0.0;
+  gsq = 0.0;
+#pragma unroll
+  for (int r = 0; r < FZ_CTAS; ++r) {
+    const FzCtl *R = cluster.map_shared_rank(&C, r);
+    glo = min(glo, R->kmin);
+    ghi = max(ghi, R->kmax);
+    gsum += R->ksum;
+    gsq += R->ksq;
+  }
+}
+
+// upper-tail standard normal quantile: z with P(Z > z) = p (Acklam's rational
+// approximation, |rel err| < 1.2e-9 -- only used to aim the first histogram)
+__device__ double fz_normal_upper_quantile(double p) {
+  const double a[6] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                       1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  const double b[5] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                       6.680131188771972e+01, -1.328068155288572e+01};
+  const double c[6] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                       -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  const double d[4] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00, 3.754408661907416e+00};
+  const double q0 = fmin(fmax(1.0 - p, 1e-12), 1.0 - 1e-12);  // lower-tail probability
+  double x;
+  if (q0 < 0.02425) {
+    const double q = sqrt(-2.0 * log(q0));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else if (q0 <= 1.0 - 0.02425) {
+    const double q = q0 - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  } else {
+    const double q = sqrt(-2.0 * log(1.0 - q0));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  }
+  return x;
+}
+
+// 16-byte read-only load that stays where it is written (issued before the
+// barrier that follows it, so its latency overlaps the next global round trip)
+__device__ __forceinline__ uint4 fz_ld_nc_v4(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Keys live in the scorer's layout: thread t owns the 8-key groups starting
+// at g*STEP + 8t (g < FZ_KG).  Passes over them read 8 keys with two 16-byte
+// shared loads (a per-key loop at 16 warps/SM is shared-memory-latency bound).
+constexpr int FZ_STEP = FZ_THREADS * 8;
+constexpr int FZ_KG = (FZ_CAP + FZ_STEP - 1) / FZ_STEP;
+__device__ __forceinline__ void fz_load8(const uint32_t *keys, int e, int m, uint32_t kk[8]) {
+  if (e + 8 <= m) {
+    const uint4 a = *reinterpret_cast<const uint4 *>(keys + e), b = *reinterpret_cast<const uint4 *>(keys + e + 4);
+    kk[0] = a.x; kk[1] = a.y; kk[2] = a.z; kk[3] = a.w;
+    kk[4] = b.x; kk[5] = b.y; kk[6] = b.z; kk[7] = b.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) kk[q] = e + q < m ? keys[e + q] : 0u;
+  }
+}
+
+// mbarrier + TMA bulk copy helpers (value-row staging)
+__device__ __forceinline__ uint32_t fz_smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void fz_mbar_init(unsigned long long *bar) {
+  asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(fz_smem_addr(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fz_mbar_expect(unsigned long long *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fz_smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fz_mbar_wait(unsigned long long *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n FZW_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra FZW_%=;\n}\n" ::"r"(
+          fz_smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fz_bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   fz_smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(fz_smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fz_bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(fz_smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fz_bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// phase timestamps of unit 0, every CTA (debug: tkv_debug_sparse_phases)
+constexpr int FZ_NMARK = 24;
+__device__ unsigned long long g_fz_phase[FZ_CTAS][FZ_NMARK];
+__device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
+#define FZ_MARK(i)                                                          \
+  do {                                                                      \
+    if (trace && blockIdx.y == 0 && tid == 0) {                             \
+      unsigned long long t_;                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      g_fz_phase[rank][i] = t_;                                             \
+    }                                                                       \
+  } while (0)
+
+template <bool ATTEND, int D, int GMAX>
+__global__ void __launch_bounds__(FZ_THREADS, 1)
+    sparse_fused_kernel(SL s, const uint16_t *__restrict__ queries, int G, const int32_t *__restrict__ channels,
+                        int d_s, int n_local, int n_topk, int32_t *__restrict__ sel_idx, int sel_stride,
+                        int32_t *__restrict__ sel_count, int32_t *__restrict__ fetch_count,
+                        double *__restrict__ scores_out, int keys_from_device, float *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  FzShared &S = *reinterpret_cast<FzShared *>(smem);
+  __shared__ FzCtl C;
+  __shared__ double qsum[128];
+  __shared__ float qsum32[128];
+  __shared__ int chs[128];
+  __shared__ double band_eps;
+  __shared__ double eps_term[128];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int u = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = *s.len;
+  const int trace = g_fz_trace;
+  int32_t *out_idx = sel_idx + (size_t)u * sel_stride;
+  const bool select_all = n <= (int64_t)n_local + n_topk;  // retriever.py:204-205
+  const int64_t ncand = n > n_local ? n - n_local : 0;     // local window starts here
+  const int64_t chunk = ((ncand + FZ_CTAS - 1) / FZ_CTAS + 15) & ~int64_t(15);
+  const int64_t j0 = rank * chunk;
+  const int m = (int)(j0 < ncand ? imin64(chunk, ncand - j0) : 0);
+  uint8_t *flags = S.flags;
+  const uint16_t *kt = s.kt + (size_t)u * s.d * s.capacity;
+  FZ_MARK(0);
+  if (tid == 0) {
+    C.band_count = 0;
+    C.overflow = 0;
+    C.hits = 0;
+    C.misses = 0;
+    if (ATTEND) fz_mbar_init(&C.bar);
+  }
+  if (select_all) {
+    for (int e = tid; e < m; e += blockDim.x) flags[e] = 1;
+    __syncthreads();
+  } else {
+    for (int i = tid; i < d_s; i += blockDim.x) chs[i] = channels[(size_t)u * d_s + i];
+    __syncthreads();
+    FZ_MARK(1);
+    // ---- 1. fp32 proxy scores (retriever.py:189) -> order-preserving keys ----
+    // Every thread issues its first two 8-token groups of scorer loads before
+    // the group-summed query is formed: the two round trips overlap.
+    uint32_t *keys32 = S.k.f.keys32;
+    uint32_t klo = 0xffffffffu, khi = 0u;
+    float fsum = 0.0f, fsq = 0.0f;
+    const bool fast8 = (d_s & 7) == 0;
+    constexpr int STEP = FZ_THREADS * 8;
+    uint4 v[2][8];
+    int e0 = tid * 8;
+    if (fast8) {
+#pragma unroll
+      for (int g2 = 0; g2 < 2; ++g2)
+        if (e0 + g2 * STEP + 8 <= m) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) v[g2][r] = fz_ld_nc_v4(kt + (size_t)chs[r] * s.capacity + j0 + e0 + g2 * STEP);
+        }
+    }
+    for (int i = tid; i < d_s; i += blockDim.x) {
+      const int ch = chs[i];
+      double q = 0.0;
+      for (int j = 0; j < G; ++j) q += h2d(queries[((size_t)u * G + j) * s.d + ch]);  // group sum (retriever.py:189)
+      qsum[i] = q;
+      qsum32[i] = (float)q;
+      // |fp32 score - float64 score| <= 2^-20 * sum_i max|K_i| |q_i| (<= 9 roundings of 2^-24 each)
+      eps_term[i] = (double)s.chmax[(size_t)u * s.d + ch] * fabs(q);
+    }
+    __syncthreads();
+    FZ_MARK(2);
+    for (; e0 < m; e0 += 2 * STEP) {
+#pragma unroll
+      for (int g2 = 0; g2 < 2; ++g2) {
+        const int eg = e0 + g2 * STEP;
+        if (eg >= m) break;
+        const int64_t j = j0 + eg;
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+        int i = 0;
+        if (fast8 && eg + 8 <= m) {
+          for (; i < d_s; i += 8) {
+            if (i > 0) {  // channel group 0 of every round was prefetched
+#pragma unroll
+              for (int r = 0; r < 8; ++r) v[g2][r] = fz_ld_nc_v4(kt + (size_t)chs[i + r] * s.capacity + j);
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const float qv = qsum32[i + r];
+              const uint32_t w[4] = {v[g2][r].x, v[g2][r].y, v[g2][r].z, v[g2][r].w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[e] = fmaf(h2f((uint16_t)(w[e >> 1] >> (16 * (e & 1)))), qv, acc[e]);
+            }
+          }
+        }
+        for (; i < d_s; ++i) {
+          const uint16_t *row = kt + (size_t)chs[i] * s.capacity + j;
+          const float qv = qsum32[i];
+          for (int e = 0; e < 8 && eg + e < m; ++e) acc[e] = fmaf(h2f(row[e]), qv, acc[e]);
+        }
+        uint32_t kk[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          kk[e] = fz_orderable32(acc[e]);
+          if (eg + e < m) {
+            klo = min(klo, kk[e]);
+            khi = max(khi, kk[e]);
+            fsum += acc[e];
+            fsq = fmaf(acc[e], acc[e], fsq);
+          }
+        }
+        if (eg + 8 <= m) {  // two 16-byte stores (no 8-way bank conflicts)
+          uint4 *dst = reinterpret_cast<uint4 *>(keys32 + eg);
+          dst[0] = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+          dst[1] = make_uint4(kk[4], kk[5], kk[6], kk[7]);
+        } else {
+          for (int e = 0; e < 8 && eg + e < m; ++e) keys32[eg + e] = kk[e];
+        }
+      }
+      if (fast8 && e0 + 2 * STEP < m) {  // next round's first channel group
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2)
+          if (e0 + 2 * STEP + g2 * STEP + 8 <= m) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+              v[g2][r] = fz_ld_nc_v4(kt + (size_t)chs[r] * s.capacity + j0 + e0 + 2 * STEP + g2 * STEP);
+          }
+      }
+    }
+    if (tid == 0) {
+      double e = 0.0;
+      for (int i = 0; i < d_s; ++i) e += eps_term[i];
+      band_eps = e * 9.5367431640625e-07;  // 2^-20
+    }
+    FZ_MARK(3);
+    uint32_t glo, ghi;
+    double gsum, gsq;
+    fz_cluster_stats(cluster, C, klo, khi, (double)fsum, (double)fsq, glo, ghi, gsum, gsq);
+    FZ_MARK(4);
+    // ---- 2. threshold range by linear histograms ----
+    // Invariant kept by every accepted pass: #{score > R_hi} < n_topk <= #{score >= R_lo}.
+    // Pass 0 aims at the Gaussian estimate of the n_topk-th score (mean + z sd,
+    // +-0.6 sd); only keys inside the aimed range touch the histogram.  A
+    // pass whose range misses the threshold falls back to the full range.
+    const double flo = (double)fz_from_orderable32(glo), fhi = (double)fz_from_orderable32(ghi);
+    double R_lo = flo, R_hi = fhi;
+    {
+      const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
+      const double z = fz_normal_upper_quantile((double)n_topk / N);
+      const double t = mu + z * sd;
+      if (sd > 0.0 && isfinite(t)) {
+        R_lo = fmax(flo, t - 0.6 * sd);
+        R_hi = fmin(fhi, t + 0.6 * sd);
+        if (!(R_hi > R_lo)) {
+          R_lo = flo;
+          R_hi = fhi;
+        }
+      }
+    }
+    bool aimed = R_lo > flo || R_hi < fhi;
+    FZ_MARK(21);
+    uint32_t *H = S.k.f.hist;  // [NB] bins + [NB] keys above the range
+    uint32_t *T = S.k.f.tot;   // cluster totals
+    for (int pass = 0; pass < 5; ++pass) {
+      const float r_lo = __double2float_rd(R_lo), r_hi = __double2float_ru(R_hi);
+      const float scale = (float)FZ_NB / (r_hi - r_lo);
+      if (!(r_hi > r_lo) || !(scale < 3.0e38f)) break;  // degenerate range: everything in it is band
+      for (int i = tid; i < FZ_NB + 4; i += blockDim.x) H[i] = 0;
+      __syncthreads();
+      if (pass == 0) FZ_MARK(22);
+      int above = 0;
+#pragma unroll
+      for (int g = 0; g < FZ_KG; ++g) {
+        const int e = g * FZ_STEP + tid * 8;
+        if (e >= m) break;
+        uint32_t kk[8];
+        fz_load8(keys32, e, m, kk);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (e + q >= m) break;
+          const float x = fz_from_orderable32(kk[q]);
+          if (x > r_hi) {
+            ++above;
+          } else if (x >= r_lo) {
+            const int b = min(FZ_NB - 1, max(0, (int)((x - r_lo) * scale)));
+            atomicAdd(&H[b], 1u);
+          }
+        }
+      }
+      if (pass == 0) FZ_MARK(23);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+      if (lane == 0 && above) atomicAdd(&H[FZ_NB], (unsigned)above);
+      if (pass == 0) FZ_MARK(5);
+      cluster.sync();
+      if (pass == 0) FZ_MARK(6);
+      // cluster totals: 16-byte DSMEM reads (DSMEM moves ~20 B/clk per SM)
+      if (tid < (FZ_NB + 4) / 4) {
+        uint4 t = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int r = 0; r < FZ_CTAS; ++r) {
+          const uint4 x = reinterpret_cast<const uint4 *>(cluster.map_shared_rank(H, r))[tid];
+          t.x += x.x; t.y += x.y; t.z += x.z; t.w += x.w;
+        }
+        reinterpret_cast<uint4 *>(T)[tid] = t;
+      }
+      __syncthreads();
+      if (pass == 0) FZ_MARK(7);
+      if (warp == 0) {
+        // descending scan by one warp: lane l owns bins NB-1-BPL*l .. NB-BPL-BPL*l
+        const int need = n_topk - (int)T[FZ_NB];
+        constexpr int BPL = FZ_NB / 32;
+        int cl = 0;
+#pragma unroll
+        for (int q = 0; q < BPL; ++q) cl += (int)T[FZ_NB - 1 - BPL * lane - q];
+        int incl = cl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int in_range = __shfl_sync(0xffffffffu, incl, 31);
+        int before = incl - cl;
+        if (need <= 0) {
+          if (lane == 0) C.status = 1;  // threshold above the range
+        } else if (in_range < need) {
+          if (lane == 0) C.status = -1;  // threshold below the range
+        } else {
+          const unsigned hit = __ballot_sync(0xffffffffu, before < need && incl >= need);
+          if (lane == __ffs(hit) - 1) {
+            for (int q = 0; q < BPL; ++q) {
+              const int b = FZ_NB - 1 - BPL * lane - q;
+              const int c = (int)T[b];
+              if (before + c >= need) {
+                C.bin = b;
+                C.inbin = c;
+                break;
+              }
+              before += c;
+            }
+            C.status = 0;
+          }
+        }
+      }
+      __syncthreads();
+      if (pass == 0) FZ_MARK(8);
+      const int status = C.status, B = C.bin, inbin = C.inbin;
+      if (status != 0) {
+        // the aimed range missed the threshold: widen it to the side that holds it
+        if (status > 0) R_lo = R_hi; else R_hi = R_lo;
+        R_lo = status > 0 ? R_lo : flo;
+        R_hi = status > 0 ? fhi : R_hi;
+        aimed = false;
+        cluster.sync();  // every CTA has read this CTA's histogram before it is cleared
+        continue;
+      }
+      // bin B's value range, widened by a rounding margin, clamped to the current range
+      const double delta = 9.5367431640625e-07 * (fabs((double)r_lo) + fabs((double)r_hi) + ((double)r_hi - r_lo));
+      const double e_lo = B == 0 ? (double)r_lo : (double)r_lo + (double)B / (double)scale - delta;
+      const double e_hi = B == FZ_NB - 1 ? (double)r_hi : (double)r_lo + (double)(B + 1) / (double)scale + delta;
+      R_lo = fmax(R_lo, e_lo);
+      R_hi = fmin(R_hi, e_hi);
+      if (inbin <= FZ_REFINE || pass == 4) break;
+      cluster.sync();  // every CTA has read this CTA's histogram before it is cleared
+    }
+    (void)aimed;
+    FZ_MARK(9);
+    // ---- 3. exact band: [R_lo - 2eps, R_hi + 2eps] rescored in float64 ----
+    const float band_hi = __double2float_ru(R_hi + 2.0 * band_eps);
+    const float band_lo = __double2float_rd(R_lo - 2.0 * band_eps);
+    int definite = 0;
+#pragma unroll
+    for (int g = 0; g < FZ_KG; ++g) {
+      const int e = g * FZ_STEP + tid * 8;
+      if (e >= m) break;
+      uint32_t kk[8];
+      fz_load8(keys32, e, m, kk);
+      uint32_t fl[2] = {0u, 0u};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (e + q >= m) break;
+        const float x = fz_from_orderable32(kk[q]);
+        uint32_t f = 0;
+        if (x > band_hi) {
+          f = 1;
+          ++definite;
+        } else if (x >= band_lo) {
+          const int slot = atomicAdd(&C.band_count, 1);
+          if (slot < FZ_BAND) {
+            const int64_t j = j0 + e + q;
+            S.k.f.band_key[slot] = orderable(fz_exact_score(kt, s.capacity, chs, qsum, d_s, j));
+            S.k.f.band_idx[slot] = (uint32_t)j;
+          } else {
+            C.overflow = 1;
+          }
+          f = 3;
+        }
+        fl[q >> 2] |= f << (8 * (q & 3));
+      }
+      if (e + 8 <= m) {
+        *reinterpret_cast<uint2 *>(flags + e) = make_uint2(fl[0], fl[1]);
+      } else {
+        for (int q = 0; e + q < m; ++q) flags[e + q] = (uint8_t)(fl[q >> 2] >> (8 * (q & 3)));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) definite += __shfl_xor_sync(0xffffffffu, definite, o);
+    if (lane == 0) C.wk[0][warp] = (unsigned long long)definite;
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < FZ_WARPS; ++w) t += (int)C.wk[0][w];
+      C.cta_count = t;
+    }
+    FZ_MARK(10);
+    cluster.sync();
+    FZ_MARK(11);
+    int cnt_r[FZ_CTAS], all_def = 0, all_band = 0, overflow = 0;
+#pragma unroll
+    for (int r = 0; r < FZ_CTAS; ++r) {
+      const FzCtl *R = cluster.map_shared_rank(&C, r);
+      cnt_r[r] = min(R->band_count, FZ_BAND);
+      all_def += R->cta_count;
+      all_band += cnt_r[r];
+      overflow |= R->overflow;
+    }
+    if (!overflow) {
+      // every CTA's band members, concatenated in rank order
+      for (int t = tid; t < all_band; t += blockDim.x) {
+        int r = 0, base = 0;
+        while (t - base >= cnt_r[r]) base += cnt_r[r++];
+        const FzShared *RS = cluster.map_shared_rank(&S, r);
+        S.k.f.all_key[t] = RS->k.f.band_key[t - base];
+        S.k.f.all_idx[t] = RS->k.f.band_idx[t - base];
+      }
+      __syncthreads();
+      const int need_b = n_topk - all_def;
+      const int mine = min(C.band_count, FZ_BAND);
+      for (int b = tid; b < mine; b += blockDim.x) {
+        const unsigned long long kb = S.k.f.band_key[b];
+        const uint32_t ib = S.k.f.band_idx[b];
+        int beaten = 0;
+        for (int o = 0; o < all_band; ++o) {
+          const unsigned long long ko = S.k.f.all_key[o];
+          const uint32_t io = S.k.f.all_idx[o];
+          beaten += (ko > kb) || (ko == kb && io > ib);  // (score desc, index desc)
+        }
+        flags[ib - j0] = beaten < need_b ? 1 : 0;
+      }
+      cluster.sync();  // band arrays read by the other CTAs
+    } else {
+      // ---- float64 radix select (degenerate inputs, e.g. huge exact-tie sets) ----
+      uint64_t *keys64 = S.k.keys64;
+      cluster.sync();  // no CTA still reads this CTA's band arrays (aliased by keys64)
+      for (int e = tid; e < m; e += blockDim.x) keys64[e] = orderable(fz_exact_score(kt, s.capacity, chs, qsum, d_s, j0 + e));
+      __syncthreads();
+      int top, need64 = n_topk;
+      unsigned long long prefix;
+      bool done;
+      fz_common_prefix(cluster, keys64, m, C, top, prefix);
+      fz_radix(cluster, keys64, m, S, C, top, prefix, need64, done);
+      fz_exact_flags(cluster, keys64, m, flags, C, top, prefix, need64, done);
+    }
+    if (scores_out) {
+      for (int e = tid; e < m; e += blockDim.x)
+        scores_out[(size_t)u * s.capacity + j0 + e] = fz_exact_score(kt, s.capacity, chs, qsum, d_s, j0 + e);
+    }
+    __syncthreads();
+  }
+  FZ_MARK(12);
+  // ---- 4. ascending output: the key groups in index order (g, thread, q) + cluster prefix offsets ----
+  // per-(group, thread) counts, packed 16 bits per group, prefix-summed in one 64-bit block scan
+  uint32_t fw[FZ_KG][2];
+  unsigned long long packed = 0ull, packed2 = 0ull;  // groups 0-3 / 4-7
+  static_assert(FZ_KG <= 8, "two packed scans cover at most 8 key groups");
+#pragma unroll
+  for (int g = 0; g < FZ_KG; ++g) {
+    const int e = g * FZ_STEP + tid * 8;
+    fw[g][0] = fw[g][1] = 0u;
+    if (e < m) {
+      if (e + 8 <= m) {
+        const uint2 x = *reinterpret_cast<const uint2 *>(flags + e);
+        fw[g][0] = x.x;
+        fw[g][1] = x.y;
+      } else {
+        for (int q = 0; e + q < m; ++q) fw[g][q >> 2] |= (uint32_t)flags[e + q] << (8 * (q & 3));
+      }
+    }
+    const unsigned long long c = (unsigned long long)(__popc(fw[g][0]) + __popc(fw[g][1]));  // flags are 0/1 bytes
+    if (g < 4) packed |= c << (16 * g);
+    else packed2 |= c << (16 * (g - 4));
+  }
+  unsigned long long tot1, tot2 = 0ull;
+  const unsigned long long pre1 = fz_block_excl_scan64(packed, C.scan64, &tot1);
+  unsigned long long pre2 = 0ull;
+  if (FZ_KG > 4 && m > 4 * FZ_STEP) pre2 = fz_block_excl_scan64(packed2, C.scan64, &tot2);
+  int gbase[FZ_KG], gpos[FZ_KG];
+  {
+    int run = 0;
+#pragma unroll
+    for (int g = 0; g < FZ_KG; ++g) {
+      const unsigned long long T = g < 4 ? tot1 : tot2, P = g < 4 ? pre1 : pre2;
+      const int sh = 16 * (g & 3);
+      gbase[g] = run;
+      gpos[g] = run + (int)((P >> sh) & 0xffffull);
+      run += (int)((T >> sh) & 0xffffull);
+    }
+  }
+  const int cta_total = (int)((tot1 & 0xffffull) + ((tot1 >> 16) & 0xffffull) + ((tot1 >> 32) & 0xffffull) +
+                              ((tot1 >> 48) & 0xffffull) + (tot2 & 0xffffull) + ((tot2 >> 16) & 0xffffull) +
+                              ((tot2 >> 32) & 0xffffull) + ((tot2 >> 48) & 0xffffull));
+  (void)gbase;
+  if (tid == 0) C.cta_count = cta_total;
+  FZ_MARK(13);
+  cluster.sync();
+  FZ_MARK(14);
+  int offset = 0, far_total = 0;
+#pragma unroll
+  for (int r = 0; r < FZ_CTAS; ++r) {
+    const int c = cluster.map_shared_rank(&C, r)->cta_count;
+    if (r < rank) offset += c;
+    far_total += c;
+  }
+  const int n_loc = (int)(n - ncand);
+  const int nrows = cta_total + (rank == FZ_CTAS - 1 ? n_loc : 0);
+  // row list (16-bit token offsets from rbase, local rows after the far ones) at the top of the overlaid region
+  const int64_t rbase = rank == FZ_CTAS - 1 ? imin64(j0, ncand) : j0;
+  const int rows_bytes = ((nrows * 2 + 127) / 128) * 128;
+  uint16_t *rows = reinterpret_cast<uint16_t *>(S.k.raw + FZ_UNION - rows_bytes);
+#pragma unroll
+  for (int g = 0; g < FZ_KG; ++g) {
+    int p = gpos[g];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      uint32_t x = fw[g][w];
+      while (x) {
+        const int bit = __ffs(x) - 1;
+        x &= x - 1u;
+        const int e = g * FZ_STEP + tid * 8 + 4 * w + (bit >> 3);
+        out_idx[offset + p] = (int32_t)(j0 + e);
+        if (ATTEND) rows[p] = (uint16_t)(j0 + e - rbase);
+        ++p;
+      }
+    }
+  }
+  if (rank == FZ_CTAS - 1) {
+    for (int i = tid; i < n_loc; i += blockDim.x) {
+      out_idx[far_total + i] = (int32_t)(ncand + i);
+      if (ATTEND) rows[cta_total + i] = (uint16_t)(ncand + i - rbase);
+    }
+    if (tid == 0) {
+      sel_count[u] = far_total + n_loc;
+      if (fetch_count) fetch_count[u] = far_total;
+    }
+  }
+  if constexpr (!ATTEND) {
+    cluster.sync();  // no CTA leaves while its shared memory may still be read
+    return;
+  } else {
+    for (int i = tid; i < G * D; i += blockDim.x)
+      S.qs[i] = h2f(queries[(size_t)u * G * D + i]) * (1.4426950408889634f / sqrtf((float)D));  // log2(e)/sqrt(d)
+    __syncthreads();
+    FZ_MARK(15);
+    // ---- 5. gather + attention over this CTA's rows ----
+    // Value rows (PCIe host store, HBM row cache or local mirror) are staged
+    // in shared memory by TMA bulk copies, every row of a round at once
+    // (one PCIe round trip); key rows come from HBM into registers while the
+    // value copies are in flight; logits go to shared memory; then each warp
+    // runs an online softmax over its rows.
+    constexpr int CPL = D / 32;  // channels per lane
+    const bool keys_host = !keys_from_device;
+    const int row_bytes = D * 2 * (keys_host ? 2 : 1) + GMAX * 4;  // staged V (+K) + logits
+    const int NR = min(1024, ((FZ_UNION - rows_bytes) / row_bytes) & ~15);
+    uint16_t *stage_v = reinterpret_cast<uint16_t *>(S.k.raw);
+    uint16_t *stage_k = stage_v + (size_t)NR * D;  // used when keys cross PCIe
+    float *zs = reinterpret_cast<float *>(S.k.raw + (size_t)NR * D * 2 * (keys_host ? 2 : 1));
+    const int64_t local_start = ncand;
+    const bool use_cache = s.cache_v != nullptr && keys_from_device;
+    int prevc = 0, pcnt = 0;
+    const int32_t *pidx = nullptr;
+    if (use_cache) {
+      prevc = *s.cache_cur;
+      pcnt = s.cache_cnt[prevc * s.units + u];
+      pidx = s.cache_idx + ((size_t)prevc * s.units + u) * s.cache_rows;
+    }
+    const int nxt = prevc ^ 1;
+    uint16_t *cv_next = use_cache ? s.cache_v + ((size_t)nxt * s.units + u) * s.cache_rows * D : nullptr;
+    int32_t *ci_next = use_cache ? s.cache_idx + ((size_t)nxt * s.units + u) * s.cache_rows : nullptr;
+    float mrun[GMAX], lrun[GMAX], acc[GMAX][CPL];
+#pragma unroll
+    for (int h = 0; h < GMAX; ++h) {
+      mrun[h] = -INFINITY;
+      lrun[h] = 0.0f;
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) acc[h][e] = 0.0f;
+    }
+    int hits = 0, misses = 0;
+    uint32_t parity = 0;
+    for (int base = 0; base < nrows; base += NR) {
+      const int cnt = min(NR, nrows - base);
+      if (tid == 0) fz_mbar_expect(&C.bar, (uint32_t)(cnt * D * 2 * (keys_host ? 2 : 1)));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses before the TMA writes
+      __syncthreads();
+      // (a) one thread per row issues the bulk copy of its value row (and key row over PCIe)
+      for (int i = tid; i < cnt; i += blockDim.x) {
+        const int64_t idx = rbase + rows[base + i];
+        const uint16_t *vp;
+        if (idx < local_start) {
+          const uint16_t *hrow = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
+          int pos_c = -1;
+          if (use_cache) {
+            const int p = s.cache_map[(size_t)u * s.capacity + idx];
+            if (p >= 0 && p < pcnt && __ldcg(&pidx[p]) == idx) pos_c = p;
+          }
+          vp = pos_c >= 0 ? s.cache_v + (((size_t)prevc * s.units + u) * s.cache_rows + pos_c) * D : hrow + D;
+          hits += pos_c >= 0;
+          misses += pos_c < 0;
+          if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, hrow, D * 2, &C.bar);
+        } else {
+          const int64_t lr = idx - s.local_offset;
+          vp = s.loc_v + ((size_t)u * s.local_capacity + lr) * D;
+          if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, s.loc_k + ((size_t)u * s.local_capacity + lr) * D, D * 2,
+                                     &C.bar);
+        }
+        fz_bulk_g2s(stage_v + (size_t)i * D, vp, D * 2, &C.bar);
+      }
+      // (b) logits of this warp's rows: key rows from HBM while the value copies fly
+      if (!keys_host) {
+        for (int i0 = warp; i0 < cnt; i0 += FZ_WARPS * 8) {
+          float kf[8][CPL];
+#pragma unroll
+          for (int jr = 0; jr < 8; ++jr) {
+            const int i = i0 + FZ_WARPS * jr;
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) kf[jr][e] = 0.0f;
+            if (i >= cnt) continue;
+            const int64_t idx = rbase + rows[base + i];
+            if (idx >= local_start || s.kdev) {
+              const uint16_t *kp = idx >= local_start
+                                       ? s.loc_k + ((size_t)u * s.local_capacity + (idx - s.local_offset)) * D
+                                       : s.kdev + ((size_t)u * s.capacity + idx) * D;
+              if constexpr (CPL == 4) {
+                const uint2 a = *reinterpret_cast<const uint2 *>(kp + lane * 4);
+                kf[jr][0] = h2f((uint16_t)a.x); kf[jr][1] = h2f((uint16_t)(a.x >> 16));
+                kf[jr][2] = h2f((uint16_t)a.y); kf[jr][3] = h2f((uint16_t)(a.y >> 16));
+              } else {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) kf[jr][e] = h2f(kp[lane * CPL + e]);
+              }
+            } else {  // key row from the channel-major scorer copy (scattered 2-byte reads)
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) kf[jr][e] = h2f(kt[((size_t)lane * CPL + e) * s.capacity + idx]);
+            }
+          }
+#pragma unroll
+          for (int jr = 0; jr < 8; ++jr) {
+            const int i = i0 + FZ_WARPS * jr;
+            if (i >= cnt) break;
+#pragma unroll
+            for (int h = 0; h < GMAX; ++h) {
+              if (h >= G) break;
+              const float *qh = S.qs + h * D + lane * CPL;
+              float dp = 0.0f;
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) dp = fmaf(qh[e], kf[jr][e], dp);
+              dp = warp_sum(dp);
+              if (lane == 0) zs[(size_t)i * GMAX + h] = dp;
+            }
+          }
+        }
+      }
+      // (c) value rows (and key rows over PCIe) have landed
+      fz_mbar_wait(&C.bar, parity);
+      parity ^= 1u;
+      if (keys_host) {
+        for (int i = warp; i < cnt; i += FZ_WARPS) {
+          const uint16_t *kp = stage_k + (size_t)i * D;
+          for (int h = 0; h < G; ++h) {
+            const float *qh = S.qs + h * D + lane * CPL;
+            float dp = 0.0f;
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) dp = fmaf(qh[e], h2f(kp[lane * CPL + e]), dp);
+            dp = warp_sum(dp);
+            if (lane == 0) zs[(size_t)i * GMAX + h] = dp;
+          }
+        }
+      }
+      __syncwarp();
+      // (d) online softmax over this warp's rows (the rows whose logits it wrote)
+      for (int i = warp; i < cnt; i += FZ_WARPS) {
+        const uint16_t *vr = stage_v + (size_t)i * D + lane * CPL;
+        float vf[CPL];
+        if constexpr (CPL == 4) {
+          const uint2 b = *reinterpret_cast<const uint2 *>(vr);
+          vf[0] = h2f((uint16_t)b.x); vf[1] = h2f((uint16_t)(b.x >> 16));
+          vf[2] = h2f((uint16_t)b.y); vf[3] = h2f((uint16_t)(b.y >> 16));
+        } else {
+#pragma unroll
+          for (int e = 0; e < CPL; ++e) vf[e] = h2f(vr[e]);
+        }
+#pragma unroll
+        for (int h = 0; h < GMAX; ++h) {
+          if (h >= G) break;
+          const float z = zs[(size_t)i * GMAX + h];
+          const float mn = fmaxf(mrun[h], z);
+          const float sc = exp2f(mrun[h] - mn), p = exp2f(z - mn);
+          lrun[h] = fmaf(lrun[h], sc, p);
+#pragma unroll
+          for (int e = 0; e < CPL; ++e) acc[h][e] = fmaf(p, vf[e], acc[h][e] * sc);
+          mrun[h] = mn;
+        }
+      }
+      // (e) this step's fetched value rows become the next step's cache, at their output rank
+      if (use_cache) {
+        for (int i = tid; i < cnt; i += blockDim.x) {
+          const int li = base + i;
+          if (li >= cta_total) continue;  // local rows are not cached
+          const int r = offset + li;
+          const int32_t idx = (int32_t)(rbase + rows[li]);
+          ci_next[r] = idx;
+          s.cache_map[(size_t)u * s.capacity + idx] = r;
+          fz_bulk_s2g(cv_next + (size_t)r * D, stage_v + (size_t)i * D, D * 2);
+        }
+        fz_bulk_commit_wait_read();  // the staged rows are read before the next round overwrites them
+      }
+      __syncthreads();
+    }
+    if (use_cache) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        hits += __shfl_xor_sync(0xffffffffu, hits, o);
+        misses += __shfl_xor_sync(0xffffffffu, misses, o);
+      }
+      if (lane == 0 && (hits | misses)) {
+        atomicAdd(&C.hits, hits);
+        atomicAdd(&C.misses, misses);
+      }
+      if (rank == 0 && tid == 0) s.cache_cnt[nxt * s.units + u] = far_total;
+    }
+    FZ_MARK(16);
+    __syncthreads();  // the staging area (aliased by the partials) is no longer read
+    FZ_MARK(17);
+    float *pm = reinterpret_cast<float *>(S.k.raw), *pl = pm + FZ_WARPS * GMAX, *pa = pl + FZ_WARPS * GMAX;
+#pragma unroll
+    for (int h = 0; h < GMAX; ++h) {
+      if (h >= G) break;
+      if (lane == 0) {
+        pm[warp * GMAX + h] = mrun[h];
+        pl[warp * GMAX + h] = lrun[h];
+      }
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) pa[((size_t)warp * GMAX + h) * D + lane * CPL + e] = acc[h][e];
+    }
+    __syncthreads();
+    for (int i = tid; i < G * D; i += blockDim.x) {
+      const int h = i / D, c = i % D;
+      float M = -INFINITY;
+      for (int w = 0; w < FZ_WARPS; ++w) M = fmaxf(M, pm[w * GMAX + h]);
+      float L = 0.0f, A = 0.0f;
+      if (M != -INFINITY) {
+        for (int w = 0; w < FZ_WARPS; ++w) {
+          const float mw = pm[w * GMAX + h];
+          if (mw == -INFINITY) continue;
+          const float sc = exp2f(mw - M);
+          L = fmaf(sc, pl[w * GMAX + h], L);
+          A = fmaf(sc, pa[((size_t)w * GMAX + h) * D + c], A);
+        }
+      }
+      S.cta_acc[i] = A;
+      if (c == 0) {
+        S.cta_m[h] = M;
+        S.cta_l[h] = L;
+      }
+    }
+    if (use_cache && tid == 0 && (C.hits | C.misses)) {
+      atomicAdd(&s.cache_stats[0], (unsigned long long)C.hits);
+      atomicAdd(&s.cache_stats[1], (unsigned long long)C.misses);
+    }
+    FZ_MARK(18);
+    cluster.sync();
+    FZ_MARK(19);
+    if (rank == 0) {
+      for (int i = tid; i < G * D; i += blockDim.x) {
+        const int h = i / D;
+        float Mr[FZ_CTAS], M = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < FZ_CTAS; ++r) {
+          Mr[r] = cluster.map_shared_rank(&S, r)->cta_m[h];
+          M = fmaxf(M, Mr[r]);
+        }
+        float L = 0.0f, A = 0.0f;
+#pragma unroll
+        for (int r = 0; r < FZ_CTAS; ++r) {
+          if (Mr[r] == -INFINITY) continue;
+          const FzShared *R = cluster.map_shared_rank(&S, r);
+          const float sc = exp2f(Mr[r] - M);
+          L = fmaf(sc, R->cta_l[h], L);
+          A = fmaf(sc, R->cta_acc[i], A);
+        }
+        out[(size_t)u * G * D + i] = A / L;
+      }
+    }
+    cluster.sync();  // rank 0 has read every CTA's partial
+    FZ_MARK(20);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+bool fused_ok(const SL &s, int n_local) {
+  const int64_t ncand = s.capacity > n_local ? s.capacity - n_local : 0;
+  const int64_t chunk = ((ncand + FZ_CTAS - 1) / FZ_CTAS + 15) & ~int64_t(15);
+  // per-thread flag granules (<= 64 flags) and 16-bit row offsets
+  return chunk <= FZ_CAP && chunk <= (int64_t)FZ_THREADS * 64 && chunk + 4096 < 65536 && s.capacity % 8 == 0;
+}
+
+template <bool ATTEND, int D, int GMAX>
+static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s,
+                                int n_local, int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count,
+                                double *scores_out, int keys_from_device, float *out, cudaStream_t st) {
+  auto kern = sparse_fused_kernel<ATTEND, D, GMAX>;
+  const size_t sm = sizeof(FzShared);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(FZ_CTAS, s.units);
+  cfg.blockDim = dim3(FZ_THREADS);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = FZ_CTAS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, s, queries, G, channels, d_s, n_local, n_topk, sel_idx, n_local + n_topk,
+                            sel_count, fetch_count, scores_out, keys_from_device, out);
+}
+
+// select only (tkv_select_tokens)
+int select_cluster(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
+                   int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, double *scores_out,
+                   cudaStream_t st) {
+  const cudaError_t e = launch_fused<false, 128, 1>(s, queries, G, channels, d_s, n_local, n_topk, sel_idx,
+                                                    sel_count, fetch_count, scores_out, 1, nullptr, st);
+  if (e != cudaSuccess) return fail(TKV_ERR_CUDA, std::string("tkv_select_tokens(cluster): ") + cudaGetErrorString(e));
+  return check_launch("tkv_select_tokens(cluster)");
+}
+
+bool select_cluster_ok(const SL &s, int n_local) { return fused_ok(s, n_local); }
+
+bool sparse_decode_supported(const SL &s, int G, int n_local) {
+  if (!fused_ok(s, n_local)) return false;
+  return (s.d == 128 && G <= 8) || (s.d == 64 && G <= 8) || (s.d == 256 && G <= 4) || (s.d == 32 && G <= 8);
+}
+
+// fused select + gather + attention (tkv_sparse_decode)
+int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
+                        int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
+                        float *out, cudaStream_t st) {
+  cudaError_t e;
+#define TKV_FZ(D, GM)                                                                                          \
+  e = launch_fused<true, D, GM>(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, \
+                                nullptr, keys_from_device, out, st)
+  if (s.d == 128 && G <= 4) TKV_FZ(128, 4);
+  else if (s.d == 128 && G <= 8) TKV_FZ(128, 8);
+  else if (s.d == 64 && G <= 8) TKV_FZ(64, 8);
+  else if (s.d == 32 && G <= 8) TKV_FZ(32, 8);
+  else if (s.d == 256 && G <= 4) TKV_FZ(256, 4);
+  else return fail(TKV_ERR_PARAMETER, "fused sparse decode supports d in {32,64,128,256} with G<=8 (G<=4 at d=256)");
+#undef TKV_FZ
+  if (e != cudaSuccess) return fail(TKV_ERR_CUDA, std::string("tkv_sparse_decode: ") + cudaGetErrorString(e));
+  return check_launch("tkv_sparse_decode");
+}
+
+}  // namespace tkv
+
+extern "C" int tkv_debug_sparse_trace(int on) {
+  return cudaMemcpyToSymbol(tkv::g_fz_trace, &on, sizeof(int)) == cudaSuccess ? 0 : 7;
+}
+
+extern "C" int tkv_debug_sparse_phases(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, tkv::g_fz_phase, sizeof(tkv::g_fz_phase)) == cudaSuccess ? 0 : 7;
+}

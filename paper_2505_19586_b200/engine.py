@@ -17,6 +17,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import ctypes as C
+
 import torch
 
 from .errors import ConfigError, ShapeError
@@ -26,6 +28,7 @@ from .kv_model import ModelConfig
 from .quantizer import QuantizedLayerKV, as_f16
 from .retriever import WORKSPACES, RetrievalConfig, stage1_select
 from . import _lib
+from ._lib import check
 
 
 @dataclass(frozen=True)
@@ -42,6 +45,7 @@ class EngineConfig:
     token_major_keys: bool = True  # keep a token-major HBM key copy for that gather (else read the scorer's
                                    # channel-major copy: no extra memory, 32x more DRAM sectors)
     row_cache: bool = True         # keep the previous step's fetched value rows in HBM (exact; rows are immutable)
+    fused_sparse: bool = True      # one launch per sparse layer (select + gather + attention); else two
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
     def validate(self) -> None:
@@ -158,6 +162,8 @@ class DecodeEngine:
         self.steps_done = 0
         self.record_selection = False
         self.profile = None  # list of (name, layer, start_event, end_event) when profiling
+        self._event_pool = None
+        self.prof_graph = None
         self.keys_from_hbm = config.keys_from_hbm
         self.last_channels: dict[int, torch.Tensor] = {}
         self.last_selection: dict[int, tuple] = {}
@@ -207,6 +213,10 @@ class DecodeEngine:
             if self.sel_ws is None:
                 self.sel_ws = torch.zeros(int(lib.tkv_select_workspace(self.units, lay.capacity)), dtype=torch.uint8,
                                           device=self.device)
+                kmax = self.retrieval.n_local + self.retrieval.n_topk
+                self.dec_ws = torch.zeros(int(lib.tkv_sparse_decode_workspace(self.units, lay.capacity, self.G, self.d,
+                                                                              kmax)),
+                                          dtype=torch.uint8, device=self.device)
 
     # -- one step --------------------------------------------------------------
     def load_step(self, hidden, queries, new_keys, new_values, non_blocking: bool = True) -> None:
@@ -239,6 +249,10 @@ class DecodeEngine:
     def _mark(self, stream):
         if self.profile is None:
             return None
+        if self._event_pool is not None:  # inside a profiled capture: an event-record node of the graph
+            ev = self._event_pool.pop()
+            check(_lib.load().tkv_event_record(C.c_void_p(ev.cuda_event), C.c_void_p(stream.cuda_stream), 1))
+            return ev
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
         return ev
@@ -251,7 +265,8 @@ class DecodeEngine:
         """Launches of this library per decode step."""
         q = sum(1 for x in self.labels if x == "q")
         s = len(self.labels) - q
-        return q * 3 + s * 5  # q: decode+combine+append; s: 2 stage-1 + select + gather/attend + append
+        per_s = 3 if self.cfg.fused_sparse else 4  # stage 1 + (fused decode | select + gather/attend) + append
+        return q * 3 + s * per_s  # q: decode+combine+append
 
     def _run_step(self) -> None:
         main = torch.cuda.current_stream(self.device)
@@ -275,17 +290,23 @@ class DecodeEngine:
             else:
                 st = self.sparse[l]
                 main.wait_event(st.s1_done)
-                t0 = self._mark(main)
-                lay.select(self.queries[l], st.channels, self.G, self.retrieval, self.sel_idx, self.sel_count,
-                           self.fetch_count, self.sel_ws)
-                self._span("select", l, t0, main)
+                if self.cfg.fused_sparse:
+                    t0 = self._mark(main)
+                    lay.decode(self.queries[l], st.channels, self.G, self.retrieval, self.sel_idx, self.sel_count,
+                               self.fetch_count, self.out[l], self.dec_ws, keys_from_device=self.keys_from_hbm)
+                    self._span("sparse_decode", l, t0, main)
+                else:
+                    t0 = self._mark(main)
+                    lay.select(self.queries[l], st.channels, self.G, self.retrieval, self.sel_idx, self.sel_count,
+                               self.fetch_count, self.sel_ws)
+                    self._span("select", l, t0, main)
+                    t0 = self._mark(main)
+                    lay.attend(self.queries[l], self.G, self.retrieval, self.sel_idx, self.sel_count, self.out[l],
+                               self.attn_ws, keys_from_device=self.keys_from_hbm)
+                    self._span("gather_attend", l, t0, main)
                 if self.record_selection:
                     self.last_channels[l] = st.channels.clone()
                     self.last_selection[l] = (self.sel_idx.clone(), self.sel_count.clone(), self.fetch_count.clone())
-                t0 = self._mark(main)
-                lay.attend(self.queries[l], self.G, self.retrieval, self.sel_idx, self.sel_count, self.out[l],
-                           self.attn_ws, keys_from_device=self.keys_from_hbm)
-                self._span("gather_attend", l, t0, main)
                 t0 = self._mark(main)
                 lay.append(self.new_keys[l], self.new_values[l])
                 self._span("sparse_append", l, t0, main)
@@ -337,6 +358,42 @@ class DecodeEngine:
         for lay, n in zip(self.layers, saved):
             lay.n = n
         self.graph = g
+
+    def capture_profiled(self) -> None:
+        """Capture the decode step with an event-record node around every
+        kernel group (cudaEventRecordExternal); ``replay_profiled`` then times
+        the kernels inside a real graph replay, without host launch gaps."""
+        L = self.model.num_layers
+        pool = [torch.cuda.Event(enable_timing=True) for _ in range(8 * L + 8)]
+        for ev in pool:
+            ev.record()  # materialise the CUDA events outside the capture
+        torch.cuda.synchronize()
+        saved = [lay.n for lay in self.layers]
+        self._event_pool, self.profile = pool, []
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                self._run_step()
+        finally:
+            self._event_pool = None
+        self._prof_spans, self.profile = self.profile, None
+        for lay, n in zip(self.layers, saved):
+            lay.n = n
+        self.prof_graph = g
+
+    def replay_profiled(self) -> dict:
+        """One step through the profiled graph; returns {name: [ms per launch]}."""
+        if self.steps_done >= self.max_steps:
+            raise ConfigError("engine max_steps exhausted")
+        self.prof_graph.replay()
+        for lay in self.layers:
+            lay.n += 1
+        self.steps_done += 1
+        torch.cuda.synchronize()
+        res: dict = {}
+        for name, layer, a, b in self._prof_spans:
+            res.setdefault(name, []).append(a.elapsed_time(b))
+        return res
 
     def cache_counters(self) -> tuple[int, int]:
         """Summed (HBM-cache hits, PCIe-fetched rows) over the sparse layers."""

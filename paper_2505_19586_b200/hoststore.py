@@ -169,6 +169,15 @@ class OffloadedLayerKV:
                                             cfg.n_local, cfg.n_topk, ptr(sel_idx), ptr(sel_count), ptr(fetch_count),
                                             ptr(scores_out), ptr(workspace), stream_ptr(stream)))
 
+    def decode(self, queries: torch.Tensor, channels: torch.Tensor, G: int, cfg: RetrievalConfig,
+               sel_idx: torch.Tensor, sel_count: torch.Tensor, fetch_count: torch.Tensor, out: torch.Tensor,
+               workspace: torch.Tensor, keys_from_device: bool = False, stream=None) -> None:
+        """One fused launch: proxy scores + exact top-k + gather + attention
+        (pipeline.py:351-376); same results as ``select`` then ``attend``."""
+        check(_lib.load().tkv_sparse_decode(C.byref(self.struct), ptr(queries), G, ptr(channels), channels.shape[1],
+                                            cfg.n_local, cfg.n_topk, ptr(sel_idx), ptr(sel_count), ptr(fetch_count),
+                                            int(keys_from_device), ptr(out), ptr(workspace), stream_ptr(stream)))
+
     def attend(self, queries: torch.Tensor, G: int, cfg: RetrievalConfig, sel_idx: torch.Tensor,
                sel_count: torch.Tensor, out: torch.Tensor, workspace: torch.Tensor, keys_from_device: bool = False,
                stream=None) -> None:

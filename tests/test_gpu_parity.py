@@ -219,9 +219,9 @@ def test_stage1_estimate_matches_oracle(tkv):
             assert np.array_equal(ch[b * 2 + kvh], ref)
 
 
-def _sparse_layer(tkv, keys, values, n_local, steps=4, keys_on_device=False):
+def _sparse_layer(tkv, keys, values, n_local, steps=4, keys_on_device=False, cache_rows=0):
     units, n, d = keys.shape
-    lay = tkv.OffloadedLayerKV(units, d, n + steps, n, n_local, keys_on_device=keys_on_device)
+    lay = tkv.OffloadedLayerKV(units, d, n + steps, n, n_local, keys_on_device=keys_on_device, cache_rows=cache_rows)
     lay.offload(keys, values)
     return lay
 
@@ -296,6 +296,139 @@ def test_cluster_select_ties_and_sizes(tkv, dist):
     for u in range(units):
         sc = O.approx_scores(queries[u * G:(u + 1) * G][:, chans[u]], keys[u][:, chans[u]])
         assert np.array_equal(idx[u, :cnt[u]], O.select_tokens(sc, cfg.n_local, cfg.n_topk))
+
+
+def _keys_for(dist, rng, shape):
+    if dist == "ties":
+        return np.round(rng.normal(size=shape))
+    if dist == "zeros":
+        return np.zeros(shape)
+    if dist == "outliers":  # a few huge keys stretch the score range: the threshold bin is crowded -> refinement
+        k = rng.normal(0, 1e-3, size=shape)
+        k[:, rng.choice(shape[1], 5, replace=False)] *= 1e5
+        return k
+    if dist == "near_ties":  # scores equal in fp32 but not in float64 -> the exact band decides
+        k = np.round(rng.normal(size=shape) * 4) / 4
+        k += rng.choice([0, 2.0 ** -10], size=shape)
+        return k
+    return rng.normal(size=shape)
+
+
+def _decode_once(tkv, lay, queries, chans, G, cfg, kod):
+    import paper_2505_19586_b200._lib as L
+    units, d = chans.shape[0], lay.head_dim
+    kmax = cfg.n_local + cfg.n_topk
+    idx = torch.zeros((units, kmax), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(units, dtype=torch.int32, device="cuda")
+    fc = torch.zeros(units, dtype=torch.int32, device="cuda")
+    out = torch.zeros((units * G, d), dtype=torch.float32, device="cuda")
+    ws = torch.zeros(int(L.load().tkv_sparse_decode_workspace(units, lay.capacity, G, d, kmax)), dtype=torch.uint8,
+                     device="cuda")
+    lay.decode(torch.tensor(queries, dtype=torch.float16, device="cuda"), torch.tensor(chans, device="cuda"), G, cfg,
+               idx, cnt, fc, out, ws, keys_from_device=kod)
+    return idx.cpu().numpy(), cnt.cpu().numpy(), fc.cpu().numpy(), out.cpu().numpy()
+
+
+def _check_decode(keys, values, queries, chans, G, cfg, res, n):
+    idx, cnt, fc, out = res
+    units = chans.shape[0]
+    ref_out = np.empty((units * G, keys.shape[2]))
+    for u in range(units):
+        qg = queries[u * G:(u + 1) * G]
+        sc = O.approx_scores(qg[:, chans[u]], keys[u][:n, chans[u]])
+        sel = O.select_tokens(sc, cfg.n_local, cfg.n_topk)
+        assert np.array_equal(idx[u, :cnt[u]], sel), u
+        assert fc[u] == int((sel < max(0, n - cfg.n_local)).sum())
+        for j in range(G):
+            ref_out[u * G + j] = O.sparse_attention(qg[j], keys[u][:n], values[u][:n], sel)
+    return rel_err(out, ref_out)
+
+
+@pytest.mark.parametrize("dist", ["normal", "ties", "zeros", "outliers", "near_ties"])
+@pytest.mark.parametrize("kod", [True, False], ids=["keys_hbm", "keys_pcie"])
+def test_fused_sparse_decode_matches_oracle(tkv, dist, kod):
+    """One launch (scores + exact top-k + gather + attention) against the
+    oracle: identical index sets (ties by the reference's index rule) and
+    outputs within 1e-5."""
+    rng = np.random.default_rng(31)
+    units, n, d, G, d_s = 3, 20000, 128, 4, 8
+    keys = cases.f16(_keys_for(dist, rng, (units, n, d)))
+    values = cases.f16(rng.normal(size=(units, n, d)))
+    queries = cases.f16(np.round(rng.normal(size=(units * G, d))) if dist != "normal" else rng.normal(size=(units * G, d)))
+    cfg = tkv.RetrievalConfig(64, 613, d_s)
+    lay = _sparse_layer(tkv, keys, values, cfg.n_local, keys_on_device=kod)
+    chans = np.stack([np.sort(rng.choice(d, d_s, replace=False)) for _ in range(units)]).astype(np.int32)
+    res = _decode_once(tkv, lay, queries, chans, G, cfg, kod)
+    assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5
+
+
+@pytest.mark.parametrize("d,G", [(64, 8), (128, 8), (32, 2), (256, 4)])
+def test_fused_sparse_decode_shapes(tkv, d, G):
+    rng = np.random.default_rng(32)
+    units, n = 2, 3000
+    keys = cases.f16(rng.normal(size=(units, n, d)))
+    values = cases.f16(rng.normal(size=(units, n, d)))
+    queries = cases.f16(rng.normal(size=(units * G, d)))
+    cfg = tkv.RetrievalConfig(16, 100, min(8, d))
+    lay = _sparse_layer(tkv, keys, values, cfg.n_local, keys_on_device=True)
+    chans = np.stack([np.sort(rng.choice(d, cfg.d_s, replace=False)) for _ in range(units)]).astype(np.int32)
+    res = _decode_once(tkv, lay, queries, chans, G, cfg, True)
+    assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [300, 130, 70, 40])
+def test_fused_sparse_decode_select_all(tkv, n):
+    """n <= n_local + n_topk: every token is attended (retriever.py:204-205),
+    including contexts shorter than the cluster's slices."""
+    rng = np.random.default_rng(33)
+    units, d, G = 2, 128, 4
+    keys = cases.f16(rng.normal(size=(units, n, d)))
+    values = cases.f16(rng.normal(size=(units, n, d)))
+    queries = cases.f16(rng.normal(size=(units * G, d)))
+    cfg = tkv.RetrievalConfig(64, 400, 8)
+    lay = _sparse_layer(tkv, keys, values, cfg.n_local, keys_on_device=True)
+    chans = np.stack([np.arange(8) for _ in range(units)]).astype(np.int32)
+    res = _decode_once(tkv, lay, queries, chans, G, cfg, True)
+    assert res[1].tolist() == [n, n]
+    assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5
+
+
+def test_fused_sparse_decode_row_cache_across_steps(tkv):
+    """Decode -> append -> decode ... with the HBM row cache: rows served from
+    the cache give the same results as the oracle at every step."""
+    rng = np.random.default_rng(34)
+    units, n0, d, G, T = 2, 8000, 128, 4, 6
+    keys = cases.f16(rng.normal(size=(units, n0 + T, d)))
+    values = cases.f16(rng.normal(size=(units, n0 + T, d)))
+    cfg = tkv.RetrievalConfig(32, 400, 8)
+    lay = _sparse_layer(tkv, keys[:, :n0], values[:, :n0], cfg.n_local, steps=T, keys_on_device=True,
+                        cache_rows=cfg.n_local + cfg.n_topk)
+    chans = np.stack([np.sort(rng.choice(d, 8, replace=False)) for _ in range(units)]).astype(np.int32)
+    base_q = rng.normal(size=(units * G, d))
+    for t in range(T):
+        n = n0 + t
+        queries = cases.f16(base_q + 0.3 * rng.normal(size=base_q.shape))  # correlated steps -> cache hits
+        res = _decode_once(tkv, lay, queries, chans, G, cfg, True)
+        assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5, t
+        lay.append(torch.tensor(keys[:, n], dtype=torch.float16, device="cuda"),
+                   torch.tensor(values[:, n], dtype=torch.float16, device="cuda"))
+    hits, misses = lay.cache_counters()
+    assert hits > 0 and misses > 0
+
+
+def test_fused_sparse_decode_128k(tkv):
+    """Config-2 head shape (131072 tokens, n_topk 2621, d_s 8) against the
+    oracle for two heads."""
+    rng = np.random.default_rng(35)
+    units, n, d, G = 2, 131072, 128, 4
+    keys = cases.f16(rng.normal(0, 1 / np.sqrt(d), size=(units, n, d)))
+    values = cases.f16(rng.normal(size=(units, n, d)))
+    queries = cases.f16(rng.normal(size=(units * G, d)))
+    cfg = tkv.RetrievalConfig(64, 2621, 8)
+    lay = _sparse_layer(tkv, keys, values, cfg.n_local, keys_on_device=True)
+    chans = np.stack([np.sort(rng.choice(d, 8, replace=False)) for _ in range(units)]).astype(np.int32)
+    res = _decode_once(tkv, lay, queries, chans, G, cfg, True)
+    assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5
 
 
 def test_host_store_gather_roundtrip(tkv):

@@ -1,5 +1,6 @@
 """Drive one sparsity-friendly layer at config-2 shapes (128k, 8 KV heads,
-G=4, n_topk=2621, d_s=8) for ncu: select (scores + top-k) then gather+attend."""
+G=4, n_topk=2621, d_s=8): the fused decode (one launch) against select then
+gather+attend, event-timed, plus stage 1.   python tools/prof_sparse.py [kfh]"""
 import sys, torch
 sys.path.insert(0, ".")
 import paper_2505_19586_b200 as P
@@ -17,26 +18,32 @@ ch = torch.stack([torch.randperm(d, generator=g, device="cuda")[:8].sort().value
 kmax = cfg.n_local + cfg.n_topk
 lib = _lib.load()
 ws = torch.zeros(int(lib.tkv_select_workspace(h, lay.capacity)), dtype=torch.uint8, device="cuda")
+dws = torch.zeros(int(lib.tkv_sparse_decode_workspace(h, lay.capacity, G, d, kmax)), dtype=torch.uint8, device="cuda")
 idx = torch.zeros((h, kmax), dtype=torch.int32, device="cuda")
 cnt = torch.zeros(h, dtype=torch.int32, device="cuda"); fc = torch.zeros_like(cnt)
 out = torch.zeros((h * G, d), dtype=torch.float32, device="cuda")
 aws = torch.zeros(int(lib.tkv_sparse_attn_workspace(h, G, d, kmax)), dtype=torch.uint8, device="cuda")
-def run():
-    lay.select(q, ch, G, cfg, idx, cnt, fc, ws)
-    lay.attend(q, G, cfg, idx, cnt, out, aws, keys_from_device=bool(kfh))
-for _ in range(3): run()
-torch.cuda.synchronize()
-ts_s, ts_a = [], []
-for _ in range(20):
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    e[0].record(); lay.select(q, ch, G, cfg, idx, cnt, fc, ws); e[1].record()
-    lay.attend(q, G, cfg, idx, cnt, out, aws, keys_from_device=bool(kfh)); e[2].record()
-    torch.cuda.synchronize(); ts_s.append(e[0].elapsed_time(e[1])); ts_a.append(e[1].elapsed_time(e[2]))
+kd = bool(kfh)
+ops = {
+    "fused": lambda: lay.decode(q, ch, G, cfg, idx, cnt, fc, out, dws, keys_from_device=kd),
+    "select": lambda: lay.select(q, ch, G, cfg, idx, cnt, fc, ws),
+    "attend": lambda: lay.attend(q, G, cfg, idx, cnt, out, aws, keys_from_device=kd),
+}
 m = lambda x: sorted(x)[len(x) // 2] * 1e3
+for name, fn in ops.items():
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()  # graph of 10 launches: no host gaps
+    with torch.cuda.graph(gr):
+        for _ in range(10): fn()
+    ts = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); gr.replay(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b) / 10)
+    print(f"{name:8s} {m(ts):7.1f} us")
 rows = int(fc.sum())
-print(f"select {m(ts_s):.1f} us; gather+attend {m(ts_a):.1f} us; fetched rows {rows}; "
-      f"PCIe bytes {rows * d * 2 * (1 if kfh else 2) / 1e6:.2f} MB -> {rows * d * 2 * (1 if kfh else 2) / (m(ts_a) * 1e-6) / 1e9:.1f} GB/s")
-# stage 1 alone: q_hat = h W_q (32 x 4096 x 128) + channel select, float64
+by = rows * d * 2 * (1 if kfh else 2)
+print(f"fetched rows {rows}; PCIe bytes {by / 1e6:.2f} MB")
 H = 4096
 w_q = (torch.randn(h * G, H, d, generator=g, device="cuda") / H ** 0.5).half()
 hid = torch.randn(1, H, generator=g, device="cuda").half()
@@ -48,10 +55,15 @@ for _ in range(20):
     a.record(); P.stage1_select(hid, w_q, lay.chmax, G, 8); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 print(f"stage1 {m(ts):.1f} us -> {w_q.numel() * 2 / (m(ts) * 1e-6) / 1e9:.0f} GB/s")
-import ctypes as C
-ph = (C.c_ulonglong * 8)()
-lay.select(q, ch, G, cfg, idx, cnt, fc, ws); torch.cuda.synchronize()
-lib.tkv_debug_select_phases(ph)
-t = list(ph)
-print("select phases (us): score %.1f minmax %.1f radix %.1f (passes %d) flags %.1f output %.1f" % (
-    (t[1]-t[0])/1e3, (t[2]-t[1])/1e3, (t[3]-t[2])/1e3, t[6], (t[4]-t[3])/1e3, (t[5]-t[4])/1e3))
+from tools.fz_phases import show, enable
+from paper_2505_19586_b200 import _lib as _L
+enable(_L.load())
+gr = torch.cuda.CUDAGraph()
+with torch.cuda.graph(gr):
+    for _ in range(10): ops["fused"]()
+ts = []
+for _ in range(10):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); gr.replay(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b) / 10)
+print(f"fused with phase marks {m(ts):7.1f} us")
+show(_L.load())
