@@ -41,6 +41,9 @@ def parse():
                     help="headline with K and V rows both gathered over PCIe (the reference's fetch_topk transfer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="sparse layers as two launches (select, gather+attend)")
+    ap.add_argument("--phases", action="store_true", help="print the fused sparse kernel's phase marks (unit 0)")
+    ap.add_argument("--cache-steps", type=int, default=4,
+                    help="HBM row cache window: a value row stays resident until unselected for this many steps (0: off)")
     ap.add_argument("--seed", type=int, default=2505)
     return ap.parse_args()
 
@@ -271,10 +274,11 @@ def main():
     L, n = model.num_layers, args.ctx
     n_topk = round(args.topk_frac * n)
     cfg = P.EngineConfig(bits=1, group_size=64, n_local=64, n_topk=n_topk, critical_channels=8,
-                         keys_from_hbm=not args.keys_over_pcie, fused_sparse=not args.unfused)
+                         keys_from_hbm=not args.keys_over_pcie, fused_sparse=not args.unfused,
+                         row_cache=args.cache_steps > 0, row_cache_steps=max(1, args.cache_steps))
     W, K = args.warmup, args.steps
     PROF = 2
-    total = W + 3 * K + 2 * PROF + 4
+    total = W + 3 * K + 2 * PROF + 8
     t_setup = time.time()
     wl = make_workload(L, (0, 1), model.num_query_heads, model.num_kv_heads, model.head_dim, n, total,
                        batch=1, seed=args.seed, device=device)
@@ -293,11 +297,9 @@ def main():
 
     # per-kernel profile: the step graph captured with an event-record node
     # around every kernel group, replayed like the timed graph (no host gaps)
-    def profile_mode(from_hbm):
+    def profile_mode():
         nonlocal step_i
-        eng.keys_from_hbm = from_hbm
         eng.capture_profiled()
-        eng.load_step(*inputs(step_i)); eng.replay_profiled(); step_i += 1  # settle the row cache in this mode
         res = {}
         c0 = eng.cache_counters()
         for _ in range(PROF):
@@ -308,16 +310,12 @@ def main():
         c1 = eng.cache_counters()
         return res, c1[0] - c0[0], c1[1] - c0[1]
 
-    prof_alt, _, _ = profile_mode(args.keys_over_pcie)  # the other key-row source
-    prof, hits, misses = profile_mode(not args.keys_over_pcie)
     n_sparse = sum(1 for x in wl.labels if x == "s")
-    fetch_rows = int(eng.fetch_count.sum().item())
-    cached_rows = hits / (PROF * n_sparse)     # per launch, served from the HBM row cache
-    pcie_rows = misses / (PROF * n_sparse)     # per launch, fetched over PCIe
-
-    # variant: the other key-row source, graph-timed for K steps
+    # variant: the other key-row source, graph-timed for K steps, then profiled
     eng.keys_from_hbm = args.keys_over_pcie
     eng.capture()
+    for _ in range(2):
+        eng.step(*inputs(step_i)); step_i += 1
     torch.cuda.synchronize()
     sv, ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sv.record()
@@ -326,6 +324,7 @@ def main():
     ev.record()
     torch.cuda.synchronize()
     ms_variant = sv.elapsed_time(ev) / K
+    prof_alt, _, _ = profile_mode()
 
     eng.keys_from_hbm = not args.keys_over_pcie
     eng.capture()
@@ -339,6 +338,7 @@ def main():
 
     # ---- device-resident timing (value) ----
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tc0 = eng.cache_counters()
     with ClockSampler(local) as clocks:
         barrier(); torch.cuda.synchronize()
         start.record()
@@ -347,6 +347,8 @@ def main():
         end.record()
         torch.cuda.synchronize(); barrier()
     ms = start.elapsed_time(end) / K
+    t_hits, t_misses = eng.cache_counters()
+    t_hits, t_misses = t_hits - tc0[0], t_misses - tc0[1]
 
     # ---- end-to-end: pinned host inputs in, outputs back to host, every step ----
     host_in = [tuple(x.cpu().pin_memory() for x in inputs(step_i + k)) for k in range(K)]
@@ -364,6 +366,18 @@ def main():
     e2.record()
     torch.cuda.synchronize(); barrier()
     ms_e2e = s2.elapsed_time(e2) / K
+
+    # per-kernel profile of the main mode, steady state (after the timed steps)
+    if args.phases:
+        _lib.load().tkv_debug_sparse_trace(1)
+    prof, hits, misses = profile_mode()
+    if args.phases and rank == 0:
+        from tools.fz_phases import show
+        _lib.load().tkv_debug_sparse_trace(0)
+        show(_lib.load())
+    fetch_rows = int(eng.fetch_count.sum().item())
+    cached_rows = hits / (PROF * n_sparse)     # per launch, served from the HBM row cache
+    pcie_rows = misses / (PROF * n_sparse)     # per launch, fetched over PCIe
 
     if world > 1:
         t = torch.tensor([ms, ms_e2e], device=device)
@@ -426,9 +440,11 @@ def main():
                      "frac": dom["frac"], "traffic": None, "kernel": dom["kernel"],
                      "timing": "CUDA events recorded as graph nodes around the kernel inside the replayed step"},
         "rooflines": rooflines,
-        "row_cache": {"rows_per_gather_from_hbm_cache": cached_rows, "rows_per_gather_over_pcie": pcie_rows,
-                      "hit_rate": cached_rows / max(1.0, cached_rows + pcie_rows),
-                      "note": "value rows fetched at step t-1 stay in HBM; exact (rows never change)"},
+        "row_cache": {"window_steps": cfg.row_cache_steps, "slots_per_head": (eng.retrieval.n_local + eng.retrieval.n_topk) * cfg.row_cache_steps,
+                      "timed_region_hit_rate": t_hits / max(1, t_hits + t_misses),
+                      "timed_region_pcie_value_bytes_per_token": t_misses * model.head_dim * 2 / K,
+                      "rows_per_launch_from_hbm_cache": cached_rows, "rows_per_launch_over_pcie": pcie_rows,
+                      "note": "value rows selected in the last window_steps steps stay in HBM; exact (rows never change)"},
         "pcie": {"memcpy_h2d_gbs": memcpy_gbs, "uva_512B_rows_gbs": uva_gbs, "uva_256B_rows_gbs": uva256_gbs,
                  "gather_bytes_per_token": gather_bytes * n_sparse, "fetched_rows_per_layer": fetch_rows,
                  "reference_fetch_topk_bytes_per_token": O.gather_bytes(fetch_rows, model.head_dim) * n_sparse},

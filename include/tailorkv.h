@@ -45,6 +45,12 @@ int tkv_abi_version(void);
  * graph being captured on that stream (cudaEventRecordExternal), so kernels
  * can be timed inside a replayed decode-step graph. */
 int tkv_event_record(void *event, void *stream, int32_t external);
+/* Instantiate a captured decode-step graph (cudaGraph_t) so that kernel
+ * nodes run at their launch priorities (the attention chain above stage 1 of
+ * the next layer); launch / destroy the executable graph. */
+int tkv_graph_instantiate(void *graph, void **exec);
+int tkv_graph_launch(void *exec, void *stream);
+int tkv_graph_destroy(void *exec);
 
 /* ------------------------------------------------------------------------
  * Quantized layer cache (quantizer.py:187-497)
@@ -130,16 +136,17 @@ typedef struct tkv_sparse_layer {
   uint16_t *host_kv;      /* pinned host store [units][capacity][2][d] (K row | V row) */
   int32_t *len;           /* device scalar */
   uint32_t *ticket;       /* device scalar scratch */
-  /* Optional step-to-step value-row cache (NULL cache_v disables it): the
-   * value rows fetched over PCIe at the previous step stay in HBM; a row
-   * selected again is read from there.  Rows never change once written, so
-   * any cached (index, row) pair stays valid. */
-  int32_t cache_rows;     /* rows per unit and buffer (>= n_local + n_topk) */
-  int32_t *cache_idx;     /* [2][units][cache_rows] ascending token indices */
-  int32_t *cache_cnt;     /* [2][units] */
-  uint16_t *cache_v;      /* [2][units][cache_rows][d] */
-  int32_t *cache_cur;     /* device scalar: buffer holding the previous step */
-  int32_t *cache_map;     /* [units][capacity] token -> last cache position (verified on use) */
+  /* Optional HBM value-row cache (cache_slots == 0 disables it): a value row
+   * fetched over PCIe stays in a slot until it has not been selected for
+   * cache_window steps; a row selected again is read from HBM.  Rows never
+   * change once written, so a cached (token, row) pair stays exact.  Needs
+   * cache_slots >= cache_window * (n_local + n_topk). */
+  int32_t cache_slots;    /* slots per unit */
+  int32_t cache_window;   /* steps a selected row stays resident */
+  int32_t *slot_tok;      /* [units][cache_slots] token held by the slot, -1 when empty */
+  int32_t *slot_stamp;    /* [units][cache_slots] *len at the row's last selection */
+  uint16_t *slot_v;       /* [units][cache_slots][d] cached value rows */
+  int32_t *tok_slot;      /* [units][capacity] token -> slot, verified against slot_tok */
   unsigned long long *cache_stats; /* [2]: rows served from HBM, rows fetched over PCIe */
 } tkv_sparse_layer;
 

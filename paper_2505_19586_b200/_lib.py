@@ -57,8 +57,8 @@ class SparseLayer(C.Structure):
         ("capacity", C.c_int64), ("local_offset", C.c_int64), ("local_capacity", C.c_int64),
         ("kt", C.c_void_p), ("chmax", C.c_void_p), ("loc_k", C.c_void_p), ("loc_v", C.c_void_p),
         ("kdev", C.c_void_p), ("host_kv", C.c_void_p), ("len", C.c_void_p), ("ticket", C.c_void_p),
-        ("cache_rows", C.c_int32), ("cache_idx", C.c_void_p), ("cache_cnt", C.c_void_p), ("cache_v", C.c_void_p),
-        ("cache_cur", C.c_void_p), ("cache_map", C.c_void_p), ("cache_stats", C.c_void_p),
+        ("cache_slots", C.c_int32), ("cache_window", C.c_int32), ("slot_tok", C.c_void_p), ("slot_stamp", C.c_void_p),
+        ("slot_v", C.c_void_p), ("tok_slot", C.c_void_p), ("cache_stats", C.c_void_p),
     ]
 
 
@@ -69,6 +69,9 @@ _SIGS = {
     "tkv_last_error": (C.c_char_p, []),
     "tkv_abi_version": (C.c_int, []),
     "tkv_event_record": (C.c_int, [_P, _P, _I32]),
+    "tkv_graph_instantiate": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "tkv_graph_launch": (C.c_int, [_P, _P]),
+    "tkv_graph_destroy": (C.c_int, [_P]),
     "tkv_qcache_sizes": (C.c_int, [_I32, _I32, _I32, _I32, _I64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "tkv_qcache_pack": (C.c_int, [C.POINTER(QCache), _P, _P, _I64, _I32, _P]),
     "tkv_qcache_append": (C.c_int, [C.POINTER(QCache), _P, _P, _P]),

@@ -51,6 +51,26 @@ extern "C" {
 const char *tkv_last_error(void) { return g_err.c_str(); }
 int tkv_abi_version(void) { return 1; }
 
+int tkv_graph_instantiate(void *graph, void **exec) {
+  cudaGraphExec_t e = nullptr;
+  const cudaError_t r = cudaGraphInstantiateWithFlags(&e, static_cast<cudaGraph_t>(graph),
+                                                      cudaGraphInstantiateFlagUseNodePriority);
+  if (r != cudaSuccess) return fail(TKV_ERR_CUDA, std::string("tkv_graph_instantiate: ") + cudaGetErrorString(r));
+  *exec = e;
+  return TKV_OK;
+}
+
+int tkv_graph_launch(void *exec, void *stream) {
+  const cudaError_t r = cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), as_stream(stream));
+  if (r != cudaSuccess) return fail(TKV_ERR_CUDA, std::string("tkv_graph_launch: ") + cudaGetErrorString(r));
+  return TKV_OK;
+}
+
+int tkv_graph_destroy(void *exec) {
+  cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
+  return TKV_OK;
+}
+
 int tkv_event_record(void *event, void *stream, int32_t external) {
   const cudaError_t e = external ? cudaEventRecordWithFlags(static_cast<cudaEvent_t>(event), as_stream(stream),
                                                             cudaEventRecordExternal)

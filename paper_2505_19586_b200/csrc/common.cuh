@@ -23,6 +23,36 @@ int check_launch(const char *what);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- launch priorities ----
+// The decode chain (attention kernels, appends) launches at the device's
+// greatest priority and stage 1 of the next layer (side stream) at the least,
+// so when both become ready together the CTA scheduler places the chain's
+// kernels first and stage 1 fills the remaining SMs.  Captured graphs keep
+// these as node priorities (instantiated with UseNodePriority, abi.cu).
+inline int launch_priority(bool high) {
+  static int lo = 1, hi = 1;
+  if (lo == 1) {
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) lo = hi = 0;
+  }
+  return high ? hi : lo;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_prio(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               bool high, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = launch_priority(high);
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- numeric helpers ----
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }

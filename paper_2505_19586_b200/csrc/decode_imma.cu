@@ -498,10 +498,10 @@ int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *w
                            : nullptr;
   if (c.bits == 1) {
     cudaFuncSetAttribute(quant_decode_imma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    quant_decode_imma_kernel<1><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks, arrive, out);
+    launch_prio(quant_decode_imma_kernel<1>, grid, dim3(IM_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, chunks, arrive, out);
   } else {
     cudaFuncSetAttribute(quant_decode_imma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    quant_decode_imma_kernel<2><<<grid, IM_WARPS * 32, sm, st>>>(c, q, G, pm, pl, pacc, chunks, arrive, out);
+    launch_prio(quant_decode_imma_kernel<2>, grid, dim3(IM_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, chunks, arrive, out);
   }
   if (!fused) launch_combine_scalar(pm, pl, pacc, c.units, chunks, G, c.d, c.len, CH, out, st);
   return check_launch("tkv_quant_decode(imma)");

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(256) append_kernel(QC c, const uint16_t *__res
 int append(const QC &c, const uint16_t *nk, const uint16_t *nv, cudaStream_t st) {
   const size_t sm = ((c.d + 15) & ~15) + 64 * 4 + (size_t)c.g * c.d;
   cudaFuncSetAttribute(append_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  append_kernel<<<c.units, 256, sm, st>>>(c, nk, nv);
+  launch_prio(append_kernel, dim3(c.units), dim3(256), sm, st, true, c, nk, nv);
   return check_launch("tkv_qcache_append");
 }
 

@@ -117,7 +117,6 @@ __global__ void sparse_append_kernel(SL s, const uint16_t *__restrict__ nk, cons
     const unsigned prev = atomicAdd(s.ticket, 1u);
     if (prev == (unsigned)gridDim.x - 1) {
       *s.ticket = 0;
-      if (s.cache_cur) *s.cache_cur ^= 1;  // this step's fetched rows become "previous"
       __threadfence();
       *s.len = (int32_t)(n + 1);
     }
@@ -125,7 +124,7 @@ __global__ void sparse_append_kernel(SL s, const uint16_t *__restrict__ nk, cons
 }
 
 int sparse_append(const SL &s, const uint16_t *nk, const uint16_t *nv, cudaStream_t st) {
-  sparse_append_kernel<<<s.units, 128, 0, st>>>(s, nk, nv);
+  launch_prio(sparse_append_kernel, dim3(s.units), dim3(128), 0, st, true, s, nk, nv);
   return check_launch("tkv_sparse_append");
 }
 
@@ -321,11 +320,11 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
   unsigned *arrive = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + pbytes);
   const int bg = B == 1 ? 1 : S1_BG;
   const dim3 grid((H + rows - 1) / rows, hq, (B + bg - 1) / bg);
-#define TKV_S1(DD)                                                                                               \
-  (B == 1 ? stage1_fused_kernel<DD, 1><<<grid, S1_THREADS, 0, st>>>(hidden, w_q, B, H, rows, part, arrive, G, chmax, \
-                                                                   d_s, q_hat, channels)                         \
-          : stage1_fused_kernel<DD, S1_BG><<<grid, S1_THREADS, 0, st>>>(hidden, w_q, B, H, rows, part, arrive, G,   \
-                                                                       chmax, d_s, q_hat, channels))
+#define TKV_S1(DD)                                                                                              \
+  (B == 1 ? launch_prio(stage1_fused_kernel<DD, 1>, grid, dim3(S1_THREADS), 0, st, false, hidden, w_q, B, H, rows, \
+                        part, arrive, G, chmax, d_s, q_hat, channels)                                            \
+          : launch_prio(stage1_fused_kernel<DD, S1_BG>, grid, dim3(S1_THREADS), 0, st, false, hidden, w_q, B, H,  \
+                        rows, part, arrive, G, chmax, d_s, q_hat, channels))
   switch (d) {
     case 128: TKV_S1(128); break;
     case 64: TKV_S1(64); break;
@@ -715,39 +714,14 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
 #pragma unroll
     for (int e = 0; e < CPL; ++e)
       q[h][e] = h < G ? h2f(queries[((size_t)u * G + h) * D + lane * CPL + e]) : 0.0f;
-  // step-to-step value-row cache: lane j < SA_RPW binary-searches row j of
-  // this warp among the rows fetched at the previous step
-  const bool use_cache = s.cache_v != nullptr && keys_from_device;
-  int prevc = 0, pcnt = 0;
-  const int32_t *pidx = nullptr;
-  if (use_cache) {
-    prevc = *s.cache_cur;
-    pcnt = s.cache_cnt[prevc * s.units + u];
-    pidx = s.cache_idx + ((size_t)prevc * s.units + u) * s.cache_rows;
-  }
-  int my_pos = -1;
-  if (use_cache && lane < SA_RPW) {
-    // token -> cache-position table (no clearing needed: an entry is trusted
-    // only if the previous buffer really holds that token at that position)
-    const int r = r0 + warp * SA_RPW + lane;
-    if (r < cnt) {
-      const int key = sel_idx[(size_t)u * sel_stride + r];
-      if (key < local_start) {
-        const int pos = s.cache_map[(size_t)u * s.capacity + key];
-        if (pos >= 0 && pos < pcnt && __ldcg(&pidx[pos]) == key) my_pos = pos;
-      }
-    }
-  }
   // issue every row load of this warp first (PCIe latency hiding)
   constexpr int CPW = (CPL + 1) / 2;  // 32-bit words per lane per row
   uint32_t kw[SA_RPW][CPW], vw[SA_RPW][CPW];
   int valid[SA_RPW], fetched[SA_RPW];
   int64_t rowidx[SA_RPW];
-  int nhit = 0;
 #pragma unroll
   for (int j = 0; j < SA_RPW; ++j) {
     const int r = r0 + warp * SA_RPW + j;
-    const int pos = __shfl_sync(0xffffffffu, my_pos, j);
     valid[j] = r < cnt;
     fetched[j] = 0;
 #pragma unroll
@@ -760,9 +734,7 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
       // key row straight from the channel-major HBM copy the scorer uses
       // (scattered 2-byte reads, no extra memory); value row over PCIe
       vp = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D + D;
-      if (pos >= 0) vp = s.cache_v + (((size_t)prevc * s.units + u) * s.cache_rows + pos) * D;
       fetched[j] = 1;
-      nhit += pos >= 0;
 #pragma unroll
       for (int e = 0; e < CPL; ++e)
         kw[j][e >> 1] |= (uint32_t)s.kt[((size_t)u * D + lane * CPL + e) * s.capacity + idx] << (16 * (e & 1));
@@ -778,9 +750,8 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
     if (idx < local_start) {
       const uint16_t *row = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
       kp = keys_from_device ? s.kdev + ((size_t)u * s.capacity + idx) * D : row;
-      vp = pos >= 0 ? s.cache_v + (((size_t)prevc * s.units + u) * s.cache_rows + pos) * D : row + D;
+      vp = row + D;
       fetched[j] = 1;
-      nhit += pos >= 0;
     } else {
       const int64_t lr = idx - s.local_offset;
       kp = s.loc_k + ((size_t)u * s.local_capacity + lr) * D;
@@ -802,34 +773,6 @@ __global__ void __launch_bounds__(SA_WARPS * 32) sparse_attn_kernel(SL s, const 
         kw[j][e >> 1] |= (uint32_t)kp[lane * CPL + e] << (16 * (e & 1));
         vw[j][e >> 1] |= (uint32_t)vp[lane * CPL + e] << (16 * (e & 1));
       }
-    }
-  }
-  if (use_cache) {
-    // this step's fetched rows become the next step's cache (same positions)
-    const int nxt = prevc ^ 1;
-    uint16_t *cv = s.cache_v + ((size_t)nxt * s.units + u) * s.cache_rows * D;
-    int32_t *ci = s.cache_idx + ((size_t)nxt * s.units + u) * s.cache_rows;
-    int nf = 0;
-#pragma unroll
-    for (int j = 0; j < SA_RPW; ++j) {
-      if (!valid[j] || !fetched[j]) continue;
-      const int r = r0 + warp * SA_RPW + j;
-      ++nf;
-      if (lane == 0) {
-        ci[r] = (int32_t)rowidx[j];
-        s.cache_map[(size_t)u * s.capacity + rowidx[j]] = r;
-      }
-      if constexpr (CPL == 4) {
-        *reinterpret_cast<uint2 *>(cv + (size_t)r * D + lane * 4) = make_uint2(vw[j][0], vw[j][1]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < CPL; ++e) cv[(size_t)r * D + lane * CPL + e] = (uint16_t)(vw[j][e >> 1] >> (16 * (e & 1)));
-      }
-    }
-    if (chunk == 0 && warp == 0 && lane == 0) s.cache_cnt[nxt * s.units + u] = cnt - (int)(n - local_start);
-    if (lane == 0 && nf) {
-      atomicAdd(&s.cache_stats[0], (unsigned long long)nhit);
-      atomicAdd(&s.cache_stats[1], (unsigned long long)(nf - nhit));
     }
   }
   float m[GMAX], l[GMAX], acc[GMAX][CPL];

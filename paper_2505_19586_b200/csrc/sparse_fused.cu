@@ -617,7 +617,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       __syncthreads();
       if (pass == 0) FZ_MARK(22);
       int above = 0;
-#pragma unroll
+      const uint32_t ord_lo = fz_orderable32(r_lo), ord_hi = fz_orderable32(r_hi), ord_w = ord_hi - ord_lo;
+#pragma unroll 1
       for (int g = 0; g < FZ_KG; ++g) {
         const int e = g * FZ_STEP + tid * 8;
         if (e >= m) break;
@@ -625,17 +626,15 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         fz_load8(keys32, e, m, kk);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          if (e + q >= m) break;
-          const float x = fz_from_orderable32(kk[q]);
-          if (x > r_hi) {
-            ++above;
-          } else if (x >= r_lo) {
+          const bool valid = e + q < m;
+          above += valid && kk[q] > ord_hi;                         // integer compares on the orderable keys
+          if (valid && kk[q] - ord_lo <= ord_w) {                   // inside [r_lo, r_hi] (rare when aimed)
+            const float x = fz_from_orderable32(kk[q]);
             const int b = min(FZ_NB - 1, max(0, (int)((x - r_lo) * scale)));
             atomicAdd(&H[b], 1u);
           }
         }
       }
-      if (pass == 0) FZ_MARK(23);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
       if (lane == 0 && above) atomicAdd(&H[FZ_NB], (unsigned)above);
@@ -717,7 +716,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     const float band_hi = __double2float_ru(R_hi + 2.0 * band_eps);
     const float band_lo = __double2float_rd(R_lo - 2.0 * band_eps);
     int definite = 0;
-#pragma unroll
+    const uint32_t ord_bhi = fz_orderable32(band_hi), ord_blo = fz_orderable32(band_lo);
+#pragma unroll 1
     for (int g = 0; g < FZ_KG; ++g) {
       const int e = g * FZ_STEP + tid * 8;
       if (e >= m) break;
@@ -726,24 +726,16 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       uint32_t fl[2] = {0u, 0u};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        if (e + q >= m) break;
-        const float x = fz_from_orderable32(kk[q]);
-        uint32_t f = 0;
-        if (x > band_hi) {
-          f = 1;
-          ++definite;
-        } else if (x >= band_lo) {
+        const bool valid = e + q < m;
+        const bool def = valid && kk[q] > ord_bhi;
+        const bool band = valid && !def && kk[q] >= ord_blo;
+        definite += def;
+        fl[q >> 2] |= (def ? 1u : band ? 3u : 0u) << (8 * (q & 3));
+        if (band) {  // rescored in float64 below, all band members at once
           const int slot = atomicAdd(&C.band_count, 1);
-          if (slot < FZ_BAND) {
-            const int64_t j = j0 + e + q;
-            S.k.f.band_key[slot] = orderable(fz_exact_score(kt, s.capacity, chs, qsum, d_s, j));
-            S.k.f.band_idx[slot] = (uint32_t)j;
-          } else {
-            C.overflow = 1;
-          }
-          f = 3;
+          if (slot < FZ_BAND) S.k.f.band_idx[slot] = (uint32_t)(j0 + e + q);
+          else C.overflow = 1;
         }
-        fl[q >> 2] |= f << (8 * (q & 3));
       }
       if (e + 8 <= m) {
         *reinterpret_cast<uint2 *>(flags + e) = make_uint2(fl[0], fl[1]);
@@ -751,6 +743,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         for (int q = 0; e + q < m; ++q) flags[e + q] = (uint8_t)(fl[q >> 2] >> (8 * (q & 3)));
       }
     }
+    __syncthreads();
+    for (int b = tid; b < min(C.band_count, FZ_BAND); b += blockDim.x)
+      S.k.f.band_key[b] = orderable(fz_exact_score(kt, s.capacity, chs, qsum, d_s, S.k.f.band_idx[b]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) definite += __shfl_xor_sync(0xffffffffu, definite, o);
     if (lane == 0) C.wk[0][warp] = (unsigned long long)definite;
@@ -873,7 +868,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
   const int nrows = cta_total + (rank == FZ_CTAS - 1 ? n_loc : 0);
   // row list (16-bit token offsets from rbase, local rows after the far ones) at the top of the overlaid region
   const int64_t rbase = rank == FZ_CTAS - 1 ? imin64(j0, ncand) : j0;
-  const int rows_bytes = ((nrows * 2 + 127) / 128) * 128;
+  // [16-bit row offsets | 32-bit cache slot codes] per row
+  const int rows_bytes = ((nrows * 2 + 127) / 128) * 128 + (ATTEND ? ((nrows * 4 + 127) / 128) * 128 : 0);
   uint16_t *rows = reinterpret_cast<uint16_t *>(S.k.raw + FZ_UNION - rows_bytes);
 #pragma unroll
   for (int g = 0; g < FZ_KG; ++g) {
@@ -914,7 +910,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     // in shared memory by TMA bulk copies, every row of a round at once
     // (one PCIe round trip); key rows come from HBM into registers while the
     // value copies are in flight; logits go to shared memory; then each warp
-    // runs an online softmax over its rows.
+    // runs an online softmax over its rows.  Rows fetched over PCIe are
+    // inserted into the HBM row cache (slots whose row was not selected in
+    // the last cache_window steps are reused).
     constexpr int CPL = D / 32;  // channels per lane
     const bool keys_host = !keys_from_device;
     const int row_bytes = D * 2 * (keys_host ? 2 : 1) + GMAX * 4;  // staged V (+K) + logits
@@ -922,18 +920,34 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     uint16_t *stage_v = reinterpret_cast<uint16_t *>(S.k.raw);
     uint16_t *stage_k = stage_v + (size_t)NR * D;  // used when keys cross PCIe
     float *zs = reinterpret_cast<float *>(S.k.raw + (size_t)NR * D * 2 * (keys_host ? 2 : 1));
+    int32_t *rslot = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(rows) + ((nrows * 2 + 127) / 128) * 128);
     const int64_t local_start = ncand;
-    const bool use_cache = s.cache_v != nullptr && keys_from_device;
-    int prevc = 0, pcnt = 0;
-    const int32_t *pidx = nullptr;
-    if (use_cache) {
-      prevc = *s.cache_cur;
-      pcnt = s.cache_cnt[prevc * s.units + u];
-      pidx = s.cache_idx + ((size_t)prevc * s.units + u) * s.cache_rows;
+    const bool use_cache = s.cache_slots > 0 && keys_from_device;
+    const int CS = s.cache_slots;
+    int32_t *stok = use_cache ? s.slot_tok + (size_t)u * CS : nullptr;
+    int32_t *sstamp = use_cache ? s.slot_stamp + (size_t)u * CS : nullptr;
+    uint16_t *sv = use_cache ? s.slot_v + (size_t)u * CS * D : nullptr;
+    int32_t *tslot = use_cache ? s.tok_slot + (size_t)u * s.capacity : nullptr;
+    // (0) row codes: >= 0 cached slot (hit, stamped with this step), -1 fetch over PCIe, -2 local mirror
+    int hits = 0, misses = 0;
+    for (int i = tid; i < nrows; i += blockDim.x) {
+      const int64_t idx = rbase + rows[i];
+      int code = -2;
+      if (idx < local_start) {
+        code = -1;
+        if (use_cache) {
+          const int p = tslot[idx];
+          if (p >= 0 && p < CS && stok[p] == (int)idx) {
+            code = p;
+            sstamp[p] = (int)n;
+          }
+        }
+        hits += code >= 0;
+        misses += code < 0;
+      }
+      rslot[i] = code;
     }
-    const int nxt = prevc ^ 1;
-    uint16_t *cv_next = use_cache ? s.cache_v + ((size_t)nxt * s.units + u) * s.cache_rows * D : nullptr;
-    int32_t *ci_next = use_cache ? s.cache_idx + ((size_t)nxt * s.units + u) * s.cache_rows : nullptr;
+    __syncthreads();
     float mrun[GMAX], lrun[GMAX], acc[GMAX][CPL];
 #pragma unroll
     for (int h = 0; h < GMAX; ++h) {
@@ -942,36 +956,84 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
 #pragma unroll
       for (int e = 0; e < CPL; ++e) acc[h][e] = 0.0f;
     }
-    int hits = 0, misses = 0;
-    uint32_t parity = 0;
-    for (int base = 0; base < nrows; base += NR) {
-      const int cnt = min(NR, nrows - base);
+    // (a) one thread per row issues the bulk copy of its value row (and key row over PCIe)
+    auto issue_round = [&](int base, int cnt) {
       if (tid == 0) fz_mbar_expect(&C.bar, (uint32_t)(cnt * D * 2 * (keys_host ? 2 : 1)));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses before the TMA writes
       __syncthreads();
-      // (a) one thread per row issues the bulk copy of its value row (and key row over PCIe)
       for (int i = tid; i < cnt; i += blockDim.x) {
         const int64_t idx = rbase + rows[base + i];
+        const int code = rslot[base + i];
         const uint16_t *vp;
-        if (idx < local_start) {
-          const uint16_t *hrow = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
-          int pos_c = -1;
-          if (use_cache) {
-            const int p = s.cache_map[(size_t)u * s.capacity + idx];
-            if (p >= 0 && p < pcnt && __ldcg(&pidx[p]) == idx) pos_c = p;
-          }
-          vp = pos_c >= 0 ? s.cache_v + (((size_t)prevc * s.units + u) * s.cache_rows + pos_c) * D : hrow + D;
-          hits += pos_c >= 0;
-          misses += pos_c < 0;
-          if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, hrow, D * 2, &C.bar);
-        } else {
+        if (code == -2) {
           const int64_t lr = idx - s.local_offset;
           vp = s.loc_v + ((size_t)u * s.local_capacity + lr) * D;
           if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, s.loc_k + ((size_t)u * s.local_capacity + lr) * D, D * 2,
                                      &C.bar);
+        } else {
+          const uint16_t *hrow = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
+          vp = code >= 0 ? sv + (size_t)code * D : hrow + D;
+          if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, hrow, D * 2, &C.bar);
         }
         fz_bulk_g2s(stage_v + (size_t)i * D, vp, D * 2, &C.bar);
       }
+    };
+    if (nrows > 0) issue_round(0, min(NR, nrows));
+    // cache slots for this step's misses (cluster-wide, while the copies fly)
+    if (use_cache) {
+      const int W = max(1, s.cache_window);
+      int32_t *F = reinterpret_cast<int32_t *>(S.flags);  // free-slot list (the flags are dead)
+      const int spc = (CS + FZ_CTAS - 1) / FZ_CTAS;
+      const int p0 = rank * spc, p1 = min(CS, p0 + spc);
+      const int per_t = (spc + FZ_THREADS - 1) / FZ_THREADS;
+      const int q0 = p0 + tid * per_t, q1 = min(p1, q0 + per_t);
+      int mt = misses;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mt += __shfl_xor_sync(0xffffffffu, mt, o);
+      if (lane == 0) C.wk[1][warp] = (unsigned long long)mt;
+      cluster.sync();  // every CTA's hit stamps are visible
+      int nf = 0;
+      for (int p = q0; p < q1; ++p) nf += stok[p] < 0 || sstamp[p] <= (int)n - W;
+      int ftot;
+      int fpos = fz_block_excl_scan(nf, C.scan, &ftot);
+      for (int p = q0; p < q1; ++p)
+        if (stok[p] < 0 || sstamp[p] <= (int)n - W) F[fpos++] = p;
+      if (tid == 0) {
+        int mtot = 0;
+        for (int w = 0; w < FZ_WARPS; ++w) mtot += (int)C.wk[1][w];
+        C.cta_count = ftot;
+        C.band_count = mtot;  // (reused) this CTA's misses
+      }
+      cluster.sync();
+      int fpre[FZ_CTAS + 1], mine_off = 0;
+      fpre[0] = 0;
+#pragma unroll
+      for (int r = 0; r < FZ_CTAS; ++r) {
+        const FzCtl *R = cluster.map_shared_rank(&C, r);
+        fpre[r + 1] = fpre[r] + R->cta_count;
+        if (r < rank) mine_off += R->band_count;
+      }
+      // ordinal of each miss inside this CTA: rows are visited in the (strided) lookup order
+      int tm = 0;
+      for (int i = tid; i < nrows; i += blockDim.x) tm += rslot[i] == -1;
+      int dummy;
+      int ord = mine_off + fz_block_excl_scan(tm, C.scan, &dummy);
+      for (int i = tid; i < nrows; i += blockDim.x) {
+        if (rslot[i] != -1) continue;
+        const int k = ord++;
+        if (k < fpre[FZ_CTAS]) {
+          int r = 0;
+          while (k >= fpre[r + 1]) ++r;
+          const int dst = cluster.map_shared_rank(F, r)[k - fpre[r]];
+          rslot[i] = -3 - dst;
+        }
+      }
+      __syncthreads();
+    }
+    uint32_t parity = 0;
+    for (int base = 0; base < nrows; base += NR) {
+      const int cnt = min(NR, nrows - base);
+      if (base > 0) issue_round(base, cnt);
       // (b) logits of this warp's rows: key rows from HBM while the value copies fly
       if (!keys_host) {
         for (int i0 = warp; i0 < cnt; i0 += FZ_WARPS * 8) {
@@ -1058,16 +1120,17 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           mrun[h] = mn;
         }
       }
-      // (e) this step's fetched value rows become the next step's cache, at their output rank
+      // (e) rows fetched over PCIe enter the HBM row cache in their assigned slots
       if (use_cache) {
         for (int i = tid; i < cnt; i += blockDim.x) {
-          const int li = base + i;
-          if (li >= cta_total) continue;  // local rows are not cached
-          const int r = offset + li;
-          const int32_t idx = (int32_t)(rbase + rows[li]);
-          ci_next[r] = idx;
-          s.cache_map[(size_t)u * s.capacity + idx] = r;
-          fz_bulk_s2g(cv_next + (size_t)r * D, stage_v + (size_t)i * D, D * 2);
+          const int code = rslot[base + i];
+          if (code > -3) continue;
+          const int dst = -3 - code;
+          const int32_t idx = (int32_t)(rbase + rows[base + i]);
+          stok[dst] = idx;
+          sstamp[dst] = (int)n;
+          tslot[idx] = dst;
+          fz_bulk_s2g(sv + (size_t)dst * D, stage_v + (size_t)i * D, D * 2);
         }
         fz_bulk_commit_wait_read();  // the staged rows are read before the next round overwrites them
       }
@@ -1083,7 +1146,6 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         atomicAdd(&C.hits, hits);
         atomicAdd(&C.misses, misses);
       }
-      if (rank == 0 && tid == 0) s.cache_cnt[nxt * s.units + u] = far_total;
     }
     FZ_MARK(16);
     __syncthreads();  // the staging area (aliased by the partials) is no longer read
@@ -1179,13 +1241,15 @@ static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, con
   cfg.blockDim = dim3(FZ_THREADS);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = FZ_CTAS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributePriority;
+  at[1].val.priority = launch_priority(true);
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, s, queries, G, channels, d_s, n_local, n_topk, sel_idx, n_local + n_topk,
                             sel_count, fetch_count, scores_out, keys_from_device, out);
 }
@@ -1204,6 +1268,7 @@ bool select_cluster_ok(const SL &s, int n_local) { return fused_ok(s, n_local); 
 
 bool sparse_decode_supported(const SL &s, int G, int n_local) {
   if (!fused_ok(s, n_local)) return false;
+  if ((s.cache_slots + FZ_CTAS - 1) / FZ_CTAS > FZ_CAP / 4) return false;  // free-slot list in the flags area
   return (s.d == 128 && G <= 8) || (s.d == 64 && G <= 8) || (s.d == 256 && G <= 4) || (s.d == 32 && G <= 8);
 }
 

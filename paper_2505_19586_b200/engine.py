@@ -44,7 +44,8 @@ class EngineConfig:
     keys_from_hbm: bool = True     # gather key rows from HBM; only V rows cross PCIe
     token_major_keys: bool = True  # keep a token-major HBM key copy for that gather (else read the scorer's
                                    # channel-major copy: no extra memory, 32x more DRAM sectors)
-    row_cache: bool = True         # keep the previous step's fetched value rows in HBM (exact; rows are immutable)
+    row_cache: bool = True         # keep fetched value rows in HBM (exact; rows are immutable)
+    row_cache_steps: int = 4       # a row stays cached until it has not been selected for this many steps
     fused_sparse: bool = True      # one launch per sparse layer (select + gather + attention); else two
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
@@ -104,6 +105,30 @@ def _label(x) -> str:
     if v in ("s", LayerKind.SPARSITY_FRIENDLY.value):
         return "s"
     raise ConfigError(f"unknown layer label {x!r}")
+
+
+class _PriorityGraph:
+    """A captured decode step instantiated by the library with per-node launch
+    priorities (cudaGraphInstantiateFlagUseNodePriority): the attention chain
+    is dispatched ahead of the next layer's stage 1 when both are ready.  The
+    torch graph object is kept alive: it owns the captured graph and the
+    memory pool of its allocations."""
+
+    def __init__(self, torch_graph: torch.cuda.CUDAGraph):
+        self.torch_graph = torch_graph
+        exe = C.c_void_p()
+        check(_lib.load().tkv_graph_instantiate(C.c_void_p(torch_graph.raw_cuda_graph()), C.byref(exe)))
+        self.exec = exe
+
+    def replay(self) -> None:
+        check(_lib.load().tkv_graph_launch(self.exec, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+    def __del__(self):
+        try:
+            if self.exec:
+                _lib.load().tkv_graph_destroy(self.exec)
+        except Exception:
+            pass
 
 
 @dataclass
@@ -198,7 +223,8 @@ class DecodeEngine:
             lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local,
                                    keys_on_device=self.cfg.keys_from_hbm and self.cfg.token_major_keys,
                                    device=self.device,
-                                   cache_rows=(self.retrieval.n_local + self.retrieval.n_topk) if self.cfg.row_cache else 0)
+                                   cache_rows=(self.retrieval.n_local + self.retrieval.n_topk) if self.cfg.row_cache else 0,
+                                   cache_window=self.cfg.row_cache_steps)
             lay.offload(k, v)
             w = as_f16(w_q, self.device)
             if w.shape[0] == self.model.num_query_heads:
@@ -352,12 +378,12 @@ class DecodeEngine:
         mirrors of the token counts are restored afterwards."""
         saved = [lay.n for lay in self.layers]
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
+        g = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(g):
             self._run_step()
         for lay, n in zip(self.layers, saved):
             lay.n = n
-        self.graph = g
+        self.graph = _PriorityGraph(g)
 
     def capture_profiled(self) -> None:
         """Capture the decode step with an event-record node around every
@@ -370,7 +396,7 @@ class DecodeEngine:
         torch.cuda.synchronize()
         saved = [lay.n for lay in self.layers]
         self._event_pool, self.profile = pool, []
-        g = torch.cuda.CUDAGraph()
+        g = torch.cuda.CUDAGraph(keep_graph=True)
         try:
             with torch.cuda.graph(g):
                 self._run_step()
@@ -379,7 +405,7 @@ class DecodeEngine:
         self._prof_spans, self.profile = self.profile, None
         for lay, n in zip(self.layers, saved):
             lay.n = n
-        self.prof_graph = g
+        self.prof_graph = _PriorityGraph(g)
 
     def replay_profiled(self) -> dict:
         """One step through the profiled graph; returns {name: [ms per launch]}."""

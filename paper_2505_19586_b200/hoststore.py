@@ -71,7 +71,8 @@ class OffloadedLayerKV:
     """One sparsity-friendly layer for ``units`` KV heads (batch x heads)."""
 
     def __init__(self, units: int, head_dim: int, capacity: int, prefill_len: int, n_local: int,
-                 keys_on_device: bool = False, numa_node: int | None = None, device=None, cache_rows: int = 0):
+                 keys_on_device: bool = False, numa_node: int | None = None, device=None, cache_rows: int = 0,
+                 cache_window: int = 1):
         _lib.require_cuda()
         dev = torch.device(device or "cuda")
         self.device = dev
@@ -91,24 +92,23 @@ class OffloadedLayerKV:
         self.host_kv = self.arena.as_tensor(units * self.capacity * 2 * d).view(units, self.capacity, 2, d)
         self._len = torch.zeros(2, dtype=torch.int32, device=dev)
         self.n = 0
-        # step-to-step value-row cache (rows fetched at the previous step stay in HBM)
-        self.cache_rows = int(cache_rows)
-        if self.cache_rows:
-            self.cache_idx = torch.zeros((2, units, self.cache_rows), dtype=torch.int32, device=dev)
-            self.cache_cnt = torch.zeros((2, units), dtype=torch.int32, device=dev)
-            self.cache_v = torch.zeros((2, units, self.cache_rows, d), dtype=torch.float16, device=dev)
-            self.cache_cur = torch.zeros(1, dtype=torch.int32, device=dev)
-            self.cache_map = torch.full((units, self.capacity), -1, dtype=torch.int32, device=dev)
+        # HBM value-row cache: rows selected within the last `cache_window` steps stay resident
+        self.cache_window = int(cache_window) if cache_rows else 0
+        self.cache_slots = int(cache_rows) * max(1, self.cache_window) if cache_rows else 0
+        if self.cache_slots:
+            self.slot_tok = torch.full((units, self.cache_slots), -1, dtype=torch.int32, device=dev)
+            self.slot_stamp = torch.full((units, self.cache_slots), -(1 << 30), dtype=torch.int32, device=dev)
+            self.slot_v = torch.zeros((units, self.cache_slots, d), dtype=torch.float16, device=dev)
+            self.tok_slot = torch.full((units, self.capacity), -1, dtype=torch.int32, device=dev)
             self.cache_stats = torch.zeros(2, dtype=torch.int64, device=dev)
         else:
-            self.cache_idx = self.cache_cnt = self.cache_v = self.cache_cur = self.cache_stats = None
-            self.cache_map = None
+            self.slot_tok = self.slot_stamp = self.slot_v = self.tok_slot = self.cache_stats = None
         self.struct = SparseLayer(units, d, self.capacity, self.local_offset, self.local_capacity,
                                   self.kt.data_ptr(), self.chmax.data_ptr(), self.loc_k.data_ptr(),
                                   self.loc_v.data_ptr(), ptr(self.kdev), self.arena.addr,
                                   self._len.data_ptr(), self._len.data_ptr() + 4,
-                                  self.cache_rows, ptr(self.cache_idx), ptr(self.cache_cnt), ptr(self.cache_v),
-                                  ptr(self.cache_cur), ptr(self.cache_map), ptr(self.cache_stats))
+                                  self.cache_slots, self.cache_window, ptr(self.slot_tok), ptr(self.slot_stamp),
+                                  ptr(self.slot_v), ptr(self.tok_slot), ptr(self.cache_stats))
 
     @property
     def keys_on_device(self) -> bool:

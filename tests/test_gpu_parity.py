@@ -219,9 +219,10 @@ def test_stage1_estimate_matches_oracle(tkv):
             assert np.array_equal(ch[b * 2 + kvh], ref)
 
 
-def _sparse_layer(tkv, keys, values, n_local, steps=4, keys_on_device=False, cache_rows=0):
+def _sparse_layer(tkv, keys, values, n_local, steps=4, keys_on_device=False, cache_rows=0, cache_window=1):
     units, n, d = keys.shape
-    lay = tkv.OffloadedLayerKV(units, d, n + steps, n, n_local, keys_on_device=keys_on_device, cache_rows=cache_rows)
+    lay = tkv.OffloadedLayerKV(units, d, n + steps, n, n_local, keys_on_device=keys_on_device, cache_rows=cache_rows,
+                               cache_window=cache_window)
     lay.offload(keys, values)
     return lay
 
@@ -393,16 +394,18 @@ def test_fused_sparse_decode_select_all(tkv, n):
     assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5
 
 
-def test_fused_sparse_decode_row_cache_across_steps(tkv):
-    """Decode -> append -> decode ... with the HBM row cache: rows served from
-    the cache give the same results as the oracle at every step."""
+@pytest.mark.parametrize("window", [1, 3])
+def test_fused_sparse_decode_row_cache_across_steps(tkv, window):
+    """Decode -> append -> decode ... with the HBM row cache (rows selected in
+    the last `window` steps stay resident): rows served from the cache give
+    the oracle's results at every step, and slots are recycled."""
     rng = np.random.default_rng(34)
-    units, n0, d, G, T = 2, 8000, 128, 4, 6
+    units, n0, d, G, T = 2, 8000, 128, 4, 10
     keys = cases.f16(rng.normal(size=(units, n0 + T, d)))
     values = cases.f16(rng.normal(size=(units, n0 + T, d)))
     cfg = tkv.RetrievalConfig(32, 400, 8)
     lay = _sparse_layer(tkv, keys[:, :n0], values[:, :n0], cfg.n_local, steps=T, keys_on_device=True,
-                        cache_rows=cfg.n_local + cfg.n_topk)
+                        cache_rows=cfg.n_local + cfg.n_topk, cache_window=window)
     chans = np.stack([np.sort(rng.choice(d, 8, replace=False)) for _ in range(units)]).astype(np.int32)
     base_q = rng.normal(size=(units * G, d))
     for t in range(T):
@@ -414,6 +417,12 @@ def test_fused_sparse_decode_row_cache_across_steps(tkv):
                    torch.tensor(values[:, n], dtype=torch.float16, device="cuda"))
     hits, misses = lay.cache_counters()
     assert hits > 0 and misses > 0
+    # every cached slot holds the value row of the token it claims
+    tok = lay.slot_tok.cpu().numpy()
+    sv = lay.slot_v.cpu().numpy().astype(np.float64)
+    for u in range(units):
+        for p in np.nonzero(tok[u] >= 0)[0]:
+            assert np.array_equal(sv[u, p], values[u, tok[u, p]])
 
 
 def test_fused_sparse_decode_128k(tkv):
