@@ -148,6 +148,10 @@ typedef struct tkv_sparse_layer {
   uint16_t *slot_v;       /* [units][cache_slots][d] cached value rows */
   int32_t *tok_slot;      /* [units][capacity] token -> slot, verified against slot_tok */
   unsigned long long *cache_stats; /* [2]: rows served from HBM, rows fetched over PCIe */
+  /* Optional [units] float: the last step's top-k score threshold per head, a
+   * hint that aims the next step's threshold search (results never depend on
+   * it; NaN or NULL = no hint). */
+  float *thresh;
 } tkv_sparse_layer;
 
 /* Prefill/offload (replaces HostPool.offload_layer memsim.py:88-93 and the

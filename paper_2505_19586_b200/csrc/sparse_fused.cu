@@ -46,6 +46,8 @@ constexpr int FZ_CAP = 18432;        // candidate keys per CTA: 8 CTAs cover 147
 constexpr int FZ_NB = 512;           // linear histogram bins per pass
 constexpr int FZ_REFINE = 96;        // refine the threshold bin while it holds more keys (cluster-wide)
 constexpr int FZ_BAND = 256;         // per-CTA cap of float64-rescored band members
+constexpr int FZ_LIST = 1536;        // per-CTA cap of the aimed candidate list
+constexpr int FZ_CAND = 6144;        // cluster-wide cap of the aimed candidate list
 constexpr int FZ_XBITS = 11;         // exact fallback: radix digit
 constexpr int FZ_XBINS = 1 << FZ_XBITS;
 
@@ -126,6 +128,7 @@ struct FzCtl {
   int scan[40];
   unsigned long long scan64[33];
   int hits, misses;
+  int list_count;
   unsigned long long bar;       // mbarrier of the value-row staging
 };
 
@@ -140,8 +143,16 @@ struct FzShared {
       uint32_t tot[FZ_NB + 4];   // cluster totals
       unsigned long long band_key[FZ_BAND];
       uint32_t band_idx[FZ_BAND];
-      unsigned long long all_key[FZ_BAND * FZ_CTAS];
-      uint32_t all_idx[FZ_BAND * FZ_CTAS];
+      union {
+        struct {  // full-range path: every CTA's band members
+          unsigned long long all_key[FZ_BAND * FZ_CTAS];
+          uint32_t all_idx[FZ_BAND * FZ_CTAS];
+        };
+        unsigned long long cand[FZ_CAND];  // candidate-list path, rank 0: the cluster's candidates
+      };
+      unsigned long long list64[FZ_LIST];  // aimed candidates (orderable key << 32 | token index)
+      uint8_t band_sel[FZ_BAND];           // rank 0: band member selected
+      uint32_t bitmap[FZ_CAP / 32];        // selected band members of this CTA
     } f;
     unsigned char raw[FZ_UNION];  // attention phase: staged rows, logits, row list, partials
   } k;
@@ -435,6 +446,7 @@ __device__ __forceinline__ void fz_bulk_commit_wait_read() {
 constexpr int FZ_NMARK = 24;
 __device__ unsigned long long g_fz_phase[FZ_CTAS][FZ_NMARK];
 __device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
+__device__ double g_fz_dbg[2][8];  // list-path attempts of unit 0 (debug)
 #define FZ_MARK(i)                                                          \
   do {                                                                      \
     if (trace && blockIdx.y == 0 && tid == 0) {                             \
@@ -480,6 +492,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     C.misses = 0;
     if (ATTEND) fz_mbar_init(&C.bar);
   }
+  bool listed = false;                 // candidate-list path: flags come from keys32 + bitmap
+  uint32_t ord_def = 0xffffffffu;      // (list path) keys above this orderable value are selected
   if (select_all) {
     for (int e = tid; e < m; e += blockDim.x) flags[e] = 1;
     __syncthreads();
@@ -585,12 +599,253 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     double gsum, gsq;
     fz_cluster_stats(cluster, C, klo, khi, (double)fsum, (double)fsq, glo, ghi, gsum, gsq);
     FZ_MARK(4);
-    // ---- 2. threshold range by linear histograms ----
+    // ---- 2a. aimed candidate list, resolved by one CTA ----
+    // Aim at the previous step's threshold of this (layer, head) (+-0.15 sd),
+    // else at the Gaussian estimate mean + z sd (+-0.2 sd).  One pass with no
+    // per-key atomics: keys above the aimed range are counted, keys inside it
+    // (widened by 2 eps) are appended as (key, index) pairs through
+    // warp-aggregated positions.  Rank 0 gathers the cluster's short list
+    // over DSMEM and finds the exact selection alone (fp32 radix select of the
+    // threshold, float64 rescoring of the +-2 eps band, reference tie rule),
+    // so the whole search costs two cluster barriers.  Each CTA then derives
+    // its flags from one integer compare plus the selected band members.  If
+    // the aim misses or a list overflows, the full-range path below runs.
+    const double flo = (double)fz_from_orderable32(glo), fhi = (double)fz_from_orderable32(ghi);
+    const double eps2 = 2.0 * band_eps;
+    uint32_t *H = S.k.f.hist;  // [NB] bins + [NB] keys above the range
+    uint32_t *T = S.k.f.tot;   // cluster totals
+    unsigned long long *list = S.k.f.list64;
+    {
+      const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
+      const float prev = s.thresh ? s.thresh[u] : __int_as_float(0x7fc00000);
+      for (int attempt = isfinite(prev) ? 0 : 1; attempt < 2 && !listed; ++attempt) {
+        const double center = attempt == 0 ? (double)prev : mu + fz_normal_upper_quantile((double)n_topk / N) * sd;
+        const double width = attempt == 0 ? 0.3 * sd : 0.3 * sd;
+        if (!(sd > 0.0) || !isfinite(center)) break;
+        const double a_lo = fmax(flo, center - width), a_hi = fmin(fhi, center + width);
+        if (!(a_hi > a_lo)) continue;
+        // the list spans the aimed range plus two band widths, so the final band always lies inside it
+        const uint32_t ord_llo = fz_orderable32(__double2float_rd(a_lo - 2.0 * eps2));
+        const uint32_t ord_lhi = fz_orderable32(__double2float_ru(a_hi + 2.0 * eps2));
+        if (tid == 0) C.list_count = 0;
+        __syncthreads();
+        FZ_MARK(9);
+        int above = 0, c = 0;
+        uint32_t cm[FZ_KG];
+#pragma unroll
+        for (int g = 0; g < FZ_KG; ++g) {
+          const int e = g * FZ_STEP + tid * 8;
+          uint32_t kk[8];
+          if (e < m) fz_load8(keys32, e, m, kk);
+          uint32_t cmask = 0u;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const bool valid = e + q < m;
+            above += valid && kk[q] > ord_lhi;
+            cmask |= (uint32_t)(valid && kk[q] >= ord_llo && kk[q] <= ord_lhi) << q;
+          }
+          cm[g] = cmask;
+          c += __popc(cmask);
+        }
+        // one warp-aggregated slot reservation for all of this thread's candidates
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+        int base = 0;
+        if (lane == 31 && wtot) base = atomicAdd(&C.list_count, wtot);
+        int pos = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+#pragma unroll
+        for (int g = 0; g < FZ_KG; ++g) {
+          const int e = g * FZ_STEP + tid * 8;
+          uint32_t cmask = cm[g];
+          while (cmask) {
+            const int q = __ffs(cmask) - 1;
+            cmask &= cmask - 1u;
+            if (pos < FZ_LIST) list[pos] = ((unsigned long long)keys32[e + q] << 32) | (uint32_t)(j0 + e + q);
+            ++pos;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+        if (lane == 0) C.wk[0][warp] = (unsigned long long)above;
+        __syncthreads();
+        if (tid == 0) {
+          int t = 0;
+          for (int w = 0; w < FZ_WARPS; ++w) t += (int)C.wk[0][w];
+          C.cta_count = t;
+        }
+        FZ_MARK(5);
+        cluster.sync();  // #1: every CTA's list and counts are complete
+        FZ_MARK(6);
+        if (rank == 0) {
+          // ---- rank 0: gather, fp32 radix select, float64 band, exact ranking ----
+          int A = 0, L = 0, ovf = 0, Lr[FZ_CTAS];
+#pragma unroll
+          for (int r = 0; r < FZ_CTAS; ++r) {
+            const FzCtl *R = cluster.map_shared_rank(&C, r);
+            A += R->cta_count;
+            Lr[r] = R->list_count;
+            ovf |= Lr[r] > FZ_LIST;
+            L += Lr[r];
+          }
+          const int need = n_topk - A;
+          int verdict = (ovf || L > FZ_CAND || need <= 0 || need > L) ? 0 : 1;
+          if (trace && blockIdx.y == 0 && tid == 0) {
+            g_fz_dbg[attempt][0] = attempt; g_fz_dbg[attempt][1] = A; g_fz_dbg[attempt][2] = L;
+            g_fz_dbg[attempt][3] = need; g_fz_dbg[attempt][4] = verdict; g_fz_dbg[attempt][5] = center;
+            g_fz_dbg[attempt][6] = width; g_fz_dbg[attempt][7] = sd;
+          }
+          unsigned long long *cand = S.k.f.cand;
+          if (verdict) {
+            for (int t = tid; t < L; t += blockDim.x) {
+              int r = 0, base = 0;
+              while (t - base >= Lr[r]) base += Lr[r++];
+              cand[t] = cluster.map_shared_rank(list, r)[t - base];
+            }
+            __syncthreads();
+            FZ_MARK(7);
+            // one 512-bin linear histogram over the list's range: the bin holding
+            // the need-th largest key bounds the threshold to [e_lo, e_hi]
+            const float r_lo = __double2float_rd(a_lo), r_hi = __double2float_ru(a_hi);
+            const float scale = (float)FZ_NB / (r_hi - r_lo);
+            const uint32_t o_lo = fz_orderable32(r_lo), o_hi = fz_orderable32(r_hi);
+            for (int i = tid; i <= FZ_NB; i += blockDim.x) H[i] = 0;
+            __syncthreads();
+            int ab = 0;
+            for (int t = tid; t < L; t += blockDim.x) {
+              const uint32_t k = (uint32_t)(cand[t] >> 32);
+              if (k > o_hi) {
+                ++ab;
+              } else if (k >= o_lo) {
+                const float x = fz_from_orderable32(k);
+                atomicAdd(&H[min(FZ_NB - 1, max(0, (int)((x - r_lo) * scale)))], 1u);
+              }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ab += __shfl_xor_sync(0xffffffffu, ab, o);
+            if (lane == 0 && ab) atomicAdd(&H[FZ_NB], (unsigned)ab);
+            if (tid == 0) C.bin = -1;
+            __syncthreads();
+            const int need2 = need - (int)H[FZ_NB];  // list members above the aimed range are selected
+            if (warp == 0 && need2 > 0) {
+              constexpr int BPL = FZ_NB / 32;
+              int cl = 0;
+#pragma unroll
+              for (int q = 0; q < BPL; ++q) cl += (int)H[FZ_NB - 1 - BPL * lane - q];
+              int incl = cl;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              int before = incl - cl;
+              const unsigned hit = __ballot_sync(0xffffffffu, before < need2 && incl >= need2);
+              if (hit && lane == __ffs(hit) - 1) {
+                for (int q = 0; q < BPL; ++q) {
+                  const int b = FZ_NB - 1 - BPL * lane - q;
+                  if (before + (int)H[b] >= need2) {
+                    C.bin = b;
+                    break;
+                  }
+                  before += (int)H[b];
+                }
+              }
+            }
+            __syncthreads();
+            FZ_MARK(8);
+            const int B = max(0, C.bin);
+            if (C.bin < 0) verdict = 0;  // the aim missed: the threshold lies outside [a_lo, a_hi]
+            const double delta = 9.5367431640625e-07 * (fabs((double)r_lo) + fabs((double)r_hi) + ((double)r_hi - r_lo));
+            const double e_lo = B == 0 ? (double)r_lo : (double)r_lo + (double)B / (double)scale - delta;
+            const double e_hi = B == FZ_NB - 1 ? (double)r_hi : (double)r_lo + (double)(B + 1) / (double)scale + delta;
+            const double T32 = 0.5 * (e_lo + e_hi);
+            const uint32_t ord_hi = fz_orderable32(__double2float_ru(e_hi + eps2));
+            const uint32_t ord_lo = fz_orderable32(__double2float_rd(e_lo - eps2));
+            if (tid == 0) {
+              C.band_count = 0;
+              C.overflow = 0;
+              C.hits = 0;  // (reused) definite count inside the list
+            }
+            __syncthreads();
+            int def = 0;
+            for (int t = tid; t < L; t += blockDim.x) {
+              const uint32_t k = (uint32_t)(cand[t] >> 32);
+              if (k > ord_hi) {
+                ++def;
+              } else if (k >= ord_lo) {
+                const int slot = atomicAdd(&C.band_count, 1);
+                if (slot < FZ_BAND) S.k.f.band_idx[slot] = (uint32_t)cand[t];
+                else C.overflow = 1;
+              }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) def += __shfl_xor_sync(0xffffffffu, def, o);
+            if (lane == 0 && def) atomicAdd(&C.hits, def);
+            __syncthreads();
+            const int nb = min(C.band_count, FZ_BAND);
+            const int need_b = n_topk - A - C.hits;
+            if (!verdict || C.overflow || need_b < 0 || need_b > nb) {
+              verdict = 0;  // the aim missed (or a band overflow): take the next attempt / full-range path
+            } else {
+              for (int b = tid; b < nb; b += blockDim.x)
+                S.k.f.band_key[b] = orderable(fz_exact_score(kt, s.capacity, chs, qsum, d_s, S.k.f.band_idx[b]));
+              __syncthreads();
+              for (int b = tid; b < nb; b += blockDim.x) {
+                const unsigned long long kb = S.k.f.band_key[b];
+                const uint32_t ib = S.k.f.band_idx[b];
+                int beaten = 0;
+                for (int o = 0; o < nb; ++o) {
+                  const unsigned long long ko = S.k.f.band_key[o];
+                  const uint32_t io = S.k.f.band_idx[o];
+                  beaten += (ko > kb) || (ko == kb && io > ib);  // (score desc, index desc)
+                }
+                S.k.f.band_sel[b] = beaten < need_b ? 1 : 0;
+              }
+              if (tid == 0) {
+                C.xprefix = ord_hi;  // keys above this orderable value are selected
+                if (s.thresh) s.thresh[u] = (float)T32;
+              }
+            }
+          }
+          if (tid == 0) C.status = verdict;
+          FZ_MARK(21);
+        }
+        cluster.sync();  // #2: rank 0's verdict, threshold and band are ready
+        FZ_MARK(22);
+        const FzCtl *R0 = cluster.map_shared_rank(&C, 0);
+        if (R0->status) {
+          ord_def = (uint32_t)R0->xprefix;
+          for (int i = tid; i < FZ_CAP / 32; i += blockDim.x) S.k.f.bitmap[i] = 0u;
+          __syncthreads();
+          const FzShared *S0 = cluster.map_shared_rank(&S, 0);
+          const int nb = min(R0->band_count, FZ_BAND);
+          for (int b = tid; b < nb; b += blockDim.x) {
+            const int64_t ib = S0->k.f.band_idx[b];
+            if (S0->k.f.band_sel[b] && ib >= j0 && ib < j0 + m)
+              atomicOr(&S.k.f.bitmap[(ib - j0) >> 5], 1u << ((ib - j0) & 31));
+          }
+          listed = true;
+        }
+        __syncthreads();
+        FZ_MARK(23);
+        if (!listed) cluster.sync();  // rank 0's reads of the lists are over before they are rebuilt
+      }
+    }
+    if (!listed) {
+    // ---- 2b. threshold range by linear histograms (full range) ----
+    if (tid == 0) {
+      C.band_count = 0;
+      C.overflow = 0;
+    }
+    __syncthreads();
     // Invariant kept by every accepted pass: #{score > R_hi} < n_topk <= #{score >= R_lo}.
     // Pass 0 aims at the Gaussian estimate of the n_topk-th score (mean + z sd,
     // +-0.6 sd); only keys inside the aimed range touch the histogram.  A
     // pass whose range misses the threshold falls back to the full range.
-    const double flo = (double)fz_from_orderable32(glo), fhi = (double)fz_from_orderable32(ghi);
     double R_lo = flo, R_hi = fhi;
     {
       const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
@@ -606,16 +861,12 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       }
     }
     bool aimed = R_lo > flo || R_hi < fhi;
-    FZ_MARK(21);
-    uint32_t *H = S.k.f.hist;  // [NB] bins + [NB] keys above the range
-    uint32_t *T = S.k.f.tot;   // cluster totals
     for (int pass = 0; pass < 5; ++pass) {
       const float r_lo = __double2float_rd(R_lo), r_hi = __double2float_ru(R_hi);
       const float scale = (float)FZ_NB / (r_hi - r_lo);
       if (!(r_hi > r_lo) || !(scale < 3.0e38f)) break;  // degenerate range: everything in it is band
       for (int i = tid; i < FZ_NB + 4; i += blockDim.x) H[i] = 0;
       __syncthreads();
-      if (pass == 0) FZ_MARK(22);
       int above = 0;
       const uint32_t ord_lo = fz_orderable32(r_lo), ord_hi = fz_orderable32(r_hi), ord_w = ord_hi - ord_lo;
 #pragma unroll 1
@@ -804,6 +1055,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       fz_radix(cluster, keys64, m, S, C, top, prefix, need64, done);
       fz_exact_flags(cluster, keys64, m, flags, C, top, prefix, need64, done);
     }
+    if (rank == 0 && tid == 0 && s.thresh) s.thresh[u] = (float)(0.5 * (R_lo + R_hi));
+    }  // full-range path
     if (scores_out) {
       for (int e = tid; e < m; e += blockDim.x)
         scores_out[(size_t)u * s.capacity + j0 + e] = fz_exact_score(kt, s.capacity, chs, qsum, d_s, j0 + e);
@@ -821,7 +1074,14 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     const int e = g * FZ_STEP + tid * 8;
     fw[g][0] = fw[g][1] = 0u;
     if (e < m) {
-      if (e + 8 <= m) {
+      if (listed) {
+        uint32_t kk[8];
+        fz_load8(S.k.f.keys32, e, m, kk);
+        const uint32_t bits = (S.k.f.bitmap[e >> 5] >> (e & 31)) & 0xffu;  // e is a multiple of 8
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          fw[g][q >> 2] |= (uint32_t)(e + q < m && (kk[q] > ord_def || ((bits >> q) & 1u))) << (8 * (q & 3));
+      } else if (e + 8 <= m) {
         const uint2 x = *reinterpret_cast<const uint2 *>(flags + e);
         fw[g][0] = x.x;
         fw[g][1] = x.y;
@@ -1295,6 +1555,10 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
 
 extern "C" int tkv_debug_sparse_trace(int on) {
   return cudaMemcpyToSymbol(tkv::g_fz_trace, &on, sizeof(int)) == cudaSuccess ? 0 : 7;
+}
+
+extern "C" int tkv_debug_sparse_attempts(double *out) {
+  return cudaMemcpyFromSymbol(out, tkv::g_fz_dbg, sizeof(tkv::g_fz_dbg)) == cudaSuccess ? 0 : 7;
 }
 
 extern "C" int tkv_debug_sparse_phases(unsigned long long *out) {

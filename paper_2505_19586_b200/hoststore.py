@@ -103,12 +103,13 @@ class OffloadedLayerKV:
             self.cache_stats = torch.zeros(2, dtype=torch.int64, device=dev)
         else:
             self.slot_tok = self.slot_stamp = self.slot_v = self.tok_slot = self.cache_stats = None
+        self.thresh = torch.full((units,), float("nan"), dtype=torch.float32, device=dev)  # top-k threshold hint
         self.struct = SparseLayer(units, d, self.capacity, self.local_offset, self.local_capacity,
                                   self.kt.data_ptr(), self.chmax.data_ptr(), self.loc_k.data_ptr(),
                                   self.loc_v.data_ptr(), ptr(self.kdev), self.arena.addr,
                                   self._len.data_ptr(), self._len.data_ptr() + 4,
                                   self.cache_slots, self.cache_window, ptr(self.slot_tok), ptr(self.slot_stamp),
-                                  ptr(self.slot_v), ptr(self.tok_slot), ptr(self.cache_stats))
+                                  ptr(self.slot_v), ptr(self.tok_slot), ptr(self.cache_stats), ptr(self.thresh))
 
     @property
     def keys_on_device(self) -> bool:

@@ -2,7 +2,7 @@
 import ctypes as C
 
 NAMES = {1: "chs", 2: "qsum", 3: "score", 4: "minmax", 5: "hist", 6: "hist-sync", 7: "totals", 8: "scan",
-         9: "passes", 10: "band", 11: "band-sync", 12: "rank", 13: "count", 14: "out-sync", 15: "rows",
+         9: "passes", 10: "band", 11: "band-sync", 12: "select", 13: "count", 14: "out-sync", 15: "rows",
          16: "gather", 17: "sync", 18: "cta-merge", 19: "merge-sync", 20: "final"}
 
 
@@ -11,16 +11,25 @@ def enable(lib, on=True):
 
 
 def show(lib):
+    dbg = (C.c_double * 16)()
+    lib.tkv_debug_sparse_attempts(dbg)
+    for a in range(2):
+        d = list(dbg)[a * 8:(a + 1) * 8]
+        print(f"  attempt {a}: above {d[1]:.0f} list {d[2]:.0f} need {d[3]:.0f} ok {d[4]:.0f} center {d[5]:.5g} "
+              f"width {d[6]:.4g} sd {d[7]:.4g}")
     ph = (C.c_ulonglong * (8 * 24))()
     lib.tkv_debug_sparse_phases(ph)
     t = [list(ph)[r * 24:(r + 1) * 24] for r in range(8)]
     t0 = min(x[0] for x in t)
+    x = t[0]
+    us = lambda a, b: (x[b] - x[a]) / 1e3  # noqa: E731
+    if x[5] and x[22] and x[5] > x[4]:
+        print(f"  list path (rank 0): setup {us(4, 9):.2f} passA {us(9, 5):.2f} sync1 {us(5, 6):.2f} "
+              f"gather {us(6, 7):.2f} radix {us(7, 8):.2f} band+rank {us(8, 21):.2f} sync2 {us(21, 22):.2f} "
+              f"bitmap {us(22, 23):.2f}")
     for r in range(8):
-        x = t[r]
-        print(f"  rank {r} detail: stats->range {(x[21] - x[4]) / 1e3:.2f} range->cleared {(x[22] - x[21]) / 1e3:.2f} "
-              f"loop {(x[23] - x[22]) / 1e3:.2f} tail {(x[5] - x[23]) / 1e3:.2f}")
         parts, prev = [], t[r][0]
-        for i in range(1, 21):
+        for i in (1, 2, 3, 4, 12, 13, 14, 15, 16, 17, 18, 19, 20):
             if t[r][i] >= prev and t[r][i] > 0:
                 parts.append(f"{NAMES[i]} {(t[r][i] - prev) / 1e3:.1f}")
                 prev = t[r][i]

@@ -267,14 +267,16 @@ int main(int argc, char **argv) {
     CK(cudaFree(d));
   }
   const int big = 262144, small = 11000;
-  if (only_mode == 9) {
+  if (only_mode == 9 || only_mode == 10) {
     // per-layer windows: 30 windows of `win` bytes, 11000 random rows of 256 B
-    // in each (row pitch 256 or 512), windows visited in turn (cold translations)
-    void *host = alloc_host(0, bytes, 0, numa);
+    // in each (row pitch 256 or 512), windows visited in turn (cold translations);
+    // mode 9: mmap+THP+cudaHostRegister, mode 10: cuMemCreate HOST_NUMA (2 MiB granularity)
+    void *host = alloc_host(only_mode == 9 ? 0 : 2, bytes, 0, numa);
     const int W = 30;
     int *d_rows;
     CK(cudaMalloc(&d_rows, sizeof(int) * small * W));
-    for (int pitch : {512, 256}) {
+    for (int nsmall : {11000, 1500}) for (int pitch : {512, 256}) {
+      const int small = nsmall;
       const size_t win = (size_t)8 * 131072 * pitch;  // 8 units x 131072 tokens
       if (win * W > bytes) { printf("arena too small\n"); return 1; }
       std::mt19937_64 g(7);
@@ -282,8 +284,8 @@ int main(int argc, char **argv) {
       for (int w = 0; w < W; ++w)
         for (int i = 0; i < small; ++i) hr[(size_t)w * small + i] = (int)((win * w + (g() % (win / pitch)) * pitch) / 256);
       CK(cudaMemcpy(d_rows, hr.data(), sizeof(int) * hr.size(), cudaMemcpyHostToDevice));
-      for (size_t touch : {(size_t)0, (size_t)4096, (size_t)65536, (size_t)2 << 20}) {
-        for (int rep = 0; rep < 3; ++rep) {
+      for (size_t touch : {(size_t)0, (size_t)65536}) {
+        for (int rep = 0; rep < 2; ++rep) {
           double tg = 0, tt = 0;
           for (int w = 0; w < W; ++w) {
             float ms;
@@ -303,8 +305,8 @@ int main(int argc, char **argv) {
             CK(cudaEventElapsedTime(&ms, a, b));
             tg += ms;
           }
-          printf("pitch %d touch-step %8zu rep %d: gather %.1f us/window (%.1f GB/s), touch %.1f us/window\n", pitch,
-                 touch, rep, tg * 1e3 / W, (double)small * 256 / (tg * 1e-3 / W) / 1e9, tt * 1e3 / W);
+          printf("rows %5d pitch %d touch-step %8zu rep %d: gather %.1f us/window (%.1f GB/s), touch %.1f us/window\n",
+                 small, pitch, touch, rep, tg * 1e3 / W, (double)small * 256 / (tg * 1e-3 / W) / 1e9, tt * 1e3 / W);
         }
       }
     }
