@@ -298,6 +298,7 @@ static int stage1_splits(int hq, int H) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int splits = (2 * sms) / hq;
+  if (const char *e = getenv("TKV_STAGE1_SPLITS")) splits = atoi(e);
   splits = max(splits, (H + 1023) / 1024);
   splits = max(1, min(splits, (H + 7) / 8));
   return splits;

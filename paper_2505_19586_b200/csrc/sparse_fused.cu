@@ -443,10 +443,11 @@ __device__ __forceinline__ void fz_bulk_commit_wait_read() {
 }
 
 // phase timestamps of unit 0, every CTA (debug: tkv_debug_sparse_phases)
-constexpr int FZ_NMARK = 24;
+constexpr int FZ_NMARK = 32;
 __device__ unsigned long long g_fz_phase[FZ_CTAS][FZ_NMARK];
 __device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
 __device__ double g_fz_dbg[2][8];  // list-path attempts of unit 0 (debug)
+__device__ unsigned long long g_fz_clk[FZ_CTAS][2];  // clock64 at the first and last mark (debug)
 #define FZ_MARK(i)                                                          \
   do {                                                                      \
     if (trace && blockIdx.y == 0 && tid == 0) {                             \
@@ -485,6 +486,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
   uint8_t *flags = S.flags;
   const uint16_t *kt = s.kt + (size_t)u * s.d * s.capacity;
   FZ_MARK(0);
+  if (trace && blockIdx.y == 0 && tid == 0) g_fz_clk[rank][0] = clock64();
   if (tid == 0) {
     C.band_count = 0;
     C.overflow = 0;
@@ -1188,6 +1190,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     int32_t *sstamp = use_cache ? s.slot_stamp + (size_t)u * CS : nullptr;
     uint16_t *sv = use_cache ? s.slot_v + (size_t)u * CS * D : nullptr;
     int32_t *tslot = use_cache ? s.tok_slot + (size_t)u * s.capacity : nullptr;
+    // Each CTA owns the slots [p0, p1) of its unit's cache: it serves hits and
+    // allocates misses only there, so no cross-CTA coordination is needed.
+    const int spc = (CS + FZ_CTAS - 1) / FZ_CTAS;
+    const int p0 = min(CS, rank * spc), p1 = min(CS, p0 + spc);
     // (0) row codes: >= 0 cached slot (hit, stamped with this step), -1 fetch over PCIe, -2 local mirror
     int hits = 0, misses = 0;
     for (int i = tid; i < nrows; i += blockDim.x) {
@@ -1197,7 +1203,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         code = -1;
         if (use_cache) {
           const int p = tslot[idx];
-          if (p >= 0 && p < CS && stok[p] == (int)idx) {
+          if (p >= p0 && p < p1 && stok[p] == (int)idx) {
             code = p;
             sstamp[p] = (int)n;
           }
@@ -1208,6 +1214,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       rslot[i] = code;
     }
     __syncthreads();
+    FZ_MARK(24);
     float mrun[GMAX], lrun[GMAX], acc[GMAX][CPL];
 #pragma unroll
     for (int h = 0; h < GMAX; ++h) {
@@ -1239,109 +1246,154 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       }
     };
     if (nrows > 0) issue_round(0, min(NR, nrows));
-    // cache slots for this step's misses (cluster-wide, while the copies fly)
+    FZ_MARK(25);
+    // cache slots for this step's misses: free slots of this CTA's partition
+    // (empty, or not selected in the last cache_window steps), in order
     if (use_cache) {
       const int W = max(1, s.cache_window);
       int32_t *F = reinterpret_cast<int32_t *>(S.flags);  // free-slot list (the flags are dead)
-      const int spc = (CS + FZ_CTAS - 1) / FZ_CTAS;
-      const int p0 = rank * spc, p1 = min(CS, p0 + spc);
-      const int per_t = (spc + FZ_THREADS - 1) / FZ_THREADS;
-      const int q0 = p0 + tid * per_t, q1 = min(p1, q0 + per_t);
-      int mt = misses;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mt += __shfl_xor_sync(0xffffffffu, mt, o);
-      if (lane == 0) C.wk[1][warp] = (unsigned long long)mt;
-      cluster.sync();  // every CTA's hit stamps are visible
       int nf = 0;
-      for (int p = q0; p < q1; ++p) nf += stok[p] < 0 || sstamp[p] <= (int)n - W;
+      for (int p = p0 + tid; p < p1; p += blockDim.x) nf += stok[p] < 0 || sstamp[p] <= (int)n - W;
       int ftot;
       int fpos = fz_block_excl_scan(nf, C.scan, &ftot);
-      for (int p = q0; p < q1; ++p)
+      for (int p = p0 + tid; p < p1; p += blockDim.x)
         if (stok[p] < 0 || sstamp[p] <= (int)n - W) F[fpos++] = p;
-      if (tid == 0) {
-        int mtot = 0;
-        for (int w = 0; w < FZ_WARPS; ++w) mtot += (int)C.wk[1][w];
-        C.cta_count = ftot;
-        C.band_count = mtot;  // (reused) this CTA's misses
-      }
-      cluster.sync();
-      int fpre[FZ_CTAS + 1], mine_off = 0;
-      fpre[0] = 0;
-#pragma unroll
-      for (int r = 0; r < FZ_CTAS; ++r) {
-        const FzCtl *R = cluster.map_shared_rank(&C, r);
-        fpre[r + 1] = fpre[r] + R->cta_count;
-        if (r < rank) mine_off += R->band_count;
-      }
-      // ordinal of each miss inside this CTA: rows are visited in the (strided) lookup order
       int tm = 0;
       for (int i = tid; i < nrows; i += blockDim.x) tm += rslot[i] == -1;
       int dummy;
-      int ord = mine_off + fz_block_excl_scan(tm, C.scan, &dummy);
+      int ord = fz_block_excl_scan(tm, C.scan, &dummy);  // (its barriers also publish F)
       for (int i = tid; i < nrows; i += blockDim.x) {
         if (rslot[i] != -1) continue;
         const int k = ord++;
-        if (k < fpre[FZ_CTAS]) {
-          int r = 0;
-          while (k >= fpre[r + 1]) ++r;
-          const int dst = cluster.map_shared_rank(F, r)[k - fpre[r]];
-          rslot[i] = -3 - dst;
-        }
+        if (k < ftot) rslot[i] = -3 - F[k];  // misses beyond the free slots are simply not cached
       }
       __syncthreads();
     }
+    FZ_MARK(26);
     uint32_t parity = 0;
     for (int base = 0; base < nrows; base += NR) {
       const int cnt = min(NR, nrows - base);
       if (base > 0) issue_round(base, cnt);
-      // (b) logits of this warp's rows: key rows from HBM while the value copies fly
+      // (b) logits of this warp's rows: key rows from HBM while the value copies fly;
+      // a batch's 16 row loads are issued before any use
       if (!keys_host) {
-        for (int i0 = warp; i0 < cnt; i0 += FZ_WARPS * 8) {
-          float kf[8][CPL];
+        for (int i0 = warp; i0 < cnt; i0 += FZ_WARPS * 16) {
+          if constexpr (CPL == 4 && GMAX == 4) {
+            uint2 kr[16];
 #pragma unroll
-          for (int jr = 0; jr < 8; ++jr) {
-            const int i = i0 + FZ_WARPS * jr;
+            for (int jr = 0; jr < 16; ++jr) {
+              const int i = i0 + FZ_WARPS * jr;
+              kr[jr] = make_uint2(0u, 0u);
+              if (i < cnt) {
+                const int64_t idx = rbase + rows[base + i];
+                const uint16_t *kp = idx >= local_start
+                                         ? s.loc_k + ((size_t)u * s.local_capacity + (idx - s.local_offset)) * D
+                                         : (s.kdev ? s.kdev + ((size_t)u * s.capacity + idx) * D : nullptr);
+                if (kp) {
+                  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(kr[jr].x), "=r"(kr[jr].y) : "l"(kp + lane * 4));
+                } else {  // key row from the channel-major scorer copy (scattered 2-byte reads)
+                  uint32_t w[4];
 #pragma unroll
-            for (int e = 0; e < CPL; ++e) kf[jr][e] = 0.0f;
-            if (i >= cnt) continue;
-            const int64_t idx = rbase + rows[base + i];
-            if (idx >= local_start || s.kdev) {
-              const uint16_t *kp = idx >= local_start
-                                       ? s.loc_k + ((size_t)u * s.local_capacity + (idx - s.local_offset)) * D
-                                       : s.kdev + ((size_t)u * s.capacity + idx) * D;
-              if constexpr (CPL == 4) {
-                const uint2 a = *reinterpret_cast<const uint2 *>(kp + lane * 4);
-                kf[jr][0] = h2f((uint16_t)a.x); kf[jr][1] = h2f((uint16_t)(a.x >> 16));
-                kf[jr][2] = h2f((uint16_t)a.y); kf[jr][3] = h2f((uint16_t)(a.y >> 16));
-              } else {
+                  for (int e = 0; e < 4; ++e) w[e] = kt[((size_t)lane * 4 + e) * s.capacity + idx];
+                  kr[jr] = make_uint2(w[0] | (w[1] << 16), w[2] | (w[3] << 16));
+                }
+              }
+            }
+            const float4 q0 = *reinterpret_cast<const float4 *>(S.qs + 0 * D + lane * 4);
+            const float4 q1 = *reinterpret_cast<const float4 *>(S.qs + 1 * D + lane * 4);
+            const float4 q2 = *reinterpret_cast<const float4 *>(S.qs + 2 * D + lane * 4);
+            const float4 q3 = *reinterpret_cast<const float4 *>(S.qs + 3 * D + lane * 4);
+#pragma unroll
+            for (int jr = 0; jr < 16; ++jr) {
+              const int i = i0 + FZ_WARPS * jr;
+              if (i >= cnt) break;
+              const float k0 = h2f((uint16_t)kr[jr].x), k1 = h2f((uint16_t)(kr[jr].x >> 16));
+              const float k2 = h2f((uint16_t)kr[jr].y), k3 = h2f((uint16_t)(kr[jr].y >> 16));
+              const float d0 = fmaf(q0.x, k0, fmaf(q0.y, k1, fmaf(q0.z, k2, q0.w * k3)));
+              const float d1 = fmaf(q1.x, k0, fmaf(q1.y, k1, fmaf(q1.z, k2, q1.w * k3)));
+              const float d2 = fmaf(q2.x, k0, fmaf(q2.y, k1, fmaf(q2.z, k2, q2.w * k3)));
+              const float d3 = fmaf(q3.x, k0, fmaf(q3.y, k1, fmaf(q3.z, k2, q3.w * k3)));
+              // transposed butterfly: 6 shuffles reduce the four head sums
+              const bool hi16 = lane & 16, hi8 = lane & 8;
+              float a0 = hi16 ? d2 : d0, a1 = hi16 ? d3 : d1;
+              a0 += __shfl_xor_sync(0xffffffffu, hi16 ? d0 : d2, 16);
+              a1 += __shfl_xor_sync(0xffffffffu, hi16 ? d1 : d3, 16);
+              float c = hi8 ? a1 : a0;
+              c += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+              c += __shfl_xor_sync(0xffffffffu, c, 4);
+              c += __shfl_xor_sync(0xffffffffu, c, 2);
+              c += __shfl_xor_sync(0xffffffffu, c, 1);
+              const int h = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
+              if ((lane & 7) == 0 && h < G) zs[(size_t)i * GMAX + h] = c;
+            }
+          } else {
+            float kf[8][CPL];
+#pragma unroll
+            for (int jr = 0; jr < 8; ++jr) {
+              const int i = i0 + FZ_WARPS * jr;
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) kf[jr][e] = 0.0f;
+              if (i >= cnt) continue;
+              const int64_t idx = rbase + rows[base + i];
+              if (idx >= local_start || s.kdev) {
+                const uint16_t *kp = idx >= local_start
+                                         ? s.loc_k + ((size_t)u * s.local_capacity + (idx - s.local_offset)) * D
+                                         : s.kdev + ((size_t)u * s.capacity + idx) * D;
 #pragma unroll
                 for (int e = 0; e < CPL; ++e) kf[jr][e] = h2f(kp[lane * CPL + e]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) kf[jr][e] = h2f(kt[((size_t)lane * CPL + e) * s.capacity + idx]);
               }
-            } else {  // key row from the channel-major scorer copy (scattered 2-byte reads)
-#pragma unroll
-              for (int e = 0; e < CPL; ++e) kf[jr][e] = h2f(kt[((size_t)lane * CPL + e) * s.capacity + idx]);
             }
-          }
 #pragma unroll
-          for (int jr = 0; jr < 8; ++jr) {
-            const int i = i0 + FZ_WARPS * jr;
-            if (i >= cnt) break;
+            for (int jr = 0; jr < 8; ++jr) {
+              const int i = i0 + FZ_WARPS * jr;
+              if (i >= cnt) break;
 #pragma unroll
-            for (int h = 0; h < GMAX; ++h) {
-              if (h >= G) break;
-              const float *qh = S.qs + h * D + lane * CPL;
-              float dp = 0.0f;
+              for (int h = 0; h < GMAX; ++h) {
+                if (h >= G) break;
+                const float *qh = S.qs + h * D + lane * CPL;
+                float dp = 0.0f;
 #pragma unroll
-              for (int e = 0; e < CPL; ++e) dp = fmaf(qh[e], kf[jr][e], dp);
-              dp = warp_sum(dp);
-              if (lane == 0) zs[(size_t)i * GMAX + h] = dp;
+                for (int e = 0; e < CPL; ++e) dp = fmaf(qh[e], kf[jr][e], dp);
+                dp = warp_sum(dp);
+                if (lane == 0) zs[(size_t)i * GMAX + h] = dp;
+              }
+            }
+            // rows 8..15 of this batch
+            for (int jr = 8; jr < 16; ++jr) {
+              const int i = i0 + FZ_WARPS * jr;
+              if (i >= cnt) break;
+              const int64_t idx = rbase + rows[base + i];
+              float kk2[CPL];
+              if (idx >= local_start || s.kdev) {
+                const uint16_t *kp = idx >= local_start
+                                         ? s.loc_k + ((size_t)u * s.local_capacity + (idx - s.local_offset)) * D
+                                         : s.kdev + ((size_t)u * s.capacity + idx) * D;
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) kk2[e] = h2f(kp[lane * CPL + e]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) kk2[e] = h2f(kt[((size_t)lane * CPL + e) * s.capacity + idx]);
+              }
+              for (int h = 0; h < G; ++h) {
+                const float *qh = S.qs + h * D + lane * CPL;
+                float dp = 0.0f;
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) dp = fmaf(qh[e], kk2[e], dp);
+                dp = warp_sum(dp);
+                if (lane == 0) zs[(size_t)i * GMAX + h] = dp;
+              }
             }
           }
         }
       }
+      if (base == 0) FZ_MARK(27);
       // (c) value rows (and key rows over PCIe) have landed
       fz_mbar_wait(&C.bar, parity);
       parity ^= 1u;
+      if (base == 0) FZ_MARK(28);
       if (keys_host) {
         for (int i = warp; i < cnt; i += FZ_WARPS) {
           const uint16_t *kp = stage_k + (size_t)i * D;
@@ -1356,30 +1408,48 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
       }
       __syncwarp();
-      // (d) online softmax over this warp's rows (the rows whose logits it wrote)
-      for (int i = warp; i < cnt; i += FZ_WARPS) {
-        const uint16_t *vr = stage_v + (size_t)i * D + lane * CPL;
-        float vf[CPL];
-        if constexpr (CPL == 4) {
-          const uint2 b = *reinterpret_cast<const uint2 *>(vr);
-          vf[0] = h2f((uint16_t)b.x); vf[1] = h2f((uint16_t)(b.x >> 16));
-          vf[2] = h2f((uint16_t)b.y); vf[3] = h2f((uint16_t)(b.y >> 16));
-        } else {
+      // (d) softmax over this warp's rows (the rows whose logits it wrote):
+      // the round's max first, one rescale, then independent accumulations
+      {
+        float mr[GMAX];
 #pragma unroll
-          for (int e = 0; e < CPL; ++e) vf[e] = h2f(vr[e]);
-        }
+        for (int h = 0; h < GMAX; ++h) mr[h] = mrun[h];
+        for (int i = warp; i < cnt; i += FZ_WARPS)
+#pragma unroll
+          for (int h = 0; h < GMAX; ++h)
+            if (h < G) mr[h] = fmaxf(mr[h], zs[(size_t)i * GMAX + h]);
 #pragma unroll
         for (int h = 0; h < GMAX; ++h) {
           if (h >= G) break;
-          const float z = zs[(size_t)i * GMAX + h];
-          const float mn = fmaxf(mrun[h], z);
-          const float sc = exp2f(mrun[h] - mn), p = exp2f(z - mn);
-          lrun[h] = fmaf(lrun[h], sc, p);
+          if (mr[h] == -INFINITY) continue;  // no rows yet
+          const float sc = exp2f(mrun[h] - mr[h]);  // 0 on the first round (mrun = -inf)
+          lrun[h] *= sc;
 #pragma unroll
-          for (int e = 0; e < CPL; ++e) acc[h][e] = fmaf(p, vf[e], acc[h][e] * sc);
-          mrun[h] = mn;
+          for (int e = 0; e < CPL; ++e) acc[h][e] *= sc;
+          mrun[h] = mr[h];
+        }
+        for (int i = warp; i < cnt; i += FZ_WARPS) {
+          const uint16_t *vr = stage_v + (size_t)i * D + lane * CPL;
+          float vf[CPL];
+          if constexpr (CPL == 4) {
+            const uint2 bv = *reinterpret_cast<const uint2 *>(vr);
+            vf[0] = h2f((uint16_t)bv.x); vf[1] = h2f((uint16_t)(bv.x >> 16));
+            vf[2] = h2f((uint16_t)bv.y); vf[3] = h2f((uint16_t)(bv.y >> 16));
+          } else {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) vf[e] = h2f(vr[e]);
+          }
+#pragma unroll
+          for (int h = 0; h < GMAX; ++h) {
+            if (h >= G) break;
+            const float p = exp2f(zs[(size_t)i * GMAX + h] - mrun[h]);
+            lrun[h] += p;
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) acc[h][e] = fmaf(p, vf[e], acc[h][e]);
+          }
         }
       }
+      if (base == 0) FZ_MARK(29);
       // (e) rows fetched over PCIe enter the HBM row cache in their assigned slots
       if (use_cache) {
         for (int i = tid; i < cnt; i += blockDim.x) {
@@ -1394,6 +1464,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
         fz_bulk_commit_wait_read();  // the staged rows are read before the next round overwrites them
       }
+      if (base == 0) FZ_MARK(30);
       __syncthreads();
     }
     if (use_cache) {
@@ -1472,6 +1543,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     }
     cluster.sync();  // rank 0 has read every CTA's partial
     FZ_MARK(20);
+    if (trace && blockIdx.y == 0 && tid == 0) g_fz_clk[rank][1] = clock64();
   }
 }
 
@@ -1557,10 +1629,14 @@ extern "C" int tkv_debug_sparse_trace(int on) {
   return cudaMemcpyToSymbol(tkv::g_fz_trace, &on, sizeof(int)) == cudaSuccess ? 0 : 7;
 }
 
+extern "C" int tkv_debug_sparse_clocks(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, tkv::g_fz_clk, sizeof(tkv::g_fz_clk)) == cudaSuccess ? 0 : 7;
+}
+
 extern "C" int tkv_debug_sparse_attempts(double *out) {
   return cudaMemcpyFromSymbol(out, tkv::g_fz_dbg, sizeof(tkv::g_fz_dbg)) == cudaSuccess ? 0 : 7;
 }
 
-extern "C" int tkv_debug_sparse_phases(unsigned long long *out) {
+extern "C" int tkv_debug_sparse_phases(unsigned long long *out) {  // [8][32]
   return cudaMemcpyFromSymbol(out, tkv::g_fz_phase, sizeof(tkv::g_fz_phase)) == cudaSuccess ? 0 : 7;
 }

@@ -17,16 +17,28 @@ def show(lib):
         d = list(dbg)[a * 8:(a + 1) * 8]
         print(f"  attempt {a}: above {d[1]:.0f} list {d[2]:.0f} need {d[3]:.0f} ok {d[4]:.0f} center {d[5]:.5g} "
               f"width {d[6]:.4g} sd {d[7]:.4g}")
-    ph = (C.c_ulonglong * (8 * 24))()
+    ph = (C.c_ulonglong * (8 * 32))()
     lib.tkv_debug_sparse_phases(ph)
-    t = [list(ph)[r * 24:(r + 1) * 24] for r in range(8)]
+    t = [list(ph)[r * 32:(r + 1) * 32] for r in range(8)]
     t0 = min(x[0] for x in t)
     x = t[0]
+    clk = (C.c_ulonglong * 16)()
+    lib.tkv_debug_sparse_clocks(clk)
+    cyc = clk[1] - clk[0]
+    if x[20] > x[0] and cyc:
+        print(f"  SM clock over the kernel (rank 0): {cyc / ((x[20] - x[0]) / 1e3):.0f} MHz ({cyc} cycles)")
     us = lambda a, b: (x[b] - x[a]) / 1e3  # noqa: E731
     if x[5] and x[22] and x[5] > x[4]:
         print(f"  list path (rank 0): setup {us(4, 9):.2f} passA {us(9, 5):.2f} sync1 {us(5, 6):.2f} "
               f"gather {us(6, 7):.2f} radix {us(7, 8):.2f} band+rank {us(8, 21):.2f} sync2 {us(21, 22):.2f} "
               f"bitmap {us(22, 23):.2f}")
+    for r in (0, 7):
+        y = t[r]
+        if y[24] and y[30]:
+            g = lambda a, b: (y[b] - y[a]) / 1e3  # noqa: E731
+            print(f"  gather rank {r}: lookups {g(15, 24):.2f} issue {g(24, 25):.2f} slots {g(25, 26):.2f} "
+                  f"logits {g(26, 27):.2f} wait {g(27, 28):.2f} softmax {g(28, 29):.2f} insert {g(29, 30):.2f} "
+                  f"rest {g(30, 16):.2f}")
     for r in range(8):
         parts, prev = [], t[r][0]
         for i in (1, 2, 3, 4, 12, 13, 14, 15, 16, 17, 18, 19, 20):
