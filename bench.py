@@ -425,8 +425,9 @@ def main():
                          "unit": "GB/s", "ms": quant_ms, "bytes": quant_bytes, "peak_source": hbm_src},
         "stage1": {"bound": "hbm", "achieved": wq_bytes / (stage1_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                    "ms": stage1_ms, "bytes": wq_bytes, "peak_source": hbm_src},
-        "sparse_append": {"ms": append_ms},
     }
+    if append_ms == append_ms:  # (separate append launch: unfused path)
+        rooflines["sparse_append"] = {"ms": append_ms}
     for r in rooflines.values():
         if "achieved" in r:
             r["frac"] = r["achieved"] / r["peak"]

@@ -206,11 +206,15 @@ int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int
  * HBM row cache, key rows from HBM when keys_from_device != 0) and exact
  * softmax attention.  Outputs are those of tkv_select_tokens followed by
  * tkv_sparse_attention; `workspace` >= tkv_sparse_decode_workspace bytes (used
- * only by shapes outside the fused kernel). */
+ * only by shapes outside the fused kernel).  With new_keys/new_values fp16
+ * [units][d] (else NULL) the step's append (tkv_sparse_append) is fused into
+ * the same launch, after the attention (attend-before-append,
+ * pipeline.py:315-413). */
 int64_t tkv_sparse_decode_workspace(int32_t units, int64_t capacity, int32_t G, int32_t d, int32_t max_rows);
 int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
                       int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
-                      int32_t *fetch_count, int32_t keys_from_device, float *out, void *workspace, void *stream);
+                      int32_t *fetch_count, int32_t keys_from_device, const uint16_t *new_keys,
+                      const uint16_t *new_values, float *out, void *workspace, void *stream);
 /* Pinned, NUMA-local host arena for the KV store (memsim.py:76-135).  numa_node
  * < 0 leaves placement to the OS.  Returns a host pointer usable by kernels
  * (UVA) or NULL. */

@@ -202,23 +202,28 @@ int tkv_topk_from_scores(const double *scores, int32_t units, int64_t n, int32_t
 
 int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
                       int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
-                      int32_t *fetch_count, int32_t keys_from_device, float *out, void *workspace, void *stream) {
+                      int32_t *fetch_count, int32_t keys_from_device, const uint16_t *new_keys,
+                      const uint16_t *new_values, float *out, void *workspace, void *stream) {
   if (int r = validate_sparse(s)) return r;
   TKV_REQUIRE(n_local >= 0 && n_local <= 4096, TKV_ERR_PARAMETER, "n_local must lie in [0, 4096]");
   TKV_REQUIRE(n_topk >= 1, TKV_ERR_PARAMETER, "n_topk must be >= 1");
   TKV_REQUIRE(d_s >= 1 && d_s <= s->d && d_s <= 128, TKV_ERR_PARAMETER, "d_s must lie in [1, min(head_dim,128)]");
   TKV_REQUIRE(G >= 1 && G <= 8, TKV_ERR_SHAPE, "group size must lie in [1, 8]");
+  TKV_REQUIRE((new_keys == nullptr) == (new_values == nullptr), TKV_ERR_PARAMETER,
+              "new_keys and new_values must both be given or both be NULL");
   if (sparse_decode_supported(*s, G, n_local))
     return sparse_decode_fused(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
-                               keys_from_device, out, as_stream(stream));
-  // shapes outside the fused kernel: select, then gather + attention (two launches)
+                               keys_from_device, out, new_keys, new_values, as_stream(stream));
+  // shapes outside the fused kernel: select, then gather + attention, then the append (three launches)
   char *ws = static_cast<char *>(workspace);
   const int64_t sel_ws = (select_workspace(s->units, s->capacity) + 255) / 256 * 256;
   if (int r = select_tokens(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, nullptr,
                             ws, as_stream(stream)))
     return r;
-  return sparse_attention(*s, queries, G, sel_idx, sel_count, n_local, n_local + n_topk, keys_from_device, out,
-                          ws + sel_ws, as_stream(stream));
+  if (int r = sparse_attention(*s, queries, G, sel_idx, sel_count, n_local, n_local + n_topk, keys_from_device, out,
+                               ws + sel_ws, as_stream(stream)))
+    return r;
+  return new_keys ? sparse_append(*s, new_keys, new_values, as_stream(stream)) : TKV_OK;
 }
 
 int64_t tkv_sparse_decode_workspace(int32_t units, int64_t capacity, int32_t G, int32_t d, int32_t max_rows) {

@@ -19,7 +19,7 @@ int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t 
 bool sparse_decode_supported(const SL &s, int G, int n_local);
 int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
-                        float *out, cudaStream_t st);
+                        float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st);
 int uva_probe(const void *host, size_t bytes, int row_bytes, const int32_t *rows, int nrows, float *sink,
               cudaStream_t st);
 int64_t calibrate_workspace(int hq, int n_q, int64_t n);

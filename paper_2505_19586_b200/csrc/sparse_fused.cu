@@ -462,7 +462,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     sparse_fused_kernel(SL s, const uint16_t *__restrict__ queries, int G, const int32_t *__restrict__ channels,
                         int d_s, int n_local, int n_topk, int32_t *__restrict__ sel_idx, int sel_stride,
                         int32_t *__restrict__ sel_count, int32_t *__restrict__ fetch_count,
-                        double *__restrict__ scores_out, int keys_from_device, float *__restrict__ out) {
+                        double *__restrict__ scores_out, int keys_from_device, float *__restrict__ out,
+                        const uint16_t *__restrict__ new_keys, const uint16_t *__restrict__ new_values) {
   extern __shared__ __align__(16) unsigned char smem[];
   FzShared &S = *reinterpret_cast<FzShared *>(smem);
   __shared__ FzCtl C;
@@ -1520,6 +1521,33 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     FZ_MARK(18);
     cluster.sync();
     FZ_MARK(19);
+    // ---- 6. the step's append (HostPool.append + mirror append, memsim.py:106-111,
+    // pipeline.py:405-413) after this step's attention (every CTA has passed the
+    // merge barrier): the new token of unit u goes to position n of every store;
+    // the last cluster to finish advances *len ----
+    if (new_keys && rank == FZ_CTAS - 1) {  // (rank 0 is merging the partials meanwhile)
+      for (int c = tid; c < D; c += blockDim.x) {
+        const uint16_t k = new_keys[(size_t)u * D + c], v = new_values[(size_t)u * D + c];
+        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 0) * D + c] = k;
+        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 1) * D + c] = v;
+        s.kt[((size_t)u * D + c) * s.capacity + n] = k;
+        float *cm = &s.chmax[(size_t)u * D + c];
+        *cm = fmaxf(*cm, fabsf(h2f(k)));
+        const int64_t lr = n - s.local_offset;
+        s.loc_k[((size_t)u * s.local_capacity + lr) * D + c] = k;
+        s.loc_v[((size_t)u * s.local_capacity + lr) * D + c] = v;
+        if (s.kdev) s.kdev[((size_t)u * s.capacity + n) * D + c] = k;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned prev = atomicAdd(s.ticket, 1u);
+        if (prev == (unsigned)s.units - 1) {
+          *s.ticket = 0;
+          __threadfence();
+          *s.len = (int32_t)(n + 1);
+        }
+      }
+    }
     if (rank == 0) {
       for (int i = tid; i < G * D; i += blockDim.x) {
         const int h = i / D;
@@ -1560,7 +1588,8 @@ bool fused_ok(const SL &s, int n_local) {
 template <bool ATTEND, int D, int GMAX>
 static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s,
                                 int n_local, int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count,
-                                double *scores_out, int keys_from_device, float *out, cudaStream_t st) {
+                                double *scores_out, int keys_from_device, float *out, cudaStream_t st,
+                                const uint16_t *new_keys = nullptr, const uint16_t *new_values = nullptr) {
   auto kern = sparse_fused_kernel<ATTEND, D, GMAX>;
   const size_t sm = sizeof(FzShared);
   static bool attr = false;
@@ -1583,7 +1612,7 @@ static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, con
   cfg.attrs = at;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, s, queries, G, channels, d_s, n_local, n_topk, sel_idx, n_local + n_topk,
-                            sel_count, fetch_count, scores_out, keys_from_device, out);
+                            sel_count, fetch_count, scores_out, keys_from_device, out, new_keys, new_values);
 }
 
 // select only (tkv_select_tokens)
@@ -1607,11 +1636,11 @@ bool sparse_decode_supported(const SL &s, int G, int n_local) {
 // fused select + gather + attention (tkv_sparse_decode)
 int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
-                        float *out, cudaStream_t st) {
+                        float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st) {
   cudaError_t e;
 #define TKV_FZ(D, GM)                                                                                          \
   e = launch_fused<true, D, GM>(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, \
-                                nullptr, keys_from_device, out, st)
+                                nullptr, keys_from_device, out, st, new_keys, new_values)
   if (s.d == 128 && G <= 4) TKV_FZ(128, 4);
   else if (s.d == 128 && G <= 8) TKV_FZ(128, 8);
   else if (s.d == 64 && G <= 8) TKV_FZ(64, 8);

@@ -291,7 +291,7 @@ class DecodeEngine:
         """Launches of this library per decode step."""
         q = sum(1 for x in self.labels if x == "q")
         s = len(self.labels) - q
-        per_s = 3 if self.cfg.fused_sparse else 4  # stage 1 + (fused decode | select + gather/attend) + append
+        per_s = 2 if self.cfg.fused_sparse else 4  # stage 1 + (fused decode+append | select + gather/attend + append)
         return q * 3 + s * per_s  # q: decode+combine+append
 
     def _run_step(self) -> None:
@@ -319,7 +319,8 @@ class DecodeEngine:
                 if self.cfg.fused_sparse:
                     t0 = self._mark(main)
                     lay.decode(self.queries[l], st.channels, self.G, self.retrieval, self.sel_idx, self.sel_count,
-                               self.fetch_count, self.out[l], self.dec_ws, keys_from_device=self.keys_from_hbm)
+                               self.fetch_count, self.out[l], self.dec_ws, keys_from_device=self.keys_from_hbm,
+                               new_keys=self.new_keys[l], new_values=self.new_values[l])
                     self._span("sparse_decode", l, t0, main)
                 else:
                     t0 = self._mark(main)
@@ -333,9 +334,10 @@ class DecodeEngine:
                 if self.record_selection:
                     self.last_channels[l] = st.channels.clone()
                     self.last_selection[l] = (self.sel_idx.clone(), self.sel_count.clone(), self.fetch_count.clone())
-                t0 = self._mark(main)
-                lay.append(self.new_keys[l], self.new_values[l])
-                self._span("sparse_append", l, t0, main)
+                if not self.cfg.fused_sparse:
+                    t0 = self._mark(main)
+                    lay.append(self.new_keys[l], self.new_values[l])
+                    self._span("sparse_append", l, t0, main)
             if self.world > 1:
                 torch.distributed.all_gather_into_tensor(self.gathered[l], self.out[l], group=self.group)
         main.wait_stream(self.side)

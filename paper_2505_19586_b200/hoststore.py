@@ -172,12 +172,22 @@ class OffloadedLayerKV:
 
     def decode(self, queries: torch.Tensor, channels: torch.Tensor, G: int, cfg: RetrievalConfig,
                sel_idx: torch.Tensor, sel_count: torch.Tensor, fetch_count: torch.Tensor, out: torch.Tensor,
-               workspace: torch.Tensor, keys_from_device: bool = False, stream=None) -> None:
+               workspace: torch.Tensor, keys_from_device: bool = False, new_keys=None, new_values=None,
+               stream=None) -> None:
         """One fused launch: proxy scores + exact top-k + gather + attention
-        (pipeline.py:351-376); same results as ``select`` then ``attend``."""
+        (pipeline.py:351-376); same results as ``select`` then ``attend``.
+        With new_keys/new_values [units, d] the step's ``append`` runs in the
+        same launch, after the attention."""
+        if (new_keys is None) != (new_values is None):
+            raise ParameterError("new_keys and new_values must both be given")
+        if new_keys is not None and self.n + 1 > self.capacity:
+            raise ParameterError("layer capacity exhausted")
         check(_lib.load().tkv_sparse_decode(C.byref(self.struct), ptr(queries), G, ptr(channels), channels.shape[1],
                                             cfg.n_local, cfg.n_topk, ptr(sel_idx), ptr(sel_count), ptr(fetch_count),
-                                            int(keys_from_device), ptr(out), ptr(workspace), stream_ptr(stream)))
+                                            int(keys_from_device), ptr(new_keys), ptr(new_values), ptr(out),
+                                            ptr(workspace), stream_ptr(stream)))
+        if new_keys is not None:
+            self.n += 1
 
     def attend(self, queries: torch.Tensor, G: int, cfg: RetrievalConfig, sel_idx: torch.Tensor,
                sel_count: torch.Tensor, out: torch.Tensor, workspace: torch.Tensor, keys_from_device: bool = False,
