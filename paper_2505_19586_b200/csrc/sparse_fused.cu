@@ -160,6 +160,7 @@ struct FzShared {
   uint32_t xhist[2][FZ_XBINS];
   uint32_t xtot[FZ_XBINS];
   float cta_m[8], cta_l[8];
+  float red_m[FZ_WARPS][8], m_new[8];  // softmax: per-warp round maxima, the CTA's new max
   float cta_acc[1024];  // this CTA's merged partial, read by rank 0 over DSMEM
   float qs[1024];       // queries [G][D] * log2(e)/sqrt(d)
 };
@@ -448,6 +449,7 @@ __device__ unsigned long long g_fz_phase[FZ_CTAS][FZ_NMARK];
 __device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
 __device__ double g_fz_dbg[2][8];  // list-path attempts of unit 0 (debug)
 __device__ unsigned long long g_fz_clk[FZ_CTAS][2];  // clock64 at the first and last mark (debug)
+__device__ unsigned long long g_fz_unit[64][FZ_CTAS][2];  // per unit and rank: globaltimer at start / end (debug)
 #define FZ_MARK(i)                                                          \
   do {                                                                      \
     if (trace && blockIdx.y == 0 && tid == 0) {                             \
@@ -488,6 +490,11 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
   const uint16_t *kt = s.kt + (size_t)u * s.d * s.capacity;
   FZ_MARK(0);
   if (trace && blockIdx.y == 0 && tid == 0) g_fz_clk[rank][0] = clock64();
+  if (trace && blockIdx.y < 64 && tid == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_fz_unit[blockIdx.y][rank][0] = t_;
+  }
   if (tid == 0) {
     C.band_count = 0;
     C.overflow = 0;
@@ -1409,26 +1416,45 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
       }
       __syncwarp();
-      // (d) softmax over this warp's rows (the rows whose logits it wrote):
-      // the round's max first, one rescale, then independent accumulations
+      // (d) softmax: the round's max per head over the whole CTA, p = exp2(z - m)
+      // once per (row, head) in shared memory, then each warp accumulates its rows
+      __syncthreads();  // every logit of the round is in zs
       {
-        float mr[GMAX];
+        float ml[GMAX];
 #pragma unroll
-        for (int h = 0; h < GMAX; ++h) mr[h] = mrun[h];
-        for (int i = warp; i < cnt; i += FZ_WARPS)
+        for (int h = 0; h < GMAX; ++h) ml[h] = -INFINITY;
+        for (int i = tid; i < cnt; i += blockDim.x)
 #pragma unroll
           for (int h = 0; h < GMAX; ++h)
-            if (h < G) mr[h] = fmaxf(mr[h], zs[(size_t)i * GMAX + h]);
+            if (h < G) ml[h] = fmaxf(ml[h], zs[(size_t)i * GMAX + h]);
 #pragma unroll
         for (int h = 0; h < GMAX; ++h) {
           if (h >= G) break;
-          if (mr[h] == -INFINITY) continue;  // no rows yet
-          const float sc = exp2f(mrun[h] - mr[h]);  // 0 on the first round (mrun = -inf)
-          lrun[h] *= sc;
 #pragma unroll
-          for (int e = 0; e < CPL; ++e) acc[h][e] *= sc;
-          mrun[h] = mr[h];
+          for (int o = 16; o > 0; o >>= 1) ml[h] = fmaxf(ml[h], __shfl_xor_sync(0xffffffffu, ml[h], o));
+          if (lane == 0) S.red_m[warp][h] = ml[h];
         }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < GMAX; ++h) {
+          if (h >= G) break;
+          float mr = mrun[h];
+          for (int w = 0; w < FZ_WARPS; ++w) mr = fmaxf(mr, S.red_m[w][h]);
+          if (mr != -INFINITY) {
+            const float sc = exp2f(mrun[h] - mr);  // 0 on the first round (mrun = -inf)
+            lrun[h] *= sc;
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) acc[h][e] *= sc;
+            mrun[h] = mr;
+          }
+          if (tid == 0) S.m_new[h] = mr;
+        }
+        __syncthreads();
+        for (int t = tid; t < cnt * G; t += blockDim.x) {
+          const int i = t / G, h = t - i * G;
+          zs[(size_t)i * GMAX + h] = exp2f(zs[(size_t)i * GMAX + h] - S.m_new[h]);
+        }
+        __syncthreads();
         for (int i = warp; i < cnt; i += FZ_WARPS) {
           const uint16_t *vr = stage_v + (size_t)i * D + lane * CPL;
           float vf[CPL];
@@ -1443,7 +1469,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
 #pragma unroll
           for (int h = 0; h < GMAX; ++h) {
             if (h >= G) break;
-            const float p = exp2f(zs[(size_t)i * GMAX + h] - mrun[h]);
+            const float p = zs[(size_t)i * GMAX + h];
             lrun[h] += p;
 #pragma unroll
             for (int e = 0; e < CPL; ++e) acc[h][e] = fmaf(p, vf[e], acc[h][e]);
@@ -1572,6 +1598,11 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     cluster.sync();  // rank 0 has read every CTA's partial
     FZ_MARK(20);
     if (trace && blockIdx.y == 0 && tid == 0) g_fz_clk[rank][1] = clock64();
+    if (trace && blockIdx.y < 64 && tid == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      g_fz_unit[blockIdx.y][rank][1] = t_;
+    }
   }
 }
 
@@ -1656,6 +1687,10 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
 
 extern "C" int tkv_debug_sparse_trace(int on) {
   return cudaMemcpyToSymbol(tkv::g_fz_trace, &on, sizeof(int)) == cudaSuccess ? 0 : 7;
+}
+
+extern "C" int tkv_debug_sparse_units(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, tkv::g_fz_unit, sizeof(tkv::g_fz_unit)) == cudaSuccess ? 0 : 7;
 }
 
 extern "C" int tkv_debug_sparse_clocks(unsigned long long *out) {

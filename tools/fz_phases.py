@@ -10,7 +10,20 @@ def enable(lib, on=True):
     lib.tkv_debug_sparse_trace(1 if on else 0)
 
 
+def show_units(lib, units=8):
+    raw = (C.c_ulonglong * (64 * 8 * 2))()
+    lib.tkv_debug_sparse_units(raw)
+    v = list(raw)
+    t0 = min(v[(u * 8 + r) * 2] for u in range(units) for r in range(8))
+    for u in range(units):
+        st = [v[(u * 8 + r) * 2] for r in range(8)]
+        en = [v[(u * 8 + r) * 2 + 1] for r in range(8)]
+        print(f"  unit {u}: start +{(min(st) - t0) / 1e3:.1f}..{(max(st) - t0) / 1e3:.1f} us, "
+              f"end +{(min(en) - t0) / 1e3:.1f}..{(max(en) - t0) / 1e3:.1f} us")
+
+
 def show(lib):
+    show_units(lib)
     dbg = (C.c_double * 16)()
     lib.tkv_debug_sparse_attempts(dbg)
     for a in range(2):
