@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
   bool listed = false;                 // candidate-list path: flags come from keys32 + bitmap
   uint32_t ord_def = 0xffffffffu;      // (list path) keys above this orderable value are selected
   if (select_all) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int e = tid; e < m; e += blockDim.x) flags[e] = 1;
     __syncthreads();
   } else {
@@ -529,6 +530,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           for (int r = 0; r < 8; ++r) v[g2][r] = fz_ld_nc_v4(kt + (size_t)chs[r] * s.capacity + j0 + e0 + g2 * STEP);
         }
     }
+    // Programmatic dependent launch: everything above (length, channels, the
+    // first scorer loads) only touches this layer's own state, so it overlaps
+    // the previous kernel's tail; the query is consumed after the wait.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int i = tid; i < d_s; i += blockDim.x) {
       const int ch = chs[i];
       double q = 0.0;
@@ -1202,6 +1207,17 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     // allocates misses only there, so no cross-CTA coordination is needed.
     const int spc = (CS + FZ_CTAS - 1) / FZ_CTAS;
     const int p0 = min(CS, rank * spc), p1 = min(CS, p0 + spc);
+    // key rows of every selected token start moving into L2 now (TMA prefetch), so the
+    // logits step below reads them from L2 instead of waiting on HBM
+    if (!keys_host && s.kdev) {
+      for (int i = tid; i < nrows; i += blockDim.x) {
+        const int64_t idx = rbase + rows[i];
+        if (idx < local_start)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.kdev + ((size_t)u * s.capacity + idx) * D),
+                       "r"((uint32_t)(D * 2))
+                       : "memory");
+      }
+    }
     // (0) row codes: >= 0 cached slot (hit, stamped with this step), -1 fetch over PCIe, -2 local mirror
     int hits = 0, misses = 0;
     for (int i = tid; i < nrows; i += blockDim.x) {
@@ -1506,6 +1522,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       }
     }
     FZ_MARK(16);
+    asm volatile("griddepcontrol.launch_dependents;");  // the next layer's kernel may start its prologue
     __syncthreads();  // the staging area (aliased by the partials) is no longer read
     FZ_MARK(17);
     float *pm = reinterpret_cast<float *>(S.k.raw), *pl = pm + FZ_WARPS * GMAX, *pa = pl + FZ_WARPS * GMAX;
@@ -1633,15 +1650,17 @@ static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, con
   cfg.blockDim = dim3(FZ_THREADS);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = FZ_CTAS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributePriority;
   at[1].val.priority = launch_priority(true);
+  at[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol in the kernel)
+  at[2].val.programmaticStreamSerializationAllowed = getenv("TKV_NO_PDL") ? 0 : 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 3;
   return cudaLaunchKernelEx(&cfg, kern, s, queries, G, channels, d_s, n_local, n_topk, sel_idx, n_local + n_topk,
                             sel_count, fetch_count, scores_out, keys_from_device, out, new_keys, new_values);
 }
