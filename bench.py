@@ -432,13 +432,25 @@ def main():
         if "achieved" in r:
             r["frac"] = r["achieved"] / r["peak"]
     dom = rooflines["sparse_decode"]
+    # DRAM traffic per launch from the committed ncu --set full capture of the same kernels
+    traffic = {}
+    tpath = ROOT / "profiles" / "r1_ncu_traffic.json"
+    if tpath.exists():
+        traffic = json.loads(tpath.read_text())
+    def _traffic(name):
+        t = traffic.get(name)
+        return None if t is None else t["dram_bytes_read"] + t["dram_bytes_write"]
+    rooflines["quant_decode"]["traffic"] = _traffic("quant_decode_imma_kernel")
     line = {
         "metric": METRIC, "value": ms, "unit": "ms/token", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "fp16 storage / 1-bit codes, fp32 accumulate", "data": "synthetic (gen_trace-shaped, GPU-generated)",
         "config": workload_config(args, n_topk),
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
-                     "frac": dom["frac"], "traffic": None, "kernel": dom["kernel"],
+                     "frac": dom["frac"], "traffic": _traffic("sparse_fused_kernel") if not args.unfused else None,
+                     "traffic_note": "DRAM bytes per launch (ncu capture, profiles/r1_ncu_traffic.json); the PCIe "
+                                     "bytes above are the kernel's algorithmic value-row misses",
+                     "kernel": dom["kernel"],
                      "timing": "CUDA events recorded as graph nodes around the kernel inside the replayed step"},
         "rooflines": rooflines,
         "row_cache": {"window_steps": cfg.row_cache_steps, "slots_per_head": (eng.retrieval.n_local + eng.retrieval.n_topk) * cfg.row_cache_steps,
