@@ -369,7 +369,8 @@ def main():
 
     # per-kernel profile of the main mode, steady state (after the timed steps)
     if args.phases:
-        _lib.load().tkv_debug_sparse_trace(1)
+        from tools.fz_phases import enable
+        enable(_lib.load())
     prof, hits, misses = profile_mode()
     if args.phases and rank == 0:
         from tools.fz_phases import show

@@ -450,6 +450,7 @@ __device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
 __device__ double g_fz_dbg[2][8];  // list-path attempts of unit 0 (debug)
 __device__ unsigned long long g_fz_clk[FZ_CTAS][2];  // clock64 at the first and last mark (debug)
 __device__ unsigned long long g_fz_unit[64][FZ_CTAS][2];  // per unit and rank: globaltimer at start / end (debug)
+__device__ int g_fz_upath[64][4];  // per unit: select path (0 list attempt 0, 1 list attempt 1, 2 full range), list size, rows, misses
 #define FZ_MARK(i)                                                          \
   do {                                                                      \
     if (trace && blockIdx.y == 0 && tid == 0) {                             \
@@ -633,11 +634,35 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     {
       const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
       const float prev = s.thresh ? s.thresh[u] : __int_as_float(0x7fc00000);
-      for (int attempt = isfinite(prev) ? 0 : 1; attempt < 2 && !listed; ++attempt) {
-        const double center = attempt == 0 ? (double)prev : mu + fz_normal_upper_quantile((double)n_topk / N) * sd;
-        const double width = attempt == 0 ? 0.3 * sd : 0.3 * sd;
-        if (!(sd > 0.0) || !isfinite(center)) break;
-        const double a_lo = fmax(flo, center - width), a_hi = fmin(fhi, center + width);
+      const double gauss = mu + fz_normal_upper_quantile((double)n_topk / N) * sd;
+      const double tprev = mu + (double)prev * sd;  // the hint is the previous threshold as a z-score
+      double last_lo = 0.0, last_hi = 0.0;
+      int dir = 0;
+      for (int attempt = 0; attempt < 2 && !listed; ++attempt) {
+        // attempt 0 spans the previous threshold and the Gaussian estimate (+-0.2 sd); after a
+        // miss, attempt 1 extends 0.6 sd beyond the side of the missed range that holds the threshold
+        double a_lo, a_hi;
+        if (attempt == 0) {
+          const double c0 = isfinite(tprev) ? fmin(tprev, gauss) : gauss;
+          const double c1 = isfinite(tprev) ? fmax(tprev, gauss) : gauss;
+          a_lo = c0 - 0.2 * sd;
+          a_hi = c1 + 0.2 * sd;
+        } else if (dir > 0) {
+          a_lo = last_hi;
+          a_hi = last_hi + 0.6 * sd;
+        } else if (dir < 0) {
+          a_lo = last_lo - 0.6 * sd;
+          a_hi = last_lo;
+        } else {
+          a_lo = gauss - 0.4 * sd;
+          a_hi = gauss + 0.4 * sd;
+        }
+        if (!(sd > 0.0) || !isfinite(a_lo) || !isfinite(a_hi)) break;
+        const double center = 0.5 * (a_lo + a_hi), width = 0.5 * (a_hi - a_lo);
+        a_lo = fmax(flo, a_lo);
+        a_hi = fmin(fhi, a_hi);
+        last_lo = a_lo;
+        last_hi = a_hi;
         if (!(a_hi > a_lo)) continue;
         // the list spans the aimed range plus two band widths, so the final band always lies inside it
         const uint32_t ord_llo = fz_orderable32(__double2float_rd(a_lo - 2.0 * eps2));
@@ -709,6 +734,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           }
           const int need = n_topk - A;
           int verdict = (ovf || L > FZ_CAND || need <= 0 || need > L) ? 0 : 1;
+          int dir = need <= 0 ? 1 : (!ovf && need > L ? -1 : 0);  // where the threshold lies if the aim missed
           if (trace && blockIdx.y == 0 && tid == 0) {
             g_fz_dbg[attempt][0] = attempt; g_fz_dbg[attempt][1] = A; g_fz_dbg[attempt][2] = L;
             g_fz_dbg[attempt][3] = need; g_fz_dbg[attempt][4] = verdict; g_fz_dbg[attempt][5] = center;
@@ -773,7 +799,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             __syncthreads();
             FZ_MARK(8);
             const int B = max(0, C.bin);
-            if (C.bin < 0) verdict = 0;  // the aim missed: the threshold lies outside [a_lo, a_hi]
+            if (C.bin < 0) {  // the aim missed: the threshold lies outside [a_lo, a_hi]
+              verdict = 0;
+              dir = need2 <= 0 ? 1 : -1;
+            }
             const double delta = 9.5367431640625e-07 * (fabs((double)r_lo) + fabs((double)r_hi) + ((double)r_hi - r_lo));
             const double e_lo = B == 0 ? (double)r_lo : (double)r_lo + (double)B / (double)scale - delta;
             const double e_hi = B == FZ_NB - 1 ? (double)r_hi : (double)r_lo + (double)(B + 1) / (double)scale + delta;
@@ -822,16 +851,24 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
               }
               if (tid == 0) {
                 C.xprefix = ord_hi;  // keys above this orderable value are selected
-                if (s.thresh) s.thresh[u] = (float)T32;
+                if (s.thresh && sd > 0.0) s.thresh[u] = (float)((T32 - mu) / sd);  // as a z-score
               }
             }
           }
-          if (tid == 0) C.status = verdict;
+          if (tid == 0) {
+            C.status = verdict;
+            C.inbin = dir;  // (reused) miss direction for the next attempt
+          }
           FZ_MARK(21);
         }
         cluster.sync();  // #2: rank 0's verdict, threshold and band are ready
         FZ_MARK(22);
         const FzCtl *R0 = cluster.map_shared_rank(&C, 0);
+        dir = R0->status ? 0 : R0->inbin;
+        if (trace && blockIdx.y < 64 && rank == 0 && tid == 0 && R0->status) {
+          g_fz_upath[blockIdx.y][0] = attempt;
+          g_fz_upath[blockIdx.y][1] = R0->list_count;
+        }
         if (R0->status) {
           ord_def = (uint32_t)R0->xprefix;
           for (int i = tid; i < FZ_CAP / 32; i += blockDim.x) S.k.f.bitmap[i] = 0u;
@@ -851,6 +888,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       }
     }
     if (!listed) {
+    if (trace && blockIdx.y < 64 && rank == 0 && tid == 0) g_fz_upath[blockIdx.y][0] = 2;
     // ---- 2b. threshold range by linear histograms (full range) ----
     if (tid == 0) {
       C.band_count = 0;
@@ -1070,7 +1108,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       fz_radix(cluster, keys64, m, S, C, top, prefix, need64, done);
       fz_exact_flags(cluster, keys64, m, flags, C, top, prefix, need64, done);
     }
-    if (rank == 0 && tid == 0 && s.thresh) s.thresh[u] = (float)(0.5 * (R_lo + R_hi));
+    if (rank == 0 && tid == 0 && s.thresh) {
+      const double N = (double)ncand, mu = gsum / N, sd = sqrt(fmax(gsq / N - mu * mu, 0.0));
+      if (sd > 0.0) s.thresh[u] = (float)((0.5 * (R_lo + R_hi) - mu) / sd);
+    }
     }  // full-range path
     if (scores_out) {
       for (int e = tid; e < m; e += blockDim.x)
@@ -1510,12 +1551,16 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       if (base == 0) FZ_MARK(30);
       __syncthreads();
     }
+    if (trace && blockIdx.y < 64 && tid == 0) {
+      atomicAdd(&g_fz_upath[blockIdx.y][2], nrows);
+    }
     if (use_cache) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         hits += __shfl_xor_sync(0xffffffffu, hits, o);
         misses += __shfl_xor_sync(0xffffffffu, misses, o);
       }
+      if (trace && blockIdx.y < 64 && lane == 0) atomicAdd(&g_fz_upath[blockIdx.y][3], misses);
       if (lane == 0 && (hits | misses)) {
         atomicAdd(&C.hits, hits);
         atomicAdd(&C.misses, misses);
@@ -1706,6 +1751,14 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
 
 extern "C" int tkv_debug_sparse_trace(int on) {
   return cudaMemcpyToSymbol(tkv::g_fz_trace, &on, sizeof(int)) == cudaSuccess ? 0 : 7;
+}
+
+extern "C" int tkv_debug_sparse_upath(int *out, int reset) {
+  if (reset) {
+    static const int zero[64 * 4] = {};
+    return cudaMemcpyToSymbol(tkv::g_fz_upath, zero, sizeof(zero)) == cudaSuccess ? 0 : 7;
+  }
+  return cudaMemcpyFromSymbol(out, tkv::g_fz_upath, sizeof(tkv::g_fz_upath)) == cudaSuccess ? 0 : 7;
 }
 
 extern "C" int tkv_debug_sparse_units(unsigned long long *out) {

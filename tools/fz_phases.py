@@ -8,18 +8,23 @@ NAMES = {1: "chs", 2: "qsum", 3: "score", 4: "minmax", 5: "hist", 6: "hist-sync"
 
 def enable(lib, on=True):
     lib.tkv_debug_sparse_trace(1 if on else 0)
+    if on:
+        lib.tkv_debug_sparse_upath(None, 1)
 
 
 def show_units(lib, units=8):
     raw = (C.c_ulonglong * (64 * 8 * 2))()
     lib.tkv_debug_sparse_units(raw)
     v = list(raw)
+    up = (C.c_int * (64 * 4))()
+    lib.tkv_debug_sparse_upath(up, 0)
     t0 = min(v[(u * 8 + r) * 2] for u in range(units) for r in range(8))
     for u in range(units):
         st = [v[(u * 8 + r) * 2] for r in range(8)]
         en = [v[(u * 8 + r) * 2 + 1] for r in range(8)]
         print(f"  unit {u}: start +{(min(st) - t0) / 1e3:.1f}..{(max(st) - t0) / 1e3:.1f} us, "
-              f"end +{(min(en) - t0) / 1e3:.1f}..{(max(en) - t0) / 1e3:.1f} us")
+              f"end +{(min(en) - t0) / 1e3:.1f}..{(max(en) - t0) / 1e3:.1f} us  path {up[u * 4]} list {up[u * 4 + 1]} "
+              f"rows {up[u * 4 + 2]} pcie rows {up[u * 4 + 3]}")
 
 
 def show(lib):
