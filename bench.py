@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="sparse layers as two launches (select, gather+attend)")
     ap.add_argument("--phases", action="store_true", help="print the fused sparse kernel's phase marks (unit 0)")
+    ap.add_argument("--no-fidelity", action="store_true", help="skip the one-step recall/cosine evaluation")
     ap.add_argument("--cache-steps", type=int, default=4,
                     help="HBM row cache window: a value row stays resident until unselected for this many steps (0: off)")
     ap.add_argument("--seed", type=int, default=2505)
@@ -278,7 +279,7 @@ def main():
                          row_cache=args.cache_steps > 0, row_cache_steps=max(1, args.cache_steps))
     W, K = args.warmup, args.steps
     PROF = 2
-    total = W + 3 * K + 2 * PROF + 8
+    total = W + 3 * K + 2 * PROF + 10
     t_setup = time.time()
     wl = make_workload(L, (0, 1), model.num_query_heads, model.num_kv_heads, model.head_dim, n, total,
                        batch=1, seed=args.seed, device=device)
@@ -366,6 +367,21 @@ def main():
     e2.record()
     torch.cuda.synchronize(); barrier()
     ms_e2e = s2.elapsed_time(e2) / K
+
+    # fidelity of one eager step against exact attention over all tokens (GPU, outside the timing)
+    fidelity = None
+    if not args.no_fidelity:
+        eng.record_selection = True
+        graph, eng.graph = eng.graph, None
+        eng.step(*inputs(step_i)); step_i += 1
+        fl = [eng.layer_fidelity(l) for l in range(L) if wl.labels[l] == "s"]
+        eng.graph, eng.record_selection = graph, False
+        fidelity = {"layers": len(fl), "recall_mean": sum(f["recall"] for f in fl) / len(fl),
+                    "recall_min": min(f["recall"] for f in fl),
+                    "selected_mass_mean": sum(f["selected_mass"] for f in fl) / len(fl),
+                    "cosine_min": min(f["cosine"] for f in fl),
+                    "note": "one step, Top-K layers, vs exact softmax attention over all tokens "
+                            "(pipeline.py:316-403 metrics, computed on the GPU)"}
 
     # per-kernel profile of the main mode, steady state (after the timed steps)
     if args.phases:
@@ -466,6 +482,7 @@ def main():
         "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",
                     "ms_per_token": ms_variant, "sparse_decode_ms": alt_ms,
                     "pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "pcie_bytes": alt_bytes},
+        "fidelity": fidelity,
         "gpu_launches": eng.kernels_per_step() * K,
         "clocks": clocks.summary(),
         "setup_s": setup_s,

@@ -215,6 +215,17 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
                       int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
                       int32_t *fetch_count, int32_t keys_from_device, const uint16_t *new_keys,
                       const uint16_t *new_values, float *out, void *workspace, void *stream);
+/* Fidelity metrics of one decode step of a sparsity-friendly layer against
+ * exact attention over its first n tokens (replaces the oracle comparison of
+ * pipeline.py:316-325, 377-403; kv_model.py:169-213; retriever.py:229-252):
+ * exact_out fp32 [units*G][128] (exact softmax(qK^T/sqrt d)V, keys from HBM,
+ * values from the host store), metrics f64 [units][2] = (recall@k of the
+ * selection against the exact top-k group-weight tokens, selected attention
+ * mass / G).  sel_idx/sel_count as written by tkv_sparse_decode; k = n_topk. */
+int64_t tkv_sparse_fidelity_workspace(int32_t units, int32_t G, int64_t n, int32_t k);
+int tkv_sparse_fidelity(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, int64_t n,
+                        const int32_t *sel_idx, const int32_t *sel_count, int32_t sel_stride, int32_t k,
+                        float *exact_out, double *metrics, void *workspace, void *stream);
 /* Pinned, NUMA-local host arena for the KV store (memsim.py:76-135).  numa_node
  * < 0 leaves placement to the OS.  Returns a host pointer usable by kernels
  * (UVA) or NULL. */

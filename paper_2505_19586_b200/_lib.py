@@ -94,6 +94,8 @@ _SIGS = {
     "tkv_sparse_decode_workspace": (C.c_int64, [_I32, _I64, _I32, _I32, _I32]),
     "tkv_sparse_decode": (C.c_int, [C.POINTER(SparseLayer), _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P,
                                     _P, _P, _P]),
+    "tkv_sparse_fidelity_workspace": (C.c_int64, [_I32, _I32, _I64, _I32]),
+    "tkv_sparse_fidelity": (C.c_int, [C.POINTER(SparseLayer), _P, _I32, _I64, _P, _P, _I32, _I32, _P, _P, _P, _P]),
     "tkv_host_store_create": (C.c_void_p, [C.c_size_t, _I32]),
     "tkv_host_store_destroy": (C.c_int, [_P, C.c_size_t]),
     "tkv_uva_read_probe": (C.c_int, [_P, C.c_size_t, _I32, _P, _I32, _P, _P]),

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtailorkv.so"
-SOURCES = ["abi.cu", "qcache.cu", "decode.cu", "decode_imma.cu", "sparse.cu", "sparse_fused.cu", "calibrate.cu"]
+SOURCES = ["abi.cu", "qcache.cu", "decode.cu", "decode_imma.cu", "sparse.cu", "sparse_fused.cu", "calibrate.cu", "fidelity.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

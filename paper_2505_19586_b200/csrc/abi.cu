@@ -1,3 +1,4 @@
+#include <algorithm>
 // extern "C" boundary: argument validation, status codes (errors.py:9-38),
 // dispatch to the kernels.  See include/tailorkv.h.
 #include <fcntl.h>
@@ -224,6 +225,20 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
                                ws + sel_ws, as_stream(stream)))
     return r;
   return new_keys ? sparse_append(*s, new_keys, new_values, as_stream(stream)) : TKV_OK;
+}
+
+int64_t tkv_sparse_fidelity_workspace(int32_t units, int32_t G, int64_t n, int32_t k) {
+  return fidelity_workspace(units, G, n, k);
+}
+
+int tkv_sparse_fidelity(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, int64_t n,
+                        const int32_t *sel_idx, const int32_t *sel_count, int32_t sel_stride, int32_t k,
+                        float *exact_out, double *metrics, void *workspace, void *stream) {
+  if (int r = validate_sparse(s)) return r;
+  TKV_REQUIRE(n >= 1 && n <= s->capacity, TKV_ERR_EMPTY_CACHE, "fidelity over an empty or oversized prefix");
+  TKV_REQUIRE(k >= 1, TKV_ERR_PARAMETER, "k must be >= 1");
+  return sparse_fidelity(*s, queries, G, n, sel_idx, sel_count, sel_stride, (int)std::min<int64_t>(k, n), exact_out,
+                         metrics, workspace, as_stream(stream));
 }
 
 int64_t tkv_sparse_decode_workspace(int32_t units, int64_t capacity, int32_t G, int32_t d, int32_t max_rows) {

@@ -20,6 +20,10 @@ bool sparse_decode_supported(const SL &s, int G, int n_local);
 int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
                         float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st);
+int64_t fidelity_workspace(int units, int G, int64_t n, int k);
+int sparse_fidelity(const SL &s, const uint16_t *queries, int G, int64_t n, const int32_t *sel_idx,
+                    const int32_t *sel_count, int sel_stride, int k, float *exact_out, double *metrics, void *ws,
+                    cudaStream_t st);
 int uva_probe(const void *host, size_t bytes, int row_bytes, const int32_t *rows, int nrows, float *sink,
               cudaStream_t st);
 int64_t calibrate_workspace(int hq, int n_q, int64_t n);

@@ -423,6 +423,21 @@ class DecodeEngine:
             res.setdefault(name, []).append(a.elapsed_time(b))
         return res
 
+    def layer_fidelity(self, l: int) -> dict:
+        """Recall, selected mass, cosine and max-abs error of sparse layer l's
+        last eager step against exact attention (pipeline.py:316-325,
+        377-403), computed on the GPU.  Needs ``record_selection``."""
+        from .fidelity import sparse_layer_fidelity
+
+        if self.labels[l] != "s":
+            raise ConfigError("fidelity metrics are defined for sparsity-friendly layers")
+        if l not in self.last_selection:
+            raise ConfigError("run an eager step with record_selection = True first")
+        idx, cnt, _ = self.last_selection[l]
+        lay = self.layers[l]
+        return sparse_layer_fidelity(lay, self.queries[l], self.G, lay.n - 1, idx, cnt, self.retrieval.n_topk,
+                                     self.out[l])
+
     def cache_counters(self) -> tuple[int, int]:
         """Summed (HBM-cache hits, PCIe-fetched rows) over the sparse layers."""
         h = m = 0

@@ -521,6 +521,39 @@ def test_engine_replays_reference_pipeline(tkv, run, graph, kfh):
         assert misses > 0 and hits + misses > 0  # the HBM row cache was exercised
 
 
+def test_gpu_fidelity_metrics_match_reference_records(tkv):
+    """Recall@k, selected mass, cosine and max-abs error of every sparse layer
+    and step, computed on the GPU against exact attention, equal the values
+    run_pipeline recorded with its float64 oracle (pipeline.py:316-403)."""
+    z = _golden_trace()
+    ref = META["pipeline"]["runs"]["default"]
+    rc = ref["config"]
+    L, h, n0, d = z["prefill_keys"].shape
+    hq = z["w_q"].shape[1]
+    T = 24
+    labels = ["q" if lab == "quantization_friendly" else "s" for lab in ref["labels"]]
+    cfg = tkv.EngineConfig(bits=rc.get("bits", 1), n_local=rc.get("n_local", 64), n_topk=rc.get("n_topk", 128),
+                           critical_channels=rc.get("critical_channels", 8))
+    eng = tkv.DecodeEngine(tkv.ModelConfig(L, hq, h, d, hq * d), labels, cfg, batch=1, max_steps=T)
+    for l in range(L):
+        eng.prefill(l, z["prefill_keys"][l][None], z["prefill_values"][l][None], z["w_q"][l])
+    eng.record_selection = True
+    dev = lambda a: torch.tensor(a[:, None], dtype=torch.float16, device="cuda")  # noqa: E731
+    checked = 0
+    for t in range(T):
+        eng.step(dev(z["hidden"][t]), dev(z["queries"][t]), dev(z["new_keys"][t]), dev(z["new_values"][t]))
+        for l in range(L):
+            if labels[l] != "s":
+                continue
+            f = eng.layer_fidelity(l)
+            assert abs(f["recall"] - ref["recall"][l][t]) <= 1.0 / cfg.n_topk + 1e-12, (l, t)
+            assert abs(f["selected_mass"] - ref["selected_mass"][l][t]) <= 1e-4, (l, t)
+            assert abs(f["cosine"] - ref["cosine"][l][t]) <= 1e-4, (l, t)
+            assert f["max_abs_err"] == pytest.approx(ref["max_abs_err"][l][t], rel=2e-2, abs=1e-4), (l, t)
+            checked += 1
+    assert checked > 0
+
+
 def test_engine_config1_shapes(tkv):
     """BASELINE config 1 shapes (Llama-8B heads, 4k, 1 Q 1-bit + 1 S layer,
     n_topk=128) on synthetic inputs against the oracle replay."""
