@@ -24,6 +24,7 @@ from .retriever import RetrievalConfig, select_topk_tokens, stage1_select
 from .hoststore import OffloadedLayerKV
 from .engine import DecodeEngine, EngineConfig, assemble, shard_plan
 from .fidelity import sparse_layer_fidelity
+from .trace import DeviceTrace, load_trace
 
 __version__ = "0.1.0"
 
@@ -32,5 +33,6 @@ __all__ = [
     "ShapeError", "TraceFormatError", "ModelConfig", "LayerKind", "SparsityProbe", "calibrate", "classify_layer",
     "default_probe_k", "dense_preference_score", "QuantizedLayerKV", "qgemv_output", "qgemv_scores",
     "quantize_layer_kv", "RetrievalConfig", "select_topk_tokens", "stage1_select", "OffloadedLayerKV",
-    "DecodeEngine", "EngineConfig", "assemble", "shard_plan", "sparse_layer_fidelity", "__version__",
+    "DecodeEngine", "EngineConfig", "assemble", "shard_plan", "sparse_layer_fidelity", "DeviceTrace", "load_trace",
+    "__version__",
 ]

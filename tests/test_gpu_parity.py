@@ -554,6 +554,29 @@ def test_gpu_fidelity_metrics_match_reference_records(tkv):
     assert checked > 0
 
 
+def test_engine_runs_reference_trace_file_on_device(tkv):
+    """A reference HKVTRACE file loaded straight to the device (trace.py
+    container, fp16 sections) drives the engine; every output matches the
+    oracle replay of the same file."""
+    from paper_2505_19586_b200.trace import load_trace
+
+    tr = load_trace(GOLD / "tiny_trace.hkv", device="cuda")
+    ref = O.read_trace_file(GOLD / "tiny_trace.hkv")
+    m = tr.header["model"]
+    labels = ["q", "s"]
+    cfg = tkv.EngineConfig(bits=1, group_size=16, n_local=4, n_topk=8, critical_channels=4)
+    eng = tkv.DecodeEngine(tkv.ModelConfig(m["num_layers"], m["num_query_heads"], m["num_kv_heads"], m["head_dim"],
+                                           m["hidden_dim"]), labels, cfg, max_steps=tr.num_steps)
+    for l in range(m["num_layers"]):
+        eng.prefill(l, tr.prefill_keys[l][None], tr.prefill_values[l][None], tr.w_q[l])
+    orc = O.replay(ref["prefill_keys"], ref["prefill_values"], ref["w_q"], ref["steps"], labels, bits=1, g=16,
+                   n_local=4, n_topk=8, d_s=4, compute_exact=False)
+    for t in range(tr.num_steps):
+        out = eng.step(*tr.step_inputs(t)).cpu().numpy()
+        for l in range(m["num_layers"]):
+            assert rel_err(out[l], orc.outputs[t][l]) <= REL_TOL, (t, l)
+
+
 def test_engine_config1_shapes(tkv):
     """BASELINE config 1 shapes (Llama-8B heads, 4k, 1 Q 1-bit + 1 S layer,
     n_topk=128) on synthetic inputs against the oracle replay."""

@@ -168,3 +168,35 @@ def test_byte_formulas():
     assert O.quant_layer_bytes(131072, 8, 128, 1, 64) == 50_331_648
     assert O.scorer_bytes(131072, 8, 8) == 16_777_216
     assert O.gather_bytes(2621 * 8, 128) == 10_735_616
+
+
+def test_package_trace_reader_matches_oracle_reader():
+    """The engine's HKVTRACE loader (fp16 tensors, no float64 round trip)
+    returns the same arrays as the oracle's restatement of trace.py."""
+    from paper_2505_19586_b200.trace import load_trace
+
+    ref = O.read_trace_file(GOLD / "tiny_trace.hkv")
+    tr = load_trace(GOLD / "tiny_trace.hkv")
+    for l in range(len(ref["prefill_keys"])):
+        assert np.array_equal(tr.prefill_keys[l].double().numpy(), ref["prefill_keys"][l])
+        assert np.array_equal(tr.prefill_values[l].double().numpy(), ref["prefill_values"][l])
+        assert np.array_equal(tr.w_q[l].double().numpy(), ref["w_q"][l])
+    for t, st in enumerate(ref["steps"]):
+        assert np.array_equal(tr.queries[t].double().numpy(), st["queries"])
+        assert np.array_equal(tr.new_values[t].double().numpy(), st["new_values"])
+        assert np.array_equal(tr.hidden[t].double().numpy(), st["hidden"])
+
+
+def test_package_trace_reader_errors(tmp_path):
+    from paper_2505_19586_b200.errors import TraceFormatError
+    from paper_2505_19586_b200.trace import load_trace
+
+    blob = (GOLD / "tiny_trace.hkv").read_bytes()
+    bad = tmp_path / "bad_magic.hkv"
+    bad.write_bytes(b"NOTATRACE" + blob[9:])
+    with pytest.raises(TraceFormatError):
+        load_trace(bad)
+    tampered = tmp_path / "tampered.hkv"
+    tampered.write_bytes(blob[:-2] + bytes([blob[-2] ^ 1, blob[-1]]))
+    with pytest.raises(TraceFormatError):
+        load_trace(tampered)
