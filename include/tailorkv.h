@@ -170,6 +170,12 @@ int tkv_sparse_append(const tkv_sparse_layer *s, const uint16_t *new_keys, const
  * units = B * hq / G.  Writes q_hat f64 [B][hq][d] (may be NULL) and
  * channels int32 [units][d_s] sorted ascending. */
 int64_t tkv_stage1_workspace(int32_t B, int32_t hq, int32_t hidden, int32_t d);
+/* Stage 1 that also starts moving the selected channel rows of `layer`'s
+ * channel-major scorer keys into L2 (TMA prefetch), so the layer's decode
+ * scores from L2.  `layer` NULL = tkv_stage1. */
+int tkv_stage1_prefetch(const uint16_t *hidden, const uint16_t *w_q, int32_t B, int32_t hq, int32_t hidden_dim,
+                        int32_t d, int32_t G, const float *chmax, int32_t d_s, double *q_hat, int32_t *channels,
+                        void *workspace, const tkv_sparse_layer *layer, void *stream);
 int tkv_stage1(const uint16_t *hidden, const uint16_t *w_q, int32_t B, int32_t hq, int32_t hidden_dim,
                int32_t d, int32_t G, const float *chmax, int32_t d_s, double *q_hat, int32_t *channels,
                void *workspace, void *stream);

@@ -86,6 +86,8 @@ _SIGS = {
     "tkv_sparse_append": (C.c_int, [C.POINTER(SparseLayer), _P, _P, _P]),
     "tkv_stage1_workspace": (C.c_int64, [_I32, _I32, _I32, _I32]),
     "tkv_stage1": (C.c_int, [_P, _P, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P]),
+    "tkv_stage1_prefetch": (C.c_int, [_P, _P, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P,
+                                      C.POINTER(SparseLayer), _P]),
     "tkv_select_workspace": (C.c_int64, [_I32, _I64]),
     "tkv_select_tokens": (C.c_int, [C.POINTER(SparseLayer), _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "tkv_topk_from_scores": (C.c_int, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P]),

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(S1_THREADS, 2) stage1_fused_kernel(const uint1
                                                                   unsigned *__restrict__ arrive, int G,
                                                                   const float *__restrict__ chmax, int d_s,
                                                                   double *__restrict__ q_hat,
-                                                                  int32_t *__restrict__ channels) {
+                                                                  int32_t *__restrict__ channels, SL pf, int prefetch) {
   constexpr int TPR = D / 8;               // threads per row
   constexpr int RG = S1_THREADS / TPR;     // row groups
   constexpr int BATCH = 8;                 // loads in flight per thread and batch
@@ -289,8 +289,24 @@ __global__ void __launch_bounds__(S1_THREADS, 2) stage1_fused_kernel(const uint1
   double *qs = reinterpret_cast<double *>(red);  // G*D <= 2048 doubles
   __shared__ double score[256];
   __shared__ int flags[256];
-  for (int b = 0; b < nb; ++b)
+  for (int b = 0; b < nb; ++b) {
     stage1_select_unit(part, splits, B, hq, D, G, chmax, d_s, q_hat, channels, b0 + b, kvh, qs, score, flags);
+    if (prefetch) {
+      // start moving the selected channel rows of the layer's scorer keys into L2: the
+      // layer's decode kernel (next on the main stream) then scores from L2, not HBM
+      const int u = (b0 + b) * hkv + kvh;
+      const int64_t len = *pf.len;
+      const int64_t bytes = len * 2;
+      const int64_t nch = (bytes + 32767) / 32768;
+      for (int64_t i = threadIdx.x; i < (int64_t)d_s * nch; i += blockDim.x) {
+        const int c = channels[(size_t)u * d_s + i / nch];
+        const int64_t o = (i % nch) * 32768;
+        const uint32_t sz = (uint32_t)min((int64_t)32768, bytes - o);
+        const char *src = reinterpret_cast<const char *>(pf.kt + ((size_t)u * D + c) * pf.capacity) + o;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((sz + 15u) & ~15u) : "memory");
+      }
+    }
+  }
 }
 
 static int stage1_splits(int hq, int H) {
@@ -311,7 +327,9 @@ int64_t stage1_workspace(int B, int hq, int H, int d) {
 }
 
 int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, int d, int G, const float *chmax,
-           int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st) {
+           int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st, const SL *pf) {
+  SL pfs = {};
+  if (pf) pfs = *pf;
   if (G > 16 || G * d > 2048) return fail(TKV_ERR_SHAPE, "stage 1 supports G*head_dim <= 2048 (G <= 16)");
   const int splits = stage1_splits(hq, H);
   const int rows = ((H + splits - 1) / splits + 7) / 8 * 8;
@@ -323,9 +341,9 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
   const dim3 grid((H + rows - 1) / rows, hq, (B + bg - 1) / bg);
 #define TKV_S1(DD)                                                                                              \
   (B == 1 ? launch_prio(stage1_fused_kernel<DD, 1>, grid, dim3(S1_THREADS), 0, st, false, hidden, w_q, B, H, rows, \
-                        part, arrive, G, chmax, d_s, q_hat, channels)                                            \
+                        part, arrive, G, chmax, d_s, q_hat, channels, pfs, pf ? 1 : 0)                           \
           : launch_prio(stage1_fused_kernel<DD, S1_BG>, grid, dim3(S1_THREADS), 0, st, false, hidden, w_q, B, H,  \
-                        rows, part, arrive, G, chmax, d_s, q_hat, channels))
+                        rows, part, arrive, G, chmax, d_s, q_hat, channels, pfs, pf ? 1 : 0))
   switch (d) {
     case 128: TKV_S1(128); break;
     case 64: TKV_S1(64); break;

@@ -6,7 +6,7 @@ int sparse_prefill(const SL &s, const uint16_t *keys, const uint16_t *values, in
 int sparse_append(const SL &s, const uint16_t *nk, const uint16_t *nv, cudaStream_t st);
 int64_t stage1_workspace(int B, int hq, int H, int d);
 int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, int d, int G, const float *chmax,
-           int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st);
+           int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st, const SL *prefetch = nullptr);
 int64_t select_workspace(int units, int64_t cap);
 int select_tokens(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                   int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, double *scores_out,

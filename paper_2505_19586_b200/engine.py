@@ -47,6 +47,7 @@ class EngineConfig:
     row_cache: bool = True         # keep fetched value rows in HBM (exact; rows are immutable)
     row_cache_steps: int = 4       # a row stays cached until it has not been selected for this many steps
     fused_sparse: bool = True      # one launch per sparse layer (select + gather + attention); else two
+    scorer_l2_prefetch: bool = True  # stage 1 starts moving the chosen scorer columns into L2
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
     def validate(self) -> None:
@@ -268,7 +269,8 @@ class DecodeEngine:
         src = l - 1 if l >= 1 else 0  # pipeline.py:273
         t0 = self._mark(self.side)
         stage1_select(self.hidden[src], st.w_q, st.layer.chmax, self.G, self.retrieval.d_s,
-                      channels=st.channels, workspace=st.s1_ws, stream=self.side)
+                      channels=st.channels, workspace=st.s1_ws, stream=self.side,
+                      prefetch_layer=st.layer if self.cfg.scorer_l2_prefetch else None)
         self._span("stage1", l, t0, self.side)
         st.s1_done.record(self.side)
 

@@ -60,7 +60,7 @@ WORKSPACES = _WS()
 
 def stage1_select(hidden: torch.Tensor, w_q: torch.Tensor, chmax: torch.Tensor, G: int, d_s: int,
                   channels: torch.Tensor | None = None, q_hat: torch.Tensor | None = None, workspace=None,
-                  stream=None) -> torch.Tensor:
+                  stream=None, prefetch_layer=None) -> torch.Tensor:
     """q_hat = hidden . W_q then the top-d_s critical channels per unit.
 
     hidden fp16 [B, hidden]; w_q fp16 [hq, hidden, d]; chmax fp32 [B*hq/G, d].
@@ -77,8 +77,13 @@ def stage1_select(hidden: torch.Tensor, w_q: torch.Tensor, chmax: torch.Tensor, 
         channels = torch.empty((units, d_s), dtype=torch.int32, device=hidden.device)
     if workspace is None:
         workspace = WORKSPACES.get("stage1", lib.tkv_stage1_workspace(B, hq, H, d), hidden.device)
-    check(lib.tkv_stage1(ptr(hidden), ptr(w_q), B, hq, H, d, G, ptr(chmax), d_s, ptr(q_hat), ptr(channels),
-                         ptr(workspace), stream_ptr(stream)))
+    if prefetch_layer is None:
+        check(lib.tkv_stage1(ptr(hidden), ptr(w_q), B, hq, H, d, G, ptr(chmax), d_s, ptr(q_hat), ptr(channels),
+                             ptr(workspace), stream_ptr(stream)))
+    else:  # also start moving the chosen scorer columns of that layer into L2
+        check(lib.tkv_stage1_prefetch(ptr(hidden), ptr(w_q), B, hq, H, d, G, ptr(chmax), d_s, ptr(q_hat),
+                                      ptr(channels), ptr(workspace), C.byref(prefetch_layer.struct),
+                                      stream_ptr(stream)))
     return channels
 
 
