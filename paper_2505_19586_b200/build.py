@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 6) -> Path:
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
         objs.append(obj)
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c", str(CSRC / src),
+        extra = os.environ.get("TKV_NVCC_DEFINES", "").split()  # experiments, e.g. -DTKV_FZ_CTAS=16
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c", str(CSRC / src),
                "-o", str(obj)]
         if verbose:
             print(" ".join(cmd))

@@ -39,7 +39,10 @@ namespace cg = cooperative_groups;
 
 namespace tkv {
 
-constexpr int FZ_CTAS = 8;
+#ifndef TKV_FZ_CTAS
+#define TKV_FZ_CTAS 8
+#endif
+constexpr int FZ_CTAS = TKV_FZ_CTAS;
 constexpr int FZ_THREADS = 512;
 constexpr int FZ_WARPS = FZ_THREADS / 32;
 constexpr int FZ_CAP = 18432;        // candidate keys per CTA: 8 CTAs cover 147,456 tokens
@@ -1688,6 +1691,7 @@ static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, con
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (FZ_CTAS > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
