@@ -577,6 +577,55 @@ def test_engine_runs_reference_trace_file_on_device(tkv):
             assert rel_err(out[l], orc.outputs[t][l]) <= REL_TOL, (t, l)
 
 
+# BASELINE.json configs 3-5 as parity cases at reduced context (the bench runs config 2):
+# (name, hq, h, hidden, q_layers, bits, batch, n, n_topk)
+_CONFIG_CASES = [
+    ("cfg3_llama8b_b2_2bit_3pct", 32, 8, 4096, (0,), 2, 2, 2048, 61),
+    ("cfg4_qwen7b_g7_1pct", 28, 4, 3584, (0,), 1, 2, 4096, 41),
+    ("cfg5_llama70b_g8_2pct", 64, 8, 8192, (0,), 1, 1, 2048, 41),
+]
+
+
+@pytest.mark.parametrize("case", _CONFIG_CASES, ids=lambda c: c[0])
+def test_engine_baseline_config_shapes(tkv, case):
+    """Engine outputs for the BASELINE config families (batch > 1, 2-bit,
+    G = 7 and G = 8 grouped-query shapes) against the oracle replay of every
+    sequence, and the Top-K selections against the oracle's."""
+    from paper_2505_19586_b200.synth import make_workload
+
+    name, hq, h, hidden, q_layers, bits, B, n, n_topk = case
+    L, T, d = 3, 3, 128
+    w = make_workload(L, q_layers, hq, h, d, n, T, batch=B, seed=17, keep_wq_for_q_layers=True)
+    cfg = tkv.EngineConfig(bits=bits, n_local=64, n_topk=n_topk, critical_channels=8)
+    eng = tkv.DecodeEngine(tkv.ModelConfig(L, hq, h, d, hidden), w.labels, cfg, batch=B, max_steps=T)
+    for l in range(L):
+        eng.prefill(l, w.prefill_keys[l], w.prefill_values[l], w.w_q[l])
+    eng.record_selection = True
+    outs, sels = [], []
+    for t in range(T):
+        outs.append(eng.step(w.hidden[t], w.queries[t], w.new_keys[t], w.new_values[t]).cpu().numpy().copy())
+        sels.append({l: tuple(x.cpu().numpy() for x in eng.last_selection[l]) for l in eng.last_selection})
+    G = hq // h
+    for b in range(B):
+        steps = [{"hidden": w.hidden[t, :, b].double().cpu().numpy(), "queries": w.queries[t, :, b].double().cpu().numpy(),
+                  "new_keys": w.new_keys[t, :, b].double().cpu().numpy(),
+                  "new_values": w.new_values[t, :, b].double().cpu().numpy()} for t in range(T)]
+        orc = O.replay([k[b].double().cpu().numpy() for k in w.prefill_keys],
+                       [v[b].double().cpu().numpy() for v in w.prefill_values],
+                       [wq.double().cpu().numpy() for wq in w.w_q], steps, w.labels, bits=bits, n_local=64,
+                       n_topk=n_topk, d_s=8, compute_exact=False)
+        for t in range(T):
+            for l in range(L):
+                o = outs[t][l].reshape(B, hq, d)[b]
+                assert rel_err(o, orc.outputs[t][l]) <= REL_TOL, (name, b, t, l)
+                if w.labels[l] == "s":
+                    idx, cnt, _ = sels[t][l]
+                    for kvh in range(h):
+                        u = b * h + kvh
+                        assert np.array_equal(idx[u, :cnt[u]], orc.selected[(l, t)][kvh]), (name, b, t, l, kvh)
+    assert G in (4, 7, 8)
+
+
 def test_engine_config1_shapes(tkv):
     """BASELINE config 1 shapes (Llama-8B heads, 4k, 1 Q 1-bit + 1 S layer,
     n_topk=128) on synthetic inputs against the oracle replay."""
