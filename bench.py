@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--unfused", action="store_true", help="sparse layers as two launches (select, gather+attend)")
     ap.add_argument("--phases", action="store_true", help="print the fused sparse kernel's phase marks (unit 0)")
     ap.add_argument("--no-fidelity", action="store_true", help="skip the one-step recall/cosine evaluation")
+    ap.add_argument("--serial-stage1", action="store_true", help="stage 1 runs in line, not overlapped")
     ap.add_argument("--no-l2-prefetch", action="store_true", help="stage 1 does not prefetch the scorer columns")
     ap.add_argument("--cache-steps", type=int, default=4,
                     help="HBM row cache window: a value row stays resident until unselected for this many steps (0: off)")
@@ -278,7 +279,7 @@ def main():
     cfg = P.EngineConfig(bits=1, group_size=64, n_local=64, n_topk=n_topk, critical_channels=8,
                          keys_from_hbm=not args.keys_over_pcie, fused_sparse=not args.unfused,
                          row_cache=args.cache_steps > 0, row_cache_steps=max(1, args.cache_steps),
-                         scorer_l2_prefetch=not args.no_l2_prefetch)
+                         scorer_l2_prefetch=not args.no_l2_prefetch, overlap_stage1=not args.serial_stage1)
     W, K = args.warmup, args.steps
     PROF = 2
     total = W + 3 * K + 2 * PROF + 10

@@ -152,6 +152,9 @@ typedef struct tkv_sparse_layer {
    * hint that aims the next step's threshold search (results never depend on
    * it; NaN or NULL = no hint). */
   float *thresh;
+  /* [units][16] (with cache_slots): per slot partition, the slot the next
+   * allocation scan starts from (the cache's clock hand), zero-initialised */
+  int32_t *slot_hand;
 } tkv_sparse_layer;
 
 /* Prefill/offload (replaces HostPool.offload_layer memsim.py:88-93 and the

@@ -447,7 +447,7 @@ __device__ __forceinline__ void fz_bulk_commit_wait_read() {
 }
 
 // phase timestamps of unit 0, every CTA (debug: tkv_debug_sparse_phases)
-constexpr int FZ_NMARK = 32;
+constexpr int FZ_NMARK = 40;
 __device__ unsigned long long g_fz_phase[FZ_CTAS][FZ_NMARK];
 __device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
 __device__ double g_fz_dbg[2][8];  // list-path attempts of unit 0 (debug)
@@ -1292,10 +1292,19 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       for (int e = 0; e < CPL; ++e) acc[h][e] = 0.0f;
     }
     // (a) one thread per row issues the bulk copy of its value row (and key row over PCIe)
+    // PCIe copies stall their issuing thread on host-page translations (one
+    // translation per random row; the GPU resolves ~75M/s), and the TMA unit
+    // serves its queue in order.  With the row cache on, the last warp issues
+    // them after every HBM copy is queued, while the other warps compute the
+    // key logits; otherwise every thread issues its rows.
+    const bool pcie_warp = use_cache;
+    const int NLW = pcie_warp ? FZ_WARPS - 1 : FZ_WARPS;  // warps computing key logits
+    auto over_pcie = [](int code) { return code == -1 || code <= -3; };
     auto issue_round = [&](int base, int cnt) {
       if (tid == 0) fz_mbar_expect(&C.bar, (uint32_t)(cnt * D * 2 * (keys_host ? 2 : 1)));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses before the TMA writes
       __syncthreads();
+      if (base == 0) FZ_MARK(34);
       for (int i = tid; i < cnt; i += blockDim.x) {
         const int64_t idx = rbase + rows[base + i];
         const int code = rslot[base + i];
@@ -1307,6 +1316,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
                                      &C.bar);
         } else {
           const uint16_t *hrow = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
+          if (pcie_warp && over_pcie(code)) continue;
           vp = code >= 0 ? sv + (size_t)code * D : hrow + D;
           if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, hrow, D * 2, &C.bar);
         }
@@ -1315,42 +1325,31 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     };
     if (nrows > 0) issue_round(0, min(NR, nrows));
     FZ_MARK(25);
-    // cache slots for this step's misses: free slots of this CTA's partition
-    // (empty, or not selected in the last cache_window steps), in order
-    if (use_cache) {
-      const int W = max(1, s.cache_window);
-      int32_t *F = reinterpret_cast<int32_t *>(S.flags);  // free-slot list (the flags are dead)
-      int nf = 0;
-      for (int p = p0 + tid; p < p1; p += blockDim.x) nf += stok[p] < 0 || sstamp[p] <= (int)n - W;
-      int ftot;
-      int fpos = fz_block_excl_scan(nf, C.scan, &ftot);
-      for (int p = p0 + tid; p < p1; p += blockDim.x)
-        if (stok[p] < 0 || sstamp[p] <= (int)n - W) F[fpos++] = p;
-      int tm = 0;
-      for (int i = tid; i < nrows; i += blockDim.x) tm += rslot[i] == -1;
-      int dummy;
-      int ord = fz_block_excl_scan(tm, C.scan, &dummy);  // (its barriers also publish F)
-      for (int i = tid; i < nrows; i += blockDim.x) {
-        if (rslot[i] != -1) continue;
-        const int k = ord++;
-        if (k < ftot) rslot[i] = -3 - F[k];  // misses beyond the free slots are simply not cached
-      }
-      __syncthreads();
-    }
-    FZ_MARK(26);
     uint32_t parity = 0;
     for (int base = 0; base < nrows; base += NR) {
       const int cnt = min(NR, nrows - base);
       if (base > 0) issue_round(base, cnt);
       // (b) logits of this warp's rows: key rows from HBM while the value copies fly;
       // a batch's 16 row loads are issued before any use
-      if (!keys_host) {
-        for (int i0 = warp; i0 < cnt; i0 += FZ_WARPS * 16) {
+      if (pcie_warp && warp == FZ_WARPS - 1) {
+        // (b') the PCIe warp: value rows over PCIe, queued behind the HBM copies
+        for (int i = lane; i < cnt; i += 32) {
+          if (!over_pcie(rslot[base + i])) continue;
+          fz_bulk_g2s(stage_v + (size_t)i * D, s.host_kv + ((size_t)u * s.capacity + rbase + rows[base + i]) * 2 * D + D,
+                      D * 2, &C.bar);
+        }
+        if (trace && blockIdx.y == 0 && lane == 0 && base == 0) {
+          unsigned long long t_;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+          g_fz_phase[rank][35] = t_;
+        }
+      } else if (!keys_host) {
+        for (int i0 = warp; i0 < cnt; i0 += NLW * 16) {
           if constexpr (CPL == 4 && GMAX == 4) {
             uint2 kr[16];
 #pragma unroll
             for (int jr = 0; jr < 16; ++jr) {
-              const int i = i0 + FZ_WARPS * jr;
+              const int i = i0 + NLW * jr;
               kr[jr] = make_uint2(0u, 0u);
               if (i < cnt) {
                 const int64_t idx = rbase + rows[base + i];
@@ -1367,13 +1366,14 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
                 }
               }
             }
+            if (base == 0 && i0 == warp) FZ_MARK(32);
             const float4 q0 = *reinterpret_cast<const float4 *>(S.qs + 0 * D + lane * 4);
             const float4 q1 = *reinterpret_cast<const float4 *>(S.qs + 1 * D + lane * 4);
             const float4 q2 = *reinterpret_cast<const float4 *>(S.qs + 2 * D + lane * 4);
             const float4 q3 = *reinterpret_cast<const float4 *>(S.qs + 3 * D + lane * 4);
 #pragma unroll
             for (int jr = 0; jr < 16; ++jr) {
-              const int i = i0 + FZ_WARPS * jr;
+              const int i = i0 + NLW * jr;
               if (i >= cnt) break;
               const float k0 = h2f((uint16_t)kr[jr].x), k1 = h2f((uint16_t)(kr[jr].x >> 16));
               const float k2 = h2f((uint16_t)kr[jr].y), k3 = h2f((uint16_t)(kr[jr].y >> 16));
@@ -1394,11 +1394,12 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
               const int h = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
               if ((lane & 7) == 0 && h < G) zs[(size_t)i * GMAX + h] = c;
             }
+            if (base == 0 && i0 == warp) FZ_MARK(33);
           } else {
             float kf[8][CPL];
 #pragma unroll
             for (int jr = 0; jr < 8; ++jr) {
-              const int i = i0 + FZ_WARPS * jr;
+              const int i = i0 + NLW * jr;
 #pragma unroll
               for (int e = 0; e < CPL; ++e) kf[jr][e] = 0.0f;
               if (i >= cnt) continue;
@@ -1416,7 +1417,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             }
 #pragma unroll
             for (int jr = 0; jr < 8; ++jr) {
-              const int i = i0 + FZ_WARPS * jr;
+              const int i = i0 + NLW * jr;
               if (i >= cnt) break;
 #pragma unroll
               for (int h = 0; h < GMAX; ++h) {
@@ -1431,7 +1432,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             }
             // rows 8..15 of this batch
             for (int jr = 8; jr < 16; ++jr) {
-              const int i = i0 + FZ_WARPS * jr;
+              const int i = i0 + NLW * jr;
               if (i >= cnt) break;
               const int64_t idx = rbase + rows[base + i];
               float kk2[CPL];
@@ -1537,6 +1538,47 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
       }
       if (base == 0) FZ_MARK(29);
+      // cache slots for this step's misses: free slots of this CTA's partition
+      // (empty, or not selected in the last cache_window steps), scanned from
+      // the partition's clock hand one block-sized chunk at a time
+      if (use_cache && base == 0) {
+        const int W = max(1, s.cache_window);
+        int32_t *F = reinterpret_cast<int32_t *>(S.flags);  // free-slot list (the flags are dead)
+        constexpr int FCAP = FZ_CAP / 4;
+        int tm = 0;
+        for (int i = tid; i < nrows; i += blockDim.x) tm += rslot[i] == -1;  // (misses of later rounds too)
+        int need;
+        int ord = fz_block_excl_scan(tm, C.scan, &need);
+        need = min(need, FCAP);
+        const int np = p1 - p0;
+        int32_t *hand = s.slot_hand ? s.slot_hand + (size_t)u * 16 + rank : nullptr;
+        const int h0 = hand && np > 0 ? ((*hand % np) + np) % np : 0;
+        int found = 0;
+        for (int k0 = 0; found < need && k0 < np; k0 += blockDim.x) {  // uniform: found, need, np
+          const int k = k0 + tid;
+          int p = 0, fr = 0;
+          if (k < np) {
+            p = p0 + (h0 + k) % np;
+            fr = stok[p] < 0 || sstamp[p] <= (int)n - W;
+          }
+          int tot;
+          const int pos = found + fz_block_excl_scan(fr, C.scan, &tot);
+          if (fr && pos < need) {
+            F[pos] = p;
+            if (pos == need - 1 && hand) *hand = (h0 + k + 1) % np;  // the hand moves past the last slot taken
+          }
+          found += tot;
+        }
+        __syncthreads();  // F
+        const int used = min(found, need);
+        for (int i = tid; i < nrows; i += blockDim.x) {
+          if (rslot[i] != -1) continue;
+          const int k = ord++;
+          if (k < used) rslot[i] = -3 - F[k];  // misses beyond the free slots are simply not cached
+        }
+        __syncthreads();
+      }
+      if (base == 0) FZ_MARK(36);
       // (e) rows fetched over PCIe enter the HBM row cache in their assigned slots
       if (use_cache) {
         for (int i = tid; i < cnt; i += blockDim.x) {
@@ -1728,7 +1770,6 @@ bool select_cluster_ok(const SL &s, int n_local) { return fused_ok(s, n_local); 
 
 bool sparse_decode_supported(const SL &s, int G, int n_local) {
   if (!fused_ok(s, n_local)) return false;
-  if ((s.cache_slots + FZ_CTAS - 1) / FZ_CTAS > FZ_CAP / 4) return false;  // free-slot list in the flags area
   return (s.d == 128 && G <= 8) || (s.d == 64 && G <= 8) || (s.d == 256 && G <= 4) || (s.d == 32 && G <= 8);
 }
 
@@ -1778,5 +1819,5 @@ extern "C" int tkv_debug_sparse_attempts(double *out) {
 }
 
 extern "C" int tkv_debug_sparse_phases(unsigned long long *out) {  // [8][32]
-  return cudaMemcpyFromSymbol(out, tkv::g_fz_phase, sizeof(tkv::g_fz_phase)) == cudaSuccess ? 0 : 7;
+  return cudaMemcpyFromSymbol(out, tkv::g_fz_phase, sizeof(tkv::g_fz_phase)) == cudaSuccess ? 0 : 7;  // [8][40]
 }

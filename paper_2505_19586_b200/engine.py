@@ -48,6 +48,7 @@ class EngineConfig:
     row_cache_steps: int = 4       # a row stays cached until it has not been selected for this many steps
     fused_sparse: bool = True      # one launch per sparse layer (select + gather + attention); else two
     scorer_l2_prefetch: bool = True  # stage 1 starts moving the chosen scorer columns into L2
+    overlap_stage1: bool = True    # stage 1 of layer l+1 runs on a side stream during layer l (else in line)
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
     def validate(self) -> None:
@@ -303,6 +304,8 @@ class DecodeEngine:
         for l in range(L):
             begin[l].record(main)
             nxt = [j for j in ((0, 1) if l == 0 else (l + 1,)) if j < L and self.labels[j] == "s"]
+            if not self.cfg.overlap_stage1:
+                nxt = [l] if self.labels[l] == "s" else []
             for j in nxt:
                 self.side.wait_event(begin[l])
                 with torch.cuda.stream(self.side):

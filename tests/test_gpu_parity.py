@@ -394,8 +394,8 @@ def test_fused_sparse_decode_select_all(tkv, n):
     assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5
 
 
-@pytest.mark.parametrize("window", [1, 3])
-def test_fused_sparse_decode_row_cache_across_steps(tkv, window):
+@pytest.mark.parametrize("window,rows", [(1, None), (3, None), (100, None), (2, 60)])
+def test_fused_sparse_decode_row_cache_across_steps(tkv, window, rows):
     """Decode -> append -> decode ... with the HBM row cache (rows selected in
     the last `window` steps stay resident): rows served from the cache give
     the oracle's results at every step, and slots are recycled."""
@@ -405,7 +405,7 @@ def test_fused_sparse_decode_row_cache_across_steps(tkv, window):
     values = cases.f16(rng.normal(size=(units, n0 + T, d)))
     cfg = tkv.RetrievalConfig(32, 400, 8)
     lay = _sparse_layer(tkv, keys[:, :n0], values[:, :n0], cfg.n_local, steps=T, keys_on_device=True,
-                        cache_rows=cfg.n_local + cfg.n_topk, cache_window=window)
+                        cache_rows=rows or cfg.n_local + cfg.n_topk, cache_window=window)  # rows: undersized cache
     chans = np.stack([np.sort(rng.choice(d, 8, replace=False)) for _ in range(units)]).astype(np.int32)
     base_q = rng.normal(size=(units * G, d))
     for t in range(T):

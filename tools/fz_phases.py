@@ -35,9 +35,9 @@ def show(lib):
         d = list(dbg)[a * 8:(a + 1) * 8]
         print(f"  attempt {a}: above {d[1]:.0f} list {d[2]:.0f} need {d[3]:.0f} ok {d[4]:.0f} center {d[5]:.5g} "
               f"width {d[6]:.4g} sd {d[7]:.4g}")
-    ph = (C.c_ulonglong * (8 * 32))()
+    ph = (C.c_ulonglong * (8 * 40))()
     lib.tkv_debug_sparse_phases(ph)
-    t = [list(ph)[r * 32:(r + 1) * 32] for r in range(8)]
+    t = [list(ph)[r * 40:(r + 1) * 40] for r in range(8)]
     t0 = min(x[0] for x in t)
     x = t[0]
     clk = (C.c_ulonglong * 16)()
@@ -54,9 +54,10 @@ def show(lib):
         y = t[r]
         if y[24] and y[30]:
             g = lambda a, b: (y[b] - y[a]) / 1e3  # noqa: E731
-            print(f"  gather rank {r}: lookups {g(15, 24):.2f} issue {g(24, 25):.2f} slots {g(25, 26):.2f} "
-                  f"logits {g(26, 27):.2f} wait {g(27, 28):.2f} softmax {g(28, 29):.2f} insert {g(29, 30):.2f} "
-                  f"rest {g(30, 16):.2f}")
+            print(f"  gather rank {r}: lookups {g(15, 24):.2f} issue-hbm {g(24, 25):.2f} logits {g(25, 27):.2f} "
+                  f"(pcie-issued at {g(25, 35):.2f}) wait {g(27, 28):.2f} softmax {g(28, 29):.2f} "
+                  f"slots {g(29, 36):.2f} insert {g(36, 30):.2f} rest {g(30, 16):.2f} | "
+                  f"logits batch0: loads-issued {g(25, 32):.2f} computed {g(32, 33):.2f}")
     for r in range(8):
         parts, prev = [], t[r][0]
         for i in (1, 2, 3, 4, 12, 13, 14, 15, 16, 17, 18, 19, 20):
