@@ -288,6 +288,9 @@ def main():
                        batch=1, seed=args.seed, device=device)
     eng = P.DecodeEngine(model, wl.labels, cfg, batch=1, max_steps=total, rank=rank, world_size=world,
                          device=device)
+    if os.environ.get("TKV_AIM"):  # tuning: first aimed range half-width (score sd)
+        import ctypes
+        _lib.load().tkv_debug_sparse_aim(ctypes.c_float(float(os.environ["TKV_AIM"])))
     for l in range(L):
         eng.prefill(l, wl.prefill_keys[l], wl.prefill_values[l], wl.w_q[l])
         wl.prefill_keys[l] = wl.prefill_values[l] = None
@@ -392,9 +395,16 @@ def main():
         enable(_lib.load())
     prof, hits, misses = profile_mode()
     if args.phases and rank == 0:
-        from tools.fz_phases import show
+        from tools.fz_phases import show, show_launches
         _lib.load().tkv_debug_sparse_trace(0)
         show(_lib.load())
+        # launch gaps inside the plain (timed) graph: one more step with the trace on
+        enable(_lib.load())
+        eng.step(*inputs(step_i)); step_i += 1
+        torch.cuda.synchronize()
+        _lib.load().tkv_debug_sparse_trace(0)
+        print("plain graph:")
+        show_launches(_lib.load())
     fetch_rows = int(eng.fetch_count.sum().item())
     cached_rows = hits / (PROF * n_sparse)     # per launch, served from the HBM row cache
     pcie_rows = misses / (PROF * n_sparse)     # per launch, fetched over PCIe

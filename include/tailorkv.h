@@ -148,9 +148,11 @@ typedef struct tkv_sparse_layer {
   uint16_t *slot_v;       /* [units][cache_slots][d] cached value rows */
   int32_t *tok_slot;      /* [units][capacity] token -> slot, verified against slot_tok */
   unsigned long long *cache_stats; /* [2]: rows served from HBM, rows fetched over PCIe */
-  /* Optional [units] float: the last step's top-k score threshold per head, a
-   * hint that aims the next step's threshold search (results never depend on
-   * it; NaN or NULL = no hint). */
+  /* Optional [units][4] float (16-byte aligned): per head, the last step's
+   * top-k score threshold as a z-score of that step's scores and a running
+   * mean of its step-to-step change (two spare floats); a hint that aims the
+   * next step's threshold search (results never depend on it; NaN or NULL =
+   * no hint). */
   float *thresh;
   /* [units][16] (with cache_slots): per slot partition, the slot the next
    * allocation scan starts from (the cache's clock hand), zero-initialised */

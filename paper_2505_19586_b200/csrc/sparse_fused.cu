@@ -310,9 +310,8 @@ __device__ __forceinline__ double fz_exact_score(const uint16_t *kt, int64_t cap
 }
 
 // cluster-wide min/max (orderable keys) and sum / sum of squares of the scores
-__device__ __forceinline__ void fz_cluster_stats(cg::cluster_group &cluster, FzCtl &C, uint32_t lo, uint32_t hi,
-                                                 double sum, double sq, uint32_t &glo, uint32_t &ghi, double &gsum,
-                                                 double &gsq) {
+// this CTA's min/max key and score moments into C (for the cluster or for rank 0)
+__device__ __forceinline__ void fz_block_stats(FzCtl &C, uint32_t lo, uint32_t hi, double sum, double sq) {
   const int tid = threadIdx.x, lane = tid & 31;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -346,6 +345,12 @@ __device__ __forceinline__ void fz_cluster_stats(cg::cluster_group &cluster, FzC
       C.ksq = y;
     }
   }
+}
+
+__device__ __forceinline__ void fz_cluster_stats(cg::cluster_group &cluster, FzCtl &C, uint32_t lo, uint32_t hi,
+                                                 double sum, double sq, uint32_t &glo, uint32_t &ghi, double &gsum,
+                                                 double &gsq) {
+  fz_block_stats(C, lo, hi, sum, sq);
   cluster.sync();
   glo = 0xffffffffu;
   ghi = 0u;
@@ -453,7 +458,21 @@ __device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
 __device__ double g_fz_dbg[2][8];  // list-path attempts of unit 0 (debug)
 __device__ unsigned long long g_fz_clk[FZ_CTAS][2];  // clock64 at the first and last mark (debug)
 __device__ unsigned long long g_fz_unit[64][FZ_CTAS][2];  // per unit and rank: globaltimer at start / end (debug)
+__device__ unsigned long long g_fz_launch[128][3];  // unit 0, rank 0, per launch: start, after the PDL wait, end (debug)
+__device__ unsigned int g_fz_nlaunch;
 __device__ int g_fz_upath[64][4];  // per unit: select path (0 list attempt 0, 1 list attempt 1, 2 full range), list size, rows, misses
+__device__ unsigned int g_fz_pathcnt[4];  // launches x units per select path (trace mode)
+__device__ float g_fz_aim = 0.0f;         // tuning: fixed half-width of the first aimed range (sd); 0 = adaptive
+
+// The threshold hint of a (layer, head), float4: x the last top-k threshold
+// as a z-score of that step's scores, y a running mean of its step-to-step
+// change (the z-score is what stays stable: the scores' mean and spread move
+// with the query; an absolute hint drifts several times faster).
+__device__ __forceinline__ void fz_store_hint(float *th, float4 old, double z) {
+  const float dz = isfinite(old.x) ? (float)fabs(z - (double)old.x) : __int_as_float(0x7fc00000);
+  th[1] = isfinite(old.y) ? (isfinite(dz) ? 0.75f * old.y + 0.25f * dz : old.y) : dz;
+  th[0] = (float)z;
+}
 #define FZ_MARK(i)                                                          \
   do {                                                                      \
     if (trace && blockIdx.y == 0 && tid == 0) {                             \
@@ -484,6 +503,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = *s.len;
   const int trace = g_fz_trace;
+  const float qnan = __int_as_float(0x7fc00000);
+  const float aim_fixed = g_fz_aim;
+  const float4 hint = s.thresh ? *reinterpret_cast<const float4 *>(s.thresh + 4 * (size_t)u) : make_float4(qnan, qnan, qnan, qnan);
   int32_t *out_idx = sel_idx + (size_t)u * sel_stride;
   const bool select_all = n <= (int64_t)n_local + n_topk;  // retriever.py:204-205
   const int64_t ncand = n > n_local ? n - n_local : 0;     // local window starts here
@@ -494,10 +516,15 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
   const uint16_t *kt = s.kt + (size_t)u * s.d * s.capacity;
   FZ_MARK(0);
   if (trace && blockIdx.y == 0 && tid == 0) g_fz_clk[rank][0] = clock64();
+  __shared__ unsigned int lslot;
   if (trace && blockIdx.y < 64 && tid == 0) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     g_fz_unit[blockIdx.y][rank][0] = t_;
+    if (blockIdx.y == 0 && rank == 0) {
+      lslot = atomicAdd(&g_fz_nlaunch, 1u) & 127u;
+      g_fz_launch[lslot][0] = t_;
+    }
   }
   if (tid == 0) {
     C.band_count = 0;
@@ -538,6 +565,11 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     // first scorer loads) only touches this layer's own state, so it overlaps
     // the previous kernel's tail; the query is consumed after the wait.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (trace && blockIdx.y == 0 && rank == 0 && tid == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      g_fz_launch[lslot][1] = t_;
+    }
     for (int i = tid; i < d_s; i += blockDim.x) {
       const int ch = chs[i];
       double q = 0.0;
@@ -619,8 +651,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     fz_cluster_stats(cluster, C, klo, khi, (double)fsum, (double)fsq, glo, ghi, gsum, gsq);
     FZ_MARK(4);
     // ---- 2a. aimed candidate list, resolved by one CTA ----
-    // Aim at the previous step's threshold of this (layer, head) (+-0.15 sd),
-    // else at the Gaussian estimate mean + z sd (+-0.2 sd).  One pass with no
+    // Aim at the previous step's threshold of this (layer, head), +-3x its
+    // usual step-to-step move, else at the Gaussian estimate mean + z sd (+-0.2 sd).  One pass with no
     // per-key atomics: keys above the aimed range are counted, keys inside it
     // (widened by 2 eps) are appended as (key, index) pairs through
     // warp-aggregated positions.  Rank 0 gathers the cluster's short list
@@ -636,27 +668,30 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     unsigned long long *list = S.k.f.list64;
     {
       const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
-      const float prev = s.thresh ? s.thresh[u] : __int_as_float(0x7fc00000);
       const double gauss = mu + fz_normal_upper_quantile((double)n_topk / N) * sd;
-      const double tprev = mu + (double)prev * sd;  // the hint is the previous threshold as a z-score
+      const bool hinted = isfinite(hint.x);
+      const double tprev = mu + (double)hint.x * sd;
       double last_lo = 0.0, last_hi = 0.0;
       int dir = 0;
       for (int attempt = 0; attempt < 2 && !listed; ++attempt) {
-        // attempt 0 spans the previous threshold and the Gaussian estimate (+-0.2 sd); after a
+        // attempt 0 spans the previous threshold (or the Gaussian estimate); after a
         // miss, attempt 1 extends 0.6 sd beyond the side of the missed range that holds the threshold
         double a_lo, a_hi;
         if (attempt == 0) {
-          const double c0 = isfinite(tprev) ? fmin(tprev, gauss) : gauss;
-          const double c1 = isfinite(tprev) ? fmax(tprev, gauss) : gauss;
-          a_lo = c0 - 0.2 * sd;
-          a_hi = c1 + 0.2 * sd;
+          // +-(3 x the usual step-to-step move of the threshold), within [0.03, 0.25] sd
+          const double w = !hinted ? 0.2
+                           : aim_fixed > 0.0f ? (double)aim_fixed
+                           : isfinite(hint.y) ? fmin(0.25, fmax(0.03, 3.0 * (double)hint.y)) : 0.1;
+          const double c = hinted ? tprev : gauss;
+          a_lo = c - w * sd;
+          a_hi = c + w * sd;
         } else if (dir > 0) {
           a_lo = last_hi;
           a_hi = last_hi + 0.6 * sd;
         } else if (dir < 0) {
           a_lo = last_lo - 0.6 * sd;
           a_hi = last_lo;
-        } else {
+        } else {  // a list overflowed
           a_lo = gauss - 0.4 * sd;
           a_hi = gauss + 0.4 * sd;
         }
@@ -854,7 +889,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
               }
               if (tid == 0) {
                 C.xprefix = ord_hi;  // keys above this orderable value are selected
-                if (s.thresh && sd > 0.0) s.thresh[u] = (float)((T32 - mu) / sd);  // as a z-score
+                if (s.thresh && sd > 0.0) fz_store_hint(s.thresh + 4 * u, hint, (T32 - mu) / sd);
               }
             }
           }
@@ -871,6 +906,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         if (trace && blockIdx.y < 64 && rank == 0 && tid == 0 && R0->status) {
           g_fz_upath[blockIdx.y][0] = attempt;
           g_fz_upath[blockIdx.y][1] = R0->list_count;
+          atomicAdd(&g_fz_pathcnt[attempt], 1u);
         }
         if (R0->status) {
           ord_def = (uint32_t)R0->xprefix;
@@ -891,7 +927,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       }
     }
     if (!listed) {
-    if (trace && blockIdx.y < 64 && rank == 0 && tid == 0) g_fz_upath[blockIdx.y][0] = 2;
+    if (trace && blockIdx.y < 64 && rank == 0 && tid == 0) {
+      g_fz_upath[blockIdx.y][0] = 2;
+      atomicAdd(&g_fz_pathcnt[2], 1u);
+    }
     // ---- 2b. threshold range by linear histograms (full range) ----
     if (tid == 0) {
       C.band_count = 0;
@@ -1113,7 +1152,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     }
     if (rank == 0 && tid == 0 && s.thresh) {
       const double N = (double)ncand, mu = gsum / N, sd = sqrt(fmax(gsq / N - mu * mu, 0.0));
-      if (sd > 0.0) s.thresh[u] = (float)((0.5 * (R_lo + R_hi) - mu) / sd);
+      if (sd > 0.0) fz_store_hint(s.thresh + 4 * u, hint, (0.5 * (R_lo + R_hi) - mu) / sd);
     }
     }  // full-range path
     if (scores_out) {
@@ -1709,6 +1748,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       unsigned long long t_;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
       g_fz_unit[blockIdx.y][rank][1] = t_;
+      if (blockIdx.y == 0 && rank == 0) g_fz_launch[lslot][2] = t_;
     }
   }
 }
@@ -1808,6 +1848,33 @@ extern "C" int tkv_debug_sparse_upath(int *out, int reset) {
 
 extern "C" int tkv_debug_sparse_units(unsigned long long *out) {
   return cudaMemcpyFromSymbol(out, tkv::g_fz_unit, sizeof(tkv::g_fz_unit)) == cudaSuccess ? 0 : 7;
+}
+
+// launch timeline of unit 0 (start, after the PDL wait, end) for the last
+// up-to-128 launches in trace mode, in launch order; returns the count
+extern "C" int tkv_debug_sparse_launches(unsigned long long *out, int reset) {
+  if (reset) {
+    const unsigned int z = 0;
+    return cudaMemcpyToSymbol(tkv::g_fz_nlaunch, &z, sizeof(z)) == cudaSuccess ? 0 : -1;
+  }
+  unsigned int cnt = 0;
+  if (cudaMemcpyFromSymbol(&cnt, tkv::g_fz_nlaunch, sizeof(cnt)) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out, tkv::g_fz_launch, sizeof(tkv::g_fz_launch)) != cudaSuccess) return -1;
+  return (int)cnt;
+}
+
+// select-path counts since the last reset (trace mode): [list attempt 0, attempt 1, full range]
+extern "C" int tkv_debug_sparse_pathcount(unsigned int *out, int reset) {
+  if (reset) {
+    const unsigned int z[4] = {0, 0, 0, 0};
+    return cudaMemcpyToSymbol(tkv::g_fz_pathcnt, z, sizeof(z)) == cudaSuccess ? 0 : 7;
+  }
+  return cudaMemcpyFromSymbol(out, tkv::g_fz_pathcnt, sizeof(tkv::g_fz_pathcnt)) == cudaSuccess ? 0 : 7;
+}
+
+// tuning: half-width (in score standard deviations) of the first aimed range
+extern "C" int tkv_debug_sparse_aim(float w) {
+  return cudaMemcpyToSymbol(tkv::g_fz_aim, &w, sizeof(w)) == cudaSuccess ? 0 : 7;
 }
 
 extern "C" int tkv_debug_sparse_clocks(unsigned long long *out) {

@@ -105,7 +105,7 @@ class OffloadedLayerKV:
         else:
             self.slot_tok = self.slot_stamp = self.slot_v = self.tok_slot = self.cache_stats = None
             self.slot_hand = None
-        self.thresh = torch.full((units,), float("nan"), dtype=torch.float32, device=dev)  # top-k threshold hint
+        self.thresh = torch.full((units, 4), float("nan"), dtype=torch.float32, device=dev)  # top-k threshold hint
         self.struct = SparseLayer(units, d, self.capacity, self.local_offset, self.local_capacity,
                                   self.kt.data_ptr(), self.chmax.data_ptr(), self.loc_k.data_ptr(),
                                   self.loc_v.data_ptr(), ptr(self.kdev), self.arena.addr,

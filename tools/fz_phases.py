@@ -10,6 +10,28 @@ def enable(lib, on=True):
     lib.tkv_debug_sparse_trace(1 if on else 0)
     if on:
         lib.tkv_debug_sparse_upath(None, 1)
+        lib.tkv_debug_sparse_launches(None, 1)
+        lib.tkv_debug_sparse_pathcount(None, 1)
+
+
+def show_launches(lib, last=31):
+    """Gaps between consecutive sparse-kernel launches (unit 0, rank 0)."""
+    raw = (C.c_ulonglong * (128 * 3))()
+    cnt = lib.tkv_debug_sparse_launches(raw, 0)
+    if cnt <= 1:
+        return
+    v = list(raw)
+    idx = [i % 128 for i in range(max(0, cnt - min(cnt, 128)), cnt)][-last:]
+    rows = [(v[i * 3], v[i * 3 + 1], v[i * 3 + 2]) for i in idx]
+    gaps = [(rows[k][0] - rows[k - 1][2]) / 1e3 for k in range(1, len(rows))]
+    waits = [(r[1] - r[0]) / 1e3 for r in rows]
+    durs = [(r[2] - r[1]) / 1e3 for r in rows]
+    starts = [(rows[k][1] - rows[k - 1][2]) / 1e3 for k in range(1, len(rows))]
+    med = lambda x: sorted(x)[len(x) // 2]  # noqa: E731
+    print(f"  launches ({len(rows)} consecutive): end->start median {med(gaps):.2f} us (min {min(gaps):.2f} max "
+          f"{max(gaps):.2f}), start->PDL-wait-done median {med(waits):.2f}, end->wait-done median {med(starts):.2f}, "
+          f"wait-done->end median {med(durs):.2f} us")
+    print("  per launch gap end->wait-done (us): " + " ".join(f"{x:.1f}" for x in starts))
 
 
 def show_units(lib, units=8):
@@ -28,6 +50,10 @@ def show_units(lib, units=8):
 
 
 def show(lib):
+    pc = (C.c_uint * 4)()
+    lib.tkv_debug_sparse_pathcount(pc, 0)
+    print(f"  select paths (units x launches): list attempt 0 {pc[0]}, attempt 1 {pc[1]}, full range {pc[2]}")
+    show_launches(lib)
     show_units(lib)
     dbg = (C.c_double * 16)()
     lib.tkv_debug_sparse_attempts(dbg)
