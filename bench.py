@@ -288,6 +288,8 @@ def main():
                        batch=1, seed=args.seed, device=device)
     eng = P.DecodeEngine(model, wl.labels, cfg, batch=1, max_steps=total, rank=rank, world_size=world,
                          device=device)
+    if os.environ.get("TKV_FZ_DBG"):  # experiments in the sparse kernel (debug bits)
+        _lib.load().tkv_debug_sparse_trace(int(os.environ["TKV_FZ_DBG"]) & ~1)
     if os.environ.get("TKV_AIM"):  # tuning: first aimed range half-width (score sd)
         import ctypes
         _lib.load().tkv_debug_sparse_aim(ctypes.c_float(float(os.environ["TKV_AIM"])))
@@ -396,13 +398,13 @@ def main():
     prof, hits, misses = profile_mode()
     if args.phases and rank == 0:
         from tools.fz_phases import show, show_launches
-        _lib.load().tkv_debug_sparse_trace(0)
+        _lib.load().tkv_debug_sparse_trace(int(os.environ.get("TKV_FZ_DBG", "0")) & ~1)
         show(_lib.load())
         # launch gaps inside the plain (timed) graph: one more step with the trace on
         enable(_lib.load())
         eng.step(*inputs(step_i)); step_i += 1
         torch.cuda.synchronize()
-        _lib.load().tkv_debug_sparse_trace(0)
+        _lib.load().tkv_debug_sparse_trace(int(os.environ.get("TKV_FZ_DBG", "0")) & ~1)
         print("plain graph:")
         show_launches(_lib.load())
     fetch_rows = int(eng.fetch_count.sum().item())

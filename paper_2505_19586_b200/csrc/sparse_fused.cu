@@ -781,8 +781,15 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           unsigned long long *cand = S.k.f.cand;
           if (verdict) {
             for (int t = tid; t < L; t += blockDim.x) {
-              int r = 0, base = 0;
-              while (t - base >= Lr[r]) base += Lr[r++];
+              int r = 0, base = 0, run = 0;
+#pragma unroll
+              for (int k = 0; k < FZ_CTAS - 1; ++k) {  // (static indices keep Lr in registers)
+                run += Lr[k];
+                if (t >= run) {
+                  r = k + 1;
+                  base = run;
+                }
+              }
               cand[t] = cluster.map_shared_rank(list, r)[t - base];
             }
             __syncthreads();
@@ -1086,7 +1093,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       if (e + 8 <= m) {
         *reinterpret_cast<uint2 *>(flags + e) = make_uint2(fl[0], fl[1]);
       } else {
-        for (int q = 0; e + q < m; ++q) flags[e + q] = (uint8_t)(fl[q >> 2] >> (8 * (q & 3)));
+#pragma unroll
+        for (int q = 0; q < 8; ++q)  // (static indices keep fl in registers)
+          if (e + q < m) flags[e + q] = (uint8_t)(fl[q >> 2] >> (8 * (q & 3)));
       }
     }
     __syncthreads();
@@ -1116,8 +1125,15 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     if (!overflow) {
       // every CTA's band members, concatenated in rank order
       for (int t = tid; t < all_band; t += blockDim.x) {
-        int r = 0, base = 0;
-        while (t - base >= cnt_r[r]) base += cnt_r[r++];
+        int r = 0, base = 0, run = 0;
+#pragma unroll
+        for (int k = 0; k < FZ_CTAS - 1; ++k) {
+          run += cnt_r[k];
+          if (t >= run) {
+            r = k + 1;
+            base = run;
+          }
+        }
         const FzShared *RS = cluster.map_shared_rank(&S, r);
         S.k.f.all_key[t] = RS->k.f.band_key[t - base];
         S.k.f.all_idx[t] = RS->k.f.band_idx[t - base];
@@ -1184,7 +1200,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         fw[g][0] = x.x;
         fw[g][1] = x.y;
       } else {
-        for (int q = 0; e + q < m; ++q) fw[g][q >> 2] |= (uint32_t)flags[e + q] << (8 * (q & 3));
+#pragma unroll
+        for (int q = 0; q < 8; ++q)  // (static indices keep fw in registers)
+          if (e + q < m) fw[g][q >> 2] |= (uint32_t)flags[e + q] << (8 * (q & 3));
       }
     }
     const unsigned long long c = (unsigned long long)(__popc(fw[g][0]) + __popc(fw[g][1]));  // flags are 0/1 bytes
@@ -1290,17 +1308,6 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     // allocates misses only there, so no cross-CTA coordination is needed.
     const int spc = (CS + FZ_CTAS - 1) / FZ_CTAS;
     const int p0 = min(CS, rank * spc), p1 = min(CS, p0 + spc);
-    // key rows of every selected token start moving into L2 now (TMA prefetch), so the
-    // logits step below reads them from L2 instead of waiting on HBM
-    if (!keys_host && s.kdev) {
-      for (int i = tid; i < nrows; i += blockDim.x) {
-        const int64_t idx = rbase + rows[i];
-        if (idx < local_start)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.kdev + ((size_t)u * s.capacity + idx) * D),
-                       "r"((uint32_t)(D * 2))
-                       : "memory");
-      }
-    }
     // (0) row codes: >= 0 cached slot (hit, stamped with this step), -1 fetch over PCIe, -2 local mirror
     int hits = 0, misses = 0;
     for (int i = tid; i < nrows; i += blockDim.x) {

@@ -1,5 +1,6 @@
 """Print the fused sparse kernel's phase timestamps (unit 0, every CTA rank)."""
 import ctypes as C
+import os
 
 NAMES = {1: "chs", 2: "qsum", 3: "score", 4: "minmax", 5: "hist", 6: "hist-sync", 7: "totals", 8: "scan",
          9: "passes", 10: "band", 11: "band-sync", 12: "select", 13: "count", 14: "out-sync", 15: "rows",
@@ -7,7 +8,7 @@ NAMES = {1: "chs", 2: "qsum", 3: "score", 4: "minmax", 5: "hist", 6: "hist-sync"
 
 
 def enable(lib, on=True):
-    lib.tkv_debug_sparse_trace(1 if on else 0)
+    lib.tkv_debug_sparse_trace((1 if on else 0) | (int(os.environ.get("TKV_FZ_DBG", "0")) & ~1))
     if on:
         lib.tkv_debug_sparse_upath(None, 1)
         lib.tkv_debug_sparse_launches(None, 1)
