@@ -108,7 +108,8 @@ int tkv_qcache_dequant(const tkv_qcache *c, int32_t unit, int32_t which, int64_t
  * qgemv_scores quantizer.py:505-533 -> softmax(/sqrt d) -> qgemv_output
  * quantizer.py:536-558).  queries fp16 [units*G][d]; out fp32 [units*G][d].
  * `workspace` >= tkv_quant_decode_workspace bytes.  impl: 0 = auto,
- * 1 = reference-shaped SIMT kernel, 2 = tensor-core (IMMA) kernel. */
+ * 1 = reference-shaped SIMT kernel, 2 = tensor-core (IMMA) kernel, persistent
+ * and TMA-pipelined, 3 = the per-chunk IMMA kernel it replaced. */
 int64_t tkv_quant_decode_workspace(const tkv_qcache *c, int32_t G);
 int tkv_quant_decode(const tkv_qcache *c, const uint16_t *queries, int32_t G, float *out,
                      void *workspace, int32_t impl, void *stream);

@@ -197,12 +197,13 @@ int64_t quant_decode_workspace(const QC &c, int G) {
 }
 
 int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st);
+int quant_decode_pipe(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st);
 bool imma_supported(const QC &c, int G);
 
 int quant_decode(const QC &c, const uint16_t *q, int G, float *out, void *ws, int impl, cudaStream_t st) {
-  if (impl == 2 || (impl == 0 && imma_supported(c, G))) {
+  if (impl == 2 || impl == 3 || (impl == 0 && imma_supported(c, G))) {
     if (!imma_supported(c, G)) return fail(TKV_ERR_PARAMETER, "tensor-core decode needs d=128, g=64, G<=4");
-    return quant_decode_imma(c, q, G, out, ws, st);
+    return impl == 3 ? quant_decode_imma(c, q, G, out, ws, st) : quant_decode_pipe(c, q, G, out, ws, st);
   }
   const int chunks = (int)((c.capacity + SIMT_CHUNK - 1) / SIMT_CHUNK);
   float *pm = reinterpret_cast<float *>(ws);

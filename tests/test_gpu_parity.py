@@ -119,11 +119,12 @@ def test_quant_decode_matches_reference(tkv, case, impl):
     assert rel_err(out, ref) <= REL_TOL
 
 
+@pytest.mark.parametrize("impl", [2, 3])
 @pytest.mark.parametrize("bits", [1, 2])
 @pytest.mark.parametrize("n,kscale", [(32768 + 17, 0.05), (5000, 0.5), (64 * 17, 0.2)])
-def test_quant_decode_tensor_core_vs_oracle(tkv, bits, n, kscale):
-    """The IMMA kernel (impl=2) at long context, dense (near-uniform) and
-    peaky attention, against the float64 oracle and the SIMT kernel."""
+def test_quant_decode_tensor_core_vs_oracle(tkv, bits, n, kscale, impl):
+    """The IMMA kernels (impl=2 pipelined, 3 per-chunk) at long context, dense
+    (near-uniform) and peaky attention, against the float64 oracle."""
     rng = np.random.default_rng(n + bits)
     h, G, d = 2, 4, 128
     keys = cases.f16(rng.normal(0, kscale, size=(h, n, d)))
@@ -134,9 +135,28 @@ def test_quant_decode_tensor_core_vs_oracle(tkv, bits, n, kscale):
     q = tkv.quantize_layer_kv(keys, values, bits, 64)
     kq, vq = O.quantize_layer(keys, values, bits, 64)
     ref = O.quant_layer_decode(queries, kq, vq)
-    out2 = q.decode(queries, impl=2).cpu().numpy()
+    out2 = q.decode(queries, impl=impl).cpu().numpy()
     assert rel_err(out2, ref) <= REL_TOL
     assert rel_err(out2, ref) <= 5e-4  # typical margin of the exact-integer design
+
+
+@pytest.mark.parametrize("bits", [1, 2])
+def test_quant_decode_pipelined_ring_wraps(tkv, bits):
+    """8 heads at 60k tokens: every CTA of the pipelined kernel streams more
+    chunks than its TMA ring has stages, so stages are refilled while other
+    warps still compute; against the oracle and the per-chunk kernel."""
+    rng = np.random.default_rng(90 + bits)
+    h, G, d, n = 8, 4, 128, 60000 + 33
+    keys = cases.f16(rng.normal(0, 0.2, size=(h, n, d)))
+    values = cases.f16(rng.normal(size=(h, n, d)))
+    queries = cases.f16(rng.normal(size=(h * G, d)))
+    q = tkv.quantize_layer_kv(keys, values, bits, 64)
+    kq, vq = O.quantize_layer(keys, values, bits, 64)
+    ref = O.quant_layer_decode(queries, kq, vq)
+    out = q.decode(queries, impl=2).cpu().numpy()
+    assert rel_err(out, ref) <= 5e-4
+    out3 = q.decode(queries, impl=3).cpu().numpy()
+    assert rel_err(out, out3) <= 5e-4
 
 
 @pytest.mark.parametrize("bits", [1, 2])
@@ -152,7 +172,7 @@ def test_quant_decode_after_appends(tkv, bits):
         if t % 29 == 0 or t == T - 1:
             kq, vq = O.quantize_layer(keys[:, :n0 + t + 1], values[:, :n0 + t + 1], bits, 64)
             ref = O.quant_layer_decode(queries, kq, vq)
-            for impl in (1, 2):
+            for impl in (1, 2, 3):
                 assert rel_err(q.decode(queries, impl=impl).cpu().numpy(), ref) <= REL_TOL
 
 
