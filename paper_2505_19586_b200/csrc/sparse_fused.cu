@@ -668,8 +668,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     unsigned long long *list = S.k.f.list64;
     {
       const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
-      const double gauss = mu + fz_normal_upper_quantile((double)n_topk / N) * sd;
       const bool hinted = isfinite(hint.x);
+      // the Gaussian estimate of the threshold (only without a hint or after an overflow)
+      auto gauss = [&]() { return mu + fz_normal_upper_quantile((double)n_topk / N) * sd; };
       const double tprev = mu + (double)hint.x * sd;
       double last_lo = 0.0, last_hi = 0.0;
       int dir = 0;
@@ -682,7 +683,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           const double w = !hinted ? 0.2
                            : aim_fixed > 0.0f ? (double)aim_fixed
                            : isfinite(hint.y) ? fmin(0.25, fmax(0.03, 3.0 * (double)hint.y)) : 0.1;
-          const double c = hinted ? tprev : gauss;
+          const double c = hinted ? tprev : gauss();
           a_lo = c - w * sd;
           a_hi = c + w * sd;
         } else if (dir > 0) {
@@ -692,8 +693,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           a_lo = last_lo - 0.6 * sd;
           a_hi = last_lo;
         } else {  // a list overflowed
-          a_lo = gauss - 0.4 * sd;
-          a_hi = gauss + 0.4 * sd;
+          const double gs = gauss();
+          a_lo = gs - 0.4 * sd;
+          a_hi = gs + 0.4 * sd;
         }
         if (!(sd > 0.0) || !isfinite(a_lo) || !isfinite(a_hi)) break;
         const double center = 0.5 * (a_lo + a_hi), width = 0.5 * (a_hi - a_lo);
@@ -1673,6 +1675,14 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       for (int e = 0; e < CPL; ++e) pa[((size_t)warp * GMAX + h) * D + lane * CPL + e] = acc[h][e];
     }
     __syncthreads();
+    // With G*D <= 512 every CTA pushes its partial into rank 0's inbox (the
+    // exact path's histograms, dead by now) with DSMEM stores before the
+    // barrier, so rank 0 merges from its own shared memory and the other CTAs
+    // leave right after the barrier; otherwise rank 0 pulls them afterwards.
+    static_assert(sizeof(S.xhist) + sizeof(S.xtot) >= (FZ_CTAS * 512 + 2 * FZ_CTAS * 8) * sizeof(float),
+                  "rank 0's partial inbox overlays the exact path's histograms");
+    const bool push = G * D <= 512;
+    float *inbox = cluster.map_shared_rank(reinterpret_cast<float *>(&S.xhist[0][0]), 0);  // [CTAS][512] + m, l
     for (int i = tid; i < G * D; i += blockDim.x) {
       const int h = i / D, c = i % D;
       float M = -INFINITY;
@@ -1687,10 +1697,18 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           A = fmaf(sc, pa[((size_t)w * GMAX + h) * D + c], A);
         }
       }
-      S.cta_acc[i] = A;
-      if (c == 0) {
-        S.cta_m[h] = M;
-        S.cta_l[h] = L;
+      if (push) {
+        inbox[rank * 512 + i] = A;
+        if (c == 0) {
+          inbox[FZ_CTAS * 512 + rank * 8 + h] = M;
+          inbox[FZ_CTAS * 512 + FZ_CTAS * 8 + rank * 8 + h] = L;
+        }
+      } else {
+        S.cta_acc[i] = A;
+        if (c == 0) {
+          S.cta_m[h] = M;
+          S.cta_l[h] = L;
+        }
       }
     }
     if (use_cache && tid == 0 && (C.hits | C.misses)) {
@@ -1727,7 +1745,27 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
       }
     }
-    if (rank == 0) {
+    if (rank == 0 && push) {
+      const float *ib = reinterpret_cast<const float *>(&S.xhist[0][0]);
+      for (int i = tid; i < G * D; i += blockDim.x) {
+        const int h = i / D;
+        float Mr[FZ_CTAS], M = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < FZ_CTAS; ++r) {
+          Mr[r] = ib[FZ_CTAS * 512 + r * 8 + h];
+          M = fmaxf(M, Mr[r]);
+        }
+        float L = 0.0f, A = 0.0f;
+#pragma unroll
+        for (int r = 0; r < FZ_CTAS; ++r) {
+          if (Mr[r] == -INFINITY) continue;
+          const float sc = exp2f(Mr[r] - M);
+          L = fmaf(sc, ib[FZ_CTAS * 512 + FZ_CTAS * 8 + r * 8 + h], L);
+          A = fmaf(sc, ib[r * 512 + i], A);
+        }
+        out[(size_t)u * G * D + i] = A / L;
+      }
+    } else if (rank == 0) {
       for (int i = tid; i < G * D; i += blockDim.x) {
         const int h = i / D;
         float Mr[FZ_CTAS], M = -INFINITY;
@@ -1748,7 +1786,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         out[(size_t)u * G * D + i] = A / L;
       }
     }
-    cluster.sync();  // rank 0 has read every CTA's partial
+    if (!push) cluster.sync();  // rank 0 has read every CTA's partial
     FZ_MARK(20);
     if (trace && blockIdx.y == 0 && tid == 0) g_fz_clk[rank][1] = clock64();
     if (trace && blockIdx.y < 64 && tid == 0) {
