@@ -35,8 +35,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ctx", type=int, default=131072)
-    ap.add_argument("--topk-frac", type=float, default=0.02)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (2 = the headline; 3-5 run the same engine at their shapes)")
+    ap.add_argument("--ctx", type=int, default=None, help="override the config's context length")
+    ap.add_argument("--topk-frac", type=float, default=None, help="override the config's Top-K fraction")
     ap.add_argument("--keys-over-pcie", action="store_true",
                     help="headline with K and V rows both gathered over PCIe (the reference's fetch_topk transfer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -48,27 +50,60 @@ def parse():
     ap.add_argument("--cache-steps", type=int, default=4,
                     help="HBM row cache window: a value row stays resident until unselected for this many steps (0: off)")
     ap.add_argument("--seed", type=int, default=2505)
-    return ap.parse_args()
+    args = ap.parse_args()
+    c = CONFIGS[args.config]
+    args.ctx = c["ctx"] if args.ctx is None else args.ctx
+    args.topk_frac = c["topk"] if args.topk_frac is None else args.topk_frac
+    args.batch, args.bits, args.q_layers, args.model = c["batch"], c["bits"], c["q_layers"], c["model"]
+    return args
+
+
+# BASELINE.json configs.  Where BASELINE.json leaves the quantized-layer set or
+# the Top-K fraction open, SURVEY.md 8(d) fixes them (stated in the workload name).
+CONFIGS = {
+    2: {"model": "LLAMA31_8B", "label": "Llama-3.1-8B", "ctx": 131072, "batch": 1, "q_layers": (0, 1), "bits": 1,
+        "topk": 0.02},
+    3: {"model": "LLAMA31_8B", "label": "Llama-3.1-8B", "ctx": 32768, "batch": 16, "q_layers": (0, 1), "bits": 2,
+        "topk": 0.03},
+    4: {"model": "QWEN25_7B", "label": "Qwen2.5-7B", "ctx": 131072, "batch": 4, "q_layers": (0,), "bits": 1,
+        "topk": 0.01},
+    5: {"model": "LLAMA31_70B", "label": "Llama-3.1-70B", "ctx": 131072, "batch": 1, "q_layers": (0, 1), "bits": 1,
+        "topk": 0.02},
+}
+
+
+def model_of(args):
+    from paper_2505_19586_b200 import kv_model
+    return getattr(kv_model, args.model)
+
+
+def metric_of(args):
+    return METRIC if args.config == 2 else f"decode ms/token, BASELINE config {args.config}"
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port of hybridkv) -- bounded sample of config 2
+# CPU reference (oracle port of hybridkv) -- bounded sample of a config
 # ---------------------------------------------------------------------------
-def cpu_reference_ms(ctx: int, n_topk: int, q_sample: int, reps: int = 1, warm: int = 0) -> tuple[float, dict]:
-    """Per-token time of the reference algorithm on host cores: 2 x quantized
+def cpu_reference_ms(args, n_topk: int, q_sample: int, reps: int = 1, warm: int = 0) -> tuple[float, dict]:
+    """Per-token time of the reference algorithm on host cores: n_Q x quantized
     layer (measured at ``q_sample`` tokens, scaled linearly -- its cost is
-    O(n)) + 30 x sparsity-friendly layer measured at the full context."""
+    O(n)) + n_S x sparsity-friendly layer measured at the full context, times
+    the batch (the reference has no batch dimension: B independent replays)."""
     import numpy as np
 
     from oracle import tailorkv_oracle as O
 
+    model = model_of(args)
+    ctx, bits = args.ctx, args.bits
     rng = np.random.default_rng(1)
-    h, hq, d, H = 8, 32, 128, 4096
+    h, hq, d, H = model.num_kv_heads, model.num_query_heads, model.head_dim, model.hidden_dim
     G = hq // h
+    n_q = len(args.q_layers)
+    n_s = model.num_layers - n_q
     f16 = lambda x: x.astype(np.float16).astype(np.float64)  # noqa: E731
     kq = f16(rng.normal(0, 0.05, size=(h, q_sample, d)))
     vq = f16(rng.normal(size=(h, q_sample, d)))
-    qk, qv = O.quantize_layer(kq, vq, 1, 64)
+    qk, qv = O.quantize_layer(kq, vq, bits, 64)
     qs = f16(rng.normal(size=(hq, d)))
     ks = f16(rng.normal(0, 1 / math.sqrt(d), size=(h, ctx, d)))
     vs = f16(rng.normal(size=(h, ctx, d)))
@@ -103,7 +138,7 @@ def cpu_reference_ms(ctx: int, n_topk: int, q_sample: int, reps: int = 1, warm: 
             tq.append(t1 - t0); ts.append(t2 - t1)
     TQ = float(np.median(tq)) * ctx / q_sample
     TS = float(np.median(ts))
-    ms = (2 * TQ + 30 * TS) * 1e3
+    ms = (n_q * TQ + n_s * TS) * args.batch * 1e3
     try:
         from threadpoolctl import threadpool_info
         threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
@@ -111,6 +146,14 @@ def cpu_reference_ms(ctx: int, n_topk: int, q_sample: int, reps: int = 1, warm: 
         threads = os.cpu_count() or 1
     info = {"q_layer_ms_at_ctx": TQ * 1e3, "s_layer_ms": TS * 1e3, "threads": threads}
     return ms, info
+
+
+def cpu_sample_text(args, q_sample, prefix=""):
+    model = model_of(args)
+    n_q = len(args.q_layers)
+    return (f"{prefix}1 quantized layer at {q_sample} tokens scaled x{args.ctx / q_sample:g} (O(n)) + 1 Top-K layer at "
+            f"{args.ctx} tokens; token = {n_q} Q + {model.num_layers - n_q} S layers"
+            + (f", x{args.batch} sequences" if args.batch > 1 else "") + "; oracle port of hybridkv (numpy)")
 
 
 def run_reference(args, rank):
@@ -121,14 +164,13 @@ def run_reference(args, rank):
     times = []
     import numpy as np
     for i in range(args.warmup + args.steps):
-        ms, info = cpu_reference_ms(args.ctx, n_topk, q_sample, reps=1, warm=0)
+        ms, info = cpu_reference_ms(args, n_topk, q_sample, reps=1, warm=0)
         if i >= args.warmup:
             times.append(ms)
     v = float(np.median(times))
-    sample = (f"per step: 1 quantized layer at {q_sample} tokens scaled x{args.ctx / q_sample:g} (O(n)) + "
-              f"1 Top-K layer at {args.ctx} tokens; token = 2 Q + 30 S layers; oracle port of hybridkv (numpy)")
+    sample = cpu_sample_text(args, q_sample, "per step: ")
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "ms/token", "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_of(args), "value": v, "unit": "ms/token", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, n_topk),
@@ -139,14 +181,20 @@ def run_reference(args, rank):
 
 
 def workload_config(args, n_topk):
+    m = model_of(args)
+    c = CONFIGS[args.config]
+    nq = len(args.q_layers)
+    qset = "{" + ",".join(map(str, args.q_layers)) + "}"
     return {
-        "workload": "config2: Llama-3.1-8B shapes, 32 layers (Q={0,1} 1-bit g=64, 30 Top-K layers), "
-                    f"ctx={args.ctx}, batch=1, n_topk={n_topk} ({args.topk_frac:.0%}), n_local=64, d_s=8",
-        "ctx": args.ctx, "batch": 1, "layers": 32, "q_layers": [0, 1], "bits": 1, "group_size": 64,
-        "n_topk": n_topk, "n_local": 64, "d_s": 8, "kv_heads": 8, "q_heads": 32, "head_dim": 128,
+        "workload": f"config{args.config}: {c['label']} shapes, {m.num_layers} layers (Q={qset} {args.bits}-bit g=64, "
+                    f"{m.num_layers - nq} Top-K layers), ctx={args.ctx}, batch={args.batch}, n_topk={n_topk} "
+                    f"({args.topk_frac:.0%}), n_local=64, d_s=8",
+        "ctx": args.ctx, "batch": args.batch, "layers": m.num_layers, "q_layers": list(args.q_layers),
+        "bits": args.bits, "group_size": 64, "n_topk": n_topk, "n_local": 64, "d_s": 8,
+        "kv_heads": m.num_kv_heads, "q_heads": m.num_query_heads, "head_dim": m.head_dim,
         "parallelism": f"kv-head shard x{args.gpus}",
         "key_rows_from": "host (PCIe)" if args.keys_over_pcie else "hbm (scorer copy); value rows over PCIe",
-        "l2": "inputs larger than L2 (>1.6 GB HBM read per step)",
+        "l2": "inputs larger than L2 (every step reads > 1 GB of HBM)",
     }
 
 
@@ -269,14 +317,14 @@ def main():
         dist.init_process_group("nccl", device_id=device)
     import paper_2505_19586_b200 as P
     from paper_2505_19586_b200 import _lib
-    from paper_2505_19586_b200.kv_model import LLAMA31_8B
     from paper_2505_19586_b200.synth import make_workload
 
     _lib.load()
-    model = LLAMA31_8B
+    model = model_of(args)
+    B = args.batch
     L, n = model.num_layers, args.ctx
     n_topk = round(args.topk_frac * n)
-    cfg = P.EngineConfig(bits=1, group_size=64, n_local=64, n_topk=n_topk, critical_channels=8,
+    cfg = P.EngineConfig(bits=args.bits, group_size=64, n_local=64, n_topk=n_topk, critical_channels=8,
                          keys_from_hbm=not args.keys_over_pcie, fused_sparse=not args.unfused,
                          row_cache=args.cache_steps > 0, row_cache_steps=max(1, args.cache_steps),
                          scorer_l2_prefetch=not args.no_l2_prefetch, overlap_stage1=not args.serial_stage1)
@@ -284,9 +332,9 @@ def main():
     PROF = 2
     total = W + 3 * K + 2 * PROF + 10
     t_setup = time.time()
-    wl = make_workload(L, (0, 1), model.num_query_heads, model.num_kv_heads, model.head_dim, n, total,
-                       batch=1, seed=args.seed, device=device)
-    eng = P.DecodeEngine(model, wl.labels, cfg, batch=1, max_steps=total, rank=rank, world_size=world,
+    wl = make_workload(L, args.q_layers, model.num_query_heads, model.num_kv_heads, model.head_dim, n, total,
+                       batch=B, seed=args.seed, device=device)
+    eng = P.DecodeEngine(model, wl.labels, cfg, batch=B, max_steps=total, rank=rank, world_size=world,
                          device=device)
     if os.environ.get("TKV_FZ_DBG"):  # experiments in the sparse kernel (debug bits)
         _lib.load().tkv_debug_sparse_trace(int(os.environ["TKV_FZ_DBG"]) & ~1)
@@ -441,16 +489,20 @@ def main():
     # default mode, the value rows that missed the HBM row cache (counted by the kernel)
     gather_bytes = O.gather_bytes(fetch_rows, d) if args.keys_over_pcie else int(pcie_rows * d * 2)
     alt_bytes = O.gather_bytes(fetch_rows, d) if not args.keys_over_pcie else fetch_rows * d * 2
-    quant_bytes = O.quant_layer_bytes(n, U, d, 1, 64)
+    quant_bytes = O.quant_layer_bytes(n, U, d, args.bits, 64)
     scorer_bytes = O.scorer_bytes(n, U, 8)
     # HBM bytes of the same launch: scorer columns + key rows (+ cached value rows)
     sparse_hbm = scorer_bytes + (0 if args.keys_over_pcie else int(fetch_rows * d * 2 + cached_rows * d * 2))
     wq_bytes = eng.hq_r * model.hidden_dim * d * 2
     rooflines = {
-        "sparse_decode": {"bound": "pcie", "achieved": gather_bytes / (sparse_ms * 1e-3) / 1e9,
-                          "peak": memcpy_gbs, "unit": "GB/s", "ms": sparse_ms, "bytes": gather_bytes,
-                          "hbm_bytes": sparse_hbm, "hbm_gbs": sparse_hbm / (sparse_ms * 1e-3) / 1e9,
-                          "peak_source": "measured pinned cudaMemcpyAsync H2D 256 MiB, this run",
+        # HBM is the resource the kernel moves most bytes through (scorer columns, key rows, cached
+        # value rows); the PCIe leg (value rows that missed the row cache) is reported beside it
+        "sparse_decode": {"bound": "hbm", "achieved": sparse_hbm / (sparse_ms * 1e-3) / 1e9,
+                          "peak": hbm_peak, "unit": "GB/s", "ms": sparse_ms, "bytes": sparse_hbm,
+                          "peak_source": hbm_src,
+                          "pcie_bytes": gather_bytes, "pcie_gbs": gather_bytes / (sparse_ms * 1e-3) / 1e9,
+                          "pcie_peak": memcpy_gbs,
+                          "pcie_peak_source": "measured pinned cudaMemcpyAsync H2D 256 MiB, this run",
                           "kernel": "sparse_fused_kernel (scores + top-k + gather + attention)" if not args.unfused
                           else "select + sparse_attn"},
         "quant_decode": {"bound": "hbm", "achieved": quant_bytes / (quant_ms * 1e-3) / 1e9, "peak": hbm_peak,
@@ -463,6 +515,7 @@ def main():
     for r in rooflines.values():
         if "achieved" in r:
             r["frac"] = r["achieved"] / r["peak"]
+    rooflines["sparse_decode"]["pcie_frac"] = rooflines["sparse_decode"]["pcie_gbs"] / memcpy_gbs
     dom = rooflines["sparse_decode"]
     # DRAM traffic per launch from the committed ncu --set full capture of the same kernels
     traffic = {}
@@ -472,16 +525,20 @@ def main():
     def _traffic(name):
         t = traffic.get(name)
         return None if t is None else t["dram_bytes_read"] + t["dram_bytes_write"]
-    rooflines["quant_decode"]["traffic"] = _traffic("quant_decode_imma_kernel")
+    rooflines["quant_decode"]["traffic"] = _traffic("quant_decode_pipe_kernel") or _traffic("quant_decode_imma_kernel")
     line = {
-        "metric": METRIC, "value": ms, "unit": "ms/token", "n_gpus": world, "steps": K, "warmup": W,
+        "metric": metric_of(args), "value": ms, "unit": "ms/token", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "fp16 storage / 1-bit codes, fp32 accumulate", "data": "synthetic (gen_trace-shaped, GPU-generated)",
+        "dtype": f"fp16 storage / {args.bits}-bit codes, fp32 accumulate",
+        "data": "synthetic (gen_trace-shaped, GPU-generated)",
         "config": workload_config(args, n_topk),
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
                      "frac": dom["frac"], "traffic": _traffic("sparse_fused_kernel") if not args.unfused else None,
-                     "traffic_note": "DRAM bytes per launch (ncu capture, profiles/r1_ncu_traffic.json); the PCIe "
-                                     "bytes above are the kernel's algorithmic value-row misses",
+                     "traffic_note": "DRAM bytes per launch (ncu capture, profiles/r1_ncu_traffic.json); below the "
+                                     "algorithmic bytes because stage 1 prefetches the scorer columns into L2",
+                     "bound_note": "the launch is a chain of dependent phases (score, cluster select, gather, "
+                                   "attention, merge; profiles/r1_kernels.md 2), so it runs well under the HBM "
+                                   "roofline; the PCIe leg is rooflines.sparse_decode.pcie_*",
                      "kernel": dom["kernel"],
                      "timing": "CUDA events recorded as graph nodes around the kernel inside the replayed step"},
         "rooflines": rooflines,
@@ -496,18 +553,17 @@ def main():
         "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",
                     "ms_per_token": ms_variant, "sparse_decode_ms": alt_ms,
-                    "pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "pcie_bytes": alt_bytes},
+                    "pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "pcie_bytes": alt_bytes,
+                    "pcie_frac": alt_bytes / (alt_ms * 1e-3) / 1e9 / memcpy_gbs},
         "fidelity": fidelity,
         "gpu_launches": eng.kernels_per_step() * K,
         "clocks": clocks.summary(),
         "setup_s": setup_s,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cms, info = cpu_reference_ms(n, n_topk, min(n, 16384))
+        cms, info = cpu_reference_ms(args, n_topk, min(n, 16384))
         line["cpu_baseline"] = {"value": cms, "unit": "ms/token", "cores": info["threads"], "kind": "port",
-                                "sample": "1 quantized layer at 16384 tokens scaled x8 (O(n)) + 1 Top-K layer at "
-                                          f"{n} tokens; token = 2 Q + 30 S layers; numpy oracle port",
-                                "detail": info}
+                                "sample": cpu_sample_text(args, min(n, 16384)), "detail": info}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

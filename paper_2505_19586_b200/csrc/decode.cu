@@ -202,7 +202,8 @@ bool imma_supported(const QC &c, int G);
 
 int quant_decode(const QC &c, const uint16_t *q, int G, float *out, void *ws, int impl, cudaStream_t st) {
   if (impl == 2 || impl == 3 || (impl == 0 && imma_supported(c, G))) {
-    if (!imma_supported(c, G)) return fail(TKV_ERR_PARAMETER, "tensor-core decode needs d=128, g=64, G<=4");
+    if (!imma_supported(c, G) || (impl == 3 && G > 4))
+      return fail(TKV_ERR_PARAMETER, "tensor-core decode needs d=128, g=64 and G<=16 (G<=4 for impl 3)");
     return impl == 3 ? quant_decode_imma(c, q, G, out, ws, st) : quant_decode_pipe(c, q, G, out, ws, st);
   }
   const int chunks = (int)((c.capacity + SIMT_CHUNK - 1) / SIMT_CHUNK);

@@ -30,8 +30,9 @@ constexpr int IM_WARPS = 4;
 constexpr float IM_QMAX = 32512.0f;            // |x| bound of the 2-digit fixed point
 constexpr float IM_MAGIC = 12582912.0f + 128.0f;  // 1.5*2^23 + 128: RNE to int, +128 digit bias
 
+// the pipelined kernel takes any G in blocks of 4 query heads; the per-chunk kernel G <= 4
 bool imma_supported(const QC &c, int G) {
-  return c.d == IM_D && c.g == IM_G && (c.bits == 1 || c.bits == 2) && G >= 1 && G <= 4;
+  return c.d == IM_D && c.g == IM_G && (c.bits == 1 || c.bits == 2) && G >= 1 && G <= 16;
 }
 
 __device__ __forceinline__ void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -225,12 +226,12 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 4) quant_decode_imma_kernel(QC 
       if ((lane & 7) == 0) {
         const int h = (b4 ? 2 : 0) + (b3 ? 1 : 0);
         S.off[gi][h] = d1;
-        S.kscale[gi][h] = m1 / IM_QMAX;
+        S.kscale[gi][h] = m1 * (1.0f / IM_QMAX);
       }
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const float mh = __shfl_sync(0xffffffffu, m1, 8 * h);
-        const float inv = mh > 0.0f ? IM_QMAX / mh : 0.0f;
+        const float inv = mh > 0.0f ? __fdividef(IM_QMAX, mh) : 0.0f;
         const float x0 = fmaf(W[h][0], inv, IM_MAGIC), x1 = fmaf(W[h][1], inv, IM_MAGIC);
         const float x2 = fmaf(W[h][2], inv, IM_MAGIC), x3 = fmaf(W[h][3], inv, IM_MAGIC);
         S.bfrag[gi][ks][(2 * h) * 4 + tqq][j] = pack_digits(x0, x1, x2, x3, 0x0051, 0, 0u);              // hi: bytes 1
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 4) quant_decode_imma_kernel(QC 
       pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 1));
       pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 2));
       pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 4));
-      const float pinv = pmax > 0.0f ? IM_QMAX / pmax : 0.0f;
+      const float pinv = pmax > 0.0f ? __fdividef(IM_QMAX, pmax) : 0.0f;
       const float vsc_h = __shfl_sync(0xffffffffu, pmax, (2 * tq) * 4) * (1.0f / IM_QMAX);  // head tq's scale
       int V[8][4];
 #pragma unroll
@@ -529,6 +530,9 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
   extern __shared__ __align__(128) unsigned char smraw[];
   QpSmem &S = *reinterpret_cast<QpSmem *>(smraw);
   const int u = blockIdx.y, split = blockIdx.x;
+  // query heads [h0, h0 + Gb) of the unit: blocks of 4 (the MMA's N = 4 heads x 2 digits);
+  // G > 4 runs ceil(G/4) head blocks whose CTAs stream the same codes (L2 serves the repeats)
+  const int h0 = 4 * blockIdx.z, Gb = min(4, G - h0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g8 = lane >> 2, tq = lane & 3;
   const int64_t n = *c.len;
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
     for (int j = 0; j < cnt && j < QP_NS; ++j) load(j);
   for (int i = tid; i < 4 * IM_D; i += blockDim.x) {
     const int h = i / IM_D;
-    S.q[h][i % IM_D] = h < G ? h2f(queries[((size_t)u * G + h) * IM_D + i % IM_D]) : 0.0f;
+    S.q[h][i % IM_D] = h < Gb ? h2f(queries[((size_t)u * G + h0 + h) * IM_D + i % IM_D]) : 0.0f;
   }
   __syncthreads();
 
@@ -616,8 +620,9 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
             const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              lo[i] = h2f(w[i] & 0xffff);
-              sc[i] = (h2f(w[i] >> 16) - lo[i]) * KINV;  // 0 for degenerate groups (all codes 0)
+              const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[i]));  // (lo, hi)
+              lo[i] = f.x;
+              sc[i] = (f.y - lo[i]) * KINV;  // 0 for degenerate groups (all codes 0)
             }
             float W[4][4], dt[4], mx[4];
 #pragma unroll
@@ -656,12 +661,12 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
             if ((lane & 7) == 0) {
               const int h = (b4 ? 2 : 0) + (b3 ? 1 : 0);
               Wp.off[h] = d1;
-              Wp.kscale[h] = m1 / IM_QMAX;
+              Wp.kscale[h] = m1 * (1.0f / IM_QMAX);
             }
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
               const float mh = __shfl_sync(0xffffffffu, m1, 8 * h);
-              const float inv = mh > 0.0f ? IM_QMAX / mh : 0.0f;
+              const float inv = mh > 0.0f ? __fdividef(IM_QMAX, mh) : 0.0f;
               const float x0 = fmaf(W[h][0], inv, IM_MAGIC), x1 = fmaf(W[h][1], inv, IM_MAGIC);
               const float x2 = fmaf(W[h][2], inv, IM_MAGIC), x3 = fmaf(W[h][3], inv, IM_MAGIC);
               Wp.bfrag[fks][(2 * h) * 4 + fq][fj] = pack_digits(x0, x1, x2, x3, 0x0051, 0, 0u);
@@ -739,10 +744,12 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
             float l0 = 0.0f, l1 = 0.0f, s0 = 0.0f, s1 = 0.0f;
             if (gt0 + tl < n) {
               const uint2 w = *reinterpret_cast<const uint2 *>(&T.vlohi[2 * (tl0 + tl)]);
-              l0 = h2f(w.x & 0xffff);
-              l1 = h2f(w.y & 0xffff);
-              s0 = (h2f(w.x >> 16) - l0) * KINV;
-              s1 = (h2f(w.y >> 16) - l1) * KINV;
+              const float2 f0 = __half22float2(*reinterpret_cast<const __half2 *>(&w.x));  // (lo, hi)
+              const float2 f1 = __half22float2(*reinterpret_cast<const __half2 *>(&w.y));
+              l0 = f0.x;
+              l1 = f1.x;
+              s0 = (f0.y - l0) * KINV;
+              s1 = (f1.y - l1) * KINV;
             }
             Wp.ps[0][tq][tl] = p * s0;
             Wp.ps[1][tq][tl] = p * s1;
@@ -774,7 +781,7 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
         pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 1));
         pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 2));
         pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, 4));
-        const float pinv = pmax > 0.0f ? IM_QMAX / pmax : 0.0f;
+        const float pinv = pmax > 0.0f ? __fdividef(IM_QMAX, pmax) : 0.0f;
         const float vsc_h = __shfl_sync(0xffffffffu, pmax, (2 * tq) * 4) * (1.0f / IM_QMAX);  // head tq's scale
         int V[8][4];
 #pragma unroll
@@ -847,7 +854,7 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
 #pragma unroll
     for (int r = 0; r < 2; ++r) wacc[(warp * 4 + tq) * IM_D + mt * 16 + g8 + 8 * r] = acc[mt][r] + zsum[mt >> 2];
   __syncthreads();
-  for (int i = tid; i < G * IM_D; i += blockDim.x) {
+  for (int i = tid; i < Gb * IM_D; i += blockDim.x) {
     const int h = i / IM_D, ch = i % IM_D;
     float M = -INFINITY;
     for (int w = 0; w < QP_WARPS; ++w) M = fmaxf(M, S.wm[w][h]);
@@ -858,7 +865,7 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
       L = fmaf(sc, S.wl[w][h], L);
       A = fmaf(sc, wacc[(w * 4 + h) * IM_D + ch], A);
     }
-    const size_t base = ((size_t)u * splits + split) * G + h;
+    const size_t base = ((size_t)u * splits + split) * G + h0 + h;
     pacc[base * IM_D + ch] = A;
     if (ch == 0) {
       pm[base] = M;
@@ -881,12 +888,13 @@ static int sm_count() {
 int quant_decode_pipe(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st) {
   const int CH = IM_CHUNK / c.bits;
   const int max_chunks = (int)((c.capacity + CH - 1) / CH);
-  const int splits = std::max(1, std::min(max_chunks, sm_count() / std::max(1, c.units)));
+  const int hblocks = (G + 3) / 4;
+  const int splits = std::max(1, std::min(max_chunks, sm_count() / std::max(1, c.units * hblocks)));
   float *pm = reinterpret_cast<float *>(ws);
   float *pl = pm + (size_t)c.units * splits * G;
   float *pacc = pl + (size_t)c.units * splits * G;
   const size_t sm = sizeof(QpSmem);
-  dim3 grid(splits, c.units);
+  dim3 grid(splits, c.units, hblocks);
   if (c.bits == 1) {
     cudaFuncSetAttribute(quant_decode_pipe_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_prio(quant_decode_pipe_kernel<1>, grid, dim3(QP_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, splits);

@@ -1392,7 +1392,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           g_fz_phase[rank][35] = t_;
         }
       } else if (!keys_host) {
-        for (int i0 = warp; i0 < cnt; i0 += NLW * 16) {
+        constexpr int RB = (CPL == 4 && GMAX == 8) ? 8 : 16;  // rows per warp and batch
+        for (int i0 = warp; i0 < cnt; i0 += NLW * RB) {
           if constexpr (CPL == 4 && GMAX == 4) {
             uint2 kr[16];
 #pragma unroll
@@ -1443,6 +1444,57 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
               if ((lane & 7) == 0 && h < G) zs[(size_t)i * GMAX + h] = c;
             }
             if (base == 0 && i0 == warp) FZ_MARK(33);
+          } else if constexpr (CPL == 4 && GMAX == 8) {
+            // up to 8 query heads (Qwen2.5-7B G=7, Llama-3.1-70B G=8): 8 head sums
+            // reduced by a 3-level transposed butterfly + 2 plain steps (9 shuffles
+            // per row instead of 8 warp sums)
+            uint2 kr[RB];
+#pragma unroll
+            for (int jr = 0; jr < RB; ++jr) {
+              const int i = i0 + NLW * jr;
+              kr[jr] = make_uint2(0u, 0u);
+              if (i < cnt) {
+                const int64_t idx = rbase + rows[base + i];
+                const uint16_t *kp = idx >= local_start
+                                         ? s.loc_k + ((size_t)u * s.local_capacity + (idx - s.local_offset)) * D
+                                         : (s.kdev ? s.kdev + ((size_t)u * s.capacity + idx) * D : nullptr);
+                if (kp) {
+                  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(kr[jr].x), "=r"(kr[jr].y) : "l"(kp + lane * 4));
+                } else {
+                  uint32_t w[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) w[e] = kt[((size_t)lane * 4 + e) * s.capacity + idx];
+                  kr[jr] = make_uint2(w[0] | (w[1] << 16), w[2] | (w[3] << 16));
+                }
+              }
+            }
+            const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+            const int hl = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+#pragma unroll
+            for (int jr = 0; jr < RB; ++jr) {
+              const int i = i0 + NLW * jr;
+              if (i >= cnt) break;
+              const float k0 = h2f((uint16_t)kr[jr].x), k1 = h2f((uint16_t)(kr[jr].x >> 16));
+              const float k2 = h2f((uint16_t)kr[jr].y), k3 = h2f((uint16_t)(kr[jr].y >> 16));
+              float dd[8];
+#pragma unroll
+              for (int h = 0; h < 8; ++h) {
+                const float4 qh = *reinterpret_cast<const float4 *>(S.qs + h * D + lane * 4);
+                dd[h] = fmaf(qh.x, k0, fmaf(qh.y, k1, fmaf(qh.z, k2, qh.w * k3)));
+              }
+              float a[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                a[j] = (b16 ? dd[j + 4] : dd[j]) + __shfl_xor_sync(0xffffffffu, b16 ? dd[j] : dd[j + 4], 16);
+              float b2[2];
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                b2[j] = (b8 ? a[j + 2] : a[j]) + __shfl_xor_sync(0xffffffffu, b8 ? a[j] : a[j + 2], 8);
+              float c = (b4 ? b2[1] : b2[0]) + __shfl_xor_sync(0xffffffffu, b4 ? b2[0] : b2[1], 4);
+              c += __shfl_xor_sync(0xffffffffu, c, 2);
+              c += __shfl_xor_sync(0xffffffffu, c, 1);
+              if ((lane & 3) == 0 && hl < G) zs[(size_t)i * GMAX + hl] = c;
+            }
           } else {
             float kf[8][CPL];
 #pragma unroll

@@ -140,6 +140,29 @@ def test_quant_decode_tensor_core_vs_oracle(tkv, bits, n, kscale, impl):
     assert rel_err(out2, ref) <= 5e-4  # typical margin of the exact-integer design
 
 
+@pytest.mark.parametrize("G", [1, 3, 5, 7, 8])
+@pytest.mark.parametrize("bits", [1, 2])
+def test_quant_decode_tensor_core_head_blocks(tkv, bits, G):
+    """GQA groups of any size on the pipelined IMMA kernel (Qwen2.5-7B G=7,
+    Llama-3.1-70B G=8): query heads run in blocks of 4, the last block ragged."""
+    rng = np.random.default_rng(300 + 10 * G + bits)
+    h, d, n = 2, 128, 9000 + 21
+    keys = cases.f16(rng.normal(0, 0.2, size=(h, n, d)))
+    keys[:, ::131] += cases.f16(rng.normal(0, 0.6, size=(h, 1, d)))
+    keys = cases.f16(keys)
+    values = cases.f16(rng.normal(size=(h, n, d)))
+    queries = cases.f16(rng.normal(size=(h * G, d)))
+    q = tkv.quantize_layer_kv(keys, values, bits, 64)
+    kq, vq = O.quantize_layer(keys, values, bits, 64)
+    ref = O.quant_layer_decode(queries, kq, vq)
+    out = q.decode(queries, impl=2).cpu().numpy()
+    assert rel_err(out, ref) <= 5e-4
+    assert np.array_equal(q.decode(queries).cpu().numpy(), out)  # impl 0 picks the tensor-core kernel
+    if G > 4:
+        with pytest.raises(tkv.ParameterError):
+            q.decode(queries, impl=3)
+
+
 @pytest.mark.parametrize("bits", [1, 2])
 def test_quant_decode_pipelined_ring_wraps(tkv, bits):
     """8 heads at 60k tokens: every CTA of the pipelined kernel streams more
