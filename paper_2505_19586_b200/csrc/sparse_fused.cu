@@ -1391,6 +1391,53 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
           g_fz_phase[rank][35] = t_;
         }
+        // cache slots for this step's misses (every round's), chosen by this warp
+        // while the others compute the key logits: free slots of this CTA's
+        // partition (empty, or not selected in the last cache_window steps),
+        // scanned from the partition's clock hand 32 at a time
+        if (base == 0) {
+          const int W = max(1, s.cache_window);
+          int32_t *F = reinterpret_cast<int32_t *>(S.flags);  // free-slot list (the selection flags are dead)
+          constexpr int FCAP = FZ_CAP / 4;
+          const unsigned lt = (1u << lane) - 1u;
+          int need = 0;
+          for (int i0 = 0; i0 < nrows; i0 += 32) {
+            const int i = i0 + lane;
+            need += __popc(__ballot_sync(0xffffffffu, i < nrows && rslot[i] == -1));
+          }
+          need = min(need, FCAP);
+          const int np = p1 - p0;
+          int32_t *hand = s.slot_hand ? s.slot_hand + (size_t)u * 16 + rank : nullptr;
+          const int h0 = hand && np > 0 ? ((*hand % np) + np) % np : 0;
+          int found = 0;
+          for (int k0 = 0; found < need && k0 < np; k0 += 32) {  // warp-uniform: found, need, np
+            const int k = k0 + lane;
+            int p = 0;
+            bool fr = false;
+            if (k < np) {
+              p = p0 + (h0 + k) % np;
+              fr = stok[p] < 0 || sstamp[p] <= (int)n - W;
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, fr);
+            const int pos = found + __popc(b & lt);
+            if (fr && pos < need) {
+              F[pos] = p;
+              if (pos == need - 1 && hand) *hand = (h0 + k + 1) % np;  // the hand moves past the last slot taken
+            }
+            found += __popc(b);
+          }
+          __syncwarp();
+          const int used = min(found, need);
+          int ord = 0;
+          for (int i0 = 0; i0 < nrows; i0 += 32) {
+            const int i = i0 + lane;
+            const bool m = i < nrows && rslot[i] == -1;
+            const unsigned b = __ballot_sync(0xffffffffu, m);
+            const int k = ord + __popc(b & lt);
+            if (m && k < used) rslot[i] = -3 - F[k];  // misses beyond the free slots are simply not cached
+            ord += __popc(b);
+          }
+        }
       } else if (!keys_host) {
         constexpr int RB = (CPL == 4 && GMAX == 8) ? 8 : 16;  // rows per warp and batch
         for (int i0 = warp; i0 < cnt; i0 += NLW * RB) {
@@ -1638,46 +1685,6 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
       }
       if (base == 0) FZ_MARK(29);
-      // cache slots for this step's misses: free slots of this CTA's partition
-      // (empty, or not selected in the last cache_window steps), scanned from
-      // the partition's clock hand one block-sized chunk at a time
-      if (use_cache && base == 0) {
-        const int W = max(1, s.cache_window);
-        int32_t *F = reinterpret_cast<int32_t *>(S.flags);  // free-slot list (the flags are dead)
-        constexpr int FCAP = FZ_CAP / 4;
-        int tm = 0;
-        for (int i = tid; i < nrows; i += blockDim.x) tm += rslot[i] == -1;  // (misses of later rounds too)
-        int need;
-        int ord = fz_block_excl_scan(tm, C.scan, &need);
-        need = min(need, FCAP);
-        const int np = p1 - p0;
-        int32_t *hand = s.slot_hand ? s.slot_hand + (size_t)u * 16 + rank : nullptr;
-        const int h0 = hand && np > 0 ? ((*hand % np) + np) % np : 0;
-        int found = 0;
-        for (int k0 = 0; found < need && k0 < np; k0 += blockDim.x) {  // uniform: found, need, np
-          const int k = k0 + tid;
-          int p = 0, fr = 0;
-          if (k < np) {
-            p = p0 + (h0 + k) % np;
-            fr = stok[p] < 0 || sstamp[p] <= (int)n - W;
-          }
-          int tot;
-          const int pos = found + fz_block_excl_scan(fr, C.scan, &tot);
-          if (fr && pos < need) {
-            F[pos] = p;
-            if (pos == need - 1 && hand) *hand = (h0 + k + 1) % np;  // the hand moves past the last slot taken
-          }
-          found += tot;
-        }
-        __syncthreads();  // F
-        const int used = min(found, need);
-        for (int i = tid; i < nrows; i += blockDim.x) {
-          if (rslot[i] != -1) continue;
-          const int k = ord++;
-          if (k < used) rslot[i] = -3 - F[k];  // misses beyond the free slots are simply not cached
-        }
-        __syncthreads();
-      }
       if (base == 0) FZ_MARK(36);
       // (e) rows fetched over PCIe enter the HBM row cache in their assigned slots
       if (use_cache) {
