@@ -1624,6 +1624,72 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
       }
       __syncwarp();
+      if (!keys_host) {
+        // (d) softmax, warp-local: a warp's rows are the rows whose logits it
+        // computed (row = warp mod NLW), so each warp runs an online softmax over
+        // them with no CTA barrier -- the round max per head (entries spread over
+        // the lanes, lane % GMAX = head), one exp2 per (row, head) written back in
+        // place, then p.v over its rows; the warp partials merge below as before
+        if (warp < NLW) {
+          const int nr = cnt > warp ? (cnt - warp + NLW - 1) / NLW : 0;
+          const int hl = lane % GMAX;
+          const int ne = nr * GMAX;
+          float wm = -INFINITY;
+          for (int e = lane; e < ne; e += 32)
+            if (hl < G) wm = fmaxf(wm, zs[(size_t)(warp + NLW * (e / GMAX)) * GMAX + hl]);
+#pragma unroll
+          for (int o = GMAX; o < 32; o <<= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+          float mh = -INFINITY;  // this lane's head's new max
+#pragma unroll
+          for (int h = 0; h < GMAX; ++h) {
+            const float mr = fmaxf(mrun[h], __shfl_sync(0xffffffffu, wm, h));
+            if (h < G && mr != -INFINITY) {
+              const float sc = exp2f(mrun[h] - mr);  // 0 on the warp's first rows (mrun = -inf)
+              lrun[h] *= sc;
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) acc[h][e] *= sc;
+              mrun[h] = mr;
+            }
+            if (h == hl) mh = mrun[h];
+          }
+          float ps = 0.0f;
+          for (int e = lane; e < ne; e += 32) {
+            if (hl >= G) continue;
+            float *zp = &zs[(size_t)(warp + NLW * (e / GMAX)) * GMAX + hl];
+            const float pv = exp2f(*zp - mh);
+            *zp = pv;
+            ps += pv;
+          }
+#pragma unroll
+          for (int o = GMAX; o < 32; o <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+#pragma unroll
+          for (int h = 0; h < GMAX; ++h) {
+            const float t = __shfl_sync(0xffffffffu, ps, h);
+            if (h < G) lrun[h] += t;
+          }
+          __syncwarp();
+          for (int i = warp; i < cnt; i += NLW) {
+            const uint16_t *vr = stage_v + (size_t)i * D + lane * CPL;
+            float vf[CPL];
+            if constexpr (CPL == 4) {
+              const uint2 bv = *reinterpret_cast<const uint2 *>(vr);
+              vf[0] = h2f((uint16_t)bv.x); vf[1] = h2f((uint16_t)(bv.x >> 16));
+              vf[2] = h2f((uint16_t)bv.y); vf[3] = h2f((uint16_t)(bv.y >> 16));
+            } else {
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) vf[e] = h2f(vr[e]);
+            }
+#pragma unroll
+            for (int h = 0; h < GMAX; ++h) {
+              if (h >= G) break;
+              const float p = zs[(size_t)i * GMAX + h];
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) acc[h][e] = fmaf(p, vf[e], acc[h][e]);
+            }
+          }
+        }
+        __syncthreads();  // the PCIe warp's cache-slot codes (rslot) before the inserts below
+      } else {
       // (d) softmax: the round's max per head over the whole CTA, p = exp2(z - m)
       // once per (row, head) in shared memory, then each warp accumulates its rows
       __syncthreads();  // every logit of the round is in zs
@@ -1683,6 +1749,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             for (int e = 0; e < CPL; ++e) acc[h][e] = fmaf(p, vf[e], acc[h][e]);
           }
         }
+      }
       }
       if (base == 0) FZ_MARK(29);
       if (base == 0) FZ_MARK(36);
