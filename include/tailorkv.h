@@ -146,7 +146,7 @@ typedef struct tkv_sparse_layer {
   int32_t cache_window;   /* steps a selected row stays resident */
   int32_t *slot_tok;      /* [units][cache_slots] token held by the slot, -1 when empty */
   int32_t *slot_stamp;    /* [units][cache_slots] *len at the row's last selection */
-  uint16_t *slot_v;       /* [units][cache_slots][d] cached value rows */
+  uint16_t *slot_v;       /* [units][cache_slots][2][d] cached (key | value) rows */
   int32_t *tok_slot;      /* [units][capacity] token -> slot, verified against slot_tok */
   unsigned long long *cache_stats; /* [2]: rows served from HBM, rows fetched over PCIe */
   /* Optional [units][4] float (16-byte aligned): per head, the last step's

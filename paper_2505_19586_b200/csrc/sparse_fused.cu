@@ -132,11 +132,14 @@ struct FzCtl {
   unsigned long long scan64[33];
   int hits, misses;
   int list_count;
-  unsigned long long bar;       // mbarrier of the value-row staging
+  unsigned long long bar;       // mbarrier of the row staging (HBM copies on the key|value slot-cache path)
+  unsigned long long bar2;      // key|value slot-cache path: the value rows fetched over PCIe
 };
 
 // dynamic shared memory
 constexpr int FZ_UNION = FZ_CAP * 8;  // bytes of the phase-overlaid region (float64 keys of the exact path)
+constexpr int FZ_XSTAGE = 26624;      // extra staging bytes: ~360 (K|V) rows per CTA fit one round
+constexpr int FZ_STAGE = FZ_UNION + FZ_CAP + FZ_XSTAGE;  // k.raw + flags (dead after the output) + xstage
 struct FzShared {
   union {
     uint64_t keys64[FZ_CAP];  // exact fallback: order-preserving float64 score keys
@@ -160,6 +163,7 @@ struct FzShared {
     unsigned char raw[FZ_UNION];  // attention phase: staged rows, logits, row list, partials
   } k;
   uint8_t flags[FZ_CAP];
+  uint8_t xstage[FZ_XSTAGE];  // with k and flags: the gather's staging region (contiguous)
   uint32_t xhist[2][FZ_XBINS];
   uint32_t xtot[FZ_XBINS];
   float cta_m[8], cta_l[8];
@@ -429,6 +433,13 @@ __device__ __forceinline__ void fz_mbar_init(unsigned long long *bar) {
 __device__ __forceinline__ void fz_mbar_expect(unsigned long long *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fz_smem_addr(bar)), "r"(bytes) : "memory");
 }
+// add bytes to the current phase's transaction count (no arrival; one thread arrives once all are queued)
+__device__ __forceinline__ void fz_mbar_expect_only(unsigned long long *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(fz_smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fz_mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fz_smem_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void fz_mbar_wait(unsigned long long *bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n FZW_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra FZW_%=;\n}\n" ::"r"(
@@ -531,7 +542,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     C.overflow = 0;
     C.hits = 0;
     C.misses = 0;
-    if (ATTEND) fz_mbar_init(&C.bar);
+    if (ATTEND) {
+      fz_mbar_init(&C.bar);
+      fz_mbar_init(&C.bar2);
+    }
   }
   bool listed = false;                 // candidate-list path: flags come from keys32 + bitmap
   uint32_t ord_def = 0xffffffffu;      // (list path) keys above this orderable value are selected
@@ -1243,12 +1257,20 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     far_total += c;
   }
   const int n_loc = (int)(n - ncand);
-  const int nrows = cta_total + (rank == FZ_CTAS - 1 ? n_loc : 0);
-  // row list (16-bit token offsets from rbase, local rows after the far ones) at the top of the overlaid region
-  const int64_t rbase = rank == FZ_CTAS - 1 ? imin64(j0, ncand) : j0;
-  // [16-bit row offsets | 32-bit cache slot codes] per row
-  const int rows_bytes = ((nrows * 2 + 127) / 128) * 128 + (ATTEND ? ((nrows * 4 + 127) / 128) * 128 : 0);
-  uint16_t *rows = reinterpret_cast<uint16_t *>(S.k.raw + FZ_UNION - rows_bytes);
+  // the local-window rows are dealt round-robin over the cluster's CTAs (local row l -> rank l % FZ_CTAS)
+  const int n_loc_mine = n_loc > rank ? (n_loc - rank + FZ_CTAS - 1) / FZ_CTAS : 0;
+  const int nrows = cta_total + (ATTEND ? n_loc_mine : 0);
+  // row list (32-bit token offsets from rbase, local rows after the far ones) at the top of the staging region
+  const int64_t rbase = imin64(j0, ncand);
+  // [32-bit row offsets | 32-bit cache slot codes] per row
+  const int rows_bytes = ((nrows * 4 + 127) / 128) * 128 + (ATTEND ? ((nrows * 4 + 127) / 128) * 128 : 0);
+  static_assert(offsetof(FzShared, flags) == FZ_UNION && offsetof(FzShared, xstage) == FZ_UNION + FZ_CAP &&
+                    offsetof(FzShared, xhist) == FZ_STAGE && offsetof(FzShared, xtot) == FZ_STAGE + sizeof(S.xhist),
+                "the staging region k.raw + flags + xstage (+ xhist + xtot) is contiguous");
+  // ranks other than 0 also stage over the exact path's histograms (dead after the select); in
+  // rank 0 they are the inbox the other CTAs push their partials into
+  const int stage_bytes = ATTEND ? FZ_STAGE + (rank != 0 ? (int)(sizeof(S.xhist) + sizeof(S.xtot)) : 0) : FZ_UNION;
+  int32_t *rows = reinterpret_cast<int32_t *>(S.k.raw + stage_bytes - rows_bytes);
 #pragma unroll
   for (int g = 0; g < FZ_KG; ++g) {
     int p = gpos[g];
@@ -1260,16 +1282,15 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         x &= x - 1u;
         const int e = g * FZ_STEP + tid * 8 + 4 * w + (bit >> 3);
         out_idx[offset + p] = (int32_t)(j0 + e);
-        if (ATTEND) rows[p] = (uint16_t)(j0 + e - rbase);
+        if (ATTEND) rows[p] = (int32_t)(j0 + e - rbase);
         ++p;
       }
     }
   }
+  if (ATTEND)
+    for (int i = tid; i < n_loc_mine; i += blockDim.x) rows[cta_total + i] = (int32_t)(ncand + rank + FZ_CTAS * i - rbase);
   if (rank == FZ_CTAS - 1) {
-    for (int i = tid; i < n_loc; i += blockDim.x) {
-      out_idx[far_total + i] = (int32_t)(ncand + i);
-      if (ATTEND) rows[cta_total + i] = (uint16_t)(ncand + i - rbase);
-    }
+    for (int i = tid; i < n_loc; i += blockDim.x) out_idx[far_total + i] = (int32_t)(ncand + i);
     if (tid == 0) {
       sel_count[u] = far_total + n_loc;
       if (fetch_count) fetch_count[u] = far_total;
@@ -1293,18 +1314,23 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     // the last cache_window steps are reused).
     constexpr int CPL = D / 32;  // channels per lane
     const bool keys_host = !keys_from_device;
-    const int row_bytes = D * 2 * (keys_host ? 2 : 1) + GMAX * 4;  // staged V (+K) + logits
-    const int NR = min(1024, ((FZ_UNION - rows_bytes) / row_bytes) & ~15);
-    uint16_t *stage_v = reinterpret_cast<uint16_t *>(S.k.raw);
-    uint16_t *stage_k = stage_v + (size_t)NR * D;  // used when keys cross PCIe
-    float *zs = reinterpret_cast<float *>(S.k.raw + (size_t)NR * D * 2 * (keys_host ? 2 : 1));
-    int32_t *rslot = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(rows) + ((nrows * 2 + 127) / 128) * 128);
-    const int64_t local_start = ncand;
     const bool use_cache = s.cache_slots > 0 && keys_from_device;
+    // key|value slot-cache path: a cached row is one 512-byte (K|V) copy from its
+    // HBM slot into a (K|V) staging row; logits are computed from the staged keys
+    const bool kvc = use_cache && s.kdev != nullptr;
+    const int row_bytes = D * 2 * (keys_host || kvc ? 2 : 1) + GMAX * 4;  // staged V (+K) + logits
+    const int NR = min(1024, ((stage_bytes - rows_bytes) / row_bytes) & ~15);
+    uint16_t *stage = reinterpret_cast<uint16_t *>(S.k.raw);
+    // staged rows: keys over PCIe: V [NR][D] then K [NR][D]; slot-cache path: [NR][K|V]; else V [NR][D]
+    auto vrow = [&](int i) -> uint16_t * { return kvc ? stage + (size_t)i * 2 * D + D : stage + (size_t)i * D; };
+    auto krow = [&](int i) -> uint16_t * { return kvc ? stage + (size_t)i * 2 * D : stage + ((size_t)NR + i) * D; };
+    float *zs = reinterpret_cast<float *>(S.k.raw + (size_t)NR * D * 2 * (keys_host || kvc ? 2 : 1));
+    int32_t *rslot = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(rows) + ((nrows * 4 + 127) / 128) * 128);
+    const int64_t local_start = ncand;
     const int CS = s.cache_slots;
     int32_t *stok = use_cache ? s.slot_tok + (size_t)u * CS : nullptr;
     int32_t *sstamp = use_cache ? s.slot_stamp + (size_t)u * CS : nullptr;
-    uint16_t *sv = use_cache ? s.slot_v + (size_t)u * CS * D : nullptr;
+    uint16_t *sv = use_cache ? s.slot_v + (size_t)u * CS * 2 * D : nullptr;  // slots hold (K|V) rows
     int32_t *tslot = use_cache ? s.tok_slot + (size_t)u * s.capacity : nullptr;
     // Each CTA owns the slots [p0, p1) of its unit's cache: it serves hits and
     // allocates misses only there, so no cross-CTA coordination is needed.
@@ -1349,6 +1375,32 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     const int NLW = pcie_warp ? FZ_WARPS - 1 : FZ_WARPS;  // warps computing key logits
     auto over_pcie = [](int code) { return code == -1 || code <= -3; };
     auto issue_round = [&](int base, int cnt) {
+      if (kvc) {
+        // every copy adds its own bytes to C.bar (HBM) or, from the PCIe warp, C.bar2;
+        // one arrival each once every copy of the round is queued
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (base == 0) FZ_MARK(34);
+        for (int i = tid; i < cnt; i += blockDim.x) {
+          const int64_t idx = rbase + rows[base + i];
+          const int code = rslot[base + i];
+          if (code >= 0) {  // hit: the slot's (K|V) row
+            fz_mbar_expect_only(&C.bar, D * 4);
+            fz_bulk_g2s(krow(i), sv + (size_t)code * 2 * D, D * 4, &C.bar);
+          } else if (code == -2) {  // local window mirror
+            const size_t lr = (size_t)u * s.local_capacity + (size_t)(idx - s.local_offset);
+            fz_mbar_expect_only(&C.bar, D * 4);
+            fz_bulk_g2s(krow(i), s.loc_k + lr * D, D * 2, &C.bar);
+            fz_bulk_g2s(vrow(i), s.loc_v + lr * D, D * 2, &C.bar);
+          } else {  // miss: key row from HBM here, value row over PCIe by the PCIe warp
+            fz_mbar_expect_only(&C.bar, D * 2);
+            fz_bulk_g2s(krow(i), s.kdev + ((size_t)u * s.capacity + idx) * D, D * 2, &C.bar);
+          }
+        }
+        __syncthreads();
+        if (tid == 0) fz_mbar_arrive(&C.bar);
+        return;
+      }
       if (tid == 0) fz_mbar_expect(&C.bar, (uint32_t)(cnt * D * 2 * (keys_host ? 2 : 1)));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses before the TMA writes
       __syncthreads();
@@ -1360,15 +1412,14 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         if (code == -2) {
           const int64_t lr = idx - s.local_offset;
           vp = s.loc_v + ((size_t)u * s.local_capacity + lr) * D;
-          if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, s.loc_k + ((size_t)u * s.local_capacity + lr) * D, D * 2,
-                                     &C.bar);
+          if (keys_host) fz_bulk_g2s(krow(i), s.loc_k + ((size_t)u * s.local_capacity + lr) * D, D * 2, &C.bar);
         } else {
           const uint16_t *hrow = s.host_kv + ((size_t)u * s.capacity + idx) * 2 * D;
           if (pcie_warp && over_pcie(code)) continue;
-          vp = code >= 0 ? sv + (size_t)code * D : hrow + D;
-          if (keys_host) fz_bulk_g2s(stage_k + (size_t)i * D, hrow, D * 2, &C.bar);
+          vp = code >= 0 ? sv + (size_t)code * 2 * D + D : hrow + D;
+          if (keys_host) fz_bulk_g2s(krow(i), hrow, D * 2, &C.bar);
         }
-        fz_bulk_g2s(stage_v + (size_t)i * D, vp, D * 2, &C.bar);
+        fz_bulk_g2s(vrow(i), vp, D * 2, &C.bar);
       }
     };
     if (nrows > 0) issue_round(0, min(NR, nrows));
@@ -1381,10 +1432,15 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       // a batch's 16 row loads are issued before any use
       if (pcie_warp && warp == FZ_WARPS - 1) {
         // (b') the PCIe warp: value rows over PCIe, queued behind the HBM copies
+        unsigned long long *pbar = kvc ? &C.bar2 : &C.bar;
         for (int i = lane; i < cnt; i += 32) {
           if (!over_pcie(rslot[base + i])) continue;
-          fz_bulk_g2s(stage_v + (size_t)i * D, s.host_kv + ((size_t)u * s.capacity + rbase + rows[base + i]) * 2 * D + D,
-                      D * 2, &C.bar);
+          if (kvc) fz_mbar_expect_only(pbar, D * 2);
+          fz_bulk_g2s(vrow(i), s.host_kv + ((size_t)u * s.capacity + rbase + rows[base + i]) * 2 * D + D, D * 2, pbar);
+        }
+        if (kvc) {
+          __syncwarp();
+          if (lane == 0) fz_mbar_arrive(pbar);
         }
         if (trace && blockIdx.y == 0 && lane == 0 && base == 0) {
           unsigned long long t_;
@@ -1397,8 +1453,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         // scanned from the partition's clock hand 32 at a time
         if (base == 0) {
           const int W = max(1, s.cache_window);
-          int32_t *F = reinterpret_cast<int32_t *>(S.flags);  // free-slot list (the selection flags are dead)
-          constexpr int FCAP = FZ_CAP / 4;
+          int32_t *F = reinterpret_cast<int32_t *>(S.cta_acc);  // free-slot list (cta_acc is written at the merge)
+          constexpr int FCAP = sizeof(S.cta_acc) / 4;
           const unsigned lt = (1u << lane) - 1u;
           int need = 0;
           for (int i0 = 0; i0 < nrows; i0 += 32) {
@@ -1438,6 +1494,69 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             ord += __popc(b);
           }
         }
+      } else if (kvc) {
+        // (b'') slot-cache path: the round's key rows (cached K|V rows, local
+        // mirror, misses' key rows from HBM) land in shared memory; this warp's
+        // rows are row = warp mod NLW, as for the register path below
+        fz_mbar_wait(&C.bar, parity);
+        if (base == 0 && warp == 0) FZ_MARK(32);
+        for (int i = warp; i < cnt; i += NLW) {
+          const uint16_t *kp = krow(i) + lane * CPL;
+          if constexpr (CPL == 4 && (GMAX == 4 || GMAX == 8)) {
+            const uint2 kb = *reinterpret_cast<const uint2 *>(kp);
+            const float k0 = h2f((uint16_t)kb.x), k1 = h2f((uint16_t)(kb.x >> 16));
+            const float k2 = h2f((uint16_t)kb.y), k3 = h2f((uint16_t)(kb.y >> 16));
+            float dd[GMAX];
+#pragma unroll
+            for (int h = 0; h < GMAX; ++h) {
+              const float4 qh = *reinterpret_cast<const float4 *>(S.qs + h * D + lane * 4);
+              dd[h] = fmaf(qh.x, k0, fmaf(qh.y, k1, fmaf(qh.z, k2, qh.w * k3)));
+            }
+            // transposed butterfly: log2(GMAX) halving steps, then plain steps
+            float c;
+            int hl;
+            if constexpr (GMAX == 8) {
+              const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+              float a[4], b2[2];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                a[j] = (b16 ? dd[j + 4] : dd[j]) + __shfl_xor_sync(0xffffffffu, b16 ? dd[j] : dd[j + 4], 16);
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                b2[j] = (b8 ? a[j + 2] : a[j]) + __shfl_xor_sync(0xffffffffu, b8 ? a[j] : a[j + 2], 8);
+              c = (b4 ? b2[1] : b2[0]) + __shfl_xor_sync(0xffffffffu, b4 ? b2[0] : b2[1], 4);
+              c += __shfl_xor_sync(0xffffffffu, c, 2);
+              c += __shfl_xor_sync(0xffffffffu, c, 1);
+              hl = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+              if ((lane & 3) == 0 && hl < G) zs[(size_t)i * GMAX + hl] = c;
+            } else {
+              const bool hi16 = lane & 16, hi8 = lane & 8;
+              float a0 = hi16 ? dd[2] : dd[0], a1 = hi16 ? dd[3] : dd[1];
+              a0 += __shfl_xor_sync(0xffffffffu, hi16 ? dd[0] : dd[2], 16);
+              a1 += __shfl_xor_sync(0xffffffffu, hi16 ? dd[1] : dd[3], 16);
+              c = hi8 ? a1 : a0;
+              c += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+              c += __shfl_xor_sync(0xffffffffu, c, 4);
+              c += __shfl_xor_sync(0xffffffffu, c, 2);
+              c += __shfl_xor_sync(0xffffffffu, c, 1);
+              hl = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
+              if ((lane & 7) == 0 && hl < G) zs[(size_t)i * GMAX + hl] = c;
+            }
+          } else {
+            float kf[CPL];
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) kf[e] = h2f(kp[e]);
+            for (int h = 0; h < G; ++h) {
+              const float *qh = S.qs + h * D + lane * CPL;
+              float dp = 0.0f;
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) dp = fmaf(qh[e], kf[e], dp);
+              dp = warp_sum(dp);
+              if (lane == 0) zs[(size_t)i * GMAX + h] = dp;
+            }
+          }
+        }
+        if (base == 0 && warp == 0) FZ_MARK(33);
       } else if (!keys_host) {
         constexpr int RB = (CPL == 4 && GMAX == 8) ? 8 : 16;  // rows per warp and batch
         for (int i0 = warp; i0 < cnt; i0 += NLW * RB) {
@@ -1607,12 +1726,12 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       }
       if (base == 0) FZ_MARK(27);
       // (c) value rows (and key rows over PCIe) have landed
-      fz_mbar_wait(&C.bar, parity);
+      fz_mbar_wait(kvc ? &C.bar2 : &C.bar, parity);
       parity ^= 1u;
       if (base == 0) FZ_MARK(28);
       if (keys_host) {
         for (int i = warp; i < cnt; i += FZ_WARPS) {
-          const uint16_t *kp = stage_k + (size_t)i * D;
+          const uint16_t *kp = krow(i);
           for (int h = 0; h < G; ++h) {
             const float *qh = S.qs + h * D + lane * CPL;
             float dp = 0.0f;
@@ -1669,7 +1788,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           }
           __syncwarp();
           for (int i = warp; i < cnt; i += NLW) {
-            const uint16_t *vr = stage_v + (size_t)i * D + lane * CPL;
+            const uint16_t *vr = vrow(i) + lane * CPL;
             float vf[CPL];
             if constexpr (CPL == 4) {
               const uint2 bv = *reinterpret_cast<const uint2 *>(vr);
@@ -1730,7 +1849,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         }
         __syncthreads();
         for (int i = warp; i < cnt; i += FZ_WARPS) {
-          const uint16_t *vr = stage_v + (size_t)i * D + lane * CPL;
+          const uint16_t *vr = vrow(i) + lane * CPL;
           float vf[CPL];
           if constexpr (CPL == 4) {
             const uint2 bv = *reinterpret_cast<const uint2 *>(vr);
@@ -1763,7 +1882,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           stok[dst] = idx;
           sstamp[dst] = (int)n;
           tslot[idx] = dst;
-          fz_bulk_s2g(sv + (size_t)dst * D, stage_v + (size_t)i * D, D * 2);
+          if (kvc)
+            fz_bulk_s2g(sv + (size_t)dst * 2 * D, krow(i), D * 4);  // the staged (K|V) row
+          else
+            fz_bulk_s2g(sv + (size_t)dst * 2 * D + D, vrow(i), D * 2);
         }
         fz_bulk_commit_wait_read();  // the staged rows are read before the next round overwrites them
       }

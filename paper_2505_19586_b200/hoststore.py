@@ -92,13 +92,13 @@ class OffloadedLayerKV:
         self.host_kv = self.arena.as_tensor(units * self.capacity * 2 * d).view(units, self.capacity, 2, d)
         self._len = torch.zeros(2, dtype=torch.int32, device=dev)
         self.n = 0
-        # HBM value-row cache: rows selected within the last `cache_window` steps stay resident
+        # HBM row cache: (key|value) rows selected within the last `cache_window` steps stay resident
         self.cache_window = int(cache_window) if cache_rows else 0
         self.cache_slots = int(cache_rows) * max(1, self.cache_window) if cache_rows else 0
         if self.cache_slots:
             self.slot_tok = torch.full((units, self.cache_slots), -1, dtype=torch.int32, device=dev)
             self.slot_stamp = torch.full((units, self.cache_slots), -(1 << 30), dtype=torch.int32, device=dev)
-            self.slot_v = torch.zeros((units, self.cache_slots, d), dtype=torch.float16, device=dev)
+            self.slot_v = torch.zeros((units, self.cache_slots, 2, d), dtype=torch.float16, device=dev)  # K|V
             self.tok_slot = torch.full((units, self.capacity), -1, dtype=torch.int32, device=dev)
             self.cache_stats = torch.zeros(2, dtype=torch.int64, device=dev)
             self.slot_hand = torch.zeros((units, 16), dtype=torch.int32, device=dev)

@@ -460,12 +460,13 @@ def test_fused_sparse_decode_row_cache_across_steps(tkv, window, rows):
                    torch.tensor(values[:, n], dtype=torch.float16, device="cuda"))
     hits, misses = lay.cache_counters()
     assert hits > 0 and misses > 0
-    # every cached slot holds the value row of the token it claims
+    # every cached slot holds the (key | value) row of the token it claims
     tok = lay.slot_tok.cpu().numpy()
     sv = lay.slot_v.cpu().numpy().astype(np.float64)
     for u in range(units):
         for p in np.nonzero(tok[u] >= 0)[0]:
-            assert np.array_equal(sv[u, p], values[u, tok[u, p]])
+            assert np.array_equal(sv[u, p, 0], keys[u, tok[u, p]])
+            assert np.array_equal(sv[u, p, 1], values[u, tok[u, p]])
 
 
 def test_fused_sparse_decode_128k(tkv):
