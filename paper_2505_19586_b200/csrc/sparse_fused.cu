@@ -1500,18 +1500,30 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         // rows are row = warp mod NLW, as for the register path below
         fz_mbar_wait(&C.bar, parity);
         if (base == 0 && warp == 0) FZ_MARK(32);
-        for (int i = warp; i < cnt; i += NLW) {
-          const uint16_t *kp = krow(i) + lane * CPL;
-          if constexpr (CPL == 4 && (GMAX == 4 || GMAX == 8)) {
-            const uint2 kb = *reinterpret_cast<const uint2 *>(kp);
+        if constexpr (CPL == 4 && (GMAX == 4 || GMAX == 8)) {
+          // batches of KR rows: all shared-memory loads first, then independent
+          // FMA + butterfly chains the scheduler can interleave
+          constexpr int KR = GMAX == 4 ? 8 : 4;
+          float4 qv[GMAX];
+#pragma unroll
+          for (int h = 0; h < GMAX; ++h) qv[h] = *reinterpret_cast<const float4 *>(S.qs + h * D + lane * 4);
+          for (int i0 = warp; i0 < cnt; i0 += NLW * KR) {
+            uint2 kbs[KR];
+#pragma unroll
+            for (int j = 0; j < KR; ++j) {
+              const int i = i0 + NLW * j;
+              kbs[j] = i < cnt ? *reinterpret_cast<const uint2 *>(krow(i) + lane * 4) : make_uint2(0u, 0u);
+            }
+#pragma unroll
+            for (int j = 0; j < KR; ++j) {
+            const int i = i0 + NLW * j;
+            if (i >= cnt) break;
+            const uint2 kb = kbs[j];
             const float k0 = h2f((uint16_t)kb.x), k1 = h2f((uint16_t)(kb.x >> 16));
             const float k2 = h2f((uint16_t)kb.y), k3 = h2f((uint16_t)(kb.y >> 16));
             float dd[GMAX];
 #pragma unroll
-            for (int h = 0; h < GMAX; ++h) {
-              const float4 qh = *reinterpret_cast<const float4 *>(S.qs + h * D + lane * 4);
-              dd[h] = fmaf(qh.x, k0, fmaf(qh.y, k1, fmaf(qh.z, k2, qh.w * k3)));
-            }
+            for (int h = 0; h < GMAX; ++h) dd[h] = fmaf(qv[h].x, k0, fmaf(qv[h].y, k1, fmaf(qv[h].z, k2, qv[h].w * k3)));
             // transposed butterfly: log2(GMAX) halving steps, then plain steps
             float c;
             int hl;
@@ -1542,7 +1554,11 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
               hl = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
               if ((lane & 7) == 0 && hl < G) zs[(size_t)i * GMAX + hl] = c;
             }
-          } else {
+            }
+          }
+        } else {
+          for (int i = warp; i < cnt; i += NLW) {
+            const uint16_t *kp = krow(i) + lane * CPL;
             float kf[CPL];
 #pragma unroll
             for (int e = 0; e < CPL; ++e) kf[e] = h2f(kp[e]);
@@ -1787,6 +1803,31 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             if (h < G) lrun[h] += t;
           }
           __syncwarp();
+          if constexpr (CPL == 4 && GMAX == 4) {
+            // batches of 4 rows: value and p loads first, then the FMAs
+            for (int i0 = warp; i0 < cnt; i0 += NLW * 4) {
+              uint2 bv[4];
+              float4 pv[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int i = i0 + NLW * j;
+                bv[j] = i < cnt ? *reinterpret_cast<const uint2 *>(vrow(i) + lane * 4) : make_uint2(0u, 0u);
+                pv[j] = i < cnt ? *reinterpret_cast<const float4 *>(&zs[(size_t)i * 4]) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float vf[4] = {h2f((uint16_t)bv[j].x), h2f((uint16_t)(bv[j].x >> 16)), h2f((uint16_t)bv[j].y),
+                                     h2f((uint16_t)(bv[j].y >> 16))};
+                const float pp[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};  // heads >= G hold 0 (never written: masked below)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  if (h >= G) break;
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) acc[h][e] = fmaf(pp[h], vf[e], acc[h][e]);
+                }
+              }
+            }
+          } else
           for (int i = warp; i < cnt; i += NLW) {
             const uint16_t *vr = vrow(i) + lane * CPL;
             float vf[CPL];
