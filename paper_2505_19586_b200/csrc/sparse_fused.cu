@@ -1344,8 +1344,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       if (idx < local_start) {
         code = -1;
         if (use_cache) {
+          // tok_slot entries are cleared when their slot is recycled (below), so an entry
+          // inside this CTA's partition is valid without reading the slot's token back
           const int p = tslot[idx];
-          if (p >= p0 && p < p1 && stok[p] == (int)idx) {
+          if (p >= p0 && p < p1) {
             code = p;
             sstamp[p] = (int)n;
           }
@@ -1432,6 +1434,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       // a batch's 16 row loads are issued before any use
       if (pcie_warp && warp == FZ_WARPS - 1) {
         // (b') the PCIe warp: value rows over PCIe, queued behind the HBM copies
+        // (queued behind the HBM copies: in front, their host-page translations held up the
+        // TMA queue by ~1 us, more than the earlier start gained)
         unsigned long long *pbar = kvc ? &C.bar2 : &C.bar;
         for (int i = lane; i < cnt; i += 32) {
           if (!over_pcie(rslot[base + i])) continue;
@@ -1478,6 +1482,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             const int pos = found + __popc(b & lt);
             if (fr && pos < need) {
               F[pos] = p;
+              const int old = stok[p];  // the recycled slot's token loses its entry (unless it moved on)
+              if (old >= 0) atomicCAS(&tslot[old], p, -1);
               if (pos == need - 1 && hand) *hand = (h0 + k + 1) % np;  // the hand moves past the last slot taken
             }
             found += __popc(b);
