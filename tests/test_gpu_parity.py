@@ -469,6 +469,32 @@ def test_fused_sparse_decode_row_cache_across_steps(tkv, window, rows):
             assert np.array_equal(sv[u, p, 1], values[u, tok[u, p]])
 
 
+@pytest.mark.parametrize("G", [4, 7])
+def test_fused_sparse_decode_row_cache_staging_rounds(tkv, G):
+    """(K|V) row cache with more selected rows per CTA than one staging round
+    holds (n_topk 6000 over an 8-CTA cluster: ~750 rows per CTA), so hits,
+    misses and local-window rows are gathered over several rounds on both
+    mbarriers, across decode steps; G=7 takes the 8-head kernel."""
+    rng = np.random.default_rng(36 + G)
+    units, n0, d, T = 2, 40000, 128, 4
+    keys = cases.f16(rng.normal(size=(units, n0 + T, d)))
+    values = cases.f16(rng.normal(size=(units, n0 + T, d)))
+    cfg = tkv.RetrievalConfig(40, 6000, 8)
+    lay = _sparse_layer(tkv, keys[:, :n0], values[:, :n0], cfg.n_local, steps=T, keys_on_device=True,
+                        cache_rows=cfg.n_local + cfg.n_topk, cache_window=2)
+    chans = np.stack([np.sort(rng.choice(d, 8, replace=False)) for _ in range(units)]).astype(np.int32)
+    base_q = rng.normal(size=(units * G, d))
+    for t in range(T):
+        n = n0 + t
+        queries = cases.f16(base_q + 0.2 * rng.normal(size=base_q.shape))
+        res = _decode_once(tkv, lay, queries, chans, G, cfg, True)
+        assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5, t
+        lay.append(torch.tensor(keys[:, n], dtype=torch.float16, device="cuda"),
+                   torch.tensor(values[:, n], dtype=torch.float16, device="cuda"))
+    hits, misses = lay.cache_counters()
+    assert hits > 0 and misses > 0
+
+
 def test_fused_sparse_decode_128k(tkv):
     """Config-2 head shape (131072 tokens, n_topk 2621, d_s 8) against the
     oracle for two heads."""

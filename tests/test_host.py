@@ -121,3 +121,37 @@ def test_head_sharded_allgather_gloo(batch, heads, G):
     for p in procs:
         p.join(timeout=60)
     assert all(err < 1e-5 for _, err in res), res
+
+
+def test_bench_configs_match_baseline():
+    """bench.py --config 2..5 carry BASELINE.json's shapes (SURVEY.md 8(d) fills the open
+    choices), and every config's units split over the GPU counts the metric names."""
+    import json
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    import bench
+    from paper_2505_19586_b200 import kv_model
+    from paper_2505_19586_b200.engine import shard_plan
+
+    base = json.loads((root / "BASELINE.json").read_text())
+    assert len(base["configs"]) == 5
+    expect = {2: (32, 8, 131072, 1, 2621), 3: (32, 8, 32768, 16, 983), 4: (28, 4, 131072, 4, 1311),
+              5: (80, 8, 131072, 1, 2621)}
+    for c, (L, h, n, B, topk) in expect.items():
+        args = type("A", (), {})()
+        cfg = bench.CONFIGS[c]
+        args.config, args.ctx, args.topk_frac = c, cfg["ctx"], cfg["topk"]
+        args.batch, args.bits, args.q_layers, args.model = cfg["batch"], cfg["bits"], cfg["q_layers"], cfg["model"]
+        args.gpus, args.keys_over_pcie = 1, False
+        m = getattr(kv_model, cfg["model"])
+        assert (m.num_layers, m.num_kv_heads, cfg["ctx"], cfg["batch"]) == (L, h, n, B)
+        w = bench.workload_config(args, round(cfg["topk"] * n))
+        assert w["n_topk"] == topk and w["layers"] == L and w["batch"] == B
+        assert w["workload"].startswith(f"config{c}:")
+        for world in (1, 2, 4, 8):
+            plan = shard_plan(B, h, world)
+            assert sum(p.batch * p.kv_heads for p in plan) == B * h
+    assert bench.metric_of(type("A", (), {"config": 2})()) == base["metric"]
