@@ -191,9 +191,15 @@ __global__ void __launch_bounds__(256) quant_decode_simt(QC c, const uint16_t *_
   }
 }
 
-int64_t quant_decode_workspace(const QC &c, int G) {
+// [split partials (m, l, acc) of the SIMT layout, which bounds the tensor-core kernels' | unit arrival
+// counters at quant_decode_arrive_offset | slack]
+int64_t quant_decode_arrive_offset(const QC &c, int G) {
   const int64_t chunks = (c.capacity + SIMT_CHUNK - 1) / SIMT_CHUNK;
-  return (int64_t)c.units * chunks * G * (2 + c.d) * (int64_t)sizeof(float) + (int64_t)c.units * 4 + 512;
+  return ((int64_t)c.units * chunks * G * (2 + c.d) * (int64_t)sizeof(float) + 255) / 256 * 256;
+}
+
+int64_t quant_decode_workspace(const QC &c, int G) {
+  return quant_decode_arrive_offset(c, G) + ((int64_t)c.units * 4 + 255) / 256 * 256 + 256;
 }
 
 int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *ws, cudaStream_t st);

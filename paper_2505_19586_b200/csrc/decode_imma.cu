@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(IM_WARPS * 32, 4) quant_decode_imma_kernel(QC 
 // The CTA's 16 warp partials are merged in shared memory; the splits are
 // merged by the combine kernel.
 // ---------------------------------------------------------------------------
-constexpr int QP_WARPS = 16;
+constexpr int QP_WARPS = 16;  // (20 warps at 96 registers spill and run 5 % slower)
 constexpr int QP_NS = 6;
 
 struct QpStage {
@@ -517,7 +517,8 @@ struct QpSmem {
 template <int BITS>
 __global__ void __launch_bounds__(QP_WARPS * 32, 1)
     quant_decode_pipe_kernel(QC c, const uint16_t *__restrict__ queries, int G, float *__restrict__ pm,
-                             float *__restrict__ pl, float *__restrict__ pacc, int splits) {
+                             float *__restrict__ pl, float *__restrict__ pacc, int splits,
+                             unsigned *__restrict__ arrive, float *__restrict__ out) {
   constexpr int CH = IM_CHUNK / BITS;  // tokens per chunk (16 KB of codes)
   constexpr int KT = 128 / BITS;       // key tile tokens
   constexpr int GPT = KT / IM_G;       // groups per key tile
@@ -872,6 +873,22 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
       pl[base] = L;
     }
   }
+  // ---- the last CTA of the unit (over splits x head blocks) merges the split partials
+  // in a fixed order (no separate combine launch) ----
+  __shared__ bool last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&arrive[u], 1u);
+    last = prev == gridDim.x * gridDim.z - 1;
+    if (last) arrive[u] = 0;  // re-armed for the next launch / graph replay
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const size_t b0 = (size_t)u * splits * G;
+  merge_partials(pm + b0, pl + b0, pacc + b0 * IM_D, G, IM_D, splits, out + (size_t)u * G * IM_D,
+                 reinterpret_cast<float *>(&S.st[0]) + QP_WARPS * 4 * IM_D);
 }
 
 static int sm_count() {
@@ -894,15 +911,18 @@ int quant_decode_pipe(const QC &c, const uint16_t *q, int G, float *out, void *w
   float *pl = pm + (size_t)c.units * splits * G;
   float *pacc = pl + (size_t)c.units * splits * G;
   const size_t sm = sizeof(QpSmem);
+  // per-unit arrival counters after the partials (quant_decode_workspace)
+  unsigned *arrive = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(ws) + quant_decode_arrive_offset(c, G));
   dim3 grid(splits, c.units, hblocks);
   if (c.bits == 1) {
     cudaFuncSetAttribute(quant_decode_pipe_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_prio(quant_decode_pipe_kernel<1>, grid, dim3(QP_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, splits);
+    launch_prio(quant_decode_pipe_kernel<1>, grid, dim3(QP_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, splits,
+                arrive, out);
   } else {
     cudaFuncSetAttribute(quant_decode_pipe_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_prio(quant_decode_pipe_kernel<2>, grid, dim3(QP_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, splits);
+    launch_prio(quant_decode_pipe_kernel<2>, grid, dim3(QP_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, splits,
+                arrive, out);
   }
-  launch_combine(pm, pl, pacc, c.units, splits, G, c.d, nullptr, 1, out, st);
   return check_launch("tkv_quant_decode(imma pipe)");
 }
 
@@ -920,10 +940,8 @@ int quant_decode_imma(const QC &c, const uint16_t *q, int G, float *out, void *w
   const bool fused = false;
   // arrival counters live at the fixed tail of the workspace (the SIMT kernel
   // uses more partial space, so both implementations can share one workspace)
-  const int64_t ws_bytes = quant_decode_workspace(c, G);
-  unsigned *arrive = fused ? reinterpret_cast<unsigned *>(reinterpret_cast<char *>(ws) + ws_bytes - 512 -
-                                                          (((int64_t)c.units * 4 + 15) & ~int64_t(15)))
-                           : nullptr;
+  unsigned *arrive =
+      fused ? reinterpret_cast<unsigned *>(reinterpret_cast<char *>(ws) + quant_decode_arrive_offset(c, G)) : nullptr;
   if (c.bits == 1) {
     cudaFuncSetAttribute(quant_decode_imma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_prio(quant_decode_imma_kernel<1>, grid, dim3(IM_WARPS * 32), sm, st, true, c, q, G, pm, pl, pacc, chunks, arrive, out);

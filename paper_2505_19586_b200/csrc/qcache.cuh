@@ -15,6 +15,7 @@ int qgemv_scores(const QC &c, int u, int64_t n, const float *q, float *logits, c
 int qgemv_output(const QC &c, int u, int64_t n, const float *w, float *out, cudaStream_t st);
 
 int64_t quant_decode_workspace(const QC &c, int G);
+int64_t quant_decode_arrive_offset(const QC &c, int G);
 int quant_decode(const QC &c, const uint16_t *q, int G, float *out, void *ws, int impl, cudaStream_t st);
 
 // Split-K partial combine shared by the quantized and sparse attention paths:

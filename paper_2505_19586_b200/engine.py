@@ -295,7 +295,11 @@ class DecodeEngine:
         q = sum(1 for x in self.labels if x == "q")
         s = len(self.labels) - q
         per_s = 2 if self.cfg.fused_sparse else 4  # stage 1 + (fused decode+append | select + gather/attend + append)
-        return q * 3 + s * per_s  # q: decode+combine+append
+        # q: decode + append; the SIMT and per-chunk tensor-core kernels add a combine launch (the pipelined
+        # tensor-core kernel merges its splits in its last CTA)
+        pipe = (self.cfg.quant_impl in (0, 2) and self.model.head_dim == 128 and self.cfg.group_size == 64
+                and self.cfg.bits in (1, 2) and self.G <= 16)
+        return q * (2 if pipe else 3) + s * per_s
 
     def _run_step(self) -> None:
         main = torch.cuda.current_stream(self.device)
@@ -315,9 +319,15 @@ class DecodeEngine:
                 t0 = self._mark(main)
                 lay.decode(self.queries[l], out=self.out[l], impl=self.cfg.quant_impl)
                 self._span("quant_decode", l, t0, main)
-                t0 = self._mark(main)
-                lay.append_token(self.new_keys[l], self.new_values[l])
-                self._span("quant_append", l, t0, main)
+                # attend, then append (pipeline.py:405-413): the append only has to land before
+                # this layer's next decode, so it runs on the side stream, off the layer chain
+                done = torch.cuda.Event()
+                done.record(main)
+                self.side.wait_event(done)
+                with torch.cuda.stream(self.side):
+                    t0 = self._mark(self.side)
+                    lay.append_token(self.new_keys[l], self.new_values[l])
+                    self._span("quant_append", l, t0, self.side)
             else:
                 st = self.sparse[l]
                 main.wait_event(st.s1_done)
