@@ -550,7 +550,10 @@ def main():
         "pcie": {"memcpy_h2d_gbs": memcpy_gbs, "uva_512B_rows_gbs": uva_gbs, "uva_256B_rows_gbs": uva256_gbs,
                  "gather_bytes_per_token": gather_bytes * n_sparse, "fetched_rows_per_layer": fetch_rows,
                  "reference_fetch_topk_bytes_per_token": O.gather_bytes(fetch_rows, model.head_dim) * n_sparse},
-        "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "DecodeEngine.step with pinned host inputs copied in and outputs read back every step; runs "
+                        "on the K steps after the device-resident ones, when the HBM row cache is warmer (its hit "
+                        "rate keeps rising over the first ~100 steps, DESIGN.md 4.5)"},
         "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",
                     "ms_per_token": ms_variant, "sparse_decode_ms": alt_ms,
                     "pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "pcie_bytes": alt_bytes,
