@@ -200,3 +200,41 @@ def test_package_trace_reader_errors(tmp_path):
     tampered.write_bytes(blob[:-2] + bytes([blob[-2] ^ 1, blob[-1]]))
     with pytest.raises(TraceFormatError):
         load_trace(tampered)
+
+
+def test_timeline_model_matches_reference_golden():
+    """paper_2505_19586_b200.timeline (the reference's decode-step timeline model, memsim.py:339-602)
+    reproduces the reference's schedule: every event start, total time, overlap and stall
+    (tests/golden/timeline.json, made by tests/golden/make_timeline_golden.py)."""
+    import json
+    from pathlib import Path
+
+    from paper_2505_19586_b200 import timeline as T
+
+    cases = json.loads((Path(__file__).parent / "golden" / "timeline.json").read_text())
+    for c in cases:
+        ev = T.build_timeline(c["labels"], T.LayerCosts(tuple(c["compute"]), c["estimate"], c["score"]),
+                              T.LinkModel(c["bandwidth"], c["latency"]), c["prefetch"], c["fetch"])
+        assert [e.label for e in ev] == c["labels_ev"]
+        r = T.simulate(ev)
+        assert np.allclose([e.start for e in ev], c["starts"], rtol=0, atol=1e-15)
+        assert r.total_seconds == pytest.approx(c["total"], abs=1e-15)
+        assert r.overlap_fraction == pytest.approx(c["overlap"], abs=1e-12)
+        assert r.stall_seconds == pytest.approx(c["stall"], abs=1e-15)
+        for k, v in c["per_layer"].items():
+            assert r.per_layer[int(k)] == pytest.approx(v, abs=1e-15)
+
+
+def test_timeline_measured_step_model():
+    """measured_step: the reference model has one compute engine, so its estimate passes serialise
+    with the layers (this engine runs them on a side stream: estimate 0 models that); PCIe bytes
+    on the link add their time to the chain they gate."""
+    from paper_2505_19586_b200 import timeline as T
+
+    labels = ["q", "q"] + ["s"] * 30
+    serial = T.measured_step(labels, 45e-6, 43e-6, 37e-6, 0, 50e9)
+    assert serial["step_seconds"] == pytest.approx(2 * 45e-6 + 30 * (43e-6 + 37e-6), rel=1e-9)
+    base = T.measured_step(labels, 45e-6, 43e-6, 0.0, 0, 50e9)
+    assert base["step_seconds"] == pytest.approx(2 * 45e-6 + 30 * 43e-6, rel=1e-9)
+    more = T.measured_step(labels, 45e-6, 43e-6, 0.0, 29_000, 50e9)
+    assert more["step_seconds"] == pytest.approx(base["step_seconds"] + 30 * 29_000 / 50e9, rel=1e-9)
