@@ -163,12 +163,15 @@ def run_reference(args, rank):
     q_sample = min(args.ctx, 16384)
     times = []
     import numpy as np
-    for i in range(args.warmup + args.steps):
+    # each sampled step is ~1-3 s of CPU work: at most 1 warm-up and 8 timed samples keep the arm
+    # within a few minutes for any --steps (the value is the median per-token time)
+    warm, reps = min(args.warmup, 1), max(1, min(args.steps, 8))
+    for i in range(warm + reps):
         ms, info = cpu_reference_ms(args, n_topk, q_sample, reps=1, warm=0)
-        if i >= args.warmup:
+        if i >= warm:
             times.append(ms)
     v = float(np.median(times))
-    sample = cpu_sample_text(args, q_sample, "per step: ")
+    sample = cpu_sample_text(args, q_sample, f"median of {reps} sampled steps; per step: ")
     line = {
         "impl": "reference", "metric": metric_of(args), "value": v, "unit": "ms/token", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
