@@ -17,6 +17,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtailorkv.so"
 SOURCES = ["abi.cu", "qcache.cu", "decode.cu", "decode_imma.cu", "sparse.cu", "sparse_fused.cu", "calibrate.cu", "fidelity.cu"]
+# extra objects: (source, object stem, defines) -- the fused sparse kernel again with 4-CTA clusters
+VARIANTS = [("sparse_fused.cu", "sparse_fused4", ["-DTKV_FZ_CTAS=4"])]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -48,12 +50,12 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 6) -> Path:
     objdir.mkdir(parents=True, exist_ok=True)
     procs = []
     objs = []
-    for src in SOURCES:
-        obj = objdir / (Path(src).stem + ".o")
+    for src, stem, defs in [(x, Path(x).stem, []) for x in SOURCES] + VARIANTS:
+        obj = objdir / (stem + ".o")
         objs.append(obj)
-        extra = os.environ.get("TKV_NVCC_DEFINES", "").split()  # experiments, e.g. -DTKV_FZ_CTAS=16
-        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c", str(CSRC / src),
-               "-o", str(obj)]
+        extra = os.environ.get("TKV_NVCC_DEFINES", "").split()  # experiments
+        cmd = [nvcc(), *NVCC_FLAGS, *defs, *extra, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c",
+               str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd))
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))

@@ -37,10 +37,16 @@
 
 namespace cg = cooperative_groups;
 
-namespace tkv {
-
 #ifndef TKV_FZ_CTAS
 #define TKV_FZ_CTAS 8
+#endif
+
+namespace tkv {
+// This file is compiled twice (build.py): 8-CTA clusters in namespace tkv, and 4-CTA
+// clusters in tkv::fz4 for many units at shorter contexts (batch decode: twice the
+// co-resident units per wave).
+#if TKV_FZ_CTAS != 8
+namespace fz4 {
 #endif
 constexpr int FZ_CTAS = TKV_FZ_CTAS;
 constexpr int FZ_THREADS = 512;
@@ -2157,6 +2163,17 @@ bool sparse_decode_supported(const SL &s, int G, int n_local) {
 int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
                         float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st) {
+#if TKV_FZ_CTAS == 8
+  // More units than 8-CTA clusters fit at once (15 on a B200) and a context that 4 CTAs
+  // cover: 4-CTA clusters run twice the units per wave.  TKV_FZ4=0/1 overrides.
+  {
+    static const int force = getenv("TKV_FZ4") ? atoi(getenv("TKV_FZ4")) : -1;
+    const bool fits4 = fz4::sparse_decode_supported(s, G, n_local);
+    if (fits4 && (force == 1 || (force < 0 && s.units > 15)))
+      return fz4::sparse_decode_fused(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
+                                      keys_from_device, out, new_keys, new_values, st);
+  }
+#endif
   cudaError_t e;
 #define TKV_FZ(D, GM)                                                                                          \
   e = launch_fused<true, D, GM>(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, \
@@ -2172,6 +2189,10 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
   return check_launch("tkv_sparse_decode");
 }
 
+#if TKV_FZ_CTAS != 8
+}  // namespace fz4
+}  // namespace tkv
+#else
 }  // namespace tkv
 
 extern "C" int tkv_debug_sparse_trace(int on) {
@@ -2228,3 +2249,4 @@ extern "C" int tkv_debug_sparse_attempts(double *out) {
 extern "C" int tkv_debug_sparse_phases(unsigned long long *out) {  // [8][32]
   return cudaMemcpyFromSymbol(out, tkv::g_fz_phase, sizeof(tkv::g_fz_phase)) == cudaSuccess ? 0 : 7;  // [8][40]
 }
+#endif  // TKV_FZ_CTAS == 8 (debug exports)

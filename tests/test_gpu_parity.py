@@ -495,6 +495,30 @@ def test_fused_sparse_decode_row_cache_staging_rounds(tkv, G):
     assert hits > 0 and misses > 0
 
 
+def test_fused_sparse_decode_many_units_4cta_clusters(tkv):
+    """More units than 8-CTA clusters fit at once (16 > 15) at a context 4 CTAs cover: the
+    decode takes the 4-CTA cluster build of the kernel (sparse_fused.cu, TKV_FZ_CTAS=4) and
+    matches the oracle across steps with the row cache on."""
+    rng = np.random.default_rng(37)
+    units, n0, d, G, T = 16, 6000, 128, 4, 3
+    keys = cases.f16(rng.normal(size=(units, n0 + T, d)))
+    values = cases.f16(rng.normal(size=(units, n0 + T, d)))
+    cfg = tkv.RetrievalConfig(24, 300, 8)
+    lay = _sparse_layer(tkv, keys[:, :n0], values[:, :n0], cfg.n_local, steps=T, keys_on_device=True,
+                        cache_rows=cfg.n_local + cfg.n_topk, cache_window=2)
+    chans = np.stack([np.sort(rng.choice(d, 8, replace=False)) for _ in range(units)]).astype(np.int32)
+    base_q = rng.normal(size=(units * G, d))
+    for t in range(T):
+        n = n0 + t
+        queries = cases.f16(base_q + 0.2 * rng.normal(size=base_q.shape))
+        res = _decode_once(tkv, lay, queries, chans, G, cfg, True)
+        assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5, t
+        lay.append(torch.tensor(keys[:, n], dtype=torch.float16, device="cuda"),
+                   torch.tensor(values[:, n], dtype=torch.float16, device="cuda"))
+    hits, misses = lay.cache_counters()
+    assert hits > 0 and misses > 0
+
+
 def test_fused_sparse_decode_128k(tkv):
     """Config-2 head shape (131072 tokens, n_topk 2621, d_s 8) against the
     oracle for two heads."""
