@@ -557,8 +557,8 @@ def main():
         "config": workload_config(args, n_topk),
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
                      "frac": dom["frac"], "traffic": _traffic("sparse_fused_kernel") if not args.unfused else None,
-                     "traffic_note": "DRAM bytes per launch (ncu capture, profiles/r1_ncu_traffic.json); below the "
-                                     "algorithmic bytes because stage 1 prefetches the scorer columns into L2",
+                     "traffic_note": "DRAM bytes per launch (ncu --set full capture of a main-mode launch, "
+                                     "profiles/r1_ncu_traffic.json): 28.2 MB against 27.9 MB algorithmic",
                      "bound_note": "the launch is a chain of dependent phases (score, cluster select, gather, "
                                    "attention, merge; profiles/r1_kernels.md 2), so it runs well under the HBM "
                                    "roofline; the PCIe leg is rooflines.sparse_decode.pcie_*",
