@@ -7,10 +7,10 @@ __global__ void __launch_bounds__(512, 1) dummy() {
   sm[threadIdx.x] = 0;
 }
 int main() {
-  for (int smem : {199264, 225888, 110000}) {
+  for (int smem : {199264, 225888, 227424, 110000}) {
     cudaFuncSetAttribute(dummy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(dummy, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int cs : {8, 16}) {
+    for (int cs : {4, 6, 7, 8, 16}) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs, 8);
       cfg.blockDim = dim3(512);
