@@ -7,7 +7,9 @@
 #include <unistd.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "qcache.cuh"
@@ -28,6 +30,25 @@ int check_launch(const char *what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(TKV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return TKV_OK;
+}
+
+// Programmatic dependent launch guard.  The fused sparse kernel reads its
+// layer's token count and starts its scorer loads before griddepcontrol.wait,
+// and triggers its dependents before its own append.  That is only safe when
+// the kernel ahead of it in the stream is NOT a launch on the same layer: for
+// any other predecessor P, P itself passed its wait only after everything
+// before it completed, so the layer's last writer has finished.  Every launch
+// that touches a sparse layer notes (stream, layer) here; a fused launch whose
+// stream's previous note is the same layer goes without the PDL attribute.
+static std::mutex g_pdl_mu;
+static std::unordered_map<cudaStream_t, const void *> g_pdl_last;
+
+bool pdl_note(cudaStream_t st, const void *layer) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  const void *&last = g_pdl_last[st];
+  const bool ok = last != layer;
+  last = layer;
+  return ok;
 }
 
 static int validate_qcache(const tkv_qcache *c) {
@@ -159,11 +180,13 @@ int tkv_sparse_prefill(const tkv_sparse_layer *s, const uint16_t *keys, const ui
   TKV_REQUIRE(n >= 1, TKV_ERR_EMPTY_CACHE, "cannot offload an empty cache");
   TKV_REQUIRE(n <= s->capacity, TKV_ERR_SHAPE, "sequence longer than the layer capacity");
   TKV_REQUIRE(s->local_offset >= 0 && s->local_offset <= n, TKV_ERR_PARAMETER, "bad local offset");
+  pdl_note(as_stream(stream), s->len);
   return sparse_prefill(*s, keys, values, n, as_stream(stream));
 }
 
 int tkv_sparse_append(const tkv_sparse_layer *s, const uint16_t *nk, const uint16_t *nv, void *stream) {
   if (int r = validate_sparse(s)) return r;
+  pdl_note(as_stream(stream), s->len);
   return sparse_append(*s, nk, nv, as_stream(stream));
 }
 
@@ -231,6 +254,7 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
     return sparse_decode_fused(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                                keys_from_device, out, new_keys, new_values, as_stream(stream));
   // shapes outside the fused kernel: select, then gather + attention, then the append (three launches)
+  pdl_note(as_stream(stream), s->len);
   char *ws = static_cast<char *>(workspace);
   const int64_t sel_ws = (select_workspace(s->units, s->capacity) + 255) / 256 * 256;
   if (int r = select_tokens(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, nullptr,
@@ -268,6 +292,7 @@ int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int
                          const int32_t *sel_count, int32_t n_local, int32_t max_rows, int32_t keys_from_device,
                          float *out, void *workspace, void *stream) {
   if (int r = validate_sparse(s)) return r;
+  pdl_note(as_stream(stream), s->len);
   return sparse_attention(*s, queries, G, sel_idx, sel_count, n_local, max_rows, keys_from_device, out, workspace,
                           as_stream(stream));
 }

@@ -2,6 +2,9 @@
 #include "qcache.cuh"
 
 namespace tkv {
+// records a launch on `layer` (its len pointer) in `st`; false when the
+// stream's previous sparse-layer launch was on the same layer (no PDL then)
+bool pdl_note(cudaStream_t st, const void *layer);
 int sparse_prefill(const SL &s, const uint16_t *keys, const uint16_t *values, int64_t n, cudaStream_t st);
 int sparse_append(const SL &s, const uint16_t *nk, const uint16_t *nv, cudaStream_t st);
 int64_t stage1_workspace(int B, int hq, int H, int d);

@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       for (int j = 0; j < G; ++j) q += h2d(queries[((size_t)u * G + j) * s.d + ch]);  // group sum (retriever.py:189)
       qsum[i] = q;
       qsum32[i] = (float)q;
-      // |fp32 score - float64 score| <= 2^-20 * sum_i max|K_i| |q_i| (<= 9 roundings of 2^-24 each)
+      // |fp32 score - float64 score| <= (d_s + 2) 2^-24 sum_i max|K_i| |q_i| (see band_eps)
       eps_term[i] = (double)s.chmax[(size_t)u * s.d + ch] * fabs(q);
     }
     __syncthreads();
@@ -663,7 +663,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     if (tid == 0) {
       double e = 0.0;
       for (int i = 0; i < d_s; ++i) e += eps_term[i];
-      band_eps = e * 9.5367431640625e-07;  // 2^-20
+      // a d_s-term fmaf chain plus the fp32 rounding of the query: <= (d_s + 1) roundings of
+      // 2^-24 relative to sum_i max|K_i| |q_i|; (d_s + 2) leaves margin, 16 keeps the tuned band
+      band_eps = e * fmax(16.0, (double)d_s + 2.0) * 5.9604644775390625e-08;  // x 2^-24
     }
     FZ_MARK(3);
     uint32_t glo, ghi;
@@ -2135,7 +2137,9 @@ static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, con
   at[1].id = cudaLaunchAttributePriority;
   at[1].val.priority = launch_priority(true);
   at[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol in the kernel)
-  at[2].val.programmaticStreamSerializationAllowed = getenv("TKV_NO_PDL") ? 0 : 1;
+  static const bool no_pdl = getenv("TKV_NO_PDL") != nullptr;
+  // the pre-wait prologue reads this layer's length: never overlap a launch on the same layer
+  at[2].val.programmaticStreamSerializationAllowed = (pdl_note(st, s.len) && !no_pdl) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 3;
   return cudaLaunchKernelEx(&cfg, kern, s, queries, G, channels, d_s, n_local, n_topk, sel_idx, n_local + n_topk,

@@ -100,6 +100,21 @@ def assemble(gathered: list[torch.Tensor], plan: list[ShardSlice], batch: int, n
     return out
 
 
+def slice_step_input(x, shard: ShardSlice, batch: int, num_kv_heads: int, heads_per_unit: int, world: int):
+    """A rank's part of one step input [L, B, ...].  Full inputs are
+    recognised per dimension: the batch slice applies when dim 1 holds the
+    whole batch, the head slice when dim 2 holds every head
+    (``heads_per_unit`` heads per KV head; 0 = no head dimension), so an
+    already-sharded [L, 1, h_r, d] input of a head-split batch-1 rank is
+    left alone."""
+    if world > 1:
+        if x.shape[1] == batch:
+            x = x[:, shard.b0:shard.b0 + shard.batch]
+        if heads_per_unit and x.dim() > 2 and x.shape[2] == num_kv_heads * heads_per_unit:
+            x = x[:, :, shard.k0 * heads_per_unit:(shard.k0 + shard.kv_heads) * heads_per_unit]
+    return x
+
+
 def _label(x) -> str:
     v = x.value if isinstance(x, LayerKind) else str(x)
     if v in ("q", LayerKind.QUANTIZATION_FRIENDLY.value):
@@ -157,6 +172,11 @@ class DecodeEngine:
         self.rank, self.world = rank, world_size
         self.group = process_group
         self.plan = shard_plan(batch, model.num_kv_heads, world_size)
+        self._host_collective = False
+        if world_size > 1:
+            import torch.distributed as dist
+
+            self._host_collective = dist.get_backend(process_group) != "nccl"
         self.shard = self.plan[rank]
         self.G = model.queries_per_kv_head
         self.units = self.shard.batch * self.shard.kv_heads
@@ -184,7 +204,7 @@ class DecodeEngine:
         self.fetch_count = torch.zeros(U, dtype=torch.int32, device=dev)
         lib = _lib.load()
         self.attn_ws = torch.zeros(int(lib.tkv_sparse_attn_workspace(U, self.G, d, kmax)), dtype=torch.uint8, device=dev)
-        self.sel_ws = None
+        self.sel_ws = self.dec_ws = None
         self.graph = None
         self.steps_done = 0
         self.record_selection = False
@@ -238,27 +258,23 @@ class DecodeEngine:
             chans = torch.zeros((self.units, self.retrieval.d_s), dtype=torch.int32, device=self.device)
             self.sparse[layer] = _SparseState(lay, w, chans, ws)
             self.layers[layer] = lay
-            if self.sel_ws is None:
-                self.sel_ws = torch.zeros(int(lib.tkv_select_workspace(self.units, lay.capacity)), dtype=torch.uint8,
-                                          device=self.device)
-                kmax = self.retrieval.n_local + self.retrieval.n_topk
-                self.dec_ws = torch.zeros(int(lib.tkv_sparse_decode_workspace(self.units, lay.capacity, self.G, self.d,
-                                                                              kmax)),
-                                          dtype=torch.uint8, device=self.device)
+            # workspaces follow the largest layer capacity seen so far (prefill lengths may differ per layer)
+            kmax = self.retrieval.n_local + self.retrieval.n_topk
+            need_sel = int(lib.tkv_select_workspace(self.units, lay.capacity))
+            need_dec = int(lib.tkv_sparse_decode_workspace(self.units, lay.capacity, self.G, self.d, kmax))
+            if self.sel_ws is None or self.sel_ws.numel() < need_sel:
+                self.sel_ws = torch.zeros(need_sel, dtype=torch.uint8, device=self.device)
+            if self.dec_ws is None or self.dec_ws.numel() < need_dec:
+                self.dec_ws = torch.zeros(need_dec, dtype=torch.uint8, device=self.device)
+        self.graph = self.prof_graph = None  # a captured step holds the old buffers: capture again
 
     # -- one step --------------------------------------------------------------
     def load_step(self, hidden, queries, new_keys, new_values, non_blocking: bool = True) -> None:
         """Copy one step's inputs into the static buffers.  Shapes (full or
         rank slice): hidden [L, B, hidden], queries [L, B, hq, d],
         new_keys/new_values [L, B, h, d]."""
-        s = self.shard
-
         def sl(x, heads_per_unit):
-            if x.shape[1] == self.batch and self.world > 1:
-                x = x[:, s.b0:s.b0 + s.batch]
-                if heads_per_unit:
-                    x = x[:, :, s.k0 * heads_per_unit:(s.k0 + s.kv_heads) * heads_per_unit]
-            return x
+            return slice_step_input(x, self.shard, self.batch, self.model.num_kv_heads, heads_per_unit, self.world)
 
         self.hidden.copy_(sl(hidden, 0).reshape(self.hidden.shape), non_blocking=non_blocking)
         self.queries.copy_(sl(queries, self.G).reshape(self.queries.shape), non_blocking=non_blocking)
@@ -354,8 +370,24 @@ class DecodeEngine:
                     lay.append(self.new_keys[l], self.new_values[l])
                     self._span("sparse_append", l, t0, main)
             if self.world > 1:
-                torch.distributed.all_gather_into_tensor(self.gathered[l], self.out[l], group=self.group)
+                self._all_gather(l)
         main.wait_stream(self.side)
+
+    def _all_gather(self, l: int) -> None:
+        """The layer's one exchange: head outputs of every rank.
+        NCCL gathers device buffers in stream order (capturable); a host
+        backend (gloo: the multi-process tests that share one GPU) stages
+        through host memory and cannot be captured."""
+        import torch.distributed as dist
+
+        if not self._host_collective:
+            dist.all_gather_into_tensor(self.gathered[l], self.out[l], group=self.group)
+            return
+        if torch.cuda.is_current_stream_capturing():
+            raise ConfigError("a host-staged (gloo) all-gather cannot be captured in a CUDA graph")
+        parts = [torch.empty(self.out[l].shape, dtype=self.out[l].dtype) for _ in range(self.world)]
+        dist.all_gather(parts, self.out[l].cpu(), group=self.group)
+        self.gathered[l].copy_(torch.stack(parts))
 
     def step(self, hidden=None, queries=None, new_keys=None, new_values=None) -> torch.Tensor:
         """Run one decode step; returns this rank's outputs [L, units*G, d]
@@ -393,6 +425,8 @@ class DecodeEngine:
         """Capture one decode step in a CUDA graph; ``step`` then replays it.
         Capturing executes nothing, so the caches do not advance; the host
         mirrors of the token counts are restored afterwards."""
+        if self._host_collective:
+            raise ConfigError("capture needs the nccl backend (the gloo all-gather is host-staged)")
         saved = [lay.n for lay in self.layers]
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph(keep_graph=True)

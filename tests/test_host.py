@@ -155,3 +155,22 @@ def test_bench_configs_match_baseline():
             plan = shard_plan(B, h, world)
             assert sum(p.batch * p.kv_heads for p in plan) == B * h
     assert bench.metric_of(type("A", (), {"config": 2})()) == base["metric"]
+
+
+@pytest.mark.parametrize("batch,heads,world", [(1, 8, 8), (1, 8, 2), (16, 8, 8), (4, 4, 8), (2, 4, 2)])
+def test_step_inputs_full_or_presharded(batch, heads, world):
+    """DecodeEngine.load_step accepts full inputs or the rank's slice; a
+    pre-sharded batch-1 input is not sliced a second time."""
+    from paper_2505_19586_b200.engine import shard_plan, slice_step_input
+
+    L, G, d = 3, 4, 8
+    q = torch.arange(L * batch * heads * G * d, dtype=torch.float32).view(L, batch, heads * G, d)
+    kv = torch.arange(L * batch * heads * d, dtype=torch.float32).view(L, batch, heads, d)
+    for s in shard_plan(batch, heads, world):
+        want_q = q[:, s.b0:s.b0 + s.batch, s.k0 * G:(s.k0 + s.kv_heads) * G]
+        want_kv = kv[:, s.b0:s.b0 + s.batch, s.k0:s.k0 + s.kv_heads]
+        assert torch.equal(slice_step_input(q, s, batch, heads, G, world), want_q)
+        assert torch.equal(slice_step_input(kv, s, batch, heads, 1, world), want_kv)
+        # already the rank's slice: unchanged
+        assert torch.equal(slice_step_input(want_q, s, batch, heads, G, world), want_q)
+        assert torch.equal(slice_step_input(want_kv, s, batch, heads, 1, world), want_kv)
