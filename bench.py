@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--keys-over-pcie", action="store_true",
                     help="headline with K and V rows both gathered over PCIe (the reference's fetch_topk transfer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--single-copy-keys", action="store_true",
+                    help="no token-major HBM key copy: key rows are gathered from the scorer's channel-major copy")
     ap.add_argument("--unfused", action="store_true", help="sparse layers as two launches (select, gather+attend)")
     ap.add_argument("--phases", action="store_true", help="print the fused sparse kernel's phase marks (unit 0)")
     ap.add_argument("--no-fidelity", action="store_true", help="skip the one-step recall/cosine evaluation")
@@ -82,108 +84,155 @@ def metric_of(args):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port of hybridkv) -- bounded sample of a config
+# CPU reference (oracle port of hybridkv) on the host cores
 # ---------------------------------------------------------------------------
-def cpu_reference_ms(args, n_topk: int, q_sample: int, reps: int = 1, warm: int = 0) -> tuple[float, dict]:
-    """Per-token time of the reference algorithm on host cores: n_Q x quantized
-    layer (measured at ``q_sample`` tokens, scaled linearly -- its cost is
-    O(n)) + n_S x sparsity-friendly layer measured at the full context, times
-    the batch (the reference has no batch dimension: B independent replays)."""
-    import numpy as np
+class CpuReference:
+    """The reference algorithm (oracle port of hybridkv, numpy float64) at the
+    config's full shapes on host cores: one quantization-friendly layer
+    (quantize_layer_kv + per-step qgemv decode + append_token) and one
+    sparsity-friendly layer (stage 1, critical-key prefetch, approx scores,
+    top-k, fetch_topk, sparse attention, append) at the full context.  A
+    decode step runs the model's layer sequence over these two layers'
+    caches (n_Q quantized + n_S Top-K layers; every layer costs the same
+    as its kind's representative, the contents do not change the work);
+    B sequences are B independent replays (the reference has no batch
+    dimension)."""
 
-    from oracle import tailorkv_oracle as O
+    def __init__(self, args, n_topk: int):
+        import numpy as np
 
-    model = model_of(args)
-    ctx, bits = args.ctx, args.bits
-    rng = np.random.default_rng(1)
-    h, hq, d, H = model.num_kv_heads, model.num_query_heads, model.head_dim, model.hidden_dim
-    G = hq // h
-    n_q = len(args.q_layers)
-    n_s = model.num_layers - n_q
-    f16 = lambda x: x.astype(np.float16).astype(np.float64)  # noqa: E731
-    kq = f16(rng.normal(0, 0.05, size=(h, q_sample, d)))
-    vq = f16(rng.normal(size=(h, q_sample, d)))
-    qk, qv = O.quantize_layer(kq, vq, bits, 64)
-    qs = f16(rng.normal(size=(hq, d)))
-    ks = f16(rng.normal(0, 1 / math.sqrt(d), size=(h, ctx, d)))
-    vs = f16(rng.normal(size=(h, ctx, d)))
-    w_q = f16(rng.normal(0, 1 / math.sqrt(H), size=(hq, H, d)))
-    hid = f16(rng.normal(size=H))
-    chmax = np.abs(ks).max(axis=1)
+        from oracle import tailorkv_oracle as O
 
-    def q_layer():
-        O.quant_layer_decode(qs, qk, qv)
-        for u in range(h):  # append_token
-            qk[u].append(kq[u, -1]); qv[u].append(vq[u, -1])
+        self.O, self.np = O, np
+        model = model_of(args)
+        self.args, self.n_topk = args, n_topk
+        ctx, bits = args.ctx, args.bits
+        rng = np.random.default_rng(1)
+        h, hq, d, H = model.num_kv_heads, model.num_query_heads, model.head_dim, model.hidden_dim
+        self.h, self.G, self.ctx = h, hq // h, ctx
+        self.n_q = len(args.q_layers)
+        self.n_s = model.num_layers - self.n_q
 
-    def s_layer():
-        qhat = O.estimate_query(w_q, hid)
-        local_start = ctx - 64
-        for u in range(h):
-            ch = O.select_channels(O.group_channel_scores(qhat[u * G:(u + 1) * G], chmax[u]), 8)
-            crit = ks[u][:, ch].copy()                  # prefetch of critical key columns
-            sc = O.approx_scores(qs[u * G:(u + 1) * G][:, ch], crit)
-            sel = O.select_tokens(sc, 64, n_topk)
+        def f16n(shape, std=1.0):
+            return (rng.standard_normal(size=shape, dtype=np.float32) * std).astype(np.float16).astype(np.float64)
+
+        kq, vq = f16n((h, ctx, d), 0.05), f16n((h, ctx, d))
+        self.new_q = (kq[:, -1].copy(), vq[:, -1].copy())
+        self.qk, self.qv = O.quantize_layer(kq, vq, bits, 64)
+        del kq, vq
+        self.qs = f16n((hq, d))
+        self.ks = f16n((h, ctx, d), 1 / math.sqrt(d))
+        self.vs = f16n((h, ctx, d))
+        self.w_q = f16n((hq, H, d), 1 / math.sqrt(H))
+        self.hid = f16n((H,))
+        self.chmax = np.abs(self.ks).max(axis=1)
+
+    def q_layer(self):
+        O = self.O
+        O.quant_layer_decode(self.qs, self.qk, self.qv)
+        for u in range(self.h):  # append_token (quantizer.py:445-451)
+            self.qk[u].append(self.new_q[0][u])
+            self.qv[u].append(self.new_q[1][u])
+
+    def s_layer(self):
+        O, np, G, ks, vs = self.O, self.np, self.G, self.ks, self.vs
+        qhat = O.estimate_query(self.w_q, self.hid)
+        local_start = self.ctx - 64
+        for u in range(self.h):
+            ch = O.select_channels(O.group_channel_scores(qhat[u * G:(u + 1) * G], self.chmax[u]), 8)
+            crit = ks[u][:, ch].copy()                  # prefetch_critical_keys (memsim.py:205-225)
+            sc = O.approx_scores(self.qs[u * G:(u + 1) * G][:, ch], crit)
+            sel = O.select_tokens(sc, 64, self.n_topk)
             far = sel[sel < local_start]
-            kf, vf = ks[u][far].copy(), vs[u][far].copy()  # fetch_topk
+            kf, vf = ks[u][far].copy(), vs[u][far].copy()  # fetch_topk (memsim.py:228-252)
             ksel = np.concatenate([kf, ks[u][sel[sel >= local_start]]])
             vsel = np.concatenate([vf, vs[u][sel[sel >= local_start]]])
             for j in range(G):
-                O.attention_weights(qs[u * G + j], ksel) @ vsel
+                O.attention_weights(self.qs[u * G + j], ksel) @ vsel
 
-    tq, ts = [], []
-    for i in range(warm + reps):
-        t0 = time.perf_counter(); q_layer(); t1 = time.perf_counter(); s_layer(); t2 = time.perf_counter()
-        if i >= warm:
-            tq.append(t1 - t0); ts.append(t2 - t1)
-    TQ = float(np.median(tq)) * ctx / q_sample
-    TS = float(np.median(ts))
-    ms = (n_q * TQ + n_s * TS) * args.batch * 1e3
+    def layer_times(self) -> tuple[float, float]:
+        """Seconds of one quantized and one Top-K layer (one sample each)."""
+        t0 = time.perf_counter()
+        self.q_layer()
+        t1 = time.perf_counter()
+        self.s_layer()
+        t2 = time.perf_counter()
+        return t1 - t0, t2 - t1
+
+    def step(self) -> float:
+        """One full decode step of one sequence (all layers), seconds."""
+        t0 = time.perf_counter()
+        for _ in range(self.n_q):
+            self.q_layer()
+        for _ in range(self.n_s):
+            self.s_layer()
+        return time.perf_counter() - t0
+
+
+def cpu_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
-        threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+        return max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
     except Exception:
-        threads = os.cpu_count() or 1
-    info = {"q_layer_ms_at_ctx": TQ * 1e3, "s_layer_ms": TS * 1e3, "threads": threads}
-    return ms, info
+        return os.cpu_count() or 1
 
 
-def cpu_sample_text(args, q_sample, prefix=""):
+def cpu_reference_ms(args, n_topk: int) -> tuple[float, dict]:
+    """Bounded in-run CPU baseline: one sample of each layer kind at the full
+    context, combined as n_Q T_Q + n_S T_S per token (times B)."""
+    ref = CpuReference(args, n_topk)
+    tq, ts = ref.layer_times()
+    ms = (ref.n_q * tq + ref.n_s * ts) * args.batch * 1e3
+    return ms, {"q_layer_ms": tq * 1e3, "s_layer_ms": ts * 1e3, "threads": cpu_threads()}
+
+
+def cpu_sample_text(args, prefix=""):
     model = model_of(args)
     n_q = len(args.q_layers)
-    return (f"{prefix}1 quantized layer at {q_sample} tokens scaled x{args.ctx / q_sample:g} (O(n)) + 1 Top-K layer at "
-            f"{args.ctx} tokens; token = {n_q} Q + {model.num_layers - n_q} S layers"
-            + (f", x{args.batch} sequences" if args.batch > 1 else "") + "; oracle port of hybridkv (numpy)")
+    return (f"{prefix}1 quantized layer + 1 Top-K layer, both at the full {args.ctx}-token context, timed once; "
+            f"token = {n_q} Q + {model.num_layers - n_q} S layers"
+            + (f", x{args.batch} sequences (independent replays)" if args.batch > 1 else "")
+            + "; oracle port of hybridkv (numpy float64)")
 
 
 def run_reference(args, rank):
+    """--impl reference: full decode steps of the reference algorithm on the
+    host cores (rank 0 only).  Each timed step runs every layer of the model
+    for one sequence (B sequences = B x that time); at most 1 warm-up and 2
+    timed steps whatever --steps/--warmup ask (a step is ~15 s of CPU work at
+    128k), and the line reports the counts actually run."""
     if rank != 0:
         return
-    n_topk = round(args.topk_frac * args.ctx)
-    q_sample = min(args.ctx, 16384)
-    times = []
     import numpy as np
-    # each sampled step is ~1-3 s of CPU work: at most 1 warm-up and 8 timed samples keep the arm
-    # within a few minutes for any --steps (the value is the median per-token time)
-    warm, reps = min(args.warmup, 1), max(1, min(args.steps, 8))
+
+    n_topk = round(args.topk_frac * args.ctx)
+    t_setup = time.perf_counter()
+    ref = CpuReference(args, n_topk)
+    setup_s = time.perf_counter() - t_setup
+    warm, reps = min(args.warmup, 1), max(1, min(args.steps, 2))
+    times = []
     for i in range(warm + reps):
-        ms, info = cpu_reference_ms(args, n_topk, q_sample, reps=1, warm=0)
+        t = ref.step()
         if i >= warm:
-            times.append(ms)
-    v = float(np.median(times))
-    sample = cpu_sample_text(args, q_sample, f"median of {reps} sampled steps; per step: ")
+            times.append(t * args.batch * 1e3)
+    v = float(np.mean(times))
+    sample = (f"{reps} timed full decode steps after {warm} warm-up (every layer of the model at the full context, "
+              f"one sequence" + (f", x{args.batch} for the batch of independent replays" if args.batch > 1 else "")
+              + "); oracle port of hybridkv (numpy float64)")
     line = {
         "impl": "reference", "metric": metric_of(args), "value": v, "unit": "ms/token", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+        "steps": reps, "warmup": warm, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": v, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, n_topk),
-        "cpu_baseline": {"value": v, "unit": "ms/token", "cores": info["threads"], "kind": "port", "sample": sample},
+        "config": workload_config(args, n_topk, args.gpus),
+        "cpu_baseline": {"value": v, "unit": "ms/token", "cores": cpu_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": setup_s,
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, n_topk):
+def workload_config(args, n_topk, world=1):
     m = model_of(args)
     c = CONFIGS[args.config]
     nq = len(args.q_layers)
@@ -195,7 +244,7 @@ def workload_config(args, n_topk):
         "ctx": args.ctx, "batch": args.batch, "layers": m.num_layers, "q_layers": list(args.q_layers),
         "bits": args.bits, "group_size": 64, "n_topk": n_topk, "n_local": 64, "d_s": 8,
         "kv_heads": m.num_kv_heads, "q_heads": m.num_query_heads, "head_dim": m.head_dim,
-        "parallelism": f"kv-head shard x{args.gpus}",
+        "parallelism": f"kv-head shard x{world}",
         "key_rows_from": "host (PCIe)" if args.keys_over_pcie else "hbm (scorer copy); value rows over PCIe",
         "l2": "inputs larger than L2 (every step reads > 1 GB of HBM)",
     }
@@ -303,8 +352,24 @@ def pcie_peaks(torch, lib_mod, device):
     return memcpy_gbs, uva_gbs, uva256_gbs
 
 
+def relaunch(args) -> int:
+    """``bench.py --gpus N`` run without a launcher: start N ranks with
+    torch.distributed.run on this node (127.0.0.1) and pass rank 0's line
+    through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -329,11 +394,12 @@ def main():
     n_topk = round(args.topk_frac * n)
     cfg = P.EngineConfig(bits=args.bits, group_size=64, n_local=64, n_topk=n_topk, critical_channels=8,
                          keys_from_hbm=not args.keys_over_pcie, fused_sparse=not args.unfused,
+                         token_major_keys=not args.single_copy_keys,
                          row_cache=args.cache_steps > 0, row_cache_steps=max(1, args.cache_steps),
                          scorer_l2_prefetch=not args.no_l2_prefetch, overlap_stage1=not args.serial_stage1)
     W, K = args.warmup, args.steps
     PROF = 2
-    total = W + 3 * K + 2 * PROF + 10
+    total = W + 3 * K + 2 * PROF + 2 * min(K, 20) + 20
     t_setup = time.time()
     wl = make_workload(L, args.q_layers, model.num_query_heads, model.num_kv_heads, model.head_dim, n, total,
                        batch=B, seed=args.seed, device=device)
@@ -396,6 +462,26 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # ---- end-to-end first (the HBM row cache is colder than in the device-resident loop after it):
+    # pinned host inputs in, outputs back to host, every step ----
+    host_in = [tuple(x.cpu().pin_memory() for x in inputs(step_i + k)) for k in range(K)]
+    host_out = torch.empty(eng.out.shape, dtype=torch.float32).pin_memory()
+    h2d = sum(x.numel() * x.element_size() for x in host_in[0])  # every rank receives the full step input
+    d2h = host_out.numel() * 4
+    barrier(); torch.cuda.synchronize()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ec0 = eng.cache_counters()
+    s2.record()
+    for k in range(K):
+        eng.step(*host_in[k]); step_i += 1
+        host_out.copy_(eng.out, non_blocking=True)
+    e2.record()
+    torch.cuda.synchronize(); barrier()
+    ms_e2e = s2.elapsed_time(e2) / K
+    ec1 = eng.cache_counters()
+    e2e_hit = (ec1[0] - ec0[0]) / max(1, (ec1[0] - ec0[0]) + (ec1[1] - ec0[1]))
+    del host_in
+
     # ---- device-resident timing (value) ----
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tc0 = eng.cache_counters()
@@ -410,22 +496,25 @@ def main():
     t_hits, t_misses = eng.cache_counters()
     t_hits, t_misses = t_hits - tc0[0], t_misses - tc0[1]
 
-    # ---- end-to-end: pinned host inputs in, outputs back to host, every step ----
-    host_in = [tuple(x.cpu().pin_memory() for x in inputs(step_i + k)) for k in range(K)]
-    host_out = torch.empty(eng.out.shape, dtype=torch.float32).pin_memory()
-    h2d = sum(x.numel() * x.element_size() for x in host_in[0])
-    if world > 1:
-        h2d = h2d  # every rank receives the full step input (replicated hidden state)
-    d2h = host_out.numel() * 4
-    barrier(); torch.cuda.synchronize()
-    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s2.record()
-    for k in range(K):
-        eng.step(*host_in[k]); step_i += 1
-        host_out.copy_(eng.out, non_blocking=True)
-    e2.record()
-    torch.cuda.synchronize(); barrier()
-    ms_e2e = s2.elapsed_time(e2) / K
+    # ---- sparse-layer period inside the timed graph (PDL kept): per-launch globaltimer stamps of the
+    # fused kernel (unit 0, CTA rank 0) over one more plain-graph step ----
+    lib = _lib.load()
+    trace_mode = int(os.environ.get("TKV_FZ_DBG", "0")) & ~1
+    lib.tkv_debug_sparse_launches(None, 1)
+    lib.tkv_debug_sparse_trace(1 | trace_mode)
+    eng.step(*inputs(step_i)); step_i += 1
+    torch.cuda.synchronize()
+    lib.tkv_debug_sparse_trace(trace_mode)
+    import ctypes as C
+    raw = (C.c_ulonglong * (128 * 3))()
+    cnt = lib.tkv_debug_sparse_launches(raw, 0)
+    stamps = [(raw[i * 3], raw[i * 3 + 1], raw[i * 3 + 2]) for i in range(min(cnt, 128))]
+    plain = None
+    if len(stamps) >= 2 and not args.unfused:
+        ends = [x[2] for x in stamps]
+        period = (ends[-1] - ends[0]) / (len(ends) - 1) / 1e6          # ms between consecutive layer ends
+        body = sorted((x[2] - x[1]) / 1e6 for x in stamps)[len(stamps) // 2]  # PDL wait -> end, median
+        plain = {"period_ms": period, "body_ms": body, "launches": len(stamps)}
 
     # fidelity of one eager step against exact attention over all tokens (GPU, outside the timing)
     fidelity = None
@@ -462,6 +551,48 @@ def main():
     cached_rows = hits / (PROF * n_sparse)     # per launch, served from the HBM row cache
     pcie_rows = misses / (PROF * n_sparse)     # per launch, fetched over PCIe
 
+    def timed(steps, src):
+        """Graph-replayed steps from ``src(k)`` inputs: (ms/token, hit rate, PCIe value rows per launch)."""
+        nonlocal step_i
+        eng.capture()
+        for k in range(2):
+            eng.step(*src(k)); step_i += 1
+        torch.cuda.synchronize()
+        c0 = eng.cache_counters()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for k in range(steps):
+            eng.step(*src(2 + k)); step_i += 1
+        b.record()
+        torch.cuda.synchronize()
+        c1 = eng.cache_counters()
+        hh, mm = c1[0] - c0[0], c1[1] - c0[1]
+        return a.elapsed_time(b) / steps, hh / max(1, hh + mm), mm / max(1, steps * n_sparse)
+
+    # ---- the same engine with the row cache off (every selected far value row over PCIe) ----
+    KX = min(K, 20)
+    cache_off = None
+    if cfg.row_cache and not args.keys_over_pcie:
+        eng.set_row_cache(False)
+        base = step_i
+        ms_off, _, _ = timed(KX, lambda k: inputs(base + k))
+        eng.set_row_cache(True)
+        cache_off = {"ms_per_token": ms_off, "steps": KX,
+                     "note": "row cache switched off on the same engine and inputs: every selected far value row "
+                             "crosses PCIe each step (key rows still from HBM)"}
+    # ---- drift workload: the reference's ChannelOutlierSpec(drift=True) step inputs (trace.py:434-436) ----
+    from paper_2505_19586_b200.synth import step_inputs
+    d_hid, d_q = step_inputs(wl, KX + 2, drift=True, seed=args.seed + 1)
+    base = step_i
+    ms_drift, hit_drift, pcie_drift = timed(KX, lambda k: (d_hid[k], d_q[k], wl.new_keys[base + k],
+                                                           wl.new_values[base + k]))
+    drift = {"ms_per_token": ms_drift, "steps": KX, "row_cache_hit_rate": hit_drift,
+             "pcie_value_rows_per_launch": pcie_drift,
+             "note": "same prefilled caches; step hidden states with the reference's per-step lognormal(0, 0.6) "
+                     "scaling of the planted outlier coordinates (synth.step_inputs, trace.py:268-275, 434-436), "
+                     "queries q = h W_q; the row cache carries over from the stationary steps"}
+    del d_hid, d_q
+
     if world > 1:
         t = torch.tensor([ms, ms_e2e], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -485,6 +616,11 @@ def main():
     else:
         sparse_ms = mean(prof.get("sparse_decode", []))
         alt_ms = mean(prof_alt.get("sparse_decode", []))
+    sparse_node_ms = sparse_ms
+    if plain is not None:
+        # the layer period inside the timed (plain) graph: consecutive sparse launches' end-to-end spacing,
+        # so n_S x period + the quantized layers fits in ms_per_step (event nodes break the PDL overlap)
+        sparse_ms = plain["period_ms"]
     append_ms = mean(prof.get("sparse_append", []))
     from oracle import tailorkv_oracle as O  # byte formulas only (memsim.py accounting)
     d = model.head_dim
@@ -507,7 +643,11 @@ def main():
                           "pcie_peak": memcpy_gbs,
                           "pcie_peak_source": "measured pinned cudaMemcpyAsync H2D 256 MiB, this run",
                           "kernel": "sparse_fused_kernel (scores + top-k + gather + attention)" if not args.unfused
-                          else "select + sparse_attn"},
+                          else "select + sparse_attn",
+                          "timing": ("layer period in the plain timed graph: (end of the last sparse launch - end of "
+                                     "the first) / (launches - 1), globaltimer stamps of unit 0's CTA rank 0"
+                                     if plain is not None else "graph event nodes"),
+                          "body_ms": plain["body_ms"] if plain else None, "graph_node_ms": sparse_node_ms},
         "quant_decode": {"bound": "hbm", "achieved": quant_bytes / (quant_ms * 1e-3) / 1e9, "peak": hbm_peak,
                          "unit": "GB/s", "ms": quant_ms, "bytes": quant_bytes, "peak_source": hbm_src},
         "stage1": {"bound": "hbm", "achieved": wq_bytes / (stage1_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -549,12 +689,27 @@ def main():
                 "model_reference_transfers_ms with the reference's per-step critical-key prefetch and K+V Top-K "
                 "fetch over the measured H2D bandwidth",
     }
+    # resident bytes against the reference's closed-form footprints (memsim.py:641-706)
+    res = eng.resident_bytes()
+    h_all = model.num_kv_heads * B
+    orig = 2 * L * n * h_all * d * 2
+    n_q = len(args.q_layers)
+    ref_hybrid = (2 * n_q * n * h_all * d * 2 * (args.bits / 16 + 2 / 64)      # hybridkv_q
+                  + n_sparse * 2 * n * h_all * 8 * 2                           # hybridkv_s (d_s = 8)
+                  + n_sparse * 64 * 2 * h_all * d * 2)                         # local windows
+    memory = {"resident": res,
+              "reference_original_bytes": orig, "reference_hybrid_device_bytes": int(ref_hybrid),
+              "reference_host_kv_bytes": n_sparse * 2 * n * h_all * d * 2,
+              "note": "hbm: this rank's device allocations by structure; the reference model keeps 2*n*h*d_s key "
+                      "columns per sparse layer on the device (hybridkv_s) and re-sends them every step, this "
+                      "engine keeps all keys resident (channel-major for the scorer, plus a token-major copy "
+                      "unless EngineConfig.token_major_keys=False) so nothing but missed value rows crosses PCIe"}
     line = {
         "metric": metric_of(args), "value": ms, "unit": "ms/token", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": f"fp16 storage / {args.bits}-bit codes, fp32 accumulate",
         "data": "synthetic (gen_trace-shaped, GPU-generated)",
-        "config": workload_config(args, n_topk),
+        "config": workload_config(args, n_topk, world),
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
                      "frac": dom["frac"], "traffic": _traffic("sparse_fused_kernel") if not args.unfused else None,
                      "traffic_note": "DRAM bytes per launch (ncu --set full capture of a main-mode launch, "
@@ -562,8 +717,7 @@ def main():
                      "bound_note": "the launch is a chain of dependent phases (score, cluster select, gather, "
                                    "attention, merge; profiles/r1_kernels.md 2), so it runs well under the HBM "
                                    "roofline; the PCIe leg is rooflines.sparse_decode.pcie_*",
-                     "kernel": dom["kernel"],
-                     "timing": "CUDA events recorded as graph nodes around the kernel inside the replayed step"},
+                     "kernel": dom["kernel"], "timing": dom["timing"]},
         "rooflines": rooflines,
         "row_cache": {"window_steps": cfg.row_cache_steps, "slots_per_head": (eng.retrieval.n_local + eng.retrieval.n_topk) * cfg.row_cache_steps,
                       "timed_region_hit_rate": t_hits / max(1, t_hits + t_misses),
@@ -574,9 +728,13 @@ def main():
                  "gather_bytes_per_token": gather_bytes * n_sparse, "fetched_rows_per_layer": fetch_rows,
                  "reference_fetch_topk_bytes_per_token": O.gather_bytes(fetch_rows, model.head_dim) * n_sparse},
         "e2e": {"value": ms_e2e, "unit": "ms/token", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "row_cache_hit_rate": e2e_hit,
                 "note": "DecodeEngine.step with pinned host inputs copied in and outputs read back every step; runs "
-                        "on the K steps after the device-resident ones, when the HBM row cache is warmer (its hit "
-                        "rate keeps rising over the first ~100 steps, DESIGN.md 4.5)"},
+                        "on the K steps right after the warm-up, BEFORE the device-resident ones, so its HBM row "
+                        "cache is the colder of the two (the hit rate rises over the first ~100 steps)"},
+        "cache_off": cache_off,
+        "drift": drift,
+        "memory": memory,
         "variant": {"key_rows_from": "hbm" if args.keys_over_pcie else "host (PCIe, the reference's fetch_topk transfer)",
                     "ms_per_token": ms_variant, "sparse_decode_ms": alt_ms,
                     "pcie_gbs": alt_bytes / (alt_ms * 1e-3) / 1e9, "pcie_bytes": alt_bytes,
@@ -585,12 +743,13 @@ def main():
         "timeline_model": timeline_model,
         "gpu_launches": eng.kernels_per_step() * K,
         "clocks": clocks.summary(),
+        "plain_graph_sparse_trace": plain,
         "setup_s": setup_s,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cms, info = cpu_reference_ms(args, n_topk, min(n, 16384))
+        cms, info = cpu_reference_ms(args, n_topk)
         line["cpu_baseline"] = {"value": cms, "unit": "ms/token", "cores": info["threads"], "kind": "port",
-                                "sample": cpu_sample_text(args, min(n, 16384)), "detail": info}
+                                "sample": cpu_sample_text(args), "detail": info}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

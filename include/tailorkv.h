@@ -174,7 +174,12 @@ int tkv_sparse_append(const tkv_sparse_layer *s, const uint16_t *new_keys, const
  * :138-148 + select_critical_channels :151-163, caller pipeline.py:271-286).
  * hidden fp16 [B][hidden]; w_q fp16 [hq][hidden][d] (this rank's q heads);
  * units = B * hq / G.  Writes q_hat f64 [B][hq][d] (may be NULL) and
- * channels int32 [units][d_s] sorted ascending. */
+ * channels int32 [units][d_s] sorted ascending.  The workspace must be zero
+ * before its first use and belong to one (B, hq, hidden, d) shape: its
+ * arrival counters re-arm themselves, so it can be reused (and replayed
+ * from a CUDA graph) without clearing.  B > 2 with d in {64, 128, 256}
+ * runs the tensor-core kernel (mma.sync, W_q read once per 16 sequences,
+ * cluster reduction); otherwise the SIMT kernel. */
 int64_t tkv_stage1_workspace(int32_t B, int32_t hq, int32_t hidden, int32_t d);
 /* Stage 1 that also starts moving the selected channel rows of `layer`'s
  * channel-major scorer keys into L2 (TMA prefetch), so the layer's decode

@@ -197,7 +197,7 @@ int64_t tkv_stage1_workspace(int32_t B, int32_t hq, int32_t hidden, int32_t d) {
 int tkv_stage1(const uint16_t *hidden, const uint16_t *w_q, int32_t B, int32_t hq, int32_t hidden_dim, int32_t d,
                int32_t G, const float *chmax, int32_t d_s, double *q_hat, int32_t *channels, void *workspace,
                void *stream) {
-  TKV_REQUIRE(B >= 1 && B <= 16, TKV_ERR_SHAPE, "batch must be in [1, 16] for stage 1");
+  TKV_REQUIRE(B >= 1 && B <= 1024, TKV_ERR_SHAPE, "batch must be in [1, 1024] for stage 1");
   TKV_REQUIRE(d >= 32 && d <= 256 && d % 32 == 0, TKV_ERR_SHAPE, "head_dim must be a multiple of 32 in [32,256]");
   TKV_REQUIRE(G >= 1 && hq % G == 0, TKV_ERR_SHAPE, "query heads not divisible by the group size");
   TKV_REQUIRE(d_s >= 1 && d_s <= d, TKV_ERR_PARAMETER, "d_s must lie in [1, head_dim]");
@@ -207,7 +207,7 @@ int tkv_stage1(const uint16_t *hidden, const uint16_t *w_q, int32_t B, int32_t h
 int tkv_stage1_prefetch(const uint16_t *hidden, const uint16_t *w_q, int32_t B, int32_t hq, int32_t hidden_dim,
                         int32_t d, int32_t G, const float *chmax, int32_t d_s, double *q_hat, int32_t *channels,
                         void *workspace, const tkv_sparse_layer *layer, void *stream) {
-  TKV_REQUIRE(B >= 1 && B <= 16, TKV_ERR_SHAPE, "batch must be in [1, 16] for stage 1");
+  TKV_REQUIRE(B >= 1 && B <= 1024, TKV_ERR_SHAPE, "batch must be in [1, 1024] for stage 1");
   TKV_REQUIRE(d >= 32 && d <= 256 && d % 32 == 0, TKV_ERR_SHAPE, "head_dim must be a multiple of 32 in [32,256]");
   TKV_REQUIRE(G >= 1 && hq % G == 0, TKV_ERR_SHAPE, "query heads not divisible by the group size");
   TKV_REQUIRE(d_s >= 1 && d_s <= d, TKV_ERR_PARAMETER, "d_s must lie in [1, head_dim]");

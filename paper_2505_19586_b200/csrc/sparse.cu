@@ -5,11 +5,14 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "qcache.cuh"
 #include "sparse.cuh"
 
 namespace tkv {
+namespace cg = cooperative_groups;
 
 // ===========================================================================
 // Prefill / append (memsim.py:88-93, 106-111; pipeline.py:183-193, 412-413)
@@ -183,6 +186,46 @@ __device__ void stage1_select_unit(const double *__restrict__ part, int splits, 
   __syncthreads();
 }
 
+// Arrival counter + channel selection (+ optional scorer-column L2 prefetch)
+// run by the last CTA to finish its partials of one KV head: sequences
+// [b0, b0+nb).  qs: G*D doubles of shared memory.
+template <int D>
+__device__ __forceinline__ void stage1_tail(const double *__restrict__ part, int splits, int B, int hq, int G,
+                                            const float *__restrict__ chmax, int d_s, double *__restrict__ q_hat,
+                                            int32_t *__restrict__ channels, unsigned *ctr, unsigned arrivals, int b0,
+                                            int nb, int kvh, const SL &pf, int prefetch, double *qs, double *score,
+                                            int *flags, bool *last) {
+  const int hkv = hq / G;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(ctr, 1u);
+    *last = prev == arrivals - 1;
+    if (*last) *ctr = 0;  // re-armed for the next launch / graph replay
+  }
+  __syncthreads();
+  if (!*last) return;
+  __threadfence();
+  for (int b = 0; b < nb; ++b) {
+    stage1_select_unit(part, splits, B, hq, D, G, chmax, d_s, q_hat, channels, b0 + b, kvh, qs, score, flags);
+    if (prefetch) {
+      // start moving the selected channel rows of the layer's scorer keys into L2: the
+      // layer's decode kernel (next on the main stream) then scores from L2, not HBM
+      const int u = (b0 + b) * hkv + kvh;
+      const int64_t len = *pf.len;
+      const int64_t bytes = len * 2;
+      const int64_t nch = (bytes + 32767) / 32768;
+      for (int64_t i = threadIdx.x; i < (int64_t)d_s * nch; i += blockDim.x) {
+        const int c = channels[(size_t)u * d_s + i / nch];
+        const int64_t o = (i % nch) * 32768;
+        const uint32_t sz = (uint32_t)min((int64_t)32768, bytes - o);
+        const char *src = reinterpret_cast<const char *>(pf.kt + ((size_t)u * D + c) * pf.capacity) + o;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((sz + 15u) & ~15u) : "memory");
+      }
+    }
+  }
+}
+
 // 16-byte read-only load kept where it is written (issued before the
 // barrier that follows, so all of a thread's W_q loads are in flight at once)
 __device__ __forceinline__ uint4 s1_ld_nc_v4(const void *p) {
@@ -275,38 +318,340 @@ __global__ void __launch_bounds__(S1_THREADS, 2) stage1_fused_kernel(const uint1
     __syncthreads();
   }
   // last arriving CTA of (sequence group, KV head) selects the channels
-  const int kvh = qh / G, hkv = hq / G;
-  unsigned *ctr = arrive + (size_t)bg * hkv + kvh;
+  const int kvh = qh / G;
+  __shared__ double score[256];
+  __shared__ int flags[256];
+  stage1_tail<D>(part, splits, B, hq, G, chmax, d_s, q_hat, channels, arrive + (size_t)bg * (hq / G) + kvh,
+                 (unsigned)(splits * G), b0, nb, kvh, pf, prefetch, reinterpret_cast<double *>(red), score, flags,
+                 &last);
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core stage 1 (head_dim a multiple of 64, up to 16 sequences per
+// launch): q_hat^T tile = h[16 x K] . W_q[K x 8] with mma.sync.m16n8k16
+// (f16 in, f32 accumulate), W_q read exactly once whatever the batch.
+// A warp owns one 64-channel block of one query head over a K sub-range.
+// B fragments come straight from 16-byte global loads: thread (g = lane/4,
+// q = lane%4) loads rows k+2q, k+2q+1, k+2q+8, k+2q+9 at channels
+// [8g, 8g+8) and pairs them with one byte-permute per register; MMA n-tile j
+// then holds channels {8g + j}, i.e. a column permutation undone when the
+// accumulators are stored.  Rows of h beyond B are zero registers, so B = 1
+// costs the same W traffic as B = 16 (the tensor core has ample slack).
+// fp32 accumulation over a warp's rows (<= 64 per batch), float64 across
+// warps and splits (same scheme as the SIMT kernel).
+// ---------------------------------------------------------------------------
+constexpr int S1M_THREADS = 256;
+
+__device__ __forceinline__ void mma_f16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                              uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t u4_word(const uint4 &v, int w) {
+  return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+}
+
+// Channel selection of one unit by one warp (retriever.py:111-163): group
+// score s_c = (sum_j |q_hat[j][c]|) * chmax_c in float64, top d_s with ties to
+// the lower index, written ascending.  sc: D doubles of this warp's shared
+// memory.  Optionally starts the L2 prefetch of the chosen scorer columns.
+template <int D>
+__device__ __forceinline__ void stage1_warp_select(const double *__restrict__ qg, int hq, int G, int b, int kvh,
+                                                   const float *__restrict__ chmax, int d_s,
+                                                   int32_t *__restrict__ channels, double *sc, const SL &pf,
+                                                   int prefetch, int b_off) {
+  constexpr int NI = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int hkv = hq / G;
+  const int u = b * hkv + kvh;
+  double s[NI];
+  float cm[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    s[i] = 0.0;
+    cm[i] = chmax[(size_t)u * D + lane + 32 * i];
+  }
+  // sum_j |q_hat_j| in ascending j (retriever.py:148); all loads of a group of 4 heads in flight at once
+  for (int j0 = 0; j0 < G; j0 += 4) {
+    double t[4][NI];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        t[jj][i] = j0 + jj < G ? __ldcg(&qg[((size_t)b * hq + kvh * G + j0 + jj) * D + lane + 32 * i]) : 0.0;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+      for (int i = 0; i < NI; ++i) s[i] += fabs(t[jj][i]);
+  }
+#pragma unroll
+  for (int i = 0; i < NI; ++i) s[i] *= (double)cm[i];  // >= 0
+  (void)sc;
+  // d_s rounds of a warp argmax (score desc, index asc: retriever.py:161), then the
+  // chosen set written ascending with ballots
+  unsigned taken = 0;  // bit i: channel lane + 32 i selected
+  for (int r = 0; r < d_s; ++r) {
+    double best = -1.0;
+    int bc = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int c = lane + 32 * i;
+      if (!((taken >> i) & 1u) && (s[i] > best || (s[i] == best && c < bc))) {
+        best = s[i];
+        bc = c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ob > best || (ob == best && oc < bc)) {
+        best = ob;
+        bc = oc;
+      }
+    }
+    if ((bc & 31) == lane) taken |= 1u << (bc >> 5);
+  }
+  int before = 0;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const bool sel = (taken >> i) & 1u;
+    const unsigned m = __ballot_sync(0xffffffffu, sel);
+    if (sel) channels[(size_t)u * d_s + before + __popc(m & lt)] = lane + 32 * i;
+    before += __popc(m);
+  }
+  __syncwarp();
+  if (prefetch) {
+    // start moving the selected channel rows of the layer's scorer keys into L2: the
+    // layer's decode kernel (next on the main stream) then scores from L2, not HBM
+    const int ug = (b_off + b) * hkv + kvh;  // unit index in the layer
+    const int64_t bytes = (int64_t)(*pf.len) * 2;
+    const int64_t nch = (bytes + 32767) / 32768;
+    __threadfence_block();
+    for (int64_t i = lane; i < (int64_t)d_s * nch; i += 32) {
+      const int c = channels[(size_t)u * d_s + i / nch];
+      const int64_t o = (i % nch) * 32768;
+      const uint32_t sz = (uint32_t)min((int64_t)32768, bytes - o);
+      const char *src = reinterpret_cast<const char *>(pf.kt + ((size_t)ug * D + c) * pf.capacity) + o;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((sz + 15u) & ~15u) : "memory");
+    }
+  }
+}
+
+// grid (CS, hq) with clusters of CS CTAs along the hidden dimension: the
+// cluster reduces its partials over distributed shared memory (fixed order,
+// float64), every CTA writes a slice of q_hat, and the last CTA of each KV
+// head selects the channels of all its sequences, one warp per sequence.
+__device__ int s1_dbg = 0;  // experiments (tools/prof_stage1.py): 1 stream only, 2 no selection, 3 time stamps
+__device__ unsigned long long s1_stamp[8];  // min start, max loop end, max cluster done, last: arrive, fence, select
+__device__ __forceinline__ unsigned long long s1_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int D>
+__global__ void __launch_bounds__(S1M_THREADS, 2) stage1_mma_kernel(const uint16_t *__restrict__ hidden,
+                                                                 const uint16_t *__restrict__ w_q, int B, int H,
+                                                                 int rows_per_cta, double *__restrict__ qg,
+                                                                 unsigned *__restrict__ arrive, int G,
+                                                                 const float *__restrict__ chmax, int d_s,
+                                                                 double *__restrict__ q_hat,
+                                                                 int32_t *__restrict__ channels, SL pf, int prefetch,
+                                                                 int b_off) {
+  constexpr int NCB = D / 64;                    // 64-channel blocks
+  constexpr int NKS = (S1M_THREADS / 32) / NCB;  // K sub-ranges per CTA
+  extern __shared__ __align__(16) unsigned char s1m_smem[];
+  __shared__ bool last;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int qh = blockIdx.y, split = blockIdx.x;
+  const int hq = gridDim.y, CS = gridDim.x;
+  const int Bp = B;  // <= 16 per launch
+  const int KS = rows_per_cta + 8;  // padded h row (halves): conflict-free A-fragment loads
+  uint16_t *hs = reinterpret_cast<uint16_t *>(s1m_smem);  // [Bp][KS]
+  const size_t o1 = ((size_t)Bp * KS * 2 + 15) & ~(size_t)15;
+  float *red = reinterpret_cast<float *>(s1m_smem + o1);                                // [NKS][Bp][D]
+  double *cpart = reinterpret_cast<double *>(s1m_smem + o1 + (size_t)NKS * Bp * D * 4);  // [CS][per]
+  const int i0 = split * rows_per_cta, nrow = min(rows_per_cta, H - i0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cb = warp % NCB, ks = warp / NCB;
+  const int g = lane >> 2, q = lane & 3;
+  const int KRW = rows_per_cta / NKS;  // rows per warp (multiple of 16)
+  const int r0 = ks * KRW;
+  const uint16_t *wb = w_q + ((size_t)qh * H + i0) * D + cb * 64 + 8 * g;
+  // h rows of this CTA first (tiny; they must not queue behind the W stream), as 16-byte vectors
+  const int nvec = Bp * (rows_per_cta / 8);
+  uint4 hv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = threadIdx.x + k * S1M_THREADS;
+    const int b = t / (rows_per_cta / 8), i = (t % (rows_per_cta / 8)) * 8;
+    hv[k] = (t < nvec && i < nrow) ? *reinterpret_cast<const uint4 *>(&hidden[(size_t)b * H + i0 + i])
+                                   : make_uint4(0u, 0u, 0u, 0u);
+  }
+  // W stream: batches of 2 k16 steps (32 rows), double-buffered in registers
+  uint4 R[2][2][4];
+  auto load_batch = [&](uint4 (&Rb)[2][4], int rb) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = r0 + rb + 16 * s + 2 * q + (r & 1) + 8 * (r >> 1);
+        if (rb + 16 * s < KRW && row < nrow)
+          Rb[s][r] = s1_ld_nc_v4(wb + (size_t)row * D);
+        else
+          Rb[s][r] = make_uint4(0u, 0u, 0u, 0u);
+      }
+  };
+  if (s1_dbg == 3 && threadIdx.x == 0) atomicMin(&s1_stamp[0], s1_now());
+  load_batch(R[0], 0);
+  load_batch(R[1], 32);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = threadIdx.x + k * S1M_THREADS;
+    if (t < nvec) {
+      const int b = t / (rows_per_cta / 8), i = (t % (rows_per_cta / 8)) * 8;
+      *reinterpret_cast<uint4 *>(&hs[b * KS + i]) = hv[k];
+    }
+  }
+  for (int t = threadIdx.x + 4 * S1M_THREADS; t < nvec; t += S1M_THREADS) {  // long hidden slices only
+    const int b = t / (rows_per_cta / 8), i = (t % (rows_per_cta / 8)) * 8;
+    *reinterpret_cast<uint4 *>(&hs[b * KS + i]) =
+        i < nrow ? *reinterpret_cast<const uint4 *>(&hidden[(size_t)b * H + i0 + i]) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  __syncthreads();
+  float acc[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[j][e] = 0.0f;
+  const bool lo_ok = g < Bp, hi_ok = g + 8 < Bp;
+  auto compute = [&](const uint4 (&Rb)[2][4], int rb) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (rb + 16 * s >= KRW) break;
+      const int kk = r0 + rb + 16 * s;
+      const uint32_t a0 = lo_ok ? *reinterpret_cast<const uint32_t *>(&hs[g * KS + kk + 2 * q]) : 0u;
+      const uint32_t a1 = hi_ok ? *reinterpret_cast<const uint32_t *>(&hs[(g + 8) * KS + kk + 2 * q]) : 0u;
+      const uint32_t a2 = lo_ok ? *reinterpret_cast<const uint32_t *>(&hs[g * KS + kk + 8 + 2 * q]) : 0u;
+      const uint32_t a3 = hi_ok ? *reinterpret_cast<const uint32_t *>(&hs[(g + 8) * KS + kk + 8 + 2 * q]) : 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
+        const uint32_t b0 = __byte_perm(u4_word(Rb[s][0], j >> 1), u4_word(Rb[s][1], j >> 1), sel);
+        const uint32_t b1 = __byte_perm(u4_word(Rb[s][2], j >> 1), u4_word(Rb[s][3], j >> 1), sel);
+        mma_f16_16816(acc[j], a0, a1, a2, a3, b0, b1);
+      }
+    }
+  };
+  for (int rb = 0; rb < KRW; rb += 64) {
+    compute(R[0], rb);
+    if (rb + 64 < KRW) load_batch(R[0], rb + 64);
+    compute(R[1], rb + 32);
+    if (rb + 96 < KRW) load_batch(R[1], rb + 96);
+  }
+  // accumulator (row b, tile column 2q+e) of n-tile j is channel cb*64 + 8*(2q+e) + j
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int b = g + 8 * (e >> 1);
+      const int c = cb * 64 + 8 * (2 * q + (e & 1)) + j;
+      if (b < Bp) red[((size_t)ks * Bp + b) * D + c] = acc[j][e];
+    }
+  if (s1_dbg == 3 && threadIdx.x == 0) atomicMax(&s1_stamp[1], s1_now());
+  if (s1_dbg == 1) {  // experiment: streaming phase only
+    if (acc[0][0] == 12345.f) qg[0] = 1.0;
+    return;
+  }
+  __syncthreads();
+  const int kvh = qh / G;
+  // cluster reduction: CTA r owns the slice [r*per, (r+1)*per) of the Bp*D values; every CTA pushes its
+  // partial of each slice into the owner's shared memory (row = its rank), one cluster barrier, then
+  // the owner sums the ranks in order (float64) and writes its slice of q_hat
+  const int tot = Bp * D, per = (tot + CS - 1) / CS;
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    double a = 0.0;
+#pragma unroll
+    for (int s = 0; s < NKS; ++s) a += (double)red[(size_t)s * Bp * D + t];
+    const int owner = t / per;
+    cluster.map_shared_rank(cpart, owner)[split * per + (t - owner * per)] = a;
+  }
+  cluster.sync();
+  {
+    const int e0 = split * per, e1 = min(tot, e0 + per);
+    for (int t = e0 + threadIdx.x; t < e1; t += blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = r < CS ? cpart[r * per + (t - e0)] : 0.0;
+      double a = 0.0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a += v[r];  // ranks in order (+0.0 beyond CS is exact)
+      const int b = t / D, c = t % D;
+      qg[((size_t)b * hq + qh) * D + c] = a;
+      if (q_hat) q_hat[((size_t)b * hq + qh) * D + c] = a;
+    }
+  }
+  if (s1_dbg == 2) return;  // experiment: no channel selection
+  if (s1_dbg == 3 && threadIdx.x == 0) atomicMax(&s1_stamp[2], s1_now());
+  // last arriving CTA of the KV head selects the channels of its sequences
+  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned prev = atomicAdd(ctr, 1u);
-    last = prev == (unsigned)(splits * G) - 1;
-    if (last) *ctr = 0;  // re-armed for the next launch / graph replay
+    const unsigned prev = atomicAdd(arrive + kvh, 1u);
+    last = prev == (unsigned)(CS * G) - 1;
+    if (last) arrive[kvh] = 0;  // re-armed for the next launch / graph replay
   }
   __syncthreads();
   if (!last) return;
+  const unsigned long long t3 = s1_now();
   __threadfence();
-  double *qs = reinterpret_cast<double *>(red);  // G*D <= 2048 doubles
-  __shared__ double score[256];
-  __shared__ int flags[256];
-  for (int b = 0; b < nb; ++b) {
-    stage1_select_unit(part, splits, B, hq, D, G, chmax, d_s, q_hat, channels, b0 + b, kvh, qs, score, flags);
-    if (prefetch) {
-      // start moving the selected channel rows of the layer's scorer keys into L2: the
-      // layer's decode kernel (next on the main stream) then scores from L2, not HBM
-      const int u = (b0 + b) * hkv + kvh;
-      const int64_t len = *pf.len;
-      const int64_t bytes = len * 2;
-      const int64_t nch = (bytes + 32767) / 32768;
-      for (int64_t i = threadIdx.x; i < (int64_t)d_s * nch; i += blockDim.x) {
-        const int c = channels[(size_t)u * d_s + i / nch];
-        const int64_t o = (i % nch) * 32768;
-        const uint32_t sz = (uint32_t)min((int64_t)32768, bytes - o);
-        const char *src = reinterpret_cast<const char *>(pf.kt + ((size_t)u * D + c) * pf.capacity) + o;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((sz + 15u) & ~15u) : "memory");
-      }
-    }
+  const unsigned long long t4 = s1_now();
+  double *sc = reinterpret_cast<double *>(red) + (size_t)warp * D;  // red is dead: D doubles per warp
+  for (int b = warp; b < Bp; b += S1M_THREADS / 32)
+    stage1_warp_select<D>(qg, hq, G, b, kvh, chmax, d_s, channels, sc, pf, prefetch, b_off);
+  if (s1_dbg == 3 && threadIdx.x == 0 && kvh == 0) {
+    s1_stamp[3] = t3;
+    s1_stamp[4] = t4;
+    s1_stamp[5] = s1_now();
   }
+}
+
+static inline int hkv_of(int hq, int G) { return hq / G; }
+
+// rows per CTA of the tensor-core kernel: about two CTAs per SM in one wave,
+// a multiple of 16 rows per warp, at most 8 splits (the splits of a query
+// head form one portable cluster)
+static int stage1_mma_rows(int hq, int H, int d) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int nks = (S1M_THREADS / 32) / (d / 64);
+  int splits = max(1, (2 * sms) / hq);
+  if (const char *e = getenv("TKV_STAGE1_SPLITS")) splits = max(1, atoi(e));
+  splits = min(splits, 8);
+  const int unit = 16 * nks;
+  int rows = (H + splits - 1) / splits;
+  rows = (rows + unit - 1) / unit * unit;
+  return rows;
+}
+
+// The tensor-core kernel reads W_q once for up to 16 sequences and reduces
+// over a cluster; with one or two sequences the SIMT kernel (no cluster
+// placement constraints, 32 warps per SM) is as fast standalone and faster
+// beside the sparse-layer clusters on the side stream (measured, DESIGN 4.3).
+static bool stage1_use_mma(int d, int B) {
+  static int force = -1;
+  if (force < 0) {
+    const char *e = getenv("TKV_STAGE1_MMA");  // 1 always, 0 never (experiments)
+    force = e ? atoi(e) : 2;
+  }
+  if (force == 0 || !(d == 64 || d == 128 || d == 256)) return false;
+  return force == 1 || B > 2;
 }
 
 static int stage1_splits(int hq, int H) {
@@ -322,7 +667,8 @@ static int stage1_splits(int hq, int H) {
 
 int64_t stage1_workspace(int B, int hq, int H, int d) {
   const int splits = stage1_splits(hq, H);
-  const int64_t part = (int64_t)splits * B * hq * d * 8;
+  int64_t part = (int64_t)splits * B * hq * d * 8;
+  if (stage1_use_mma(d, B)) part = std::max(part, (int64_t)std::min(B, 16) * hq * d * 8);
   return (part + 255) / 256 * 256 + (int64_t)((B + S1_BG - 1) / S1_BG) * hq * 4 + 256;
 }
 
@@ -331,6 +677,67 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
   SL pfs = {};
   if (pf) pfs = *pf;
   if (G > 16 || G * d > 2048) return fail(TKV_ERR_SHAPE, "stage 1 supports G*head_dim <= 2048 (G <= 16)");
+  if (stage1_use_mma(d, B) && H % 8 == 0 && (reinterpret_cast<uintptr_t>(hidden) & 15) == 0) {
+    // tensor-core path: up to 16 sequences per launch, W_q read once per launch
+    const int rows = stage1_mma_rows(hq, H, d);
+    const int splits = (H + rows - 1) / rows;
+    double *part = reinterpret_cast<double *>(ws);
+    const int64_t pbytes = ((int64_t)std::min(B, 16) * hq * d * 8 + 255) / 256 * 256;
+    unsigned *arrive = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + pbytes);
+    const int nks = (S1M_THREADS / 32) / (d / 64);
+    static bool dbg_set = false;
+    if (!dbg_set) {
+      dbg_set = true;
+      if (const char *e = getenv("TKV_STAGE1_DBG")) {
+        const int v = atoi(e);
+        cudaMemcpyToSymbol(s1_dbg, &v, sizeof(int));
+      }
+    }
+    for (int b0 = 0; b0 < B; b0 += 16) {
+      const int nb = std::min(16, B - b0);
+      const size_t smem = (((size_t)nb * (rows + 8) * 2 + 15) & ~(size_t)15) + (size_t)nks * nb * d * 4 +
+                          ((size_t)nb * d + 8) * 8;
+      const uint16_t *hb = hidden + (size_t)b0 * H;
+      double *qb = q_hat ? q_hat + (size_t)b0 * hq * d : nullptr;
+      int32_t *cbp = channels + (size_t)b0 * hkv_of(hq, G) * d_s;
+      const float *mb = chmax + (size_t)b0 * hkv_of(hq, G) * d;
+      cudaError_t e = cudaSuccess;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(splits, hq);
+      cfg.blockDim = dim3(S1M_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributePriority;
+      static const bool hip = getenv("TKV_STAGE1_HIPRIO") && atoi(getenv("TKV_STAGE1_HIPRIO"));
+      at[0].val.priority = launch_priority(hip);
+      at[1].id = cudaLaunchAttributeClusterDimension;
+      at[1].val.clusterDim.x = splits;
+      at[1].val.clusterDim.y = 1;
+      at[1].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+#define TKV_S1M(DD)                                                                                         \
+  {                                                                                                         \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      cudaFuncSetAttribute(stage1_mma_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); \
+      attr = true;                                                                                          \
+    }                                                                                                       \
+    e = cudaLaunchKernelEx(&cfg, stage1_mma_kernel<DD>, hb, w_q, nb, H, rows, part, arrive, G, mb, d_s, qb,  \
+                           cbp, pfs, pf ? 1 : 0, b0);                                                       \
+  }
+      if (smem > 160 * 1024) return fail(TKV_ERR_SHAPE, "stage 1: hidden size too large for the split plan");
+      switch (d) {
+        case 64: TKV_S1M(64); break;
+        case 128: TKV_S1M(128); break;
+        default: TKV_S1M(256); break;
+      }
+#undef TKV_S1M
+      if (e != cudaSuccess) return check_launch("tkv_stage1");
+    }
+    return check_launch("tkv_stage1");
+  }
   const int splits = stage1_splits(hq, H);
   const int rows = ((H + splits - 1) / splits + 7) / 8 * 8;
   if (rows > 1024) return fail(TKV_ERR_SHAPE, "stage 1: hidden size too large for the split plan");
@@ -946,3 +1353,13 @@ int uva_probe(const void *host, size_t bytes, int row_bytes, const int32_t *rows
 }
 
 }  // namespace tkv
+
+extern "C" int tkv_debug_stage1_stamps(unsigned long long *out, int reset) {
+  if (reset) {
+    unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(tkv::s1_stamp, init, sizeof(init));
+  } else {
+    cudaMemcpyFromSymbol(out, tkv::s1_stamp, sizeof(unsigned long long) * 8);
+  }
+  return 0;
+}

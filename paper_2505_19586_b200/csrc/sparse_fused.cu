@@ -136,7 +136,8 @@ struct FzCtl {
   double wsum[2][32];
   int scan[40];
   unsigned long long scan64[33];
-  int hits, misses;
+  int hits, misses;  // row-cache counters of the gather (use_cache)
+  int definite;      // select: candidate-list keys above the exact band
   int list_count;
   unsigned long long bar;       // mbarrier of the row staging (HBM copies on the key|value slot-cache path)
   unsigned long long bar2;      // key|value slot-cache path: the value rows fetched over PCIe
@@ -881,7 +882,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             if (tid == 0) {
               C.band_count = 0;
               C.overflow = 0;
-              C.hits = 0;  // (reused) definite count inside the list
+              C.definite = 0;  // keys of the list above the band
             }
             __syncthreads();
             int def = 0;
@@ -897,10 +898,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) def += __shfl_xor_sync(0xffffffffu, def, o);
-            if (lane == 0 && def) atomicAdd(&C.hits, def);
+            if (lane == 0 && def) atomicAdd(&C.definite, def);
             __syncthreads();
             const int nb = min(C.band_count, FZ_BAND);
-            const int need_b = n_topk - A - C.hits;
+            const int need_b = n_topk - A - C.definite;
             if (!verdict || C.overflow || need_b < 0 || need_b > nb) {
               verdict = 0;  // the aim missed (or a band overflow): take the next attempt / full-range path
             } else {

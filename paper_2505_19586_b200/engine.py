@@ -487,6 +487,37 @@ class DecodeEngine:
         return sparse_layer_fidelity(lay, self.queries[l], self.G, lay.n - 1, idx, cnt, self.retrieval.n_topk,
                                      self.out[l])
 
+    def set_row_cache(self, enabled: bool) -> None:
+        """Row cache on/off for every sparse layer; the step must be captured
+        again (``capture``) for a graph to pick it up."""
+        for st in self.sparse.values():
+            st.layer.set_row_cache(enabled)
+        self.graph = self.prof_graph = None
+
+    def resident_bytes(self) -> dict:
+        """Bytes this rank keeps resident, by structure: HBM (quantized caches,
+        scorer keys, token-major key copy, row cache, local windows, W_q,
+        workspaces) and pinned host memory (the offloaded K/V store)."""
+        def nb(t):
+            return 0 if t is None else t.numel() * t.element_size()
+
+        q = sum(sum(nb(b) for b in self.layers[l]._bufs) for l in range(len(self.labels)) if self.labels[l] == "q")
+        kt = kdev = cache = loc = wq = host = other = 0
+        for st in self.sparse.values():
+            lay = st.layer
+            kt += nb(lay.kt)
+            kdev += nb(lay.kdev)
+            cache += sum(nb(x) for x in (lay.slot_tok, lay.slot_stamp, lay.slot_v, lay.tok_slot, lay.slot_hand))
+            loc += nb(lay.loc_k) + nb(lay.loc_v)
+            wq += nb(st.w_q)
+            other += nb(lay.chmax) + nb(st.s1_ws) + nb(lay.thresh)
+            host += lay.arena.nbytes
+        ws = nb(self.sel_ws) + nb(self.dec_ws) + nb(self.attn_ws)
+        ws += sum(sum(nb(w) for w in self.layers[l]._ws.values()) for l in range(len(self.labels)) if self.labels[l] == "q")
+        hbm = {"quantized_caches": q, "scorer_keys_channel_major": kt, "token_major_key_copy": kdev,
+               "row_cache": cache, "local_windows": loc, "w_q": wq, "workspaces_and_small": ws + other}
+        return {"hbm": hbm, "hbm_total": sum(hbm.values()), "pinned_host_kv": host}
+
     def cache_counters(self) -> tuple[int, int]:
         """Summed (HBM-cache hits, PCIe-fetched rows) over the sparse layers."""
         h = m = 0

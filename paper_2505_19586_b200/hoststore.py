@@ -144,6 +144,13 @@ class OffloadedLayerKV:
         check(_lib.load().tkv_sparse_append(C.byref(self.struct), ptr(k), ptr(v), stream_ptr(stream)))
         self.n += 1
 
+    def set_row_cache(self, enabled: bool) -> None:
+        """Switch the HBM row cache on or off for later launches (a captured
+        graph keeps the setting it was captured with).  Results are identical
+        either way: cached rows are exact copies, and rows appended while the
+        cache is off are simply not cached."""
+        self.struct.cache_slots = self.cache_slots if enabled else 0
+
     def cache_counters(self) -> tuple[int, int]:
         """(rows served from the HBM row cache, rows fetched over PCIe) so far."""
         if self.cache_stats is None:

@@ -76,7 +76,9 @@ def stage1_select(hidden: torch.Tensor, w_q: torch.Tensor, chmax: torch.Tensor, 
     if channels is None:
         channels = torch.empty((units, d_s), dtype=torch.int32, device=hidden.device)
     if workspace is None:
-        workspace = WORKSPACES.get("stage1", lib.tkv_stage1_workspace(B, hq, H, d), hidden.device)
+        # one zero-initialised workspace per shape: its arrival counters re-arm themselves, but a buffer shared
+        # across shapes would put one shape's partials where another keeps its counters
+        workspace = WORKSPACES.get(f"stage1:{B}:{hq}:{H}:{d}", lib.tkv_stage1_workspace(B, hq, H, d), hidden.device)
     if prefetch_layer is None:
         check(lib.tkv_stage1(ptr(hidden), ptr(w_q), B, hq, H, d, G, ptr(chmax), d_s, ptr(q_hat), ptr(channels),
                              ptr(workspace), stream_ptr(stream)))

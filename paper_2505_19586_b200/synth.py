@@ -11,7 +11,10 @@ Structure kept from the reference generator:
 * sparse layers: keys N(0, 1/sqrt(d)) with the outlier channels carrying 95 %
   of the energy, plus dominant tokens in the first 60 % boosted along the
   group-summed query direction (trace.py:466-502);
-* values N(0, 1); everything stored as fp16 (trace.py:505-513).
+* values N(0, 1); everything stored as fp16 (trace.py:505-513);
+* ``drift``: the per-step query emphasis wanders across the outlier channels,
+  each planted hidden coordinate scaled by lognormal(0, 0.6) every step
+  (ChannelOutlierSpec.drift, trace.py:268-275, 434-436).
 """
 
 from __future__ import annotations
@@ -32,11 +35,31 @@ class Workload:
     queries: torch.Tensor   # [T, L, B, hq, d] fp16
     new_keys: torch.Tensor  # [T, L, B, h, d] fp16
     new_values: torch.Tensor
+    h_base: torch.Tensor | None = None       # [hidden] fp32: the step hidden state's mean
+    drift_coords: torch.Tensor | None = None  # hidden coordinates of the planted outlier channels
+    w_q_all: list | None = None              # fp16 W_q of every layer (query generation for new inputs)
+
+
+def _step_hidden(h_base, coords, steps, L, batch, randn, drift, gen):
+    """Step hidden states (trace.py:431-441): h_base + N(0, 0.25) for layer 0
+    (outlier coordinates scaled by lognormal(0, 0.6) per step with drift,
+    trace.py:434-436), then adjacent-layer drift 0.1."""
+    hidden_dim = h_base.numel()
+    hid = torch.empty(steps, L, batch, hidden_dim, device=h_base.device)
+    for t in range(steps):
+        base = h_base[None, :] + randn(batch, hidden_dim, std=0.25)
+        if drift and coords is not None and coords.numel():
+            amp = torch.exp(0.6 * torch.randn(batch, coords.numel(), generator=gen, device=h_base.device))
+            base[:, coords] *= amp
+        hid[t, 0] = base
+        for l in range(1, L):
+            hid[t, l] = math.sqrt(1 - 0.01) * hid[t, l - 1] + 0.1 * randn(batch, hidden_dim)
+    return hid
 
 
 def make_workload(num_layers: int, q_layers, hq: int, h: int, d: int, n: int, steps: int, batch: int = 1,
                   seed: int = 0, device="cuda", num_outliers: int = 8, ratio: float = 0.95,
-                  num_dominant: int = 4, keep_wq_for_q_layers: bool = False) -> Workload:
+                  num_dominant: int = 4, keep_wq_for_q_layers: bool = False, drift: bool = False) -> Workload:
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     hidden_dim = hq * d
@@ -52,7 +75,7 @@ def make_workload(num_layers: int, q_layers, hq: int, h: int, d: int, n: int, st
     amp = 2.0
     col_mag = math.sqrt(ratio_eff / (1.0 - ratio_eff) * (d - o) / o)
     h_base = randn(hidden_dim)
-    w_q, outl = [], []
+    w_q, outl, all_coords = [], [], []
     for l in range(L):
         W = randn(hq, hidden_dim, d, std=1.0 / math.sqrt(hidden_dim))
         ch = torch.randperm(d, generator=g, device=device)[:o].sort().values
@@ -65,14 +88,11 @@ def make_workload(num_layers: int, q_layers, hq: int, h: int, d: int, n: int, st
                     W[heads, :, c] *= 0.1
                     W[heads, int(coords[kvh, j]), c] += col_mag / amp
                     h_base[int(coords[kvh, j])] = amp
+            all_coords.append(coords.reshape(-1))
         w_q.append(W)
         outl.append(ch)
-    hid = torch.empty(steps, L, batch, hidden_dim, device=device)
-    for t in range(steps):
-        base = h_base[None, :] + randn(batch, hidden_dim, std=0.25)
-        hid[t, 0] = base
-        for l in range(1, L):
-            hid[t, l] = math.sqrt(1 - 0.01) * hid[t, l - 1] + 0.1 * randn(batch, hidden_dim)
+    coords_all = torch.unique(torch.cat(all_coords)) if all_coords else None
+    hid = _step_hidden(h_base, coords_all, steps, L, batch, randn, drift, g)
     hid16 = hid.half()
     queries = torch.empty(steps, L, batch, hq, d, device=device, dtype=torch.float16)
     for l in range(L):
@@ -110,5 +130,29 @@ def make_workload(num_layers: int, q_layers, hq: int, h: int, d: int, n: int, st
         pk.append(k.half())
         pv.append(v)
         new_k[:, l] = nk.half()
-    w16 = [w.half() if (labels[l] == "s" or keep_wq_for_q_layers) else None for l, w in enumerate(w_q)]
-    return Workload(labels, pk, pv, w16, hid16, queries, new_k, new_v)
+    w_all = [w.half() for w in w_q]
+    w16 = [w if (labels[l] == "s" or keep_wq_for_q_layers) else None for l, w in enumerate(w_all)]
+    return Workload(labels, pk, pv, w16, hid16, queries, new_k, new_v, h_base=h_base, drift_coords=coords_all,
+                    w_q_all=w_all)
+
+
+def step_inputs(wl: Workload, steps: int, drift: bool, seed: int) -> tuple:
+    """Fresh decode-step inputs for a prefilled workload: hidden states (with
+    or without the reference's per-step outlier drift) and the queries
+    q = h W_q they induce; the appended K/V rows are the workload's own.
+    Returns (hidden [T, L, B, hidden], queries [T, L, B, hq, d]) fp16."""
+    dev = wl.h_base.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+
+    def randn(*shape, std=1.0):
+        return torch.randn(*shape, generator=g, device=dev, dtype=torch.float32) * std
+
+    L = len(wl.labels)
+    batch = wl.hidden.shape[2]
+    hid = _step_hidden(wl.h_base, wl.drift_coords, steps, L, batch, randn, drift, g)
+    hq, d = wl.queries.shape[3], wl.queries.shape[4]
+    queries = torch.empty(steps, L, batch, hq, d, device=dev, dtype=torch.float16)
+    for l in range(L):
+        queries[:, l] = torch.einsum("tbi,hid->tbhd", hid[:, l], wl.w_q_all[l].float()).half()
+    return hid.half(), queries
