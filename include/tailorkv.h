@@ -114,12 +114,51 @@ int64_t tkv_quant_decode_workspace(const tkv_qcache *c, int32_t G);
 int tkv_quant_decode(const tkv_qcache *c, const uint16_t *queries, int32_t G, float *out,
                      void *workspace, int32_t impl, void *stream);
 
-/* Raw quantized GEMVs for one unit (replaces qgemv_scores / qgemv_output).
- * logits fp32 [n] unscaled; weights fp32 [n] -> out fp32 [d]. */
-int tkv_qgemv_scores(const tkv_qcache *c, int32_t unit, int64_t n, const float *query, float *logits,
+/* Raw quantized GEMVs for one unit (replace qgemv_scores quantizer.py:505-533
+ * and qgemv_output :536-558), float64 like the reference: logits [n] of a
+ * query [d] over the unit's keys (complete groups + fp16 residual rows), and
+ * weights [n] @ the unit's dequantized values -> out [d].  Deterministic
+ * (fixed-order reductions); qgemv_output needs a workspace of
+ * tkv_qgemv_output_workspace bytes. */
+int tkv_qgemv_scores(const tkv_qcache *c, int32_t unit, int64_t n, const double *query, double *logits,
                      void *stream);
-int tkv_qgemv_output(const tkv_qcache *c, int32_t unit, int64_t n, const float *weights, float *out,
-                     void *stream);
+int64_t tkv_qgemv_output_workspace(const tkv_qcache *c, int64_t n);
+int tkv_qgemv_output(const tkv_qcache *c, int32_t unit, int64_t n, const double *weights, double *out,
+                     void *workspace, void *stream);
+
+/* GQT1 import (replaces GroupQuantizedTensor.from_bytes quantizer.py:383-422):
+ * the HOST blob's codes, zero points / scales and key residual go into one
+ * unit of the cache (which 0 = keys, PER_CHANNEL blob; 1 = values, PER_TOKEN)
+ * and *len becomes the blob's row count.  device_ws: >= blob_len bytes of
+ * device memory (staging).  Header/section checks raise TKV_ERR_ENCODING
+ * like the reference.  Synchronous.  A blob exported from fp16 inputs
+ * re-exports byte-identically. */
+int tkv_qcache_import(const tkv_qcache *c, int32_t unit, int32_t which, const uint8_t *blob, int64_t blob_len,
+                      uint8_t *device_ws, void *stream);
+
+/* float64 helpers over caller device arrays for the reference-signature
+ * API (paper_2505_19586_b200/hybridkv.py):
+ * - attention: softmax(q K^T / sqrt(d)) per query row (kv_model.py:169-194),
+ *   optionally over the index list sel[m] (sparse_attention retriever.py:214-226),
+ *   weights [rows][m] and/or out = weights @ V [rows][d]; workspace rows*m doubles;
+ * - approx_scores (retriever.py:166-189): critical_keys [n][d_s] @ sum_g q[g];
+ * - channel selection (retriever.py:111-163): scores[c] = sum_g |q_hat[g][c]| *
+ *   chmax[c] (channel_abs_max NULL: scores = q_hat[0][c] as given), top d_s
+ *   with ties to the lower index, ascending;
+ * - host gather (memsim.py:118-127): K and V rows of one unit from the pinned
+ *   host store by UVA loads into device buffers [m][d];
+ * - sum_at: sum of w[idx[i]] for i < *count (sparse_error's kept mass). */
+int tkv_attention_f64(const double *queries, int32_t rows, const double *keys, const double *values, int64_t n,
+                      int32_t d, const int64_t *sel, int64_t m, double *workspace, double *weights, double *out,
+                      void *stream);
+int tkv_approx_scores_f64(const double *query_critical, int32_t G, const double *critical_keys, int64_t n,
+                          int32_t d_s, double *out, void *stream);
+int tkv_channel_select_f64(const double *q_hat, int32_t G, const double *channel_abs_max, int32_t d, int32_t d_s,
+                           double *scores, int32_t *selected, void *stream);
+struct tkv_sparse_layer;
+int tkv_host_gather(const struct tkv_sparse_layer *s, int32_t unit, const int64_t *indices, int64_t m, uint16_t *out_keys,
+                    uint16_t *out_values, void *stream);
+int tkv_sum_at(const double *w, const int32_t *indices, const int32_t *count, double *out, void *stream);
 
 /* ------------------------------------------------------------------------
  * Sparsity-friendly layer (retriever.py:84-226, memsim.py:76-252)

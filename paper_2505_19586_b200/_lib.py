@@ -82,7 +82,14 @@ _SIGS = {
     "tkv_quant_decode_workspace": (C.c_int64, [C.POINTER(QCache), _I32]),
     "tkv_quant_decode": (C.c_int, [C.POINTER(QCache), _P, _I32, _P, _P, _I32, _P]),
     "tkv_qgemv_scores": (C.c_int, [C.POINTER(QCache), _I32, _I64, _P, _P, _P]),
-    "tkv_qgemv_output": (C.c_int, [C.POINTER(QCache), _I32, _I64, _P, _P, _P]),
+    "tkv_qgemv_output_workspace": (C.c_int64, [C.POINTER(QCache), _I64]),
+    "tkv_qgemv_output": (C.c_int, [C.POINTER(QCache), _I32, _I64, _P, _P, _P, _P]),
+    "tkv_qcache_import": (C.c_int, [C.POINTER(QCache), _I32, _I32, C.c_char_p, _I64, _P, _P]),
+    "tkv_attention_f64": (C.c_int, [_P, _I32, _P, _P, _I64, _I32, _P, _I64, _P, _P, _P, _P]),
+    "tkv_approx_scores_f64": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P]),
+    "tkv_channel_select_f64": (C.c_int, [_P, _I32, _P, _I32, _I32, _P, _P, _P]),
+    "tkv_host_gather": (C.c_int, [C.POINTER(SparseLayer), _I32, _P, _I64, _P, _P, _P]),
+    "tkv_sum_at": (C.c_int, [_P, _P, _P, _P, _P]),
     "tkv_sparse_prefill": (C.c_int, [C.POINTER(SparseLayer), _P, _P, _I64, _P]),
     "tkv_sparse_append": (C.c_int, [C.POINTER(SparseLayer), _P, _P, _P]),
     "tkv_stage1_workspace": (C.c_int64, [_I32, _I32, _I32, _I32]),

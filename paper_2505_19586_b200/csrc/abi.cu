@@ -155,14 +155,89 @@ int tkv_quant_decode(const tkv_qcache *c, const uint16_t *queries, int32_t G, fl
   return quant_decode(*c, queries, G, out, workspace, impl, as_stream(stream));
 }
 
-int tkv_qgemv_scores(const tkv_qcache *c, int32_t unit, int64_t n, const float *query, float *logits, void *stream) {
+int tkv_qgemv_scores(const tkv_qcache *c, int32_t unit, int64_t n, const double *query, double *logits,
+                     void *stream) {
   if (int r = validate_qcache(c)) return r;
+  TKV_REQUIRE(unit >= 0 && unit < c->units, TKV_ERR_PARAMETER, "unit out of range");
+  TKV_REQUIRE(n >= 1 && n <= c->capacity, TKV_ERR_EMPTY_CACHE, "token count out of range");
   return qgemv_scores(*c, unit, n, query, logits, as_stream(stream));
 }
 
-int tkv_qgemv_output(const tkv_qcache *c, int32_t unit, int64_t n, const float *weights, float *out, void *stream) {
+int64_t tkv_qgemv_output_workspace(const tkv_qcache *c, int64_t n) { return qgemv_output_workspace(*c, n); }
+
+int tkv_qgemv_output(const tkv_qcache *c, int32_t unit, int64_t n, const double *weights, double *out,
+                     void *workspace, void *stream) {
   if (int r = validate_qcache(c)) return r;
-  return qgemv_output(*c, unit, n, weights, out, as_stream(stream));
+  TKV_REQUIRE(unit >= 0 && unit < c->units, TKV_ERR_PARAMETER, "unit out of range");
+  TKV_REQUIRE(n >= 1 && n <= c->capacity, TKV_ERR_EMPTY_CACHE, "token count out of range");
+  return qgemv_output(*c, unit, n, weights, out, workspace, as_stream(stream));
+}
+
+int tkv_qcache_import(const tkv_qcache *c, int32_t unit, int32_t which, const uint8_t *blob, int64_t blob_len,
+                      uint8_t *device_ws, void *stream) {
+  if (int r = validate_qcache(c)) return r;
+  TKV_REQUIRE(unit >= 0 && unit < c->units, TKV_ERR_PARAMETER, "unit out of range");
+  TKV_REQUIRE(which == 0 || which == 1, TKV_ERR_PARAMETER, "which must be 0 (keys) or 1 (values)");
+  TKV_REQUIRE(blob != nullptr && blob_len >= 24, TKV_ERR_ENCODING, "quantized tensor blob truncated");
+  TKV_REQUIRE(std::memcmp(blob, "GQT1", 4) == 0, TKV_ERR_ENCODING, "bad quantized tensor magic");
+  auto u32 = [&](int o) {
+    return (uint32_t)blob[o] | ((uint32_t)blob[o + 1] << 8) | ((uint32_t)blob[o + 2] << 16) |
+           ((uint32_t)blob[o + 3] << 24);
+  };
+  const int bits = blob[4], axis = blob[5], g = blob[6] | (blob[7] << 8);
+  const int64_t rows = u32(8), d = u32(12), res_rows = u32(16), packed_len = u32(20);
+  TKV_REQUIRE(axis == (which == 0 ? 1 : 2), TKV_ERR_ENCODING, "blob axis does not match keys/values");
+  TKV_REQUIRE(bits == c->bits && g == c->g && d == c->d, TKV_ERR_ENCODING,
+              "blob bits / group size / head_dim differ from the cache");
+  TKV_REQUIRE(packed_len == (rows * d * bits + 7) / 8, TKV_ERR_ENCODING, "packed code section has the wrong length");
+  TKV_REQUIRE(which == 0 ? rows % g == 0 && res_rows < g : res_rows == 0, TKV_ERR_ENCODING,
+              "row counts inconsistent with the group size");
+  const int64_t grid = which == 0 ? (rows / g) * d : rows * ((d + g - 1) / g);
+  const int64_t need = 24 + packed_len + 4 * grid + 2 * res_rows * d;
+  TKV_REQUIRE(blob_len >= need, TKV_ERR_ENCODING, "parameter or residual section truncated");
+  TKV_REQUIRE(rows + res_rows <= c->capacity, TKV_ERR_SHAPE, "blob longer than the cache capacity");
+  TKV_REQUIRE(device_ws != nullptr, TKV_ERR_PARAMETER, "device workspace of blob_len bytes required");
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemcpyAsync(device_ws, blob, need, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return check_launch("tkv_qcache_import (copy)");
+  int r = import_blob(*c, unit, which, device_ws, rows, res_rows, packed_len, st);
+  if (r == TKV_OK && cudaStreamSynchronize(st) != cudaSuccess) return check_launch("tkv_qcache_import");
+  return r;
+}
+
+int tkv_attention_f64(const double *queries, int32_t rows, const double *keys, const double *values, int64_t n,
+                      int32_t d, const int64_t *sel, int64_t m, double *workspace, double *weights, double *out,
+                      void *stream) {
+  TKV_REQUIRE(rows >= 1 && d >= 1, TKV_ERR_SHAPE, "attention needs at least one query row");
+  TKV_REQUIRE(n >= 1 && m >= 1, TKV_ERR_EMPTY_CACHE, "attention over an empty cache");
+  TKV_REQUIRE(workspace != nullptr, TKV_ERR_PARAMETER, "workspace of rows * m doubles required");
+  return attention_f64(queries, rows, keys, values, n, d, sel, m, workspace, weights, out, as_stream(stream));
+}
+
+int tkv_approx_scores_f64(const double *query_critical, int32_t G, const double *critical_keys, int64_t n,
+                          int32_t d_s, double *out, void *stream) {
+  TKV_REQUIRE(G >= 1 && d_s >= 1 && d_s <= 4096 && n >= 0, TKV_ERR_SHAPE, "bad approx_scores shape");
+  if (n == 0) return TKV_OK;
+  return approx_scores_f64(query_critical, G, critical_keys, n, d_s, out, as_stream(stream));
+}
+
+int tkv_channel_select_f64(const double *q_hat, int32_t G, const double *channel_abs_max, int32_t d, int32_t d_s,
+                           double *scores, int32_t *selected, void *stream) {
+  TKV_REQUIRE(G >= 1 && d >= 1 && d <= 4096, TKV_ERR_SHAPE, "bad channel-score shape");
+  TKV_REQUIRE(d_s >= 1 && d_s <= d, TKV_ERR_PARAMETER, "d_s must lie in [1, head_dim]");
+  return channel_select_f64(q_hat, G, channel_abs_max, d, d_s, scores, selected, as_stream(stream));
+}
+
+int tkv_host_gather(const tkv_sparse_layer *s, int32_t unit, const int64_t *indices, int64_t m, uint16_t *out_keys,
+                    uint16_t *out_values, void *stream) {
+  TKV_REQUIRE(s != nullptr && s->host_kv != nullptr, TKV_ERR_PARAMETER, "layer has no host store");
+  TKV_REQUIRE(unit >= 0 && unit < s->units, TKV_ERR_PARAMETER, "unit out of range");
+  TKV_REQUIRE(s->d % 8 == 0, TKV_ERR_SHAPE, "head_dim must be a multiple of 8");
+  return host_gather(*s, unit, indices, m, out_keys, out_values, as_stream(stream));
+}
+
+int tkv_sum_at(const double *w, const int32_t *indices, const int32_t *count, double *out, void *stream) {
+  return sum_at(w, indices, count, out, as_stream(stream));
 }
 
 static int validate_sparse(const tkv_sparse_layer *s) {

@@ -141,6 +141,10 @@ __device__ __forceinline__ uint32_t encode_code(float xf, float lof, float hif, 
   return (uint32_t)min(max(ri, 0), 3);
 }
 
+__device__ __forceinline__ void atomic_max_pos(float *addr, float v) {
+  atomicMax(reinterpret_cast<int *>(addr), __float_as_int(v));  // v >= 0
+}
+
 // Group scale as used by decode: (hi-lo)/(2^b-1), 1 when degenerate.
 __device__ __forceinline__ float group_scale_f(float lo, float hi, int bits) {
   float s = (hi - lo) / (float)((1 << bits) - 1);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Quantized layer cache: prefill pack, decode append, GQT1 export, dequant,
 // raw GEMVs.  Reference: hybridkv/quantizer.py:187-558.
 #include <cstdio>
@@ -7,10 +8,6 @@
 #include "qcache.cuh"
 
 namespace tkv {
-
-__device__ __forceinline__ void atomic_max_pos(float *addr, float v) {
-  atomicMax(reinterpret_cast<int *>(addr), __float_as_int(v));  // v >= 0
-}
 
 // ---------------------------------------------------------------------------
 // Pack keys: one CTA per (key tile, unit).  quantizer.py:277-293.
@@ -456,29 +453,86 @@ int dequant(const QC &c, int u, int which, int64_t n, float *out, cudaStream_t s
   return check_launch("tkv_qcache_dequant");
 }
 
-__global__ void qgemv_scores_kernel(QC c, int u, int64_t n, const float *__restrict__ q, float *logits) {
-  const int64_t ncomp = (n / c.g) * c.g;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+// qgemv_scores (quantizer.py:505-533), float64 like the reference:
+// logit_t = sum_c code[t,c] (q_c s[g,c]) + sum_c q_c z[g,c] over complete
+// groups, residual rows @ q.  One warp per token, lanes over channels.
+__global__ void __launch_bounds__(256) qgemv_scores_kernel(QC c, int u, int64_t n, const double *__restrict__ q,
+                                                           double *__restrict__ logits) {
+  const int lane = threadIdx.x & 31, d = c.d, g = c.g;
+  const int64_t ncomp = (n / g) * g;
+  const double den = (double)((1 << c.bits) - 1);
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     double acc = 0.0;
-    for (int ch = 0; ch < c.d; ++ch) acc += (double)key_hat(c, u, t, ch, ncomp) * (double)q[ch];
-    logits[t] = (float)acc;
+    for (int ch = lane; ch < d; ch += 32) {
+      if (t >= ncomp) {
+        acc = fma(h2d(c.key_resid[((size_t)u * g + (t - ncomp)) * d + ch]), q[ch], acc);
+      } else {
+        const uint32_t w = c.key_lohi[((size_t)u * (c.capacity / g) + t / g) * d + ch];
+        const double lo = h2d(w & 0xffff), hi = h2d(w >> 16);
+        double s = (hi - lo) / den;
+        if (s == 0.0) s = 1.0;
+        acc = fma((double)key_code_at(c, u, t, ch), q[ch] * s, acc);
+        acc = fma(q[ch], lo, acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) logits[t] = acc;
   }
 }
 
-__global__ void qgemv_output_kernel(QC c, int u, int64_t n, const float *__restrict__ w, float *out) {
-  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ch >= c.d) return;
+// qgemv_output (quantizer.py:536-558), float64: out_c = sum_t w_t (code[t,c]
+// s[t,cb] + z[t,cb]).  Pass 1: CTA per 1024-token chunk, threads over
+// (token lane, channel), fixed-order partials; pass 2 sums the chunks in order.
+constexpr int QG_CHUNK = 1024;
+__global__ void __launch_bounds__(256) qgemv_output_part_kernel(QC c, int u, int64_t n, const double *__restrict__ w,
+                                                                double *__restrict__ part) {
+  __shared__ double red[256];
+  const int d = c.d, nb = (d + c.g - 1) / c.g;
+  const int lanes = 256 / d;  // token lanes (d <= 256)
+  const int ch = threadIdx.x % d, tl = threadIdx.x / d;
+  const double den = (double)((1 << c.bits) - 1);
+  const int64_t t0 = (int64_t)blockIdx.x * QG_CHUNK, t1 = imin64(n, t0 + QG_CHUNK);
   double acc = 0.0;
-  for (int64_t t = 0; t < n; ++t) acc += (double)w[t] * (double)val_hat(c, u, t, ch);
-  out[ch] = (float)acc;
+  if (tl < lanes) {
+    for (int64_t t = t0 + tl; t < t1; t += lanes) {
+      const uint32_t pr = c.val_lohi[((size_t)u * c.capacity + t) * nb + ch / c.g];
+      const double lo = h2d(pr & 0xffff), hi = h2d(pr >> 16);
+      double s = (hi - lo) / den;
+      if (s == 0.0) s = 1.0;
+      acc = fma(w[t], fma((double)val_code_at(c, u, t, ch), s, lo), acc);
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < d) {
+    double a = 0.0;
+    for (int l = 0; l < lanes; ++l) a += red[l * d + threadIdx.x];
+    part[(size_t)blockIdx.x * d + threadIdx.x] = a;
+  }
 }
 
-int qgemv_scores(const QC &c, int u, int64_t n, const float *q, float *logits, cudaStream_t st) {
-  qgemv_scores_kernel<<<148, 256, 0, st>>>(c, u, n, q, logits);
+__global__ void qgemv_output_sum_kernel(const double *__restrict__ part, int chunks, int d, double *__restrict__ out) {
+  for (int ch = threadIdx.x; ch < d; ch += blockDim.x) {
+    double a = 0.0;
+    for (int k = 0; k < chunks; ++k) a += part[(size_t)k * d + ch];
+    out[ch] = a;
+  }
+}
+
+int64_t qgemv_output_workspace(const QC &c, int64_t n) { return ((n + QG_CHUNK - 1) / QG_CHUNK) * c.d * 8 + 256; }
+
+int qgemv_scores(const QC &c, int u, int64_t n, const double *q, double *logits, cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>(1184, (n + 7) / 8);
+  qgemv_scores_kernel<<<std::max(blocks, 1), 256, 0, st>>>(c, u, n, q, logits);
   return check_launch("tkv_qgemv_scores");
 }
-int qgemv_output(const QC &c, int u, int64_t n, const float *w, float *out, cudaStream_t st) {
-  qgemv_output_kernel<<<(c.d + 63) / 64, 64, 0, st>>>(c, u, n, w, out);
+int qgemv_output(const QC &c, int u, int64_t n, const double *w, double *out, void *ws, cudaStream_t st) {
+  const int chunks = (int)((n + QG_CHUNK - 1) / QG_CHUNK);
+  double *part = static_cast<double *>(ws);
+  qgemv_output_part_kernel<<<chunks, 256, 0, st>>>(c, u, n, w, part);
+  qgemv_output_sum_kernel<<<1, 256, 0, st>>>(part, chunks, c.d, out);
   return check_launch("tkv_qgemv_output");
 }
 

@@ -84,6 +84,20 @@ class QuantizedLayerKV:
         obj.n = n
         return obj
 
+    def grow(self, capacity: int) -> None:
+        """Re-home the cache into buffers for ``capacity`` tokens (device
+        copies of every unit's token prefix; the layouts are per-unit blocks
+        whose token order does not depend on the capacity)."""
+        if capacity <= self.capacity:
+            return
+        bigger = QuantizedLayerKV(self.units, self.head_dim, self.bits, self.group_size, capacity, device=self.device)
+        for old, new in zip(self._bufs, bigger._bufs):
+            o, nw = old.view(self.units, -1), new.view(self.units, -1)
+            nw[:, :o.shape[1]].copy_(o)
+        bigger._len.copy_(self._len)
+        self._bufs, self._len, self.capacity, self.struct = bigger._bufs, bigger._len, bigger.capacity, bigger.struct
+        self._ws = {}
+
     # -- properties ---------------------------------------------------------
     @property
     def num_heads(self) -> int:
@@ -143,6 +157,16 @@ class QuantizedLayerKV:
         check(lib.tkv_qcache_export(C.byref(self.struct), unit, w, self.n, ptr(out), stream_ptr()))
         return out.cpu().numpy().tobytes()
 
+    def import_bytes(self, unit: int, which: str, blob: bytes) -> None:
+        """Load a GQT1 blob (GroupQuantizedTensor.to_bytes, quantizer.py:358-422)
+        into one unit's keys or values; the device token count becomes the
+        blob's row count (all units share it)."""
+        w = 0 if which == "keys" else 1
+        blob = bytes(blob)
+        ws = torch.empty(max(len(blob), 1), dtype=torch.uint8, device=self.device)
+        check(_lib.load().tkv_qcache_import(C.byref(self.struct), unit, w, blob, len(blob), ptr(ws), stream_ptr()))
+        self.n = int(self._len[0].item())
+
     def dequantize(self, unit: int, which: str = "keys") -> torch.Tensor:
         """[n, d] fp32 reconstruction (quantizer.py:335-352)."""
         out = torch.empty((self.n, self.head_dim), dtype=torch.float32, device=self.device)
@@ -156,23 +180,37 @@ def quantize_layer_kv(keys, values, bits: int, group_size: int, capacity: int | 
     return QuantizedLayerKV.from_kv(keys, values, bits, group_size, capacity)
 
 
-def qgemv_scores(query, qkv: QuantizedLayerKV, unit: int = 0) -> torch.Tensor:
-    """Unscaled logits of one head over its quantized keys (quantizer.py:505-533)."""
-    q = torch.as_tensor(np.asarray(query, np.float32) if not isinstance(query, torch.Tensor) else query)
-    q = q.to(device=qkv.device, dtype=torch.float32).reshape(-1).contiguous()
-    if q.numel() != qkv.head_dim:
-        raise ShapeError(f"query dim {q.numel()} != head_dim {qkv.head_dim}")
-    out = torch.empty(qkv.n, dtype=torch.float32, device=qkv.device)
-    check(_lib.load().tkv_qgemv_scores(C.byref(qkv.struct), unit, qkv.n, ptr(q), ptr(out), stream_ptr()))
+def _f64_vector(x, device, name: str, size: int) -> torch.Tensor:
+    t = torch.as_tensor(np.asarray(x, np.float64) if not isinstance(x, torch.Tensor) else x)
+    t = t.to(device=device, dtype=torch.float64).reshape(-1).contiguous()
+    if t.numel() != size:
+        raise ShapeError(f"{name} has {t.numel()} entries, expected {size}")
+    return t
+
+
+def qgemv_scores(query, qkv: QuantizedLayerKV, unit: int = 0, n: int | None = None) -> torch.Tensor:
+    """Unscaled float64 logits [n] of one head over its quantized keys
+    (quantizer.py:505-533): complete groups from the codes, the trailing
+    rows from the fp16 residual."""
+    n = qkv.n if n is None else n
+    if n < 1:
+        raise EmptyCacheError("scores over an empty cache")
+    q = _f64_vector(query, qkv.device, "query", qkv.head_dim)
+    out = torch.empty(n, dtype=torch.float64, device=qkv.device)
+    check(_lib.load().tkv_qgemv_scores(C.byref(qkv.struct), unit, n, ptr(q), ptr(out), stream_ptr()))
     return out
 
 
-def qgemv_output(weights, qkv: QuantizedLayerKV, unit: int = 0) -> torch.Tensor:
-    """``w V`` of one head over its quantized values (quantizer.py:536-558)."""
-    w = torch.as_tensor(np.asarray(weights, np.float32) if not isinstance(weights, torch.Tensor) else weights)
-    w = w.to(device=qkv.device, dtype=torch.float32).reshape(-1).contiguous()
-    if w.numel() != qkv.n:
-        raise ShapeError(f"weights length {w.numel()} != token count {qkv.n}")
-    out = torch.empty(qkv.head_dim, dtype=torch.float32, device=qkv.device)
-    check(_lib.load().tkv_qgemv_output(C.byref(qkv.struct), unit, qkv.n, ptr(w), ptr(out), stream_ptr()))
+def qgemv_output(weights, qkv: QuantizedLayerKV, unit: int = 0, n: int | None = None) -> torch.Tensor:
+    """float64 ``w V`` [d] of one head over its quantized values
+    (quantizer.py:536-558)."""
+    n = qkv.n if n is None else n
+    if n < 1:
+        raise EmptyCacheError("output over an empty cache")
+    w = _f64_vector(weights, qkv.device, "weights", n)
+    lib = _lib.load()
+    ws = torch.empty(int(lib.tkv_qgemv_output_workspace(C.byref(qkv.struct), n)), dtype=torch.uint8,
+                     device=qkv.device)
+    out = torch.empty(qkv.head_dim, dtype=torch.float64, device=qkv.device)
+    check(lib.tkv_qgemv_output(C.byref(qkv.struct), unit, n, ptr(w), ptr(out), ptr(ws), stream_ptr()))
     return out
