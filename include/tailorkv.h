@@ -197,6 +197,12 @@ typedef struct tkv_sparse_layer {
   /* [units][16] (with cache_slots): per slot partition, the slot the next
    * allocation scan starts from (the cache's clock hand), zero-initialised */
   int32_t *slot_hand;
+  /* Attention-sink tokens (an extension; the reference has none, 0 = the
+   * reference's selection): tokens [0, n_sink) are always selected besides
+   * the local window and the n_topk best of [n_sink, n - n_local), so
+   * sel_idx needs n_local + n_topk + n_sink entries per unit.  Fused decode
+   * and cluster select only (other paths fail with TKV_ERR_PARAMETER). */
+  int32_t n_sink;
 } tkv_sparse_layer;
 
 /* Prefill/offload (replaces HostPool.offload_layer memsim.py:88-93 and the

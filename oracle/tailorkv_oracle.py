@@ -354,6 +354,24 @@ def select_tokens(scores, n_local, n_topk) -> np.ndarray:
     return np.sort(np.concatenate([order[:n_topk], np.arange(start, n)]))
 
 
+def select_tokens_sinks(scores, n_local, n_topk, n_sink) -> np.ndarray:
+    """EXTENSION (not in the reference; north_star's "sink/local-window
+    tokens"): ``select_tokens`` with tokens [0, n_sink) always selected and
+    the Top-K taken over [n_sink, n - n_local) by the same rule (score desc,
+    index desc).  n_sink = 0 is exactly ``select_tokens``
+    (``retriever.py:192-211``)."""
+    s = np.asarray(scores, np.float64)
+    n = s.size
+    if n_sink == 0:
+        return select_tokens(s, n_local, n_topk)
+    if n <= n_local + n_topk + n_sink:
+        return np.arange(n)
+    ls = n - n_local
+    cand = np.arange(n_sink, ls)
+    top = cand[np.lexsort((-cand, -s[cand]))[:n_topk]]
+    return np.sort(np.concatenate([np.arange(n_sink), top, np.arange(ls, n)]))
+
+
 def sparse_attention(q, keys, values, selected) -> np.ndarray:
     """Exact softmax attention over the selected rows (``retriever.py:214-226``)."""
     sel = np.asarray(selected, np.intp)

@@ -59,7 +59,7 @@ class SparseLayer(C.Structure):
         ("kdev", C.c_void_p), ("host_kv", C.c_void_p), ("len", C.c_void_p), ("ticket", C.c_void_p),
         ("cache_slots", C.c_int32), ("cache_window", C.c_int32), ("slot_tok", C.c_void_p), ("slot_stamp", C.c_void_p),
         ("slot_v", C.c_void_p), ("tok_slot", C.c_void_p), ("cache_stats", C.c_void_p), ("thresh", C.c_void_p),
-        ("slot_hand", C.c_void_p),
+        ("slot_hand", C.c_void_p), ("n_sink", C.c_int32),
     ]
 
 

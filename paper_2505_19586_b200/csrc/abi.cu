@@ -329,6 +329,7 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
     return sparse_decode_fused(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                                keys_from_device, out, new_keys, new_values, as_stream(stream));
   // shapes outside the fused kernel: select, then gather + attention, then the append (three launches)
+  TKV_REQUIRE(s->n_sink == 0, TKV_ERR_PARAMETER, "attention sinks need the fused sparse decode (shape unsupported)");
   pdl_note(as_stream(stream), s->len);
   char *ws = static_cast<char *>(workspace);
   const int64_t sel_ws = (select_workspace(s->units, s->capacity) + 255) / 256 * 256;

@@ -1088,6 +1088,7 @@ int select_tokens(const SL &s, const uint16_t *queries, int G, const int32_t *ch
   if (select_cluster_ok(s, n_local) && !getenv("TKV_SELECT_MULTIKERNEL"))
     return select_cluster(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                           scores_out, st);
+  if (s.n_sink) return fail(TKV_ERR_PARAMETER, "attention sinks need the cluster select (shape unsupported)");
   SelWS w = carve(ws, s.units, s.capacity);
   const int blocks = (int)imin64(2048, (s.capacity + 255) / 256);
   score_hist_kernel<<<dim3(blocks, s.units), 256, 0, st>>>(s, queries, G, channels, d_s, n_local, n_topk, w,

@@ -510,6 +510,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
   extern __shared__ __align__(16) unsigned char smem[];
   FzShared &S = *reinterpret_cast<FzShared *>(smem);
   __shared__ FzCtl C;
+  // attention sinks (extension, s.n_sink = 0 for the reference): their keys are forced above every
+  // score, so the n_topk + n_sink best candidates are the sinks plus the n_topk best of the rest
+  const int n_sink = s.n_sink;
+  n_topk += n_sink;
   __shared__ double qsum[128];
   __shared__ float qsum32[128];
   __shared__ int chs[128];
@@ -635,8 +639,9 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
         uint32_t kk[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          kk[e] = fz_orderable32(acc[e]);
-          if (eg + e < m) {
+          const bool sink = j + e < n_sink;
+          kk[e] = sink ? 0xffffffffu : fz_orderable32(acc[e]);
+          if (eg + e < m && !sink) {
             klo = min(klo, kk[e]);
             khi = max(khi, kk[e]);
             fsum += acc[e];
@@ -690,10 +695,10 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     uint32_t *T = S.k.f.tot;   // cluster totals
     unsigned long long *list = S.k.f.list64;
     {
-      const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
+      const double N = (double)(ncand - imin64(ncand, n_sink)), mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
       const bool hinted = isfinite(hint.x);
       // the Gaussian estimate of the threshold (only without a hint or after an overflow)
-      auto gauss = [&]() { return mu + fz_normal_upper_quantile((double)n_topk / N) * sd; };
+      auto gauss = [&]() { return mu + fz_normal_upper_quantile((double)(n_topk - n_sink) / N) * sd; };
       const double tprev = mu + (double)hint.x * sd;
       double last_lo = 0.0, last_hi = 0.0;
       int dir = 0;
@@ -975,8 +980,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     // pass whose range misses the threshold falls back to the full range.
     double R_lo = flo, R_hi = fhi;
     {
-      const double N = (double)ncand, mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
-      const double z = fz_normal_upper_quantile((double)n_topk / N);
+      const double N = (double)(ncand - imin64(ncand, n_sink)), mu = gsum / N, var = fmax(gsq / N - mu * mu, 0.0), sd = sqrt(var);
+      const double z = fz_normal_upper_quantile((double)(n_topk - n_sink) / N);
       const double t = mu + z * sd;
       if (sd > 0.0 && isfinite(t)) {
         R_lo = fmax(flo, t - 0.6 * sd);
@@ -1182,7 +1187,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       // ---- float64 radix select (degenerate inputs, e.g. huge exact-tie sets) ----
       uint64_t *keys64 = S.k.keys64;
       cluster.sync();  // no CTA still reads this CTA's band arrays (aliased by keys64)
-      for (int e = tid; e < m; e += blockDim.x) keys64[e] = orderable(fz_exact_score(kt, s.capacity, chs, qsum, d_s, j0 + e));
+      for (int e = tid; e < m; e += blockDim.x)
+        keys64[e] = j0 + e < n_sink ? ~0ull : orderable(fz_exact_score(kt, s.capacity, chs, qsum, d_s, j0 + e));
       __syncthreads();
       int top, need64 = n_topk;
       unsigned long long prefix;
@@ -1192,7 +1198,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       fz_exact_flags(cluster, keys64, m, flags, C, top, prefix, need64, done);
     }
     if (rank == 0 && tid == 0 && s.thresh) {
-      const double N = (double)ncand, mu = gsum / N, sd = sqrt(fmax(gsq / N - mu * mu, 0.0));
+      const double N = (double)(ncand - imin64(ncand, n_sink)), mu = gsum / N, sd = sqrt(fmax(gsq / N - mu * mu, 0.0));
       if (sd > 0.0) fz_store_hint(s.thresh + 4 * u, hint, (0.5 * (R_lo + R_hi) - mu) / sd);
     }
     }  // full-range path
@@ -2143,7 +2149,8 @@ static cudaError_t launch_fused(const SL &s, const uint16_t *queries, int G, con
   at[2].val.programmaticStreamSerializationAllowed = (pdl_note(st, s.len) && !no_pdl) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 3;
-  return cudaLaunchKernelEx(&cfg, kern, s, queries, G, channels, d_s, n_local, n_topk, sel_idx, n_local + n_topk,
+  return cudaLaunchKernelEx(&cfg, kern, s, queries, G, channels, d_s, n_local, n_topk, sel_idx,
+                            n_local + n_topk + s.n_sink,
                             sel_count, fetch_count, scores_out, keys_from_device, out, new_keys, new_values);
 }
 

@@ -19,6 +19,7 @@ from dataclasses import dataclass, field
 
 import ctypes as C
 
+import numpy as np
 import torch
 
 from .errors import ConfigError, ShapeError
@@ -41,6 +42,7 @@ class EngineConfig:
     n_local: int = 64
     n_topk: int = 128
     critical_channels: int = 8
+    n_sink: int = 0                # extension: attention-sink tokens always selected (0 = the reference)
     keys_from_hbm: bool = True     # gather key rows from HBM; only V rows cross PCIe
     token_major_keys: bool = True  # keep a token-major HBM key copy for that gather (else read the scorer's
                                    # channel-major copy: no extra memory, 32x more DRAM sectors)
@@ -54,7 +56,7 @@ class EngineConfig:
     def validate(self) -> None:
         if self.bits not in (1, 2):
             raise ConfigError(f"bits must be 1 or 2 on the engine path, got {self.bits}")
-        if self.n_local < 0 or self.n_topk < 1 or self.critical_channels < 1:
+        if self.n_local < 0 or self.n_topk < 1 or self.critical_channels < 1 or self.n_sink < 0:
             raise ConfigError("token/channel budgets out of range")
 
 
@@ -183,13 +185,14 @@ class DecodeEngine:
         self.hq_r = self.shard.kv_heads * self.G
         self.d = model.head_dim
         self.device = torch.device(device or "cuda")
-        self.retrieval = RetrievalConfig(config.n_local, config.n_topk, min(config.critical_channels, self.d))
+        self.retrieval = RetrievalConfig(config.n_local, config.n_topk, min(config.critical_channels, self.d),
+                                         config.n_sink)
         self.layers: list = [None] * model.num_layers
         self.sparse: dict[int, _SparseState] = {}
         self.prefill_len = None
         self.side = torch.cuda.Stream(device=self.device)
         L, U, d = model.num_layers, self.units, self.d
-        kmax = self.retrieval.n_local + self.retrieval.n_topk
+        kmax = self.retrieval.max_selected
         dev = self.device
         # static per-step buffers (graph inputs/outputs)
         self.hidden = torch.zeros((L, self.shard.batch, model.hidden_dim), dtype=torch.float16, device=dev)
@@ -245,8 +248,8 @@ class DecodeEngine:
             lay = OffloadedLayerKV(self.units, self.d, cap, n, self.retrieval.n_local,
                                    keys_on_device=self.cfg.keys_from_hbm and self.cfg.token_major_keys,
                                    device=self.device,
-                                   cache_rows=(self.retrieval.n_local + self.retrieval.n_topk) if self.cfg.row_cache else 0,
-                                   cache_window=self.cfg.row_cache_steps)
+                                   cache_rows=self.retrieval.max_selected if self.cfg.row_cache else 0,
+                                   cache_window=self.cfg.row_cache_steps, n_sink=self.retrieval.n_sink)
             lay.offload(k, v)
             w = as_f16(w_q, self.device)
             if w.shape[0] == self.model.num_query_heads:
@@ -259,7 +262,7 @@ class DecodeEngine:
             self.sparse[layer] = _SparseState(lay, w, chans, ws)
             self.layers[layer] = lay
             # workspaces follow the largest layer capacity seen so far (prefill lengths may differ per layer)
-            kmax = self.retrieval.n_local + self.retrieval.n_topk
+            kmax = self.retrieval.max_selected
             need_sel = int(lib.tkv_select_workspace(self.units, lay.capacity))
             need_dec = int(lib.tkv_sparse_decode_workspace(self.units, lay.capacity, self.G, self.d, kmax))
             if self.sel_ws is None or self.sel_ws.numel() < need_sel:
@@ -274,6 +277,8 @@ class DecodeEngine:
         rank slice): hidden [L, B, hidden], queries [L, B, hq, d],
         new_keys/new_values [L, B, h, d]."""
         def sl(x, heads_per_unit):
+            if not isinstance(x, torch.Tensor):  # numpy / array-like step inputs (fp16 storage)
+                x = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float16)))
             return slice_step_input(x, self.shard, self.batch, self.model.num_kv_heads, heads_per_unit, self.world)
 
         self.hidden.copy_(sl(hidden, 0).reshape(self.hidden.shape), non_blocking=non_blocking)

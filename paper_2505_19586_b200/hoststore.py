@@ -72,7 +72,7 @@ class OffloadedLayerKV:
 
     def __init__(self, units: int, head_dim: int, capacity: int, prefill_len: int, n_local: int,
                  keys_on_device: bool = False, numa_node: int | None = None, device=None, cache_rows: int = 0,
-                 cache_window: int = 1):
+                 cache_window: int = 1, n_sink: int = 0):
         _lib.require_cuda()
         dev = torch.device(device or "cuda")
         self.device = dev
@@ -112,7 +112,8 @@ class OffloadedLayerKV:
                                   self._len.data_ptr(), self._len.data_ptr() + 4,
                                   self.cache_slots, self.cache_window, ptr(self.slot_tok), ptr(self.slot_stamp),
                                   ptr(self.slot_v), ptr(self.tok_slot), ptr(self.cache_stats), ptr(self.thresh),
-                                  ptr(self.slot_hand))
+                                  ptr(self.slot_hand), int(n_sink))
+        self.n_sink = int(n_sink)
 
     @property
     def keys_on_device(self) -> bool:
@@ -143,6 +144,10 @@ class OffloadedLayerKV:
             raise ParameterError("layer capacity exhausted")
         check(_lib.load().tkv_sparse_append(C.byref(self.struct), ptr(k), ptr(v), stream_ptr(stream)))
         self.n += 1
+
+    def _check_sinks(self, cfg: RetrievalConfig) -> None:
+        if cfg.n_sink != self.n_sink:
+            raise ParameterError(f"RetrievalConfig.n_sink={cfg.n_sink} but the layer was built with n_sink={self.n_sink}")
 
     def set_row_cache(self, enabled: bool) -> None:
         """Switch the HBM row cache on or off for later launches (a captured
@@ -176,6 +181,7 @@ class OffloadedLayerKV:
                sel_idx: torch.Tensor, sel_count: torch.Tensor, fetch_count: torch.Tensor, workspace: torch.Tensor,
                scores_out: torch.Tensor | None = None, stream=None) -> None:
         """Proxy scores with the true query + exact top-k (retriever.py:166-211)."""
+        self._check_sinks(cfg)
         check(_lib.load().tkv_select_tokens(C.byref(self.struct), ptr(queries), G, ptr(channels), channels.shape[1],
                                             cfg.n_local, cfg.n_topk, ptr(sel_idx), ptr(sel_count), ptr(fetch_count),
                                             ptr(scores_out), ptr(workspace), stream_ptr(stream)))
@@ -188,6 +194,7 @@ class OffloadedLayerKV:
         (pipeline.py:351-376); same results as ``select`` then ``attend``.
         With new_keys/new_values [units, d] the step's ``append`` runs in the
         same launch, after the attention."""
+        self._check_sinks(cfg)
         if (new_keys is None) != (new_values is None):
             raise ParameterError("new_keys and new_values must both be given")
         if new_keys is not None and self.n + 1 > self.capacity:

@@ -30,8 +30,16 @@ class RetrievalConfig:
     n_local: int = 64
     n_topk: int = 128
     d_s: int = 8
+    n_sink: int = 0  # extension: tokens [0, n_sink) always selected (attention sinks); 0 = the reference
+
+    @property
+    def max_selected(self) -> int:
+        """Selected rows per head at most: sinks + Top-K + local window."""
+        return self.n_local + self.n_topk + self.n_sink
 
     def __post_init__(self) -> None:
+        if self.n_sink < 0:
+            raise ParameterError(f"n_sink must be >= 0, got {self.n_sink}")
         if self.n_local < 0:
             raise ParameterError(f"n_local must be >= 0, got {self.n_local}")
         if self.n_topk < 1:

@@ -238,3 +238,16 @@ def test_timeline_measured_step_model():
     assert base["step_seconds"] == pytest.approx(2 * 45e-6 + 30 * 43e-6, rel=1e-9)
     more = T.measured_step(labels, 45e-6, 43e-6, 0.0, 29_000, 50e9)
     assert more["step_seconds"] == pytest.approx(base["step_seconds"] + 30 * 29_000 / 50e9, rel=1e-9)
+
+
+def test_select_tokens_sinks_extension():
+    """The sink extension reduces to the reference rule at n_sink = 0 and
+    always keeps [0, n_sink) plus exactly n_topk others outside the window."""
+    rng = np.random.default_rng(4)
+    s = np.round(rng.normal(size=3000))
+    assert np.array_equal(O.select_tokens_sinks(s, 16, 200, 0), O.select_tokens(s, 16, 200))
+    sel = O.select_tokens_sinks(s, 16, 200, 5)
+    assert sel.size == 16 + 200 + 5 and np.all(sel[:5] == np.arange(5))
+    rest = sel[(sel >= 5) & (sel < 3000 - 16)]
+    assert np.array_equal(rest, np.sort(O.select_tokens(s[5:], 16, 200)[:200] + 5))
+    assert np.array_equal(O.select_tokens_sinks(s[:100], 16, 50, 40), np.arange(100))
