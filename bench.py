@@ -500,15 +500,22 @@ def main():
     # fused kernel (unit 0, CTA rank 0) over one more plain-graph step ----
     lib = _lib.load()
     trace_mode = int(os.environ.get("TKV_FZ_DBG", "0")) & ~1
+    from tools.fz_phases import wide_enable, wide_launches
     lib.tkv_debug_sparse_launches(None, 1)
     lib.tkv_debug_sparse_trace(1 | trace_mode)
+    wide_enable(lib)
     eng.step(*inputs(step_i)); step_i += 1
     torch.cuda.synchronize()
     lib.tkv_debug_sparse_trace(trace_mode)
+    wide_enable(lib, False)
     import ctypes as C
     raw = (C.c_ulonglong * (128 * 3))()
     cnt = lib.tkv_debug_sparse_launches(raw, 0)
     stamps = [(raw[i * 3], raw[i * 3 + 1], raw[i * 3 + 2]) for i in range(min(cnt, 128))]
+    sparse_kernel = "cluster (sparse_fused_kernel, one 8-CTA cluster per unit)"
+    if not stamps:  # the wide decode ran (few units per GPU)
+        stamps = wide_launches(lib)
+        sparse_kernel = f"wide (sparse_wide_kernel, {_lib.wide_parts(eng.units)} CTAs per unit)"
     plain = None
     if len(stamps) >= 2 and not args.unfused:
         ends = [x[2] for x in stamps]
@@ -547,6 +554,13 @@ def main():
         _lib.load().tkv_debug_sparse_trace(int(os.environ.get("TKV_FZ_DBG", "0")) & ~1)
         print("plain graph:")
         show_launches(_lib.load())
+        from tools.fz_phases import wide_enable, wide_show
+        wide_enable(_lib.load())
+        eng.step(*inputs(step_i)); step_i += 1
+        torch.cuda.synchronize()
+        wide_enable(_lib.load(), False)
+        print("plain graph, wide decode:")
+        wide_show(_lib.load(), _lib.wide_parts(eng.units))
     fetch_rows = int(eng.fetch_count.sum().item())
     cached_rows = hits / (PROF * n_sparse)     # per launch, served from the HBM row cache
     pcie_rows = misses / (PROF * n_sparse)     # per launch, fetched over PCIe
@@ -642,10 +656,10 @@ def main():
                           "pcie_bytes": gather_bytes, "pcie_gbs": gather_bytes / (sparse_ms * 1e-3) / 1e9,
                           "pcie_peak": memcpy_gbs,
                           "pcie_peak_source": "measured pinned cudaMemcpyAsync H2D 256 MiB, this run",
-                          "kernel": "sparse_fused_kernel (scores + top-k + gather + attention)" if not args.unfused
-                          else "select + sparse_attn",
+                          "kernel": (f"{sparse_kernel}: scores + top-k + gather + attention + append"
+                                     if not args.unfused else "select + sparse_attn"),
                           "timing": ("layer period in the plain timed graph: (end of the last sparse launch - end of "
-                                     "the first) / (launches - 1), globaltimer stamps of unit 0's CTA rank 0"
+                                     "the first) / (launches - 1), globaltimer stamps of unit 0"
                                      if plain is not None else "graph event nodes"),
                           "body_ms": plain["body_ms"] if plain else None, "graph_node_ms": sparse_node_ms},
         "quant_decode": {"bound": "hbm", "achieved": quant_bytes / (quant_ms * 1e-3) / 1e9, "peak": hbm_peak,

@@ -194,8 +194,9 @@ typedef struct tkv_sparse_layer {
    * next step's threshold search (results never depend on it; NaN or NULL =
    * no hint). */
   float *thresh;
-  /* [units][16] (with cache_slots): per slot partition, the slot the next
-   * allocation scan starts from (the cache's clock hand), zero-initialised */
+  /* [units][TKV_MAX_PARTS] (with cache_slots): per slot partition, the slot
+   * the next allocation scan starts from (the cache's clock hand),
+   * zero-initialised */
   int32_t *slot_hand;
   /* Attention-sink tokens (an extension; the reference has none, 0 = the
    * reference's selection): tokens [0, n_sink) are always selected besides
@@ -203,7 +204,15 @@ typedef struct tkv_sparse_layer {
    * sel_idx needs n_local + n_topk + n_sink entries per unit.  Fused decode
    * and cluster select only (other paths fail with TKV_ERR_PARAMETER). */
   int32_t n_sink;
+  /* Optional [units][TKV_MAX_PARTS][2] float (NaN-initialised): the wide
+   * decode's per-partition threshold hint (z-score of the last top-k
+   * threshold against that partition's own score moments, running mean of
+   * its step-to-step change).  Like `thresh`, it only aims the search. */
+  float *part_hint;
 } tkv_sparse_layer;
+
+/* Token partitions per unit of the wide sparse decode (and slot_hand stride). */
+#define TKV_MAX_PARTS 256
 
 /* Prefill/offload (replaces HostPool.offload_layer memsim.py:88-93 and the
  * local mirror of pipeline.py:183-193): keys/values fp16 [units][n][d] on the
@@ -267,8 +276,12 @@ int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int
  * exact top-k plus the local window, gather (value rows over PCIe or from the
  * HBM row cache, key rows from HBM when keys_from_device != 0) and exact
  * softmax attention.  Outputs are those of tkv_select_tokens followed by
- * tkv_sparse_attention; `workspace` >= tkv_sparse_decode_workspace bytes (used
- * only by shapes outside the fused kernel).  With new_keys/new_values fp16
+ * tkv_sparse_attention; `workspace` >= tkv_sparse_decode_workspace bytes, zero
+ * before its first use (its tail holds the wide decode's per-unit barrier and
+ * merge counters, which every launch leaves at zero again; the rest is
+ * scratch).  With few units per GPU (units x partitions <= SMs) the decode
+ * spreads each unit over several CTAs (the wide decode: one grid barrier per
+ * unit on the common path); otherwise one thread-block cluster per unit.  With new_keys/new_values fp16
  * [units][d] (else NULL) the step's append (tkv_sparse_append) is fused into
  * the same launch, after the attention (attend-before-append,
  * pipeline.py:315-413). */

@@ -59,8 +59,11 @@ class SparseLayer(C.Structure):
         ("kdev", C.c_void_p), ("host_kv", C.c_void_p), ("len", C.c_void_p), ("ticket", C.c_void_p),
         ("cache_slots", C.c_int32), ("cache_window", C.c_int32), ("slot_tok", C.c_void_p), ("slot_stamp", C.c_void_p),
         ("slot_v", C.c_void_p), ("tok_slot", C.c_void_p), ("cache_stats", C.c_void_p), ("thresh", C.c_void_p),
-        ("slot_hand", C.c_void_p), ("n_sink", C.c_int32),
+        ("slot_hand", C.c_void_p), ("n_sink", C.c_int32), ("part_hint", C.c_void_p),
     ]
+
+
+MAX_PARTS = 256  # TKV_MAX_PARTS (tailorkv.h)
 
 
 _P = C.c_void_p
@@ -143,6 +146,18 @@ def load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def set_sparse_kernel(mode: int) -> None:
+    """Which kernel runs a fused sparse decode: -1 auto (the wide decode when a
+    GPU holds few units, else one cluster per unit), 0 always the cluster
+    kernel, 1 the wide decode whenever the shape allows (tests, experiments)."""
+    load().tkv_debug_sparse_wide(int(mode))
+
+
+def wide_parts(units: int) -> int:
+    """Token partitions (CTAs) per unit of the wide sparse decode on this GPU."""
+    return int(load().tkv_wide_parts(int(units)))
 
 
 def check(status: int) -> None:

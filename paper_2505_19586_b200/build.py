@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtailorkv.so"
-SOURCES = ["abi.cu", "qcache.cu", "decode.cu", "decode_imma.cu", "sparse.cu", "sparse_fused.cu", "calibrate.cu", "fidelity.cu", "refops.cu"]
+SOURCES = ["abi.cu", "qcache.cu", "decode.cu", "decode_imma.cu", "sparse.cu", "sparse_fused.cu", "calibrate.cu", "fidelity.cu", "refops.cu", "sparse_wide.cu"]
 # extra objects: (source, object stem, defines) -- the fused sparse kernel again with 4-CTA clusters
 VARIANTS = [("sparse_fused.cu", "sparse_fused4", ["-DTKV_FZ_CTAS=4"])]
 NVCC_FLAGS = [

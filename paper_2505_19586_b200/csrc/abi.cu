@@ -314,6 +314,12 @@ int tkv_topk_from_scores(const double *scores, int32_t units, int64_t n, int32_t
   return topk_from_scores(scores, units, n, n_local, n_topk, sel_idx, sel_count, workspace, as_stream(stream));
 }
 
+// byte sizes of the wide decode's regions at the front of the decode workspace
+static void decode_ws_parts(int units, int d, int64_t *ctl_b, int64_t *scr_b) {
+  *ctl_b = (wide::ctl_bytes(units, d) + 255) / 256 * 256;
+  *scr_b = (wide::scratch_bytes(units, d) + 255) / 256 * 256;
+}
+
 int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
                       int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
                       int32_t *fetch_count, int32_t keys_from_device, const uint16_t *new_keys,
@@ -325,13 +331,20 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
   TKV_REQUIRE(G >= 1 && G <= 8, TKV_ERR_SHAPE, "group size must lie in [1, 8]");
   TKV_REQUIRE((new_keys == nullptr) == (new_values == nullptr), TKV_ERR_PARAMETER,
               "new_keys and new_values must both be given or both be NULL");
+  // workspace: [wide counters | wide scratch | the unfused path's region] (decode_ws_parts)
+  int64_t ctl_b, scr_b;
+  decode_ws_parts(s->units, s->d, &ctl_b, &scr_b);
+  char *ws0 = static_cast<char *>(workspace);
+  if (wide::supported(*s, G, n_local, d_s, keys_from_device))
+    return wide::decode(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
+                        keys_from_device, out, new_keys, new_values, ws0, ws0 + ctl_b, as_stream(stream));
   if (sparse_decode_supported(*s, G, n_local))
     return sparse_decode_fused(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                                keys_from_device, out, new_keys, new_values, as_stream(stream));
-  // shapes outside the fused kernel: select, then gather + attention, then the append (three launches)
+  // shapes outside the fused kernels: select, then gather + attention, then the append (three launches)
   TKV_REQUIRE(s->n_sink == 0, TKV_ERR_PARAMETER, "attention sinks need the fused sparse decode (shape unsupported)");
   pdl_note(as_stream(stream), s->len);
-  char *ws = static_cast<char *>(workspace);
+  char *ws = ws0 + ctl_b + scr_b;
   const int64_t sel_ws = (select_workspace(s->units, s->capacity) + 255) / 256 * 256;
   if (int r = select_tokens(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count, nullptr,
                             ws, as_stream(stream)))
@@ -357,7 +370,10 @@ int tkv_sparse_fidelity(const tkv_sparse_layer *s, const uint16_t *queries, int3
 }
 
 int64_t tkv_sparse_decode_workspace(int32_t units, int64_t capacity, int32_t G, int32_t d, int32_t max_rows) {
-  return (select_workspace(units, capacity) + 255) / 256 * 256 + sparse_attn_workspace(units, G, d, max_rows);
+  int64_t ctl_b, scr_b;
+  decode_ws_parts(units, d, &ctl_b, &scr_b);
+  return ctl_b + scr_b + (select_workspace(units, capacity) + 255) / 256 * 256 +
+         sparse_attn_workspace(units, G, d, max_rows);
 }
 
 int64_t tkv_sparse_attn_workspace(int32_t units, int32_t G, int32_t d, int32_t max_rows) {

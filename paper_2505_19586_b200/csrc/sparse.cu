@@ -245,8 +245,11 @@ __device__ __forceinline__ uint4 s1_ld_nc_v4(const void *p) {
 // of each (sequence group, KV head) runs the channel selection (no second
 // launch).
 constexpr int S1_THREADS = 512;
-template <int D, int BG>
-__global__ void __launch_bounds__(S1_THREADS, 2) stage1_fused_kernel(const uint16_t *__restrict__ hidden,
+// T threads per CTA: 512 in general; 256 for one sequence, so a stage-1 CTA (256 x 64 registers,
+// ~15 KB of shared memory) fits on an SM beside a wide sparse-decode CTA (512 x 96 registers)
+// and stage 1 streams W_q on every SM while the decode chain runs
+template <int D, int BG, int T = S1_THREADS>
+__global__ void __launch_bounds__(T, T == 256 ? 4 : 2) stage1_fused_kernel(const uint16_t *__restrict__ hidden,
                                                                   const uint16_t *__restrict__ w_q, int B, int H,
                                                                   int rows_per_cta, double *__restrict__ part,
                                                                   unsigned *__restrict__ arrive, int G,
@@ -254,10 +257,10 @@ __global__ void __launch_bounds__(S1_THREADS, 2) stage1_fused_kernel(const uint1
                                                                   double *__restrict__ q_hat,
                                                                   int32_t *__restrict__ channels, SL pf, int prefetch) {
   constexpr int TPR = D / 8;               // threads per row
-  constexpr int RG = S1_THREADS / TPR;     // row groups
+  constexpr int RG = T / TPR;              // row groups
   constexpr int BATCH = 8;                 // loads in flight per thread and batch
   __shared__ float hs[BG][1024];
-  __shared__ float red[S1_THREADS * 8];
+  __shared__ float red[T * 8];
   __shared__ bool last;
   const int qh = blockIdx.y, split = blockIdx.x, bg = blockIdx.z;
   const int hq = gridDim.y, splits = gridDim.x;
@@ -746,8 +749,20 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
   unsigned *arrive = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + pbytes);
   const int bg = B == 1 ? 1 : S1_BG;
   const dim3 grid((H + rows - 1) / rows, hq, (B + bg - 1) / bg);
+  {
+    // one sequence: the 256-thread CTAs share SMs with the wide sparse decode, which runs with
+    // the maximum shared-memory carveout; the same carveout lets both kernels sit on one SM
+    static bool carve = false;
+    if (!carve) {
+      carve = true;
+      cudaFuncSetAttribute(stage1_fused_kernel<128, 1, 256>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(stage1_fused_kernel<64, 1, 256>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(stage1_fused_kernel<256, 1, 256>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(stage1_fused_kernel<32, 1, 256>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+  }
 #define TKV_S1(DD)                                                                                              \
-  (B == 1 ? launch_prio(stage1_fused_kernel<DD, 1>, grid, dim3(S1_THREADS), 0, st, false, hidden, w_q, B, H, rows, \
+  (B == 1 ? launch_prio(stage1_fused_kernel<DD, 1, 256>, grid, dim3(256), 0, st, false, hidden, w_q, B, H, rows,  \
                         part, arrive, G, chmax, d_s, q_hat, channels, pfs, pf ? 1 : 0)                           \
           : launch_prio(stage1_fused_kernel<DD, S1_BG>, grid, dim3(S1_THREADS), 0, st, false, hidden, w_q, B, H,  \
                         rows, part, arrive, G, chmax, d_s, q_hat, channels, pfs, pf ? 1 : 0))

@@ -26,6 +26,15 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
                         float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st);
 }  // namespace fz4
+namespace wide {  // the wide decode (sparse_wide.cu): P CTAs per unit, for few units per GPU
+bool supported(const SL &s, int G, int n_local, int d_s, int keys_from_device);
+int64_t ctl_bytes(int units, int d);      // per-unit counters + histograms (zero between launches)
+int64_t scratch_bytes(int units, int d);  // per-unit headers, lists, partials
+int parts_for(int units);
+int decode(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local, int n_topk,
+           int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device, float *out,
+           const uint16_t *new_keys, const uint16_t *new_values, void *ctl, void *scratch, cudaStream_t st);
+}  // namespace wide
 int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
                         float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st);

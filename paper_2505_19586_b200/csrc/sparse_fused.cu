@@ -1482,7 +1482,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
           }
           need = min(need, FCAP);
           const int np = p1 - p0;
-          int32_t *hand = s.slot_hand ? s.slot_hand + (size_t)u * 16 + rank : nullptr;
+          int32_t *hand = s.slot_hand ? s.slot_hand + (size_t)u * TKV_MAX_PARTS + rank : nullptr;
           const int h0 = hand && np > 0 ? ((*hand % np) + np) % np : 0;
           int found = 0;
           for (int k0 = 0; found < need && k0 < np; k0 += 32) {  // warp-uniform: found, need, np

@@ -101,18 +101,19 @@ class OffloadedLayerKV:
             self.slot_v = torch.zeros((units, self.cache_slots, 2, d), dtype=torch.float16, device=dev)  # K|V
             self.tok_slot = torch.full((units, self.capacity), -1, dtype=torch.int32, device=dev)
             self.cache_stats = torch.zeros(2, dtype=torch.int64, device=dev)
-            self.slot_hand = torch.zeros((units, 16), dtype=torch.int32, device=dev)
+            self.slot_hand = torch.zeros((units, _lib.MAX_PARTS), dtype=torch.int32, device=dev)
         else:
             self.slot_tok = self.slot_stamp = self.slot_v = self.tok_slot = self.cache_stats = None
             self.slot_hand = None
         self.thresh = torch.full((units, 4), float("nan"), dtype=torch.float32, device=dev)  # top-k threshold hint
+        self.part_hint = torch.full((units, _lib.MAX_PARTS, 2), float("nan"), dtype=torch.float32, device=dev)
         self.struct = SparseLayer(units, d, self.capacity, self.local_offset, self.local_capacity,
                                   self.kt.data_ptr(), self.chmax.data_ptr(), self.loc_k.data_ptr(),
                                   self.loc_v.data_ptr(), ptr(self.kdev), self.arena.addr,
                                   self._len.data_ptr(), self._len.data_ptr() + 4,
                                   self.cache_slots, self.cache_window, ptr(self.slot_tok), ptr(self.slot_stamp),
                                   ptr(self.slot_v), ptr(self.tok_slot), ptr(self.cache_stats), ptr(self.thresh),
-                                  ptr(self.slot_hand), int(n_sink))
+                                  ptr(self.slot_hand), int(n_sink), self.part_hint.data_ptr())
         self.n_sink = int(n_sink)
 
     @property

@@ -143,7 +143,8 @@ def test_engine_two_ranks_match_one_rank(tkv, batch):
     after the per-layer all-gather every rank holds the full head outputs,
     the selections of each rank's units equal the one-rank engine's, and the
     outputs equal it within fp32 split-K rounding (the quantized decode's
-    split count follows the units per GPU)."""
+    split count and the sparse decode's partitions per unit follow the units
+    per GPU)."""
     import torch.multiprocessing as mp
 
     n, steps, seed, world = 6000, 3, 5, 2
@@ -163,10 +164,9 @@ def test_engine_two_ranks_match_one_rank(tkv, batch):
         for l in range(_MODEL["num_layers"]):
             a, b = outs[:, l].reshape(-1, 128), ref_out[:, l].reshape(-1, 128)
             err_l = np.max(np.linalg.norm(a - b, axis=1) / np.maximum(np.linalg.norm(b, axis=1), 1e-30))
-            if l in _Q_LAYERS:
-                assert err_l <= 1e-5, (rank, l, err_l)
-            else:  # one cluster per unit either way: bit-identical
-                assert np.array_equal(a, b), (rank, l, err_l)
+            # the quantized decode's split count and the wide sparse decode's token partitions per
+            # unit both follow the units per GPU, so the fp32 summation order differs by rank count
+            assert err_l <= 1e-5, (rank, l, err_l)
         for t in range(steps):
             for l, (shard, idx, cnt, fc) in sels[t].items():
                 _, ridx, rcnt, rfc = ref_sel[t][l]

@@ -92,3 +92,57 @@ def show(lib):
                 parts.append(f"{NAMES[i]} {(t[r][i] - prev) / 1e3:.1f}")
                 prev = t[r][i]
         print(f"rank {r} start+{(t[r][0] - t0) / 1e3:.1f}: " + " ".join(parts) + f" | end {(prev - t0) / 1e3:.1f} us")
+
+
+WIDE_MARKS = {1: "pdl-wait", 2: "tma", 3: "score", 4: "list", 6: "barrier", 14: "r:sync", 15: "r:hdr",
+              16: "r:lists+counts", 17: "r:hist", 18: "r:band", 19: "r:f64", 20: "r:rank", 21: "r:pcount",
+              8: "resolve-end", 9: "output", 10: "gather", 11: "merge-arrive", 12: "final-merge", 13: "append"}
+WIDE_ORDER = [1, 2, 3, 4, 6, 14, 15, 16, 17, 18, 19, 20, 21, 8, 9, 10, 11, 12, 13]
+
+
+def wide_enable(lib, on=True):
+    lib.tkv_debug_wide_trace(1 if on else 0)
+    if on:
+        lib.tkv_debug_wide_launches(None, 1)
+
+
+def wide_launches(lib):
+    """[(start, after-wait, end)] of unit 0 for the launches since the last reset (<= 128)."""
+    raw = (C.c_ulonglong * (128 * 3))()
+    cnt = lib.tkv_debug_wide_launches(raw, 0)
+    v = list(raw)
+    idx = [i % 128 for i in range(max(0, cnt - min(cnt, 128)), cnt)]
+    return [(v[i * 3], v[i * 3 + 1], v[i * 3 + 2]) for i in idx]
+
+
+def wide_show(lib, parts=18):
+    """Per-partition phase marks of unit 0 in the last wide launch, and launch gaps."""
+    pc = (C.c_uint * 4)()
+    lib.tkv_debug_wide_paths(pc)
+    print(f"  wide select paths (units x launches): list 0 {pc[0]}, list 1 {pc[1]}, radix {pc[2]}, exact radix {pc[3]}")
+    rows = wide_launches(lib)
+    if len(rows) > 1:
+        med = lambda x: sorted(x)[len(x) // 2]  # noqa: E731
+        per = [(rows[k][2] - rows[k - 1][2]) / 1e3 for k in range(1, len(rows))]
+        wait = [(r[1] - r[0]) / 1e3 for r in rows]
+        body = [(r[2] - r[1]) / 1e3 for r in rows]
+        gap = [(rows[k][1] - rows[k - 1][2]) / 1e3 for k in range(1, len(rows))]
+        print(f"  wide launches ({len(rows)}): period median {med(per):.2f} us, start->wait-done {med(wait):.2f}, "
+              f"wait-done->end {med(body):.2f}, prev end->wait-done {med(gap):.2f}")
+    dbg = (C.c_int * 8)()
+    lib.tkv_debug_wide_dbg(dbg)
+    print(f"  unit 0 lists: merged {dbg[0]}, in window {dbg[4]}, band {dbg[1]}, need in band {dbg[2]}, "
+          f"above all lists {dbg[3]}")
+    mk = (C.c_ulonglong * (32 * 24))()
+    lib.tkv_debug_wide_marks(mk)
+    t = [list(mk)[p * 24:(p + 1) * 24] for p in range(min(parts, 32))]
+    t0 = min(x[1] for x in t if x[1])
+    for p, x in enumerate(t):
+        parts_s, prev = [], x[1]
+        for i in WIDE_ORDER:
+            if i == 1 or not x[i] or x[i] < prev:
+                continue
+            parts_s.append(f"{WIDE_MARKS[i]} {(x[i] - prev) / 1e3:.2f}")
+            prev = x[i]
+        print(f"  part {p:2d} start {(x[0] - t0) / 1e3:+.2f} wait-done {(x[1] - t0) / 1e3:+.2f}: " + " ".join(parts_s)
+              + f" | end {(prev - t0) / 1e3:.2f} us")

@@ -1,0 +1,22 @@
+#!/usr/bin/env bash
+# ncu evidence for the bench's kernels (run on the GPU box from the repo root):
+#   1. launch list of one main-mode step (cold, serialised; compare shares, not absolutes)
+#   2. --set full captures of a main-mode sparse launch, the quantized decode and stage 1
+# Outputs land in gpurun_out/ncu_*; bench lines printed under ncu are never bench values.
+set -u
+OUT=gpurun_out
+mkdir -p $OUT
+TAG=${1:-r2}
+BENCH="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-fidelity"
+NCU=ncu
+# only this repo's kernels (torch's workload generation is skipped by the name filter); the
+# variant mode runs first (~9 steps x 64 launches), so -s 900 lands in the main mode
+$NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k 'regex:^(?!.*(native|at_cuda|at::|cub)).*' -s 900 -c 128 --csv --log-file $OUT/ncu_${TAG}_launches.csv $BENCH > $OUT/ncu_${TAG}_launches.log 2>&1
+for spec in "sparse_fused:400" "quant_decode_pipe:20" "stage1:400"; do
+    name=${spec%%:*}; skip=${spec##*:}
+    $NCU --set full --clock-control none --import-source on -k regex:$name -s $skip -c 1 \
+        -o $OUT/ncu_${TAG}_$name -f $BENCH > $OUT/ncu_${TAG}_$name.log 2>&1
+    $NCU -i $OUT/ncu_${TAG}_$name.ncu-rep --page raw --csv > $OUT/ncu_${TAG}_${name}_raw.csv 2>/dev/null
+    $NCU -i $OUT/ncu_${TAG}_$name.ncu-rep --page details > $OUT/ncu_${TAG}_${name}_details.txt 2>/dev/null
+done
