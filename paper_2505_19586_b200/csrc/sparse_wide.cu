@@ -64,19 +64,26 @@ constexpr int WK_D = 128;                       // head_dim of this kernel
 constexpr int WK_MAXM = 8192;                   // candidate tokens per partition
 constexpr int WK_MAXDS = 8;                     // critical channels staged by TMA
 constexpr int WK_RAW = WK_MAXDS * WK_MAXM * 2;  // 128 KB: scorer columns -> merged lists -> staged rows
-constexpr int WK_MAXLOC = 1024;                 // local-window rows per partition
+constexpr int WK_MAXLOC = 512;                  // local-window rows per partition
 constexpr int WK_KEYS = (WK_MAXM + WK_MAXLOC) * 4;  // keys32, then the partition's row list
 constexpr int WK_LCAP = 1024;                   // list entries per partition and attempt
-constexpr int WK_GCAP = 8192;                   // merged list entries per unit (64 KB of SMEM)
+constexpr int WK_GCAP = 4096;                   // merged list entries per unit (64 KB of SMEM)
 constexpr int WK_BAND = 512;                    // band members rescored in float64
-constexpr int WK_NB = 1024;                     // resolve histogram bins
+constexpr int WK_NB = 1024;                     // resolve histogram bins (two per thread)
 constexpr int WK_HB = 2048;                     // radix bins (fallback)
 constexpr int WK_NHIST = 12;                    // 3 fp32 passes + 9 (float64 score, index) passes
 constexpr int WK_GS = 16;                       // merge group size when P > 32
-constexpr int WK_FCAP = 1024;                   // cache slots allocated per partition and step
-constexpr int WK_NMARK = 24;
+constexpr int WK_FCAP = 512;                    // cache slots allocated per partition and round
+constexpr int WK_NMARK = 32;
 constexpr unsigned WK_SPIN_LIMIT = 1u << 26;    // ~seconds: a stuck barrier becomes an error, not a hang
-static_assert(WK_GCAP * 8 + TKV_MAX_PARTS * 64 <= WK_RAW, "merged list + header table fit the scorer region");
+// a list entry: (order-preserving fp32 key << 32 | token index) and the token's float64 score
+// (exact: computed from the partition's fp16 scorer columns in SMEM, in the reference's channel order)
+struct LEnt {
+  unsigned long long kidx;
+  double s;
+};
+static_assert(WK_GCAP * 16 + TKV_MAX_PARTS * 64 <= WK_RAW, "merged list + header table fit the scorer region");
+static_assert(WK_NB == 2 * WK_THREADS && WK_MAXM / 32 <= WK_THREADS, "one thread per bin pair / mask word");
 
 // ---------------------------------------------------------------------------
 // helpers
@@ -180,11 +187,11 @@ struct Hdr {  // one partition's published state for one attempt (64 B)
 };
 static_assert(sizeof(Hdr) == 64, "header layout");
 constexpr int CTL_WORDS = 64;  // bar_count, bar_gen, merge_final, fallback, err, merge_group[16] ...
-enum { C_BAR = 0, C_GEN = 1, C_FINAL = 2, C_FALLBACK = 3, C_ERR = 4, C_GROUP = 8 };
+enum { C_BAR = 0, C_GEN = 1, C_FINAL = 2, C_FALLBACK = 3, C_ERR = 4, C_GROUP = 8 };  // [C_BAR, C_GEN]: one u64
 __host__ __device__ constexpr int64_t ctl_unit_bytes() { return CTL_WORDS * 4 + (int64_t)WK_NHIST * WK_HB * 4; }
 __host__ __device__ constexpr int part_floats(int gmax) { return gmax * WK_D + 2 * gmax; }
 __host__ __device__ inline int64_t scratch_unit_bytes(int P) {
-  const int64_t hdr = 2LL * P * 64, lists = 2LL * P * WK_LCAP * 8, counts = ((int64_t)P * 4 + 255) / 256 * 256;
+  const int64_t hdr = 2LL * P * 64, lists = 2LL * P * WK_LCAP * 16, counts = ((int64_t)P * 4 + 255) / 256 * 256;
   const int NG = (P + WK_GS - 1) / WK_GS + 1;
   const int64_t parts = (int64_t)(P + NG) * part_floats(8) * 4;
   return (hdr + lists + counts + parts + 255) / 256 * 256;
@@ -211,6 +218,7 @@ struct WSh {
   int chs[WK_MAXDS];
   double qsum[WK_MAXDS];
   float qsum32[WK_MAXDS];
+  double eps_term[WK_MAXDS];
   double band_eps;
   uint32_t r_lo[WK_WARPS], r_hi[WK_WARPS];
   double r_sum[WK_WARPS], r_sq[WK_WARPS];
@@ -246,12 +254,15 @@ struct WSh {
   int scan[WK_WARPS + 1];
   int offset, far_total, cta_total;
   int hits, misses, last, free_slots[WK_FCAP];
+  int nrest;
   float m_new[8];
   // compact-path state
   float fsum, fsq;
   uint32_t llo, lhi;
   float wlo_f, whi_f;
   int cnt_a, cnt_b, cnt_c;
+  uint32_t amask[WK_MAXM / 32];  // selected keys of this partition, 32 per word (index order)
+
   int wtot[WK_WARPS], wbase[WK_WARPS];
 };
 
@@ -259,7 +270,7 @@ struct UnitWs {
   unsigned *ctl;
   unsigned *hist;
   Hdr *hdr;                    // [2][P]
-  unsigned long long *lists;   // [2][P][LCAP]
+  LEnt *lists;                 // [2][P][LCAP]
   int *counts;                 // [P]
   float *part;                 // [P + NG][part_floats(8)]
 };
@@ -272,29 +283,63 @@ __device__ __forceinline__ UnitWs unit_ws(const WArgs &a, int u, int P) {
   unsigned char *s = a.scratch + (size_t)u * a.scratch_unit;
   w.hdr = reinterpret_cast<Hdr *>(s);
   s += 2LL * P * 64;
-  w.lists = reinterpret_cast<unsigned long long *>(s);
-  s += 2LL * P * WK_LCAP * 8;
+  w.lists = reinterpret_cast<LEnt *>(s);
+  s += 2LL * P * WK_LCAP * 16;
   w.counts = reinterpret_cast<int *>(s);
   s += ((int64_t)P * 4 + 255) / 256 * 256;
   w.part = reinterpret_cast<float *>(s);
   return w;
 }
 
-// one unit's grid barrier (sense by generation); thread 0 spins, bounded
+// one unit's grid barrier: a 64-bit word (arrivals | generation << 32).  The
+// last of P arrivals adds 2^32 - (P - 1), which resets the arrivals and bumps
+// the generation in one atomic; the others poll the generation.  Thread 0
+// spins, bounded (a stuck barrier becomes an error flag, never a hang).
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// split form: arrive (thread 0; returns the generation to wait past), then wait
+__device__ __forceinline__ unsigned unit_arrive(unsigned *ctl, int P) {
+  __syncthreads();
+  unsigned g = 0;
+  if (threadIdx.x == 0) {
+    unsigned long long *word = reinterpret_cast<unsigned long long *>(&ctl[C_BAR]);
+    __threadfence();  // this CTA's lists and header before the arrival
+    const unsigned long long old = atomicAdd(word, 1ull);
+    g = (unsigned)(old >> 32);
+    if ((unsigned)old == (unsigned)P - 1) atomicAdd(word, (1ull << 32) - (unsigned long long)P);
+  }
+  return g;
+}
+__device__ __forceinline__ void unit_wait(unsigned *ctl, unsigned g) {
+  if (threadIdx.x == 0) {
+    const unsigned long long *word = reinterpret_cast<const unsigned long long *>(&ctl[C_BAR]);
+    unsigned it = 0;
+    while ((unsigned)(ld_acquire64(word) >> 32) == g) {
+      if (++it > WK_SPIN_LIMIT) {
+        atomicExch(&ctl[C_ERR], 1u);
+        atomicExch(&g_wk_err, 1u);
+        break;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
 __device__ __forceinline__ void unit_barrier(unsigned *ctl, int P) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = ld_acquire(&ctl[C_GEN]);
-    __threadfence();
-    const unsigned old = atomicAdd(&ctl[C_BAR], 1u);
-    if (old == (unsigned)P - 1) {
-      atomicExch(&ctl[C_BAR], 0u);
-      __threadfence();
-      atomicAdd(&ctl[C_GEN], 1u);
+    unsigned long long *word = reinterpret_cast<unsigned long long *>(&ctl[C_BAR]);
+    __threadfence();  // this CTA's lists and header before the arrival
+    const unsigned long long old = atomicAdd(word, 1ull);
+    const unsigned g = (unsigned)(old >> 32);
+    if ((unsigned)old == (unsigned)P - 1) {
+      atomicAdd(word, (1ull << 32) - (unsigned long long)P);
     } else {
       unsigned it = 0;
-      while (ld_acquire(&ctl[C_GEN]) == g) {
-        __nanosleep(32);
+      while ((unsigned)(ld_acquire64(word) >> 32) == g) {
         if (++it > WK_SPIN_LIMIT) {
           atomicExch(&ctl[C_ERR], 1u);
           atomicExch(&g_wk_err, 1u);
@@ -399,16 +444,171 @@ __device__ __forceinline__ double exact_score(const uint16_t *kt, int64_t cap, c
 // trace marks of unit 0 (partitions < 32)
 constexpr int WK_TRACE_P = 32;
 __device__ int g_wk_trace;
+__device__ int g_wk_exp;  // experiments
 __device__ unsigned long long g_wk_mark[WK_TRACE_P][WK_NMARK];
 __device__ unsigned int g_wk_path[4];  // select paths taken (units x launches): list 0, list 1, radix, exact radix
 __device__ int g_wk_dbg[8];  // unit 0, partition 0, last launch: merged list, band, need_b, keys above all lists
 __device__ unsigned long long g_wk_launch[128][3];  // unit 0 per launch: start (partition 0), after the PDL wait, end
 __device__ unsigned int g_wk_nlaunch;
+__device__ unsigned long long g_wk_uend[64];  // last launch: each unit's final-merge end (trace mode)
+__device__ unsigned long long g_wk_lastexit;  // latest CTA exit (trace mode)
 #define WK_MARK(i)                                                      \
   do {                                                                  \
     if (trace && blockIdx.y == 0 && blockIdx.x < WK_TRACE_P && tid == 0) \
       g_wk_mark[blockIdx.x][i] = gtime();                               \
   } while (0)
+
+// ---------------------------------------------------------------------------
+// gather helpers (out of line: one copy of the code, however many rounds)
+// ---------------------------------------------------------------------------
+struct GCtx {
+  const uint16_t *loc_k, *loc_v, *kdev, *host_kv;
+  uint16_t *sv;
+  int32_t *stok, *sstamp, *tslot, *hand;
+  int64_t capacity, local_capacity, local_offset, ncand;
+  int u, n, p0, p1, window;
+  bool use_cache, kfd;
+};
+
+// row codes: >= 0 cached slot (a hit, stamped with this step), -1 over PCIe, -2 local mirror
+__device__ __noinline__ void lookup_rows(const GCtx &c, const int32_t *rows, int32_t *codes, int cnt, int *hits,
+                                         int *misses) {
+  int h = 0, mm = 0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int64_t idx = rows[i];
+    int code = -2;
+    if (idx < c.ncand) {
+      code = -1;
+      if (c.use_cache) {
+        const int p = c.tslot[idx];
+        if (p >= c.p0 && p < c.p1) {
+          code = p;
+          c.sstamp[p] = c.n;
+        }
+      }
+      h += code >= 0;
+      mm += code < 0;
+    }
+    codes[i] = code;
+  }
+  h = __reduce_add_sync(0xffffffffu, h);
+  mm = __reduce_add_sync(0xffffffffu, mm);
+  if ((threadIdx.x & 31) == 0 && (h | mm)) {
+    atomicAdd(hits, h);
+    atomicAdd(misses, mm);
+  }
+}
+
+// a round's HBM copies (every thread): cached (K|V) slot rows, local rows, the keys of misses from
+// the token-major copy; one expect-tx per warp, one arrival
+__device__ __noinline__ void issue_hbm(const GCtx &c, const int32_t *rows, const int32_t *codes, int cnt,
+                                       uint16_t *stage, unsigned long long *bar) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t bytes = 0;
+  for (int i = tid; i < cnt; i += blockDim.x) {
+    const int code = codes[i];
+    bytes += code >= 0 || code == -2 ? WK_D * 4 : (c.kfd ? WK_D * 2 : 0);
+  }
+  bytes = __reduce_add_sync(0xffffffffu, bytes);
+  if (lane == 0 && bytes) mbar_expect(bar, bytes);
+  __syncwarp();
+  for (int i = tid; i < cnt; i += blockDim.x) {
+    const int64_t idx = rows[i];
+    const int code = codes[i];
+    uint16_t *dst = stage + (size_t)i * 2 * WK_D;
+    if (code >= 0) {
+      bulk_g2s(dst, c.sv + (size_t)code * 2 * WK_D, WK_D * 4, bar);
+    } else if (code == -2) {
+      const size_t lr = (size_t)c.u * c.local_capacity + (size_t)(idx - c.local_offset);
+      bulk_g2s(dst, c.loc_k + lr * WK_D, WK_D * 2, bar);
+      bulk_g2s(dst + WK_D, c.loc_v + lr * WK_D, WK_D * 2, bar);
+    } else if (c.kfd) {
+      bulk_g2s(dst, c.kdev + ((size_t)c.u * c.capacity + idx) * WK_D, WK_D * 2, bar);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) mbar_arrive(bar);
+}
+
+// a round's PCIe copies, queued behind the HBM ones: value rows of misses (keys from HBM) or whole
+// (K|V) host rows (keys over PCIe); by one warp (with the row cache) or by every thread
+__device__ __noinline__ void issue_pcie(const GCtx &c, const int32_t *rows, const int32_t *codes, int cnt,
+                                        uint16_t *stage, unsigned long long *bar, bool one_warp) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t0 = one_warp ? lane : tid, ts = one_warp ? 32 : (int)blockDim.x;
+  uint32_t pbytes = 0;
+  for (int i = t0; i < cnt; i += ts) {
+    const int code = codes[i];
+    if (code == -1 || code <= -3) pbytes += c.kfd ? WK_D * 2 : WK_D * 4;
+  }
+  pbytes = __reduce_add_sync(0xffffffffu, pbytes);
+  if (lane == 0 && pbytes) mbar_expect(bar, pbytes);
+  __syncwarp();
+  for (int i = t0; i < cnt; i += ts) {
+    const int code = codes[i];
+    if (code != -1 && code > -3) continue;
+    const uint16_t *hrow = c.host_kv + ((size_t)c.u * c.capacity + rows[i]) * 2 * WK_D;
+    uint16_t *dst = stage + (size_t)i * 2 * WK_D;
+    if (c.kfd) bulk_g2s(dst + WK_D, hrow + WK_D, WK_D * 2, bar);
+    else bulk_g2s(dst, hrow, WK_D * 4, bar);
+  }
+  if (one_warp) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+  } else {
+    __syncthreads();
+    if (tid == 0) mbar_arrive(bar);
+  }
+}
+
+// cache slots for the misses (code -1) among codes[0, cnt), picked by one warp: free slots (empty,
+// or not selected in the last `window` steps) of this partition, scanned from its clock hand 32 at
+// a time, so the slots recycled are the ones filled longest ago; a miss becomes -3 - slot
+// (misses beyond the free slots stay uncached)
+__device__ __noinline__ void alloc_slots(const GCtx &c, int32_t *codes, int cnt, int *free_slots) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int Wn = max(1, c.window);
+  int need = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    need += __popc(__ballot_sync(0xffffffffu, i < cnt && codes[i] == -1));
+  }
+  need = min(need, WK_FCAP);
+  const int np = c.p1 - c.p0;
+  const int h0 = c.hand && np > 0 ? ((*c.hand % np) + np) % np : 0;
+  int found = 0;
+  for (int k0 = 0; found < need && k0 < np; k0 += 32) {
+    const int kk = k0 + lane;
+    int p = 0;
+    bool fr = false;
+    if (kk < np) {
+      p = c.p0 + (h0 + kk) % np;
+      fr = c.stok[p] < 0 || c.sstamp[p] <= c.n - Wn;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, fr);
+    const int pos = found + __popc(b & lt);
+    if (fr && pos < need) {
+      free_slots[pos] = p;
+      const int old = c.stok[p];  // the recycled slot's token loses its entry (unless it moved on)
+      if (old >= 0) atomicCAS(&c.tslot[old], p, -1);
+      if (pos == need - 1 && c.hand) *c.hand = (h0 + kk + 1) % np;
+    }
+    found += __popc(b);
+  }
+  __syncwarp();
+  const int used = min(found, need);
+  int ord = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    const bool mm = i < cnt && codes[i] == -1;
+    const unsigned b = __ballot_sync(0xffffffffu, mm);
+    const int kk = ord + __popc(b & lt);
+    if (mm && kk < used) codes[i] = -3 - free_slots[kk];
+    ord += __popc(b);
+  }
+  __syncwarp();
+}
 
 // The rare select paths (the aimed lists missed or overflowed): an exact radix
 // select of the k-th fp32 key through global histograms, then the band around
@@ -468,9 +668,10 @@ __device__ __noinline__ uint32_t select_fallback(WSh &S, const FbArgs &f, int &p
       }
       // the band around the exact k-th fp32 value, resolved with lists (keys in the band only)
       const float vk = from_ord32(prefix);
+      if (tid == 0) S.e_lo = S.e_hi = (double)vk;  // (the next step's aim)
       const uint32_t ord_lo = ord32(__double2float_rd((double)vk - eps2));
       const uint32_t ord_hi = ord32(__double2float_ru((double)vk + eps2));
-      unsigned long long *mylist = W.lists + ((size_t)buf * P + r) * WK_LCAP;
+      LEnt *mylist = W.lists + ((size_t)buf * P + r) * WK_LCAP;
       if (tid == 0) {
         S.list_count = 0;
         S.above = 0;
@@ -482,7 +683,7 @@ __device__ __noinline__ uint32_t select_fallback(WSh &S, const FbArgs &f, int &p
         above += key > ord_hi;
         if (key >= ord_lo && key <= ord_hi) {
           const int pos = atomicAdd(&S.list_count, 1);
-          if (pos < WK_LCAP) mylist[pos] = ((unsigned long long)key << 32) | (uint32_t)(j0 + e);
+          if (pos < WK_LCAP) mylist[pos].kidx = ((unsigned long long)key << 32) | (uint32_t)(j0 + e);
         }
       }
       above = block_sum(above, S.scan);
@@ -527,7 +728,7 @@ __device__ __noinline__ uint32_t select_fallback(WSh &S, const FbArgs &f, int &p
             if (S.lstart[mid] <= t) lo = mid;
             else hi = mid;
           }
-          const unsigned long long c = __ldcg(W.lists + ((size_t)buf * P + lo) * WK_LCAP + (t - S.lstart[lo]));
+          const unsigned long long c = __ldcg(&W.lists[((size_t)buf * P + lo) * WK_LCAP + (t - S.lstart[lo])].kidx);
           S.band_idx[t] = (uint32_t)c;
           S.band_key[t] = orderable(exact_score(kt, cap, S.chs, S.qsum, d_s, (uint32_t)c));
         }
@@ -655,6 +856,10 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 __device__ __noinline__ void merge_partials_w(const float *src, int cnt, int PF, int gmax, int G, float *mls,
                                               float *dst, float *out) {
   const int tid = threadIdx.x;
+  // the first element's partials are requested before the maxima/sums are staged: one round trip
+  float v[32];  // every partial of this element in flight at once (cnt <= 32)
+#pragma unroll
+  for (int q = 0; q < 32; ++q) v[q] = q < cnt && tid < G * WK_D ? __ldcg(src + (size_t)q * PF + tid) : 0.0f;
   for (int t = tid; t < cnt * 2 * gmax; t += blockDim.x) {
     const int q = t / (2 * gmax), j = t % (2 * gmax);
     mls[t] = __ldcg(src + (size_t)q * PF + gmax * WK_D + j);
@@ -662,23 +867,21 @@ __device__ __noinline__ void merge_partials_w(const float *src, int cnt, int PF,
   __syncthreads();
   for (int i = tid; i < G * WK_D; i += blockDim.x) {
     const int h = i / WK_D;
+    if (i != tid) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = q < cnt ? __ldcg(src + (size_t)q * PF + i) : 0.0f;
+    }
     float M = -INFINITY;
 #pragma unroll 1
     for (int q = 0; q < cnt; ++q) M = fmaxf(M, mls[q * 2 * gmax + h]);
     float L = 0.0f, Ac = 0.0f;
-#pragma unroll 1
-    for (int q0 = 0; q0 < cnt; q0 += 4) {
-      float v[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = q0 + j < cnt ? __ldcg(src + (size_t)(q0 + j) * PF + i) : 0.0f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float mq = q0 + j < cnt ? mls[(q0 + j) * 2 * gmax + h] : -INFINITY;
-        if (mq == -INFINITY) continue;
-        const float sc = exp2f(mq - M);
-        L = fmaf(sc, mls[(q0 + j) * 2 * gmax + gmax + h], L);
-        Ac = fmaf(sc, v[j], Ac);
-      }
+    for (int q = 0; q < 32; ++q) {
+      const float mq = q < cnt ? mls[q * 2 * gmax + h] : -INFINITY;
+      if (mq == -INFINITY) continue;
+      const float sc = exp2f(mq - M);
+      L = fmaf(sc, mls[q * 2 * gmax + gmax + h], L);
+      Ac = fmaf(sc, v[q], Ac);
     }
     if (out) {
       out[i] = Ac / L;
@@ -702,7 +905,6 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
   float *qs = reinterpret_cast<float *>(smem + WK_RAW + WK_KEYS);  // [G][D] * log2(e)/sqrt(d)
   const int u = blockIdx.y, r = blockIdx.x, P = gridDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = (1u << lane) - 1u;
   const int trace = g_wk_trace;
   const int G = a.G, d_s = a.d_s;
   const int64_t n = *s.len;  // same-layer launches never overlap under PDL (pdl_note)
@@ -751,26 +953,63 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
 #pragma unroll 1
   for (int i = tid; i < G * WK_D; i += blockDim.x)
     qs[i] = h2f(a.queries[(size_t)u * G * WK_D + i]) * (1.4426950408889634f / sqrtf((float)WK_D));
-  if (!select_all && tid < d_s) {
+  if (!select_all && tid < d_s) {  // every load of a channel's group sum and channel max in flight at once
     const int ch = S.chs[tid];
+    uint16_t qv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) qv[j] = j < G ? a.queries[((size_t)u * G + j) * WK_D + ch] : (uint16_t)0;
+    const float cm = s.chmax[(size_t)u * WK_D + ch];
     double q = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < G; ++j) q += h2d(a.queries[((size_t)u * G + j) * WK_D + ch]);  // retriever.py:189
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < G) q += h2d(qv[j]);  // retriever.py:189 (group sum, in head order)
     S.qsum[tid] = q;
     S.qsum32[tid] = (float)q;
+    S.eps_term[tid] = (double)cm * fabs(q);
   }
   __syncthreads();
   if (tid == 0 && !select_all) {
     double e = 0.0;
 #pragma unroll 1
-    for (int i = 0; i < d_s; ++i) e += (double)s.chmax[(size_t)u * WK_D + S.chs[i]] * fabs(S.qsum[i]);
+    for (int i = 0; i < d_s; ++i) e += S.eps_term[i];
     // |fp32 score - float64 score| <= (d_s + 1) 2^-24 sum_i max|K_i| |q_i| (a d_s-term fmaf chain plus
     // the query's fp32 rounding); (d_s + 2), at least 16, as in the cluster kernel
     S.band_eps = e * fmax(16.0, (double)d_s + 2.0) * 5.9604644775390625e-08;
   }
   uint32_t ord_def = 0xffffffffu;  // keys above are selected (plus S.bitmap members)
-  bool use_bitmap = false;
   int path = -1;
+  // gather context
+  const int n_loc = (int)(n - ncand);
+  const int n_loc_mine = n_loc > r ? (n_loc - r + P - 1) / P : 0;
+  const int CS = s.cache_slots;
+  const bool kfd = a.keys_from_device != 0;
+  const bool use_cache = CS > 0 && kfd;  // (K|V) slot cache (needs the token-major keys: dispatch checks s.kdev)
+  uint16_t *stage = reinterpret_cast<uint16_t *>(smem);
+  GCtx gc;
+  {
+    const int spc = (CS + P - 1) / P;  // this partition owns the slots [p0, p1)
+    gc.loc_k = s.loc_k;
+    gc.loc_v = s.loc_v;
+    gc.kdev = s.kdev;
+    gc.host_kv = s.host_kv;
+    gc.sv = use_cache ? s.slot_v + (size_t)u * CS * 2 * WK_D : nullptr;
+    gc.stok = use_cache ? s.slot_tok + (size_t)u * CS : nullptr;
+    gc.sstamp = use_cache ? s.slot_stamp + (size_t)u * CS : nullptr;
+    gc.tslot = use_cache ? s.tok_slot + (size_t)u * s.capacity : nullptr;
+    gc.hand = use_cache && s.slot_hand ? s.slot_hand + (size_t)u * TKV_MAX_PARTS + r : nullptr;
+    gc.capacity = s.capacity;
+    gc.local_capacity = s.local_capacity;
+    gc.local_offset = s.local_offset;
+    gc.ncand = ncand;
+    gc.u = u;
+    gc.n = (int)n;
+    gc.p0 = min(CS, r * spc);
+    gc.p1 = min(CS, gc.p0 + spc);
+    gc.window = s.cache_window;
+    gc.use_cache = use_cache;
+    gc.kfd = kfd;
+  }
+  if (tid == 0) S.hits = S.misses = 0;
   if (!select_all) {
     // ---- 1. fp32 proxy scores -> order-preserving keys; the partition's moments ----
     if (m > 0) mbar_wait(&S.bar_tma, 0);
@@ -815,14 +1054,22 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
         atomicMin(&S.klo, klo);
         atomicMax(&S.khi, khi);
         atomicAdd(&S.nval, nval);
-        atomicAdd(&S.fsum, fsum);
-        atomicAdd(&S.fsq, fsq);
+        S.r_sum[warp] = (double)fsum;  // summed in warp order below: the moments (and so the aim, the
+        S.r_sq[warp] = (double)fsq;    // partitions' aims and hints) are deterministic
       }
       __syncthreads();
       if (tid == 0) {
+        double su = 0.0, sq = 0.0;
+#pragma unroll 1
+        for (int w = 0; w < WK_WARPS; ++w) {
+          su += S.r_sum[w];
+          sq += S.r_sq[w];
+        }
+        S.fsum = (float)su;
+        S.fsq = (float)sq;
         const int nv = S.nval;
-        S.mu = nv ? (double)S.fsum / nv : 0.0;
-        S.sd = nv ? sqrt(fmax((double)S.fsq / nv - S.mu * S.mu, 0.0)) : 0.0;
+        S.mu = nv ? su / nv : 0.0;
+        S.sd = nv ? sqrt(fmax(sq / nv - S.mu * S.mu, 0.0)) : 0.0;
       }
     }
     WK_MARK(3);
@@ -830,8 +1077,9 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
     const double N = (double)(ncand - imin64(ncand, n_sink));
     float2 *hint = s.part_hint ? reinterpret_cast<float2 *>(s.part_hint) + (size_t)u * TKV_MAX_PARTS + r : nullptr;
     const float2 hv = hint ? *hint : make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
-    unsigned long long *cand = reinterpret_cast<unsigned long long *>(smem);  // the merged lists (raw is dead)
-    Hdr *htab = reinterpret_cast<Hdr *>(smem + WK_GCAP * 8);                // the unit's headers
+    // after the first list pass: [merged lists | the unit's headers]
+    LEnt *cand = reinterpret_cast<LEnt *>(smem);
+    Hdr *htab = reinterpret_cast<Hdr *>(smem + WK_GCAP * 16);
     int buf = 0, dir = 0;
     bool done = false;
     // ---- 2. aimed list attempts ----
@@ -847,7 +1095,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
             w = isfinite(hv.y) ? fmin(0.3, fmax(0.06, 3.0 * (double)hv.y)) : 0.15;
           } else {
             c = mu + normal_upper_quantile((double)(k - n_sink) / fmax(N, 1.0)) * sd;
-            w = 0.25;
+            w = 0.12;
           }
           wlo = c - w * sd;
           whi = c + w * sd;
@@ -876,7 +1124,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
       // list keys in [llo, lhi] (global), count keys above lhi
       {
         const uint32_t llo = S.llo, lhi = S.lhi;
-        unsigned long long *mylist = W.lists + ((size_t)buf * P + r) * WK_LCAP;
+        LEnt *mylist = W.lists + ((size_t)buf * P + r) * WK_LCAP;
         int above = 0;
 #pragma unroll 1
         for (int g = 0; g < 2; ++g) {  // uniform trip count: the warp votes below need every lane
@@ -891,6 +1139,17 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
               mask |= (uint32_t)(valid && key >= llo && key <= lhi) << q;
             }
           }
+          {  // keys above the list are selected whenever this attempt succeeds: their mask words
+            uint32_t amsk = 0u;
+            if (e < m) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) amsk |= (uint32_t)(e + q < m && keys32[e + q] > lhi) << q;
+            }
+            amsk <<= 8 * (lane & 3);
+            amsk |= __shfl_xor_sync(0xffffffffu, amsk, 1);
+            amsk |= __shfl_xor_sync(0xffffffffu, amsk, 2);
+            if ((lane & 3) == 0 && g * WK_THREADS * 8 + tid * 8 < WK_MAXM) S.amask[(g * WK_THREADS * 8 + tid * 8) >> 5] = amsk;
+          }
           const int c = __popc(mask);
           const int incl = warp_incl_scan(c, lane);
           const int wtot = __shfl_sync(0xffffffffu, incl, 31);
@@ -901,7 +1160,21 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
           while (mask) {
             const int q = __ffs(mask) - 1;
             mask &= mask - 1u;
-            if (pos < WK_LCAP) mylist[pos] = ((unsigned long long)keys32[e + q] << 32) | (uint32_t)(j0 + e + q);
+            if (pos < WK_LCAP) {
+              // exact_score: from the SMEM columns on the first attempt (same channel order); later
+              // attempts run after the merged lists overwrote them, and read the scorer copy in HBM
+              double sc = 0.0;
+              if (attempt == 0) {
+#pragma unroll 1
+                for (int i = 0; i < d_s; ++i) sc = fma(h2d(raw[(size_t)i * WK_MAXM + e + q]), S.qsum[i], sc);
+              } else {
+                sc = exact_score(kt, s.capacity, S.chs, S.qsum, d_s, j0 + e + q);
+              }
+              LEnt le;
+              le.kidx = ((unsigned long long)keys32[e + q] << 32) | (uint32_t)(j0 + e + q);
+              le.s = sc;
+              mylist[pos] = le;
+            }
             ++pos;
           }
         }
@@ -1014,6 +1287,11 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
       }
       __syncthreads();
       if (attempt == 0) WK_MARK(15);
+      if (trace && u == 0 && r == 0 && tid == 0 && attempt == 0) {
+        g_wk_dbg[5] = S.ovf;
+        g_wk_dbg[6] = S.Ltot;
+        g_wk_dbg[7] = (int)S.XL - (int)S.XH;
+      }
       if (!S.ovf && S.XL <= S.XH) {
         const int Ltot = S.Ltot;
         const uint32_t XL = S.XL, XH = S.XH;
@@ -1027,9 +1305,12 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
             if (S.lstart[mid] <= t) lo = mid;
             else hi = mid;
           }
-          const unsigned long long c = __ldcg(W.lists + ((size_t)buf * P + lo) * WK_LCAP + (t - S.lstart[lo]));
-          cand[t] = c;
-          const uint32_t key = (uint32_t)(c >> 32);
+          const LEnt *src = W.lists + ((size_t)buf * P + lo) * WK_LCAP + (t - S.lstart[lo]);
+          LEnt le;
+          le.kidx = __ldcg(&src->kidx);
+          le.s = __ldcg(&src->s);
+          cand[t] = le;
+          const uint32_t key = (uint32_t)(le.kidx >> 32);
           ab += key > XH;
           in += key >= XL && key <= XH;
         }
@@ -1055,13 +1336,25 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
           const float scale = flat ? 0.0f : (float)WK_NB / (r_hi - r_lo);
 #pragma unroll 1
           for (int t = tid; t < Ltot; t += blockDim.x) {
-            const uint32_t key = (uint32_t)(cand[t] >> 32);
+            const uint32_t key = (uint32_t)(cand[t].kidx >> 32);
             if (key < XL || key > XH) continue;
             const int b = flat ? 0 : min(WK_NB - 1, max(0, (int)((from_ord32(key) - r_lo) * scale)));
             atomicAdd(&S.hist[b], 1u);
           }
           __syncthreads();
-          if (warp == 0) top_bin(S.hist, WK_NB, need, &S.bin, &S.definite);
+          {
+            // the bin holding the need-th largest entry: thread t owns bins NB-1-2t, NB-2-2t (descending)
+            const int b0 = WK_NB - 1 - 2 * tid, b1 = b0 - 1;
+            const int h0 = (int)S.hist[b0], c2 = h0 + (int)S.hist[b1];
+            const int incl = warp_incl_scan(c2, lane);
+            if (lane == 31) S.wtot[warp] = incl;
+            if (tid == 0) S.bin = -1;
+            __syncthreads();
+            int pre = incl - c2;
+#pragma unroll 1
+            for (int w = 0; w < warp; ++w) pre += S.wtot[w];
+            if (pre < need && pre + c2 >= need) S.bin = pre + h0 >= need ? b0 : b1;
+          }
           __syncthreads();
           if (attempt == 0) WK_MARK(17);
           const int B = S.bin;
@@ -1077,13 +1370,17 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
           if (st) {
 #pragma unroll 1
             for (int t = tid; t < Ltot; t += blockDim.x) {
-              const uint32_t key = (uint32_t)(cand[t] >> 32);
+              const uint32_t key = (uint32_t)(cand[t].kidx >> 32);
               if (key > ord_hi) {
                 atomicAdd(&S.cnt_c, 1);
               } else if (key >= ord_lo) {
                 const int slot = atomicAdd(&S.band_n, 1);
-                if (slot < WK_BAND) S.band_idx[slot] = (uint32_t)cand[t];
-                else S.band_ovf = 1;
+                if (slot < WK_BAND) {
+                  S.band_idx[slot] = (uint32_t)cand[t].kidx;
+                  S.band_key[slot] = orderable(cand[t].s);  // the exact score came with the list
+                } else {
+                  S.band_ovf = 1;
+                }
               }
             }
             __syncthreads();
@@ -1100,12 +1397,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
             st = !S.band_ovf && need_b >= 0 && need_b <= nb;
             if (st) {
 #pragma unroll 1
-              for (int b = tid; b < nb; b += blockDim.x)
-                S.band_key[b] = orderable(exact_score(kt, s.capacity, S.chs, S.qsum, d_s, S.band_idx[b]));
-#pragma unroll 1
               for (int i = tid; i < P; i += blockDim.x) S.pcount[i] = (int)htab[i].above;
-#pragma unroll 1
-              for (int i = tid; i < WK_MAXM / 32; i += blockDim.x) S.bitmap[i] = 0u;
               __syncthreads();
               if (attempt == 0) WK_MARK(19);
 #pragma unroll 1
@@ -1121,15 +1413,18 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
                 if (beaten < need_b) {
                   atomicAdd(&S.pcount[(int)((int64_t)ib / chunk)], 1);
                   if ((int64_t)ib >= j0 && (int64_t)ib < j0 + m)
-                    atomicOr(&S.bitmap[((int64_t)ib - j0) >> 5], 1u << (((int64_t)ib - j0) & 31));
+                    atomicOr(&S.amask[((int64_t)ib - j0) >> 5], 1u << (((int64_t)ib - j0) & 31));
                 }
               }
               if (attempt == 0) WK_MARK(20);
               // every partition's count: keys above its list + list keys above the band + band members
 #pragma unroll 1
               for (int t = tid; t < Ltot; t += blockDim.x) {
-                const uint32_t key = (uint32_t)(cand[t] >> 32);
-                if (key > ord_hi) atomicAdd(&S.pcount[(int)((uint32_t)cand[t] / (uint32_t)chunk)], 1);
+                const uint32_t key = (uint32_t)(cand[t].kidx >> 32), ib = (uint32_t)cand[t].kidx;
+                if (key <= ord_hi) continue;
+                atomicAdd(&S.pcount[(int)(ib / (uint32_t)chunk)], 1);
+                if ((int64_t)ib >= j0 && (int64_t)ib < j0 + m)  // this partition's list keys above the band
+                  atomicOr(&S.amask[((int64_t)ib - j0) >> 5], 1u << (((int64_t)ib - j0) & 31));
               }
               if (tid == 0) {
                 S.ord_def = ord_hi;
@@ -1153,19 +1448,13 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
         done = true;
         path = attempt;
         ord_def = S.ord_def;
-        use_bitmap = true;
-        if (tid == 0 && hint && S.sd > 0.0) {  // this partition's hint for the next step
-          const double z = (0.5 * (S.e_lo + S.e_hi) - S.mu) / S.sd;
-          const float dz = isfinite(hv.x) ? (float)fabs(z - (double)hv.x) : __int_as_float(0x7fc00000);
-          const float y = isfinite(hv.y) ? (isfinite(dz) ? 0.75f * hv.y + 0.25f * dz : hv.y) : dz;
-          *hint = make_float2((float)z, y);
-        }
       }
       buf ^= 1;
       if (!done && dir == 0) break;  // overflow or an uncovered band: the radix path decides
       __syncthreads();
     }
     if (!done) {
+      if (tid == 0) S.e_lo = S.e_hi = __longlong_as_double(0x7ff8000000000000ll);
       FbArgs fa;
       fa.kt = kt;
       fa.cap = s.capacity;
@@ -1183,33 +1472,42 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
       fa.buf = buf;
       fa.eps2 = eps2;
       ord_def = select_fallback(S, fa, path);
-      use_bitmap = true;
+      __syncthreads();
+#pragma unroll 1
+      for (int w = warp; w < WK_MAXM / 32; w += WK_WARPS) {  // the fallback's selection as mask words
+        const int e = w * 32 + lane;
+        const bool sel = e < m && (keys32[e] > ord_def || ((S.bitmap[w] >> lane) & 1u));
+        const unsigned b = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) S.amask[w] = b;
+      }
+    }
+  }
+  if (!select_all && tid == 0) {  // this partition's hint for the next step (from whichever path decided)
+    float2 *hint = s.part_hint ? reinterpret_cast<float2 *>(s.part_hint) + (size_t)u * TKV_MAX_PARTS + r : nullptr;
+    const double T = 0.5 * (S.e_lo + S.e_hi);
+    if (hint && S.sd > 0.0 && isfinite(T)) {
+      const float2 hv = *hint;
+      const double z = (T - S.mu) / S.sd;
+      const float dz = isfinite(hv.x) ? (float)fabs(z - (double)hv.x) : __int_as_float(0x7fc00000);
+      const float y = isfinite(hv.y) ? (isfinite(dz) ? 0.75f * hv.y + 0.25f * dz : hv.y) : dz;
+      *hint = make_float2((float)z, y);
     }
   }
   WK_MARK(8);
   if (trace && tid == 0 && r == 0 && path >= 0) atomicAdd(&g_wk_path[path], 1u);
-  // ---- 3. ascending output.  Warp w owns keys [512 w, 512 w + 512) in lane-consecutive groups of 32
-  // (conflict-free); a 16-bit register mask keeps its flags, ballots give the positions ----
-  uint32_t fl = 0u;
-  int wt = 0;
+  // ---- 3. ascending output from the mask words: one word (32 keys) per thread ----
+  if (select_all) {
 #pragma unroll 1
-  for (int q = 0; q < 16; ++q) {
-    const int e = warp * 512 + q * 32 + lane;
-    const bool sel = e < m && (select_all || keys32[e] > ord_def ||
-                               (use_bitmap && ((S.bitmap[e >> 5] >> (e & 31)) & 1u)));
-    fl |= (uint32_t)sel << q;
-    wt += __popc(__ballot_sync(0xffffffffu, sel));
-  }
-  if (lane == 0) S.wtot[warp] = wt;
-  __syncthreads();  // every key read: the row list below overwrites keys32
-  if (tid == 0) {
-    int run = 0;
-#pragma unroll 1
-    for (int w = 0; w < WK_WARPS; ++w) {
-      S.wbase[w] = run;
-      run += S.wtot[w];
+    for (int w = tid; w < WK_MAXM / 32; w += blockDim.x) {
+      const int e = w * 32;
+      S.amask[w] = e >= m ? 0u : (m - e >= 32 ? 0xffffffffu : ((1u << (m - e)) - 1u));
     }
-    S.cta_total = run;
+  }
+  __syncthreads();
+  const uint32_t myw = tid < WK_MAXM / 32 ? S.amask[tid] : 0u;
+  int cta_total;
+  const int wpos = block_excl_scan(__popc(myw), S.scan, &cta_total);
+  if (tid == 0) {
     if (select_all) {
       S.offset = (int)j0;
       S.far_total = (int)ncand;
@@ -1225,26 +1523,22 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
     }
   }
   __syncthreads();
-  const int offset = S.offset, far_total = S.far_total, cta_total = S.cta_total;
-  int32_t *rows = reinterpret_cast<int32_t *>(keys32);  // the partition's rows (global token indices)
+  const int offset = S.offset, far_total = S.far_total;
+  int32_t *rows = reinterpret_cast<int32_t *>(keys32);  // rows still to gather (global token indices)
   int32_t *out_idx = a.sel_idx + (size_t)u * a.sel_stride;
   {
-    int run = S.wbase[warp];
+    uint32_t x = myw;
+    int p = wpos;
 #pragma unroll 1
-    for (int q = 0; q < 16; ++q) {
-      const bool sel = (fl >> q) & 1u;
-      const unsigned b = __ballot_sync(0xffffffffu, sel);
-      if (sel) {
-        const int p = run + __popc(b & lt);
-        const int32_t idx = (int32_t)(j0 + warp * 512 + q * 32 + lane);
-        out_idx[offset + p] = idx;
-        rows[p] = idx;
-      }
-      run += __popc(b);
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1u;
+      const int32_t idx = (int32_t)(j0 + tid * 32 + b);
+      out_idx[offset + p] = idx;
+      rows[p++] = idx;
     }
   }
-  const int n_loc = (int)(n - ncand);
-  const int n_loc_mine = n_loc > r ? (n_loc - r + P - 1) / P : 0;
+  const int nrest = cta_total + n_loc_mine;
 #pragma unroll 1
   for (int i = tid; i < n_loc_mine; i += blockDim.x) rows[cta_total + i] = (int32_t)(ncand + r + (int64_t)P * i);
   if (r == P - 1) {
@@ -1255,60 +1549,19 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
       if (a.fetch_count) a.fetch_count[u] = far_total;
     }
   }
-  const int nrows = cta_total + n_loc_mine;
-  if (tid == 0) {
-    S.hits = 0;
-    S.misses = 0;
-  }
   __syncthreads();
   WK_MARK(9);
-  // ---- 4. gather + attention over this partition's rows ----
+  // ---- 4. gather + attention over this partition's rows, in rounds of NR staged rows ----
   constexpr int CPL = WK_D / 32;  // channels per lane
-  const int CS = s.cache_slots;
-  const bool kfd = a.keys_from_device != 0;
-  const bool use_cache = CS > 0 && kfd;  // (K|V) slot cache (needs the token-major keys: dispatch checks s.kdev)
   const int NW = use_cache ? WK_WARPS - 1 : WK_WARPS;  // warps computing logits (the last one issues PCIe copies)
-  const int rs_bytes = ((nrows * 4 + 127) / 128) * 128;
+  const int rs_bytes = ((nrest * 4 + 127) / 128) * 128;
   int32_t *rslot = reinterpret_cast<int32_t *>(smem + WK_RAW - rs_bytes);
   const int row_bytes = 2 * WK_D * 2 + GMAX * 4;  // staged (K|V) row + its logits
   const int NR = min(512, ((WK_RAW - rs_bytes) / row_bytes) & ~15);
-  uint16_t *stage = reinterpret_cast<uint16_t *>(smem);
   float *zs = reinterpret_cast<float *>(smem + (size_t)NR * 2 * WK_D * 2);
-  int32_t *stok = use_cache ? s.slot_tok + (size_t)u * CS : nullptr;
-  int32_t *sstamp = use_cache ? s.slot_stamp + (size_t)u * CS : nullptr;
-  uint16_t *sv = use_cache ? s.slot_v + (size_t)u * CS * 2 * WK_D : nullptr;
-  int32_t *tslot = use_cache ? s.tok_slot + (size_t)u * s.capacity : nullptr;
-  const int spc = (CS + P - 1) / P;  // this partition owns the slots [p0, p1)
-  const int p0 = min(CS, r * spc), p1 = min(CS, p0 + spc);
-  {
-    // row codes: >= 0 cached slot (hit, stamped), -1 over PCIe, -2 local mirror, <= -3 over PCIe into slot -3-code
-    int hits = 0, misses = 0;
-#pragma unroll 1
-    for (int i = tid; i < nrows; i += blockDim.x) {
-      const int64_t idx = rows[i];
-      int code = -2;
-      if (idx < ncand) {
-        code = -1;
-        if (use_cache) {
-          const int p = tslot[idx];
-          if (p >= p0 && p < p1) {
-            code = p;
-            sstamp[p] = (int)n;
-          }
-        }
-        hits += code >= 0;
-        misses += code < 0;
-      }
-      rslot[i] = code;
-    }
-    hits = __reduce_add_sync(0xffffffffu, hits);
-    misses = __reduce_add_sync(0xffffffffu, misses);
-    if (lane == 0 && (hits | misses)) {
-      atomicAdd(&S.hits, hits);
-      atomicAdd(&S.misses, misses);
-    }
-  }
+  lookup_rows(gc, rows, rslot, nrest, &S.hits, &S.misses);
   __syncthreads();
+  WK_MARK(22);
   float mrun[GMAX], lrun[GMAX], acc[GMAX][CPL];
 #pragma unroll
   for (int h = 0; h < GMAX; ++h) {
@@ -1319,103 +1572,18 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
   }
   uint32_t parity = 0;
 #pragma unroll 1
-  for (int base = 0; base < nrows; base += NR) {
-    const int cnt = min(NR, nrows - base);
+  for (int base = 0; base < nrest; base += NR) {
+    const int32_t *rr = rows + base;
+    int32_t *cc = rslot + base;
+    const int cnt = min(NR, nrest - base);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic SMEM accesses before the TMA writes
     __syncthreads();
-    // (a) HBM copies by every thread: cached (K|V) slot rows, local rows, keys of misses (token-major copy)
-#pragma unroll 1
-    for (int i = tid; i < cnt; i += blockDim.x) {
-      const int64_t idx = rows[base + i];
-      const int code = rslot[base + i];
-      uint16_t *dst = stage + (size_t)i * 2 * WK_D;
-      if (code >= 0) {
-        mbar_expect(&S.bar_hbm, WK_D * 4);
-        bulk_g2s(dst, sv + (size_t)code * 2 * WK_D, WK_D * 4, &S.bar_hbm);
-      } else if (code == -2) {
-        const size_t lr = (size_t)u * s.local_capacity + (size_t)(idx - s.local_offset);
-        mbar_expect(&S.bar_hbm, WK_D * 4);
-        bulk_g2s(dst, s.loc_k + lr * WK_D, WK_D * 2, &S.bar_hbm);
-        bulk_g2s(dst + WK_D, s.loc_v + lr * WK_D, WK_D * 2, &S.bar_hbm);
-      } else if (kfd) {
-        mbar_expect(&S.bar_hbm, WK_D * 2);
-        bulk_g2s(dst, s.kdev + ((size_t)u * s.capacity + idx) * WK_D, WK_D * 2, &S.bar_hbm);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) mbar_arrive(&S.bar_hbm);
-    // (b) PCIe copies, queued behind the HBM ones: value rows of misses (keys from HBM) or whole
-    // (K|V) host rows (keys over PCIe); with the row cache one warp issues them (and picks the
-    // misses' cache slots) while the others compute the logits
-    if (!use_cache || warp == WK_WARPS - 1) {
-      const int t0 = use_cache ? lane : tid, ts = use_cache ? 32 : WK_THREADS;
-#pragma unroll 1
-      for (int i = t0; i < cnt; i += ts) {
-        const int code = rslot[base + i];
-        if (code != -1 && code > -3) continue;
-        const uint16_t *hrow = s.host_kv + ((size_t)u * s.capacity + rows[base + i]) * 2 * WK_D;
-        uint16_t *dst = stage + (size_t)i * 2 * WK_D;
-        mbar_expect(&S.bar_pcie, kfd ? WK_D * 2 : WK_D * 4);
-        if (kfd) bulk_g2s(dst + WK_D, hrow + WK_D, WK_D * 2, &S.bar_pcie);
-        else bulk_g2s(dst, hrow, WK_D * 4, &S.bar_pcie);
-      }
-      if (use_cache) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.bar_pcie);
-        // cache slots for this step's misses (all rounds), picked here while the other warps compute
-        // the logits: free slots (empty, or not selected in the last cache_window steps) of this
-        // partition, scanned from its clock hand 32 at a time
-        if (base == 0) {
-          const int Wn = max(1, s.cache_window);
-          int need = 0;
-#pragma unroll 1
-          for (int i0 = 0; i0 < nrows; i0 += 32) {
-            const int i = i0 + lane;
-            need += __popc(__ballot_sync(0xffffffffu, i < nrows && rslot[i] == -1));
-          }
-          need = min(need, WK_FCAP);
-          const int np = p1 - p0;
-          int32_t *hand = s.slot_hand ? s.slot_hand + (size_t)u * TKV_MAX_PARTS + r : nullptr;
-          const int h0 = hand && np > 0 ? ((*hand % np) + np) % np : 0;
-          int found = 0;
-#pragma unroll 1
-          for (int k0 = 0; found < need && k0 < np; k0 += 32) {
-            const int kk = k0 + lane;
-            int p = 0;
-            bool fr = false;
-            if (kk < np) {
-              p = p0 + (h0 + kk) % np;
-              fr = stok[p] < 0 || sstamp[p] <= (int)n - Wn;
-            }
-            const unsigned b = __ballot_sync(0xffffffffu, fr);
-            const int pos = found + __popc(b & lt);
-            if (fr && pos < need) {
-              S.free_slots[pos] = p;
-              const int old = stok[p];  // the recycled slot's token loses its entry (unless it moved on)
-              if (old >= 0) atomicCAS(&tslot[old], p, -1);
-              if (pos == need - 1 && hand) *hand = (h0 + kk + 1) % np;
-            }
-            found += __popc(b);
-          }
-          __syncwarp();
-          const int used = min(found, need);
-          int ord = 0;
-#pragma unroll 1
-          for (int i0 = 0; i0 < nrows; i0 += 32) {
-            const int i = i0 + lane;
-            const bool mm = i < nrows && rslot[i] == -1;
-            const unsigned b = __ballot_sync(0xffffffffu, mm);
-            const int kk = ord + __popc(b & lt);
-            if (mm && kk < used) rslot[i] = -3 - S.free_slots[kk];  // misses beyond the free slots stay uncached
-            ord += __popc(b);
-          }
-        }
-      }
-    }
-    if (!use_cache) {
-      __syncthreads();
-      if (tid == 0) mbar_arrive(&S.bar_pcie);
-    }
+    issue_hbm(gc, rr, cc, cnt, stage, &S.bar_hbm);
+    if (base == 0) WK_MARK(23);
+    // with the row cache the last warp issues the PCIe copies and then picks the misses' cache
+    // slots (all rounds) while the others compute the logits
+    if (!use_cache || warp == WK_WARPS - 1) issue_pcie(gc, rr, cc, cnt, stage, &S.bar_pcie, use_cache);
+    if (use_cache && warp == WK_WARPS - 1 && base == 0) alloc_slots(gc, rslot, nrest, S.free_slots);
     // (c) logits of this warp's rows (row = warp mod NW); keys over PCIe wait for those rows first
     if (warp < NW) {
       mbar_wait(&S.bar_hbm, parity);
@@ -1464,6 +1632,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
         }
       }
       __syncwarp();
+      if (base == 0) WK_MARK(24);
       // (d) value rows landed; warp-local online softmax over this warp's rows, then p.v
       if (kfd) mbar_wait(&S.bar_pcie, parity);
       const int nr = cnt > warp ? (cnt - warp + NW - 1) / NW : 0;
@@ -1519,22 +1688,24 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
         }
       }
     }
+    if (base == 0) WK_MARK(25);
     __syncthreads();  // the PCIe warp's slot codes before the inserts
     // (e) rows fetched over PCIe enter the HBM row cache in their assigned slots
     if (use_cache) {
 #pragma unroll 1
       for (int i = tid; i < cnt; i += blockDim.x) {
-        const int code = rslot[base + i];
+        const int code = cc[i];
         if (code > -3) continue;
         const int dst = -3 - code;
-        const int32_t idx = rows[base + i];
-        stok[dst] = idx;
-        sstamp[dst] = (int)n;
-        tslot[idx] = dst;
-        bulk_s2g(sv + (size_t)dst * 2 * WK_D, stage + (size_t)i * 2 * WK_D, WK_D * 4);
+        const int32_t idx = rr[i];
+        gc.stok[dst] = idx;
+        gc.sstamp[dst] = (int)n;
+        gc.tslot[idx] = dst;
+        bulk_s2g(gc.sv + (size_t)dst * 2 * WK_D, stage + (size_t)i * 2 * WK_D, WK_D * 4);
       }
       bulk_commit_wait_read();
     }
+    if (base == 0) WK_MARK(26);
     parity ^= 1u;
     __syncthreads();
   }
@@ -1576,6 +1747,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
       mypart[GMAX * WK_D + GMAX + h] = L;
     }
   }
+  WK_MARK(27);
   if (use_cache && tid == 0 && (S.hits | S.misses)) {
     atomicAdd(&s.cache_stats[0], (unsigned long long)S.hits);
     atomicAdd(&s.cache_stats[1], (unsigned long long)S.misses);
@@ -1596,6 +1768,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
   }
   __syncthreads();
   WK_MARK(11);
+  if (trace && tid == 0) atomicMax(&g_wk_lastexit, gtime());
   if (!S.last) return;
   float *mls = reinterpret_cast<float *>(smem + 96 * 1024);  // [<= 32][2 GMAX]
   float *gpart = W.part + (size_t)P * PF;
@@ -1618,15 +1791,21 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
     merge_partials_w(gpart, NG, PF, GMAX, G, mls, nullptr, uout);
   }
   WK_MARK(12);
-  if (trace && u == 0 && tid == 0) g_wk_launch[(__ldcg(&g_wk_nlaunch) - 1u) & 127u][2] = gtime();
+  if (trace && tid == 0) {
+    const unsigned long long t_ = gtime();
+    if (u == 0) g_wk_launch[(__ldcg(&g_wk_nlaunch) - 1u) & 127u][2] = t_;
+    if (u < 64) g_wk_uend[u] = t_;
+  }
   // ---- the final merger: the step's append (HostPool.append + mirror append, memsim.py:106-111,
   // pipeline.py:405-413), after every partition of the unit finished reading this step's state ----
   if (a.new_keys) {
 #pragma unroll 1
     for (int c = tid; c < WK_D; c += blockDim.x) {
       const uint16_t kx = a.new_keys[(size_t)u * WK_D + c], vx = a.new_values[(size_t)u * WK_D + c];
-      s.host_kv[(((size_t)u * s.capacity + n) * 2 + 0) * WK_D + c] = kx;
-      s.host_kv[(((size_t)u * s.capacity + n) * 2 + 1) * WK_D + c] = vx;
+      if (!g_wk_exp) {
+        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 0) * WK_D + c] = kx;
+        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 1) * WK_D + c] = vx;
+      }
       s.kt[((size_t)u * WK_D + c) * s.capacity + n] = kx;
       float *cm = &s.chmax[(size_t)u * WK_D + c];
       *cm = fmaxf(*cm, fabsf(h2f(kx)));
@@ -1654,6 +1833,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
     if (tid == 0) atomicExch(&W.ctl[C_FALLBACK], 0u);
   }
   WK_MARK(13);
+  if (trace && tid == 0) atomicMax(&g_wk_lastexit, gtime());
 }
 
 // ---------------------------------------------------------------------------
@@ -1791,6 +1971,13 @@ extern "C" int tkv_debug_wide_launches(unsigned long long *out, int reset) {
 }
 extern "C" int tkv_debug_wide_dbg(int *out) {  // [8]
   return cudaMemcpyFromSymbol(out, tkv::wide::g_wk_dbg, sizeof(tkv::wide::g_wk_dbg)) == cudaSuccess ? 0 : 7;
+}
+extern "C" int tkv_debug_wide_unit_ends(unsigned long long *out) {  // [64] + latest CTA exit
+  cudaMemcpyFromSymbol(out + 64, tkv::wide::g_wk_lastexit, sizeof(unsigned long long));
+  return cudaMemcpyFromSymbol(out, tkv::wide::g_wk_uend, sizeof(tkv::wide::g_wk_uend)) == cudaSuccess ? 0 : 7;
+}
+extern "C" int tkv_debug_wide_exp(int v) {
+  return cudaMemcpyToSymbol(tkv::wide::g_wk_exp, &v, sizeof(int)) == cudaSuccess ? 0 : 7;
 }
 extern "C" int tkv_wide_parts(int32_t units) { return tkv::wide::parts_for(units); }
 // bounded-wait timeouts of the wide decode since the last reset (0 = none; 1 unit barrier, 2 mbarrier)

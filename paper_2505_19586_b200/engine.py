@@ -15,6 +15,8 @@ Per step and layer l (pipeline.py order, attend-before-append):
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import ctypes as C
@@ -30,6 +32,11 @@ from .quantizer import QuantizedLayerKV, as_f16
 from .retriever import WORKSPACES, RetrievalConfig, stage1_select
 from . import _lib
 from ._lib import check
+
+
+# timing experiments only: skip stage 1 inside the step (channels keep their last values; results are
+# then not the reference's) to see what the rest of the step costs
+_SKIP_STAGE1 = os.environ.get("TKV_SKIP_STAGE1") == "1"
 
 
 @dataclass(frozen=True)
@@ -290,9 +297,10 @@ class DecodeEngine:
         st = self.sparse[l]
         src = l - 1 if l >= 1 else 0  # pipeline.py:273
         t0 = self._mark(self.side)
-        stage1_select(self.hidden[src], st.w_q, st.layer.chmax, self.G, self.retrieval.d_s,
-                      channels=st.channels, workspace=st.s1_ws, stream=self.side,
-                      prefetch_layer=st.layer if self.cfg.scorer_l2_prefetch else None)
+        if not _SKIP_STAGE1:
+            stage1_select(self.hidden[src], st.w_q, st.layer.chmax, self.G, self.retrieval.d_s,
+                          channels=st.channels, workspace=st.s1_ws, stream=self.side,
+                          prefetch_layer=st.layer if self.cfg.scorer_l2_prefetch else None)
         self._span("stage1", l, t0, self.side)
         st.s1_done.record(self.side)
 

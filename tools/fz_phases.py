@@ -96,8 +96,10 @@ def show(lib):
 
 WIDE_MARKS = {1: "pdl-wait", 2: "tma", 3: "score", 4: "list", 6: "barrier", 14: "r:sync", 15: "r:hdr",
               16: "r:lists+counts", 17: "r:hist", 18: "r:band", 19: "r:f64", 20: "r:rank", 21: "r:pcount",
-              8: "resolve-end", 9: "output", 10: "gather", 11: "merge-arrive", 12: "final-merge", 13: "append"}
-WIDE_ORDER = [1, 2, 3, 4, 6, 14, 15, 16, 17, 18, 19, 20, 21, 8, 9, 10, 11, 12, 13]
+              8: "resolve-end", 9: "output", 22: "g:lookup", 23: "g:issue", 24: "g:logits(w0)",
+              25: "g:softmax+pv(w0)", 26: "g:insert", 10: "gather-end", 27: "partial", 11: "merge-arrive",
+              12: "final-merge", 13: "append"}
+WIDE_ORDER = [1, 2, 3, 4, 6, 14, 15, 16, 17, 18, 19, 20, 21, 8, 9, 22, 23, 24, 25, 26, 10, 27, 11, 12, 13]
 
 
 def wide_enable(lib, on=True):
@@ -129,13 +131,20 @@ def wide_show(lib, parts=18):
         gap = [(rows[k][1] - rows[k - 1][2]) / 1e3 for k in range(1, len(rows))]
         print(f"  wide launches ({len(rows)}): period median {med(per):.2f} us, start->wait-done {med(wait):.2f}, "
               f"wait-done->end {med(body):.2f}, prev end->wait-done {med(gap):.2f}")
+    ue = (C.c_ulonglong * 65)()
+    lib.tkv_debug_wide_unit_ends(ue)
+    if rows:
+        wd = rows[-1][1]
+        ends = [(x - wd) / 1e3 for x in list(ue)[:8] if x]
+        print("  unit final-merge ends after wait-done (us): " + " ".join(f"{x:.1f}" for x in ends)
+              + f"; latest CTA exit (any launch) {(ue[64] - wd) / 1e3:.1f}")
     dbg = (C.c_int * 8)()
     lib.tkv_debug_wide_dbg(dbg)
     print(f"  unit 0 lists: merged {dbg[0]}, in window {dbg[4]}, band {dbg[1]}, need in band {dbg[2]}, "
-          f"above all lists {dbg[3]}")
-    mk = (C.c_ulonglong * (32 * 24))()
+          f"above all lists {dbg[3]}; first attempt: overflow {dbg[5]} merged {dbg[6]} XL-XH {dbg[7]}")
+    mk = (C.c_ulonglong * (32 * 32))()
     lib.tkv_debug_wide_marks(mk)
-    t = [list(mk)[p * 24:(p + 1) * 24] for p in range(min(parts, 32))]
+    t = [list(mk)[p * 32:(p + 1) * 32] for p in range(min(parts, 32))]
     t0 = min(x[1] for x in t if x[1])
     for p, x in enumerate(t):
         parts_s, prev = [], x[1]
