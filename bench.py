@@ -407,8 +407,6 @@ def main():
                          device=device)
     if os.environ.get("TKV_FZ_DBG"):  # experiments in the sparse kernel (debug bits)
         _lib.load().tkv_debug_sparse_trace(int(os.environ["TKV_FZ_DBG"]) & ~1)
-    if os.environ.get("TKV_WIDE_EXP"):  # experiments in the wide decode
-        _lib.load().tkv_debug_wide_exp(int(os.environ["TKV_WIDE_EXP"]))
     if os.environ.get("TKV_AIM"):  # tuning: first aimed range half-width (score sd)
         import ctypes
         _lib.load().tkv_debug_sparse_aim(ctypes.c_float(float(os.environ["TKV_AIM"])))

@@ -514,6 +514,30 @@ struct QpSmem {
   float wm[QP_WARPS][4], wl[QP_WARPS][4];
 };
 
+// logits of the fp16 residual group for this lane's 8 token slots (mt, r): z[mt * 2 + r]
+__device__ __noinline__ void qp_residual_logits(const uint16_t *kres, const float *qh, int64_t gt0, int64_t ncomp,
+                                                int64_t n, int g8, float *z) {
+  const float inv_sqrt_d = 0.08838834764831845f;
+  for (int mt = 0; mt < 4; ++mt)
+    for (int r = 0; r < 2; ++r) {
+      const int tl = mt * 16 + g8 + 8 * r;
+      const int64_t Tt = gt0 + tl;
+      float a = -INFINITY;
+      if (Tt < n) {
+        const uint16_t *kr = kres + (size_t)(Tt - ncomp) * IM_D;
+        a = 0.0f;
+#pragma unroll 4
+        for (int ch = 0; ch < IM_D; ch += 2) {
+          const uint32_t pr = *reinterpret_cast<const uint32_t *>(kr + ch);
+          a = fmaf(h2f(pr & 0xffff), qh[ch], a);
+          a = fmaf(h2f(pr >> 16), qh[ch + 1], a);
+        }
+        a *= inv_sqrt_d;
+      }
+      z[mt * 2 + r] = a;
+    }
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(QP_WARPS * 32, 1)
     quant_decode_pipe_kernel(QC c, const uint16_t *__restrict__ queries, int G, float *__restrict__ pm,
@@ -606,7 +630,7 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) X[ks] = T.kc[(tw * 4 + ks) * 32 + lane];
       }
-#pragma unroll
+#pragma unroll 1  // one group's code (~12 KB of SASS) per iteration: the loop body stays in the I-cache
       for (int gl = 0; gl < GPT; ++gl) {
         const int64_t gt0 = tile_t0 + gl * IM_G;  // group's first token
         if (gt0 >= n) break;
@@ -697,26 +721,9 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1)
             z[mt][1] = fmaf(fmaf((float)Cc[2], 256.0f, (float)Cc[3]), sc, off) * inv_sqrt_d;
           }
         } else {
-          // the fp16 residual group (< g rows, quantizer.py:529-530): plain FMAs
-#pragma unroll
-          for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const int tl = mt * 16 + g8 + 8 * r;
-              const int64_t Tt = gt0 + tl;
-              float a = -INFINITY;
-              if (Tt < n) {
-                const uint16_t *kr = kres + (size_t)(Tt - ncomp) * IM_D;
-                a = 0.0f;
-                for (int ch = 0; ch < IM_D; ch += 2) {
-                  const uint32_t pr = *reinterpret_cast<const uint32_t *>(kr + ch);
-                  a = fmaf(h2f(pr & 0xffff), S.q[tq][ch], a);
-                  a = fmaf(h2f(pr >> 16), S.q[tq][ch + 1], a);
-                }
-                a *= inv_sqrt_d;
-              }
-              z[mt][r] = a;
-            }
+          // the fp16 residual group (< g rows, quantizer.py:529-530): plain FMAs, out of line
+          // (at most one group per launch; its code must not sit in the hot loop)
+          qp_residual_logits(kres, &S.q[tq][0], gt0, ncomp, n, g8, &z[0][0]);
         }
         if (gt0 + IM_G > n) {  // mask tokens beyond n (complete groups never straddle n)
 #pragma unroll

@@ -558,6 +558,15 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
       fz_mbar_init(&C.bar2);
     }
   }
+  // The step's new row goes to the pinned host store now, not in the final append: nothing reads row
+  // n during this step (attend before append), and a posted PCIe store still in flight when the grid
+  // ends delays its completion -- and the next layer's PDL wait -- by ~3.5 us (tools/pdl_probe.cu).
+  if (ATTEND && new_keys && rank == FZ_CTAS - 1 && tid < 2 * D / 8) {
+    const int half = tid / (D / 8), c8 = (tid % (D / 8)) * 8;  // 16-byte pieces of K then V
+    const uint16_t *src = (half ? new_values : new_keys) + (size_t)u * D + c8;
+    *reinterpret_cast<uint4 *>(s.host_kv + (((size_t)u * s.capacity + n) * 2 + half) * D + c8) =
+        *reinterpret_cast<const uint4 *>(src);
+  }
   bool listed = false;                 // candidate-list path: flags come from keys32 + bitmap
   uint32_t ord_def = 0xffffffffu;      // (list path) keys above this orderable value are selected
   if (select_all) {
@@ -2035,9 +2044,7 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     if (new_keys && rank == FZ_CTAS - 1) {  // (rank 0 is merging the partials meanwhile)
       for (int c = tid; c < D; c += blockDim.x) {
         const uint16_t k = new_keys[(size_t)u * D + c], v = new_values[(size_t)u * D + c];
-        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 0) * D + c] = k;
-        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 1) * D + c] = v;
-        s.kt[((size_t)u * D + c) * s.capacity + n] = k;
+        s.kt[((size_t)u * D + c) * s.capacity + n] = k;  // (the host store row went out at kernel start)
         float *cm = &s.chmax[(size_t)u * D + c];
         *cm = fmaxf(*cm, fabsf(h2f(k)));
         const int64_t lr = n - s.local_offset;

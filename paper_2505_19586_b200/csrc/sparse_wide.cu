@@ -444,7 +444,6 @@ __device__ __forceinline__ double exact_score(const uint16_t *kt, int64_t cap, c
 // trace marks of unit 0 (partitions < 32)
 constexpr int WK_TRACE_P = 32;
 __device__ int g_wk_trace;
-__device__ int g_wk_exp;  // experiments
 __device__ unsigned long long g_wk_mark[WK_TRACE_P][WK_NMARK];
 __device__ unsigned int g_wk_path[4];  // select paths taken (units x launches): list 0, list 1, radix, exact radix
 __device__ int g_wk_dbg[8];  // unit 0, partition 0, last launch: merged list, band, need_b, keys above all lists
@@ -937,6 +936,15 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
 #pragma unroll 1
     for (int i = 0; i < d_s; ++i)
       bulk_g2s(raw + (size_t)i * WK_MAXM, kt + (size_t)S.chs[i] * s.capacity + j0, (uint32_t)(m8 * 2), &S.bar_tma);
+  }
+  // The step's new row goes to the pinned host store now, not in the final append: nothing reads row
+  // n during this step (attend before append), and a posted PCIe store still in flight when the grid
+  // ends delays its completion -- and the next layer's PDL wait -- by ~3.5 us (tools/pdl_probe.cu).
+  if (a.new_keys && r == P - 1 && tid < 2 * WK_D / 8) {
+    const int half = tid / (WK_D / 8), c8 = (tid % (WK_D / 8)) * 8;  // 16-byte pieces of K then V
+    const uint16_t *src = (half ? a.new_values : a.new_keys) + (size_t)u * WK_D + c8;
+    *reinterpret_cast<uint4 *>(s.host_kv + (((size_t)u * s.capacity + n) * 2 + half) * WK_D + c8) =
+        *reinterpret_cast<const uint4 *>(src);
   }
   // every CTA of this grid is resident once all have passed this point, so the next layer's kernel
   // (which only reads its own layer before its own wait) may start placing CTAs
@@ -1802,11 +1810,7 @@ __global__ void __maxnreg__(96) sparse_wide_kernel(SL s, WArgs a) {
 #pragma unroll 1
     for (int c = tid; c < WK_D; c += blockDim.x) {
       const uint16_t kx = a.new_keys[(size_t)u * WK_D + c], vx = a.new_values[(size_t)u * WK_D + c];
-      if (!g_wk_exp) {
-        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 0) * WK_D + c] = kx;
-        s.host_kv[(((size_t)u * s.capacity + n) * 2 + 1) * WK_D + c] = vx;
-      }
-      s.kt[((size_t)u * WK_D + c) * s.capacity + n] = kx;
+      s.kt[((size_t)u * WK_D + c) * s.capacity + n] = kx;  // (the host store row went out at kernel start)
       float *cm = &s.chmax[(size_t)u * WK_D + c];
       *cm = fmaxf(*cm, fabsf(h2f(kx)));
       const int64_t lr = n - s.local_offset;
@@ -1975,9 +1979,6 @@ extern "C" int tkv_debug_wide_dbg(int *out) {  // [8]
 extern "C" int tkv_debug_wide_unit_ends(unsigned long long *out) {  // [64] + latest CTA exit
   cudaMemcpyFromSymbol(out + 64, tkv::wide::g_wk_lastexit, sizeof(unsigned long long));
   return cudaMemcpyFromSymbol(out, tkv::wide::g_wk_uend, sizeof(tkv::wide::g_wk_uend)) == cudaSuccess ? 0 : 7;
-}
-extern "C" int tkv_debug_wide_exp(int v) {
-  return cudaMemcpyToSymbol(tkv::wide::g_wk_exp, &v, sizeof(int)) == cudaSuccess ? 0 : 7;
 }
 extern "C" int tkv_wide_parts(int32_t units) { return tkv::wide::parts_for(units); }
 // bounded-wait timeouts of the wide decode since the last reset (0 = none; 1 unit barrier, 2 mbarrier)
