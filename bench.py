@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--cache-steps", type=int, default=4,
                     help="HBM row cache window: a value row stays resident until unselected for this many steps (0: off)")
     ap.add_argument("--seed", type=int, default=2505)
+    ap.add_argument("--shard-of", type=int, default=1,
+                    help="run rank 0's share of an N-GPU kv-head shard on this GPU without the all-gather "
+                         "(per-GPU work of the multi-GPU configuration; not the headline)")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     args.ctx = c["ctx"] if args.ctx is None else args.ctx
@@ -244,7 +247,8 @@ def workload_config(args, n_topk, world=1):
         "ctx": args.ctx, "batch": args.batch, "layers": m.num_layers, "q_layers": list(args.q_layers),
         "bits": args.bits, "group_size": 64, "n_topk": n_topk, "n_local": 64, "d_s": 8,
         "kv_heads": m.num_kv_heads, "q_heads": m.num_query_heads, "head_dim": m.head_dim,
-        "parallelism": f"kv-head shard x{world}",
+        "parallelism": (f"kv-head shard x{world}" if getattr(args, "shard_of", 1) <= 1 else
+                        f"rank 0's share of a kv-head shard x{args.shard_of} on one GPU, all-gather not run"),
         "key_rows_from": "host (PCIe)" if args.keys_over_pcie else "hbm (scorer copy); value rows over PCIe",
         "l2": "inputs larger than L2 (every step reads > 1 GB of HBM)",
     }
@@ -403,8 +407,12 @@ def main():
     t_setup = time.time()
     wl = make_workload(L, args.q_layers, model.num_query_heads, model.num_kv_heads, model.head_dim, n, total,
                        batch=B, seed=args.seed, device=device)
-    eng = P.DecodeEngine(model, wl.labels, cfg, batch=B, max_steps=total, rank=rank, world_size=world,
-                         device=device)
+    if args.shard_of > 1:  # one rank's share of an N-GPU run, collective not run (see --help)
+        eng = P.DecodeEngine(model, wl.labels, cfg, batch=B, max_steps=total, rank=0, world_size=args.shard_of,
+                             process_group="none", device=device)
+    else:
+        eng = P.DecodeEngine(model, wl.labels, cfg, batch=B, max_steps=total, rank=rank, world_size=world,
+                             device=device)
     if os.environ.get("TKV_FZ_DBG"):  # experiments in the sparse kernel (debug bits)
         _lib.load().tkv_debug_sparse_trace(int(os.environ["TKV_FZ_DBG"]) & ~1)
     if os.environ.get("TKV_AIM"):  # tuning: first aimed range half-width (score sd)

@@ -149,9 +149,10 @@ def load():
 
 
 def set_sparse_kernel(mode: int) -> None:
-    """Which kernel runs a fused sparse decode: -1 auto (the wide decode when a
-    GPU holds few units, else one cluster per unit), 0 always the cluster
-    kernel, 1 the wide decode whenever the shape allows (tests, experiments)."""
+    """Which kernel runs a fused sparse decode: -1 auto (one thread-block
+    cluster per unit; the wide decode only for shapes the cluster kernel
+    cannot take), 0 never the wide decode, 1 the wide decode whenever the
+    shape allows (tests, experiments)."""
     load().tkv_debug_sparse_wide(int(mode))
 
 

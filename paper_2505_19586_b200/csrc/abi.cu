@@ -335,7 +335,7 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
   int64_t ctl_b, scr_b;
   decode_ws_parts(s->units, s->d, &ctl_b, &scr_b);
   char *ws0 = static_cast<char *>(workspace);
-  if (wide::supported(*s, G, n_local, d_s, keys_from_device))
+  if (wide::supported(*s, G, n_local, d_s, keys_from_device, sparse_decode_supported(*s, G, n_local)))
     return wide::decode(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                         keys_from_device, out, new_keys, new_values, ws0, ws0 + ctl_b, as_stream(stream));
   if (sparse_decode_supported(*s, G, n_local))

@@ -205,25 +205,38 @@ __device__ __forceinline__ void merge_partials(const float *pm, const float *pl,
     ll[i] = __ldcg(&pl[i]);
   }
   __syncthreads();
-  if (threadIdx.x < G) {
-    const int h = threadIdx.x;
+  // one warp per head: the maximum, the rescale factors and the sum over the partials (lane-strided,
+  // then a fixed butterfly: the summation order is deterministic)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int h = warp; h < G; h += nw) {
     float M = -INFINITY;
-    for (int ci = 0; ci < nvalid; ++ci) M = fmaxf(M, sc[ci * G + h]);
+    for (int ci = lane; ci < nvalid; ci += 32) M = fmaxf(M, sc[ci * G + h]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.0f;
-    for (int ci = 0; ci < nvalid; ++ci) {
+    for (int ci = lane; ci < nvalid; ci += 32) {
       const float m = sc[ci * G + h];
       const float e = m == -INFINITY ? 0.0f : __expf(m - M);
+      L = fmaf(e, ll[ci * G + h], L);
       sc[ci * G + h] = e;
-      L += e * ll[ci * G + h];
     }
-    ll[h] = L;  // reuse slot h (chunk 0 entries are consumed above)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    __syncwarp();
+    if (lane == 0) ll[h] = L;  // (slot h of chunk 0: its lane has consumed it above)
   }
   __syncthreads();
   for (int i = threadIdx.x; i < G * d; i += blockDim.x) {
     const int h = i / d, c = i % d;
     float A = 0.0f;
-#pragma unroll 8
-    for (int ci = 0; ci < nvalid; ++ci) A += sc[ci * G + h] * __ldcg(&pacc[((size_t)ci * G + h) * d + c]);
+    for (int c0 = 0; c0 < nvalid; c0 += 16) {  // 16 partials in flight per thread
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = c0 + j < nvalid ? __ldcg(&pacc[((size_t)(c0 + j) * G + h) * d + c]) : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < nvalid) A = fmaf(sc[(c0 + j) * G + h], v[j], A);
+    }
     out[(size_t)h * d + c] = A / ll[h];
   }
 }

@@ -27,7 +27,7 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
                         float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st);
 }  // namespace fz4
 namespace wide {  // the wide decode (sparse_wide.cu): P CTAs per unit, for few units per GPU
-bool supported(const SL &s, int G, int n_local, int d_s, int keys_from_device);
+bool supported(const SL &s, int G, int n_local, int d_s, int keys_from_device, bool cluster_ok);
 int64_t ctl_bytes(int units, int d);      // per-unit counters + histograms (zero between launches)
 int64_t scratch_bytes(int units, int d);  // per-unit headers, lists, partials
 int parts_for(int units);

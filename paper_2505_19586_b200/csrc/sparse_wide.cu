@@ -1868,14 +1868,18 @@ static int g_force = -1;  // tkv_debug_sparse_wide: runtime override of TKV_WIDE
 
 bool reserve(int units, int d) { return d == WK_D && sm_count() / std::max(1, units) >= 4; }
 
-bool supported(const SL &s, int G, int n_local, int d_s, int keys_from_device) {
+// Auto (mode -1) prefers the cluster kernel: measured equal at 8 units per GPU and faster at 1-4 units
+// (both are bound by the serial latency of their phases, and the wide decode's unit
+// barrier, list exchange and two-level merge grow with its partitions); the wide decode runs when
+// forced, or when the cluster kernel cannot take the shape.
+bool supported(const SL &s, int G, int n_local, int d_s, int keys_from_device, bool cluster_ok) {
   const int md = g_force >= 0 ? g_force : mode();
-  if (md == 0) return false;
+  if (md == 0 || (md < 0 && cluster_ok)) return false;
   if (!(s.d == WK_D && G >= 1 && G <= 8 && d_s >= 1 && d_s <= WK_MAXDS && s.capacity % 8 == 0)) return false;
   if (keys_from_device && s.kdev == nullptr) return false;  // key rows from the scorer copy: cluster kernel
   if (!reserve(s.units, s.d)) return false;
   const int P = parts_for(s.units);
-  if (P < (md == 1 ? 2 : 4)) return false;
+  if (P < 2) return false;
   const int64_t ncand = s.capacity > n_local ? s.capacity - n_local : 0;
   const int64_t chunk = ((ncand + P - 1) / P + 15) & ~int64_t(15);
   if (chunk > WK_MAXM) return false;

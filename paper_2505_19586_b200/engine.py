@@ -182,7 +182,12 @@ class DecodeEngine:
         self.group = process_group
         self.plan = shard_plan(batch, model.num_kv_heads, world_size)
         self._host_collective = False
-        if world_size > 1:
+        # process_group == "none": rank `rank`'s share of a world_size-GPU run without the collective
+        # (bench.py --shard-of: per-GPU work of a multi-GPU configuration measured on one GPU)
+        self._no_collective = process_group == "none"
+        if self._no_collective:
+            self.group = None
+        elif world_size > 1:
             import torch.distributed as dist
 
             self._host_collective = dist.get_backend(process_group) != "nccl"
@@ -382,7 +387,7 @@ class DecodeEngine:
                     t0 = self._mark(main)
                     lay.append(self.new_keys[l], self.new_values[l])
                     self._span("sparse_append", l, t0, main)
-            if self.world > 1:
+            if self.world > 1 and not self._no_collective:
                 self._all_gather(l)
         main.wait_stream(self.side)
 

@@ -24,3 +24,14 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(params=["cluster", "wide"])
+def sparse_kernel(request):
+    """Run a sparse-decode test on both fused kernels: one thread-block cluster
+    per unit (the default) and the wide decode (P CTAs per unit)."""
+    from paper_2505_19586_b200 import _lib
+
+    _lib.set_sparse_kernel(0 if request.param == "cluster" else 1)
+    yield request.param
+    _lib.set_sparse_kernel(-1)

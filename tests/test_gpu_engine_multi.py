@@ -27,7 +27,7 @@ def tkv():
 
 
 @pytest.mark.parametrize("cache", [0, 1], ids=["no_cache", "row_cache"])
-def test_fused_decode_append_back_to_back(tkv, cache):
+def test_fused_decode_append_back_to_back(tkv, cache, sparse_kernel):
     """T decode+append launches on one layer queued without a host sync (the
     documented OffloadedLayerKV.decode(..., new_keys=, new_values=) call):
     step t must see exactly n0 + t tokens (pipeline.py:315-413,

@@ -390,7 +390,7 @@ def _check_decode(keys, values, queries, chans, G, cfg, res, n):
 
 @pytest.mark.parametrize("dist", ["normal", "ties", "zeros", "outliers", "near_ties"])
 @pytest.mark.parametrize("kod", [True, False], ids=["keys_hbm", "keys_pcie"])
-def test_fused_sparse_decode_matches_oracle(tkv, dist, kod):
+def test_fused_sparse_decode_matches_oracle(tkv, dist, kod, sparse_kernel):
     """One launch (scores + exact top-k + gather + attention) against the
     oracle: identical index sets (ties by the reference's index rule) and
     outputs within 1e-5."""
@@ -421,7 +421,7 @@ def test_fused_sparse_decode_shapes(tkv, d, G):
 
 
 @pytest.mark.parametrize("n", [300, 130, 70, 40])
-def test_fused_sparse_decode_select_all(tkv, n):
+def test_fused_sparse_decode_select_all(tkv, n, sparse_kernel):
     """n <= n_local + n_topk: every token is attended (retriever.py:204-205),
     including contexts shorter than the cluster's slices."""
     rng = np.random.default_rng(33)
@@ -438,7 +438,7 @@ def test_fused_sparse_decode_select_all(tkv, n):
 
 
 @pytest.mark.parametrize("window,rows", [(1, None), (3, None), (100, None), (2, 60)])
-def test_fused_sparse_decode_row_cache_across_steps(tkv, window, rows):
+def test_fused_sparse_decode_row_cache_across_steps(tkv, window, rows, sparse_kernel):
     """Decode -> append -> decode ... with the HBM row cache (rows selected in
     the last `window` steps stay resident): rows served from the cache give
     the oracle's results at every step, and slots are recycled."""
@@ -519,7 +519,7 @@ def test_fused_sparse_decode_many_units_4cta_clusters(tkv):
     assert hits > 0 and misses > 0
 
 
-def test_fused_sparse_decode_128k(tkv):
+def test_fused_sparse_decode_128k(tkv, sparse_kernel):
     """Config-2 head shape (131072 tokens, n_topk 2621, d_s 8) against the
     oracle for two heads."""
     rng = np.random.default_rng(35)
@@ -571,7 +571,7 @@ def _golden_trace():
 @pytest.mark.parametrize("graph,kfh", [(False, True), (False, False), (True, True)],
                          ids=["eager-keys_hbm", "eager-keys_pcie", "graph-keys_hbm"])
 @pytest.mark.parametrize("run", list(cases.PIPELINE_CONFIGS), ids=str)
-def test_engine_replays_reference_pipeline(tkv, run, graph, kfh):
+def test_engine_replays_reference_pipeline(tkv, run, graph, kfh, sparse_kernel):
     z = _golden_trace()
     ref = META["pipeline"]["runs"][run]
     rc = ref["config"]

@@ -90,7 +90,7 @@ def _run_and_check(tkv, w, hq, h, d, bits, B, n_topk, T, graph_from=None):
     return hits, misses
 
 
-def test_config2_sparse_layers_128k_multistep_row_cache_and_hint(tkv):
+def test_config2_sparse_layers_128k_multistep_row_cache_and_hint(tkv, sparse_kernel):
     """131,072-token sparse layers, 4 KV heads, 6 steps with the per-step
     outlier drift (trace.py:268-275), row cache W=4 and the threshold hint on:
     selections, channels, fetch counts and outputs equal the oracle's at every

@@ -43,7 +43,7 @@ def _decode(tkv, lay, queries, chans, G, cfg, kod=True):
 @pytest.mark.parametrize("n_sink", [1, 4, 37])
 @pytest.mark.parametrize("dist", ["normal", "ties", "near_ties"])
 @pytest.mark.parametrize("n", [20000, 700, 150])
-def test_fused_decode_with_sinks_matches_oracle(tkv, n_sink, dist, n):
+def test_fused_decode_with_sinks_matches_oracle(tkv, n_sink, dist, n, sparse_kernel):
     rng = np.random.default_rng(n_sink * 7 + n)
     units, d, G, d_s = 3, 128, 4, 8
     keys = cases.f16(_keys_for(dist, rng, (units, n, d)))
