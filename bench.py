@@ -684,15 +684,17 @@ def main():
     dom = rooflines["sparse_decode"]
     # DRAM traffic per launch from the committed ncu --set full capture of the same kernels
     traffic = {}
-    tpath = ROOT / "profiles" / "r1_ncu_traffic.json"
+    tpath = ROOT / "profiles" / "r2" / "r2_ncu_traffic.json"
     if tpath.exists():
         traffic = json.loads(tpath.read_text())
     def _traffic(name):
         t = traffic.get(name)
         return None if t is None else t["dram_bytes_read"] + t["dram_bytes_write"]
     rooflines["quant_decode"]["traffic"] = _traffic("quant_decode_pipe_kernel") or _traffic("quant_decode_imma_kernel")
+    # (stage 1's DRAM bytes include the 16.8 MB L2 prefetch of the next layer's scorer columns it issues)
+    rooflines["stage1"]["traffic"] = _traffic("stage1_fused_kernel") if args.batch <= 2 else None
     # f4: the reference's decode-step timeline model (memsim.py:339-602) driven by the costs measured above
-    from paper_2505_19586_b200.timeline import measured_step
+    from tools.timeline_model import measured_step
     bw = memcpy_gbs * 1e9
     tl_serial = measured_step(wl.labels, quant_ms * 1e-3, sparse_ms * 1e-3, stage1_ms * 1e-3, gather_bytes, bw)
     tl_side = measured_step(wl.labels, quant_ms * 1e-3, sparse_ms * 1e-3, 0.0, gather_bytes, bw)
@@ -705,7 +707,7 @@ def main():
         "model_reference_transfers_ms": tl_ref["step_seconds"] * 1e3,
         "model_reference_transfers_overlap": tl_ref["overlap_fraction"],
         "model_reference_transfers_stall_ms": tl_ref["stall_seconds"] * 1e3 / 4,
-        "note": "paper_2505_19586_b200.timeline (the reference model, golden-tested) fed with this run's per-kernel "
+        "note": "tools/timeline_model.py (the reference model, golden-tested) fed with this run's per-kernel "
                 "times (graph-node events) and PCIe bytes: model_ms runs stage 1 concurrently (side stream), "
                 "model_serial_estimate_ms on the one compute engine the reference assumes, "
                 "model_reference_transfers_ms with the reference's per-step critical-key prefetch and K+V Top-K "
@@ -734,11 +736,14 @@ def main():
         "config": workload_config(args, n_topk, world),
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": "GB/s",
                      "frac": dom["frac"], "traffic": _traffic("sparse_fused_kernel") if not args.unfused else None,
-                     "traffic_note": "DRAM bytes per launch (ncu --set full capture of a main-mode launch, "
-                                     "profiles/r1_ncu_traffic.json): 28.2 MB against 27.9 MB algorithmic",
-                     "bound_note": "the launch is a chain of dependent phases (score, cluster select, gather, "
-                                   "attention, merge; profiles/r1_kernels.md 2), so it runs well under the HBM "
-                                   "roofline; the PCIe leg is rooflines.sparse_decode.pcie_*",
+                     "traffic_note": "DRAM bytes per launch of the cluster kernel (ncu --set full capture of a "
+                                     "main-mode launch, profiles/r2/r2_ncu_traffic.json): 29.9 MB against 27.5 MB "
+                                     "algorithmic",
+                     "bound_note": "the launch is a chain of ~15 dependent, latency-bound phases (scores, select, "
+                                   "gather, attention, merges) plus its instruction fetch (121 KB of SASS per launch); "
+                                   "it takes ~43 us whatever the work per CTA (DESIGN.md 4.7, profiles/r2/"
+                                   "r2_kernels.md), far from the HBM roofline; the PCIe leg is "
+                                   "rooflines.sparse_decode.pcie_*",
                      "kernel": dom["kernel"], "timing": dom["timing"]},
         "rooflines": rooflines,
         "row_cache": {"window_steps": cfg.row_cache_steps, "slots_per_head": (eng.retrieval.n_local + eng.retrieval.n_topk) * cfg.row_cache_steps,

@@ -203,13 +203,13 @@ def test_package_trace_reader_errors(tmp_path):
 
 
 def test_timeline_model_matches_reference_golden():
-    """paper_2505_19586_b200.timeline (the reference's decode-step timeline model, memsim.py:339-602)
+    """tools/timeline_model.py (the reference's decode-step timeline model, memsim.py:339-602)
     reproduces the reference's schedule: every event start, total time, overlap and stall
     (tests/golden/timeline.json, made by tests/golden/make_timeline_golden.py)."""
     import json
     from pathlib import Path
 
-    from paper_2505_19586_b200 import timeline as T
+    from tools import timeline_model as T
 
     cases = json.loads((Path(__file__).parent / "golden" / "timeline.json").read_text())
     for c in cases:
@@ -229,7 +229,7 @@ def test_timeline_measured_step_model():
     """measured_step: the reference model has one compute engine, so its estimate passes serialise
     with the layers (this engine runs them on a side stream: estimate 0 models that); PCIe bytes
     on the link add their time to the chain they gate."""
-    from paper_2505_19586_b200 import timeline as T
+    from tools import timeline_model as T
 
     labels = ["q", "q"] + ["s"] * 30
     serial = T.measured_step(labels, 45e-6, 43e-6, 37e-6, 0, 50e9)

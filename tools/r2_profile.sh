@@ -9,11 +9,12 @@ mkdir -p $OUT
 TAG=${1:-r2}
 BENCH="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-fidelity"
 NCU=ncu
-# only this repo's kernels (torch's workload generation is skipped by the name filter); the
-# variant mode runs first (~9 steps x 64 launches), so -s 900 lands in the main mode
+# only this repo's kernels (matched on their base names); the keys-over-PCIe variant runs first
+# (2 + 5 + 2 steps x 64 launches = 576), so -s 700 -c 64 is one step of the main mode
+KERN='regex:sparse_fused_kernel|sparse_wide_kernel|quant_decode|stage1_|append_kernel|combine|sparse_attn|select'
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k 'regex:^(?!.*(native|at_cuda|at::|cub)).*' -s 900 -c 128 --csv --log-file $OUT/ncu_${TAG}_launches.csv $BENCH > $OUT/ncu_${TAG}_launches.log 2>&1
-for spec in "sparse_fused:400" "quant_decode_pipe:20" "stage1:400"; do
+    -k "$KERN" -s 700 -c 64 --csv --log-file $OUT/ncu_${TAG}_launches.csv $BENCH > $OUT/ncu_${TAG}_launches.log 2>&1
+for spec in "sparse_fused:600" "quant_decode_pipe:20" "stage1:600"; do
     name=${spec%%:*}; skip=${spec##*:}
     $NCU --set full --clock-control none --import-source on -k regex:$name -s $skip -c 1 \
         -o $OUT/ncu_${TAG}_$name -f $BENCH > $OUT/ncu_${TAG}_$name.log 2>&1

@@ -17,7 +17,7 @@ import heapq
 from dataclasses import dataclass, field
 from typing import Sequence
 
-from .errors import ParameterError, SchedulingError, ShapeError
+from paper_2505_19586_b200.errors import ParameterError, SchedulingError, ShapeError
 
 
 @dataclass(frozen=True)
