@@ -10,151 +10,284 @@
 namespace tkv {
 
 // ---------------------------------------------------------------------------
-// Pack keys: one CTA per (key tile, unit).  quantizer.py:277-293.
+// Prefill pack (quantize_layer_kv, quantizer.py:252-293, 479-497): HBM-bound.
+// The codec is a monotone step function of x inside a group, so each group's
+// codes are fixed by 2^b - 1 fp16 thresholds: T_k = the smallest fp16 x in
+// [lo, hi] whose float64 reference code is >= k, found by a short search next
+// to the real-valued boundary.  Encoding is then fp16x2 compares, with no
+// division and no float64 per element; code(x) = sum_k [x >= T_k] is exactly
+// the reference's code for every fp16 x in the group.  A degenerate group
+// (hi == lo, code 0) gets NaN thresholds, which no compare passes.
+// Tiles are staged with 16-byte loads into padded rows (conflict-free SMEM),
+// group min/max uses fp16x2 min/max (exact), the MMA-native words are
+// assembled straight from the tile and written 8 bytes per thread
+// (consecutive threads, consecutive words), and the largest group scale is
+// reduced per CTA and published with one atomic per CTA.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void block_max_pos(float v, float *sm, float *gaddr) {
+  // v >= 0: the int bits are monotone
+  const int vi = __reduce_max_sync(0xffffffffu, __float_as_int(v));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int *>(sm), vi);
+  __syncthreads();
+  if (threadIdx.x == 0 && *sm > 0.0f) atomic_max_pos(gaddr, *sm);
+}
+
+// The reference code of x (quantizer.py:66-117) in float64, without encode_code's fp32 fast path.
+__device__ __noinline__ int ref_code(float xf, float lof, float hif, int bits) {
+  if (bits == 1) return 2.0 * (double)xf >= __dadd_rn((double)hif, (double)lof) ? 1 : 0;
+  const double sd = __ddiv_rn(__dsub_rn((double)hif, (double)lof), 3.0);
+  const double vd = __ddiv_rn(__dsub_rn((double)xf, (double)lof), sd);
+  double r = floor(__dadd_rn(fabs(vd), 0.5));
+  if (vd < 0) r = -r;
+  return min(max((int)r, 0), 3);
+}
+
+// Group min/max with fp16 min/max, which order -0 below +0: a zero minimum is
+// stored as -0 when the group holds a -0 (the reference's float64 min keeps
+// the sign of the zero it meets; with both signs present its pick follows
+// numpy's reduction order and is not reproduced).  The sign of a zero maximum
+// never reaches an output (only hi - lo is used).
+__device__ __forceinline__ uint16_t hmin_bits(uint16_t a, uint16_t b) {
+  return __half_as_ushort(__hmin(__ushort_as_half(a), __ushort_as_half(b)));
+}
+__device__ __forceinline__ uint16_t hmax_bits(uint16_t a, uint16_t b) {
+  return __half_as_ushort(__hmax(__ushort_as_half(a), __ushort_as_half(b)));
+}
+
+// fp16 bits <-> a signed order index (-0 and +0 both map to 0).
+__device__ __forceinline__ int h_ord(uint16_t h) { return (h & 0x8000u) ? -(int)(h & 0x7fffu) : (int)h; }
+__device__ __forceinline__ uint16_t h_unord(int o) { return o < 0 ? (uint16_t)(0x8000u | (uint32_t)(-o)) : (uint16_t)o; }
+
+// T_k for one group (lo <= hi as fp16 bits), k = 1 .. 2^b - 1.
+__device__ uint16_t code_threshold(uint16_t lob, uint16_t hib, int bits, int k) {
+  const float lof = h2f(lob), hif = h2f(hib);
+  if (!(hif > lof)) return 0x7fffu;  // degenerate: code 0 everywhere
+  const float est = fminf(fmaxf(lof + ((float)k - 0.5f) * ((hif - lof) / (float)((1 << bits) - 1)), lof), hif);
+  const int olo = h_ord(lob), ohi = h_ord(hib);
+  int o = min(max(h_ord(__half_as_ushort(__float2half_rn(est))), olo), ohi);
+  if (ref_code(h2f(h_unord(o)), lof, hif, bits) >= k) {
+    while (o > olo && ref_code(h2f(h_unord(o - 1)), lof, hif, bits) >= k) --o;
+  } else {
+    do ++o;
+    while (o < ohi && ref_code(h2f(h_unord(o)), lof, hif, bits) < k);
+  }
+  return h_unord(o);
+}
+
+__device__ __forceinline__ uint32_t hge2_mask(uint32_t x, uint32_t t) {
+  return __hge2_mask(*reinterpret_cast<__half2 *>(&x), *reinterpret_cast<__half2 *>(&t));
+}
+
+// Code bits of two fp16 (x) against per-element thresholds t[0..NT) (half2 each): the masks are nested
+// (T_1 <= T_2 <= T_3), so bit 0 of the count is their XOR and bit 1 is the second mask.  The result
+// holds element 0's code at bit `sh` and element 1's at bit 16 + sh.
+template <int BITS>
+__device__ __forceinline__ uint32_t code_bits2(uint32_t x, const uint32_t *t, int sh) {
+  if constexpr (BITS == 1) {
+    return hge2_mask(x, t[0]) & (0x00010001u << sh);
+  } else {
+    const uint32_t m1 = hge2_mask(x, t[0]), m2 = hge2_mask(x, t[1]), m3 = hge2_mask(x, t[2]);
+    return ((m1 ^ m2 ^ m3) & (0x00010001u << sh)) | (m2 & (0x00020002u << sh));
+  }
+}
+
+constexpr int PK_PAD = 16;  // key tile row padding (fp16): rows 8 banks apart for 8-byte loads
+constexpr int PK_SEG = 4;   // row segments per key group in the min/max
+
+// Pack keys: one CTA per (key tile of Tk = 16*8/b tokens, unit); groups are G tokens x 1 channel.
+template <int BITS, int G>
 __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__restrict__ keys, int64_t n,
                                                          int64_t n_complete) {
+  constexpr int Tk = 16 * (8 / BITS), NT = (1 << BITS) - 1, KS = 8 / BITS, GR = Tk / G, SR = G / PK_SEG;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int d = c.d, bits = c.bits, g = c.g;
-  const int Tk = key_tile_tokens(bits);
+  __shared__ float bmax;
+  const int d = c.d;
   const int u = blockIdx.y;
   const int64_t t0 = (int64_t)blockIdx.x * Tk;
   if (t0 >= n_complete) return;
   const int rows = (int)imin64(Tk, n_complete - t0);  // complete groups only
-  uint16_t *tile = reinterpret_cast<uint16_t *>(smem);               // [Tk][d]
-  uint8_t *codes = reinterpret_cast<uint8_t *>(smem + (size_t)Tk * d * 2);  // [Tk][d]
-  uint32_t *lohi = reinterpret_cast<uint32_t *>(codes + (size_t)Tk * d);      // [Tk/g][d]
+  const int RS = d + PK_PAD, P2 = d / 2;               // row stride (fp16), channel pairs
+  uint16_t *tile = reinterpret_cast<uint16_t *>(smem);                                      // [Tk][RS]
+  uint32_t *thr = reinterpret_cast<uint32_t *>(tile + (size_t)Tk * RS);                    // [GR][NT][d/2] fp16x2
+  uint2 *red = reinterpret_cast<uint2 *>(thr + (size_t)GR * NT * P2);                      // [GR][SEG][d/2]
+  if (threadIdx.x == 0) bmax = 0.0f;
   const uint16_t *src = keys + ((size_t)u * n + t0) * d;
-  // stage the tile (16-byte vectors; d % 32 == 0 keeps rows 16B aligned)
-  const int vec_per_row = d / 8;
-  for (int v = threadIdx.x; v < rows * vec_per_row; v += blockDim.x) {
-    reinterpret_cast<uint4 *>(tile)[v] = __ldg(reinterpret_cast<const uint4 *>(src) + v);
-  }
+  const int vpr = d / 8;
+#pragma unroll 4
+  for (int v = threadIdx.x; v < rows * vpr; v += blockDim.x)
+    *reinterpret_cast<uint4 *>(tile + (size_t)(v / vpr) * RS + (v % vpr) * 8) =
+        __ldg(reinterpret_cast<const uint4 *>(src) + v);
+  // groups past `rows` (a partial last tile) get NaN thresholds: code 0
+  for (int i = rows / G * NT * P2 + threadIdx.x; i < GR * NT * P2; i += blockDim.x) thr[i] = 0x7fff7fffu;
   __syncthreads();
-  const int groups = rows / g;
-  for (int p = threadIdx.x; p < groups * d; p += blockDim.x) {
-    const int grp = p / d, ch = p % d;
-    float lo = h2f(tile[(grp * g) * d + ch]), hi = lo;
-    uint16_t lob = tile[(grp * g) * d + ch], hib = lob;
-    for (int r = 1; r < g; ++r) {
-      uint16_t xb = tile[(grp * g + r) * d + ch];
-      float x = h2f(xb);
-      if (x < lo) { lo = x; lob = xb; }
-      if (x > hi) { hi = x; hib = xb; }
-    }
-    // canonicalise -0.0 so the fp16 bits reproduce float64 min/max values
-    if (lo == 0.0f) lob = 0x0000u;
-    if (hi == 0.0f) hib = 0x0000u;
-    const uint32_t w = pack_lohi(lob, hib);
-    lohi[p] = w;
-    c.key_lohi[((size_t)u * (c.capacity / g) + (t0 / g) + grp) * d + ch] = w;
-    atomic_max_pos(&c.val_smax[2 * u + 1], hi > lo ? (hi - lo) / (float)((1 << bits) - 1) : 0.0f);
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < Tk * d; p += blockDim.x) {
-    const int t = p / d, ch = p % d;
-    uint8_t code = 0;
-    if (t < rows) {
-      const uint32_t w = lohi[(t / g) * d + ch];
-      code = (uint8_t)encode_code(h2f(tile[p]), h2f((uint16_t)(w & 0xffff)), h2f((uint16_t)(w >> 16)), bits);
-    }
-    codes[p] = code;
-  }
-  __syncthreads();
-  // assemble native words for this tile: (d/32) * 32 lanes * 4 roles
-  const int nwords = (d / 32) * 128;
-  uint32_t *dst = c.key_codes + ((size_t)u * (c.capacity / Tk) + blockIdx.x) * nwords;
-  const int kslots = 8 / bits;
-  for (int wi = threadIdx.x; wi < nwords; wi += blockDim.x) {
-    const int role = wi & 3, lane = (wi >> 2) & 31, ks = wi >> 7;
-    const int g8 = lane >> 2, tq = lane & 3;
-    uint32_t word = 0;
+  const int groups = rows / G;
+  for (int it = threadIdx.x; it < groups * PK_SEG * P2; it += blockDim.x) {
+    const int p = it % P2, r0 = (it / P2) * SR;  // (grp, seg) rows are contiguous
+    const uint32_t *col = reinterpret_cast<const uint32_t *>(tile) + (size_t)r0 * (RS / 2) + p;
+    uint32_t w = col[0];
+    __half2 lo = *reinterpret_cast<__half2 *>(&w), hi = lo;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int ch = 32 * ks + 4 * tq + i + 16 * (role >> 1);
-      for (int k = 0; k < kslots; ++k) {
-        const int t = 16 * k + g8 + 8 * (role & 1);
-        word |= (uint32_t)codes[t * d + ch] << (8 * i + k * bits);
+    for (int r = 1; r < SR; ++r) {
+      w = col[r * (RS / 2)];
+      lo = __hmin2(lo, *reinterpret_cast<__half2 *>(&w));
+      hi = __hmax2(hi, *reinterpret_cast<__half2 *>(&w));
+    }
+    red[it] = make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+  }
+  __syncthreads();
+  float smax = 0.0f;
+  uint16_t *thr16 = reinterpret_cast<uint16_t *>(thr);
+  for (int it = threadIdx.x; it < groups * d; it += blockDim.x) {
+    const int ch = it % d, grp = it / d;
+    const int e = ch & 1;
+    uint16_t lb = 0, hb = 0;
+#pragma unroll
+    for (int sg = 0; sg < PK_SEG; ++sg) {
+      const uint2 lh = red[((size_t)grp * PK_SEG + sg) * P2 + (ch >> 1)];
+      const uint16_t l = (uint16_t)(e ? lh.x >> 16 : lh.x), h = (uint16_t)(e ? lh.y >> 16 : lh.y);
+      lb = sg ? hmin_bits(lb, l) : l;
+      hb = sg ? hmax_bits(hb, h) : h;
+    }
+    const float lf = h2f(lb), hf = h2f(hb);
+    c.key_lohi[((size_t)u * (c.capacity / G) + (t0 / G) + grp) * d + ch] = pack_lohi(lb, hb);  // zero signs: hmin_bits
+    smax = fmaxf(smax, hf > lf ? (hf - lf) / (float)NT : 0.0f);
+#pragma unroll
+    for (int k = 1; k <= NT; ++k) thr16[((size_t)grp * NT + k - 1) * d + ch] = code_threshold(lb, hb, BITS, k);
+  }
+  block_max_pos(smax, &bmax, &c.val_smax[2 * u + 1]);  // (its __syncthreads also publishes thr)
+  // native words: thread (ks, lane, role pair rp) writes roles 2rp, 2rp+1 (tokens +0 / +8) of
+  // channels ch0 .. ch0+3; token 16k + g8 + 8r lies in group 16k / G
+  uint2 *dst = reinterpret_cast<uint2 *>(c.key_codes + ((size_t)u * (c.capacity / Tk) + blockIdx.x) * (d / 32) * 128);
+  for (int q = threadIdx.x; q < d * 2; q += blockDim.x) {
+    const int rp = q & 1, lane = (q >> 1) & 31, ks = q >> 6;
+    const int g8 = lane >> 2, tq = lane & 3;
+    const int ch0 = 32 * ks + 16 * rp + 4 * tq;
+    uint32_t a0[2] = {0u, 0u}, a1[2] = {0u, 0u};  // channels (0,1) and (2,3): code of slot k at bit k*b (+16)
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const uint2 *tk = reinterpret_cast<const uint2 *>(thr + (size_t)((16 * k) / G) * NT * P2 + ch0 / 2);
+      uint32_t tx[NT], ty[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const uint2 tt = tk[j * (P2 / 2)];
+        tx[j] = tt.x;
+        ty[j] = tt.y;
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint2 x = *reinterpret_cast<const uint2 *>(tile + (size_t)(16 * k + g8 + 8 * r) * RS + ch0);
+        a0[r] |= code_bits2<BITS>(x.x, tx, k * BITS);
+        a1[r] |= code_bits2<BITS>(x.y, ty, k * BITS);
       }
     }
-    dst[wi] = word;
+    dst[(ks * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(a0[0], a1[0], 0x6420), __byte_perm(a0[1], a1[1], 0x6420));
   }
 }
 
-// ---------------------------------------------------------------------------
-// Pack values: one CTA per (32-token tile, unit).  quantizer.py:252-275.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *__restrict__ values, int64_t n,
-                                                           int64_t row0, int64_t src_rows) {
-  // row0: first token index of this call (prefill: 0).  src holds rows [row0, row0+src_rows).
+constexpr int PV_TOK = 128;  // tokens per value CTA (4 value tiles)
+constexpr int PV_PAD = 8;    // value tile row padding (fp16): conflict-free 16-byte row loads and 2-byte gathers
+
+// Pack values: one CTA per 128 tokens of one unit; groups are 1 token x G channels (a ragged last block
+// allowed).  Thread (token, block) takes the group's min/max and thresholds; thread (tile, set, lane, role
+// pair) then encodes and assembles its two words straight from the tile.
+template <int BITS, int G>
+__global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *__restrict__ values, int64_t n) {
+  constexpr int NT = (1 << BITS) - 1, KS = 8 / BITS, PER = 16 * KS;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int d = c.d, bits = c.bits, g = c.g;
-  const int nb = (d + g - 1) / g;
+  __shared__ float bmax;
+  const int d = c.d;
+  const int nb = (d + G - 1) / G;
+  const int TS = (nb * NT) | 1;  // threshold words per token (odd: 4 tokens on distinct banks)
   const int u = blockIdx.y;
-  const int64_t t0 = (int64_t)blockIdx.x * 32;
+  const int64_t t0 = (int64_t)blockIdx.x * PV_TOK;
   if (t0 >= n) return;
-  const int rows = (int)imin64(32, n - t0);
-  uint16_t *tile = reinterpret_cast<uint16_t *>(smem);                  // [32][d]
-  uint8_t *codes = reinterpret_cast<uint8_t *>(smem + 32 * d * 2);       // [32][d]
-  uint32_t *lohi = reinterpret_cast<uint32_t *>(codes + 32 * d);         // [32][nb]
-  __shared__ float smax;
-  if (threadIdx.x == 0) smax = 0.0f;
-  const uint16_t *src = values + ((size_t)u * src_rows + (t0 - row0)) * d;
-  const int vec_per_row = d / 8;
-  for (int v = threadIdx.x; v < rows * vec_per_row; v += blockDim.x)
-    reinterpret_cast<uint4 *>(tile)[v] = __ldg(reinterpret_cast<const uint4 *>(src) + v);
+  const int rows = (int)imin64(PV_TOK, n - t0);
+  const int RS = d + PV_PAD;
+  uint16_t *tile = reinterpret_cast<uint16_t *>(smem);                          // [PV_TOK][RS]
+  uint32_t *thr = reinterpret_cast<uint32_t *>(tile + (size_t)PV_TOK * RS);     // [PV_TOK][TS] fp16x2 (broadcast)
+  if (threadIdx.x == 0) bmax = 0.0f;
+  const uint16_t *src = values + ((size_t)u * n + t0) * d;
+  const int vpr = d / 8;
+#pragma unroll 4
+  for (int v = threadIdx.x; v < rows * vpr; v += blockDim.x)
+    *reinterpret_cast<uint4 *>(tile + (size_t)(v / vpr) * RS + (v % vpr) * 8) =
+        __ldg(reinterpret_cast<const uint4 *>(src) + v);
   __syncthreads();
-  for (int p = threadIdx.x; p < rows * nb; p += blockDim.x) {
-    const int t = p / nb, b = p % nb;
-    const int c0 = b * g, c1 = min(d, c0 + g);
-    uint16_t lob = tile[t * d + c0], hib = lob;
-    float lo = h2f(lob), hi = lo;
-    for (int ch = c0 + 1; ch < c1; ++ch) {
-      const uint16_t xb = tile[t * d + ch];
-      const float x = h2f(xb);
-      if (x < lo) { lo = x; lob = xb; }
-      if (x > hi) { hi = x; hib = xb; }
-    }
-    if (lo == 0.0f) lob = 0;
-    if (hi == 0.0f) hib = 0;
-    const uint32_t w = pack_lohi(lob, hib);
-    lohi[p] = w;
-    c.val_lohi[((size_t)u * c.capacity + t0 + t) * nb + b] = w;
-    atomic_max_pos(&smax, group_scale_f(lo, hi, bits));
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < 32 * d; p += blockDim.x) {
-    const int t = p / d, ch = p % d;
-    uint8_t code = 0;
-    if (t < rows) {
-      const uint32_t w = lohi[t * nb + ch / g];
-      code = (uint8_t)encode_code(h2f(tile[p]), h2f((uint16_t)(w & 0xffff)), h2f((uint16_t)(w >> 16)), bits);
-    }
-    codes[p] = code;
-  }
-  __syncthreads();
-  const int sets = val_sets(d, bits);
-  const int per = 16 * (8 / bits);
-  const int kslots = 8 / bits;
-  const int nwords = sets * 128;
-  uint32_t *dst = c.val_codes + ((size_t)u * (c.capacity / 32) + blockIdx.x) * nwords;
-  for (int wi = threadIdx.x; wi < nwords; wi += blockDim.x) {
-    const int role = wi & 3, lane = (wi >> 2) & 31, set = wi >> 7;
-    const int g8 = lane >> 2, tq = lane & 3;
-    uint32_t word = 0;
+  float smax = 0.0f;
+  for (int p = threadIdx.x; p < PV_TOK * nb; p += blockDim.x) {
+    const int t = p % PV_TOK, b = p / PV_TOK;
+    uint32_t *tt = thr + (size_t)t * TS + b * NT;
+    if (t >= rows) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int t = 4 * tq + i + 16 * (role >> 1);
-      for (int k = 0; k < kslots; ++k) {
-        const int ch = set * per + 16 * k + g8 + 8 * (role & 1);
-        if (ch < d) word |= (uint32_t)codes[t * d + ch] << (8 * i + k * bits);
+      for (int k = 0; k < NT; ++k) tt[k] = 0x7fff7fffu;  // code 0
+      continue;
+    }
+    const int c0 = b * G, c1 = min(d, c0 + G);  // a multiple of 16 channels (d % 32 == 0, G % 16 == 0)
+    const uint4 *row = reinterpret_cast<const uint4 *>(tile + (size_t)t * RS + c0);
+    __half2 lo, hi;
+    for (int v = 0; v < (c1 - c0) / 8; ++v) {
+      const uint4 x = row[v];
+      const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const __half2 h = *reinterpret_cast<const __half2 *>(&xs[j]);
+        lo = (v | j) ? __hmin2(lo, h) : h;
+        hi = (v | j) ? __hmax2(hi, h) : h;
       }
     }
-    // a partial tile (append path) must keep bits of tokens already present
-    if (row0 > t0) word |= dst[wi];
-    dst[wi] = word;
+    const __half l = __hmin(__low2half(lo), __high2half(lo)), h = __hmax(__low2half(hi), __high2half(hi));
+    const uint16_t lb = __half_as_ushort(l), hb = __half_as_ushort(h);  // zero signs: see hmin_bits
+    c.val_lohi[((size_t)u * c.capacity + t0 + t) * nb + b] = pack_lohi(lb, hb);
+    smax = fmaxf(smax, group_scale_f(__half2float(l), __half2float(h), BITS));
+#pragma unroll
+    for (int k = 1; k <= NT; ++k) {
+      const uint32_t tk = code_threshold(lb, hb, BITS, k);
+      tt[k - 1] = tk | (tk << 16);
+    }
   }
-  if (threadIdx.x == 0) atomic_max_pos(&c.val_smax[2 * u], smax);
+  block_max_pos(smax, &bmax, &c.val_smax[2 * u]);  // (its __syncthreads also publishes thr)
+  const int sets = val_sets(d, BITS);
+  const int ntiles = (rows + 31) / 32;
+  uint2 *dst = reinterpret_cast<uint2 *>(c.val_codes + ((size_t)u * (c.capacity / 32) + t0 / 32) * sets * 128);
+  // thread (tile vt, set, lane, role pair rp) writes roles 2rp, 2rp+1 (channels +0 / +8): byte i holds token
+  // 4tq + i + 16rp, bits k*b channel set*PER + 16k + g8 (+8); both channels of a pair lie in one group
+  for (int q = threadIdx.x; q < ntiles * sets * 64; q += blockDim.x) {
+    const int rp = q & 1, lane = (q >> 1) & 31, set = (q >> 6) % sets, vt = q / (sets * 64);
+    const int g8 = lane >> 2, tq = lane & 3;
+    const int tb = vt * 32 + 4 * tq + 16 * rp;
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};  // token i: channel +0 code at bit k*b, channel +8 at 16 + k*b
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const int ch = set * PER + 16 * k + g8;
+      if (ch < d) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint16_t *xr = tile + (size_t)(tb + i) * RS + ch;
+          const uint32_t x = (uint32_t)xr[0] | ((uint32_t)xr[8] << 16);
+          acc[i] |= code_bits2<BITS>(x, thr + (size_t)(tb + i) * TS + (ch / G) * NT, k * BITS);
+        }
+      }
+    }
+    const uint32_t p01 = __byte_perm(acc[0], acc[1], 0x6420), p23 = __byte_perm(acc[2], acc[3], 0x6420);
+    dst[((vt * sets + set) * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(p01, p23, 0x6420), __byte_perm(p01, p23, 0x7531));
+  }
+}
+
+template <int BITS, int G>
+static void launch_pack(const QC &c, const uint16_t *keys, const uint16_t *values, int64_t n, int64_t n_complete,
+                        cudaStream_t st) {
+  constexpr int Tk = 16 * (8 / BITS), NT = (1 << BITS) - 1, GR = Tk / G;
+  if (n_complete > 0) {
+    const size_t sm = (size_t)Tk * (c.d + PK_PAD) * 2 + (size_t)GR * NT * c.d * 2 + (size_t)GR * PK_SEG * (c.d / 2) * 8;
+    cudaFuncSetAttribute(pack_keys_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid((unsigned)((n_complete + Tk - 1) / Tk), c.units);
+    pack_keys_kernel<BITS, G><<<grid, 256, sm, st>>>(c, keys, n, n_complete);
+  }
+  const int nb = (c.d + G - 1) / G;
+  const size_t sm = (size_t)PV_TOK * (c.d + PV_PAD) * 2 + (size_t)PV_TOK * ((nb * NT) | 1) * 4;
+  cudaFuncSetAttribute(pack_values_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid((unsigned)((n + PV_TOK - 1) / PV_TOK), c.units);
+  pack_values_kernel<BITS, G><<<grid, 256, sm, st>>>(c, values, n);
 }
 
 __global__ void copy_residual_kernel(QC c, const uint16_t *__restrict__ keys, int64_t n, int64_t n_complete) {
@@ -188,25 +321,21 @@ int pack(const QC &c, const uint16_t *keys, const uint16_t *values, int64_t n, i
     if (cudaStreamSynchronize(st) != cudaSuccess) return fail(TKV_ERR_CUDA, "finite check failed");
     if (h) return fail(TKV_ERR_NUMERIC, "matrix contains non-finite values");
   }
-  const int Tk = key_tile_tokens(c.bits);
   const int64_t n_complete = (n / c.g) * c.g;
   cudaMemsetAsync(c.val_smax, 0, sizeof(float) * 2 * c.units, st);
-  if (n_complete > 0) {
-    const size_t sm = (size_t)Tk * c.d * 3 + (size_t)(Tk / c.g) * c.d * 4;
-    cudaFuncSetAttribute(pack_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((unsigned)((n_complete + Tk - 1) / Tk), c.units);
-    pack_keys_kernel<<<grid, 256, sm, st>>>(c, keys, n, n_complete);
+  switch (c.bits * 1000 + c.g) {
+    case 1016: launch_pack<1, 16>(c, keys, values, n, n_complete, st); break;
+    case 1032: launch_pack<1, 32>(c, keys, values, n, n_complete, st); break;
+    case 1064: launch_pack<1, 64>(c, keys, values, n, n_complete, st); break;
+    case 1128: launch_pack<1, 128>(c, keys, values, n, n_complete, st); break;
+    case 2016: launch_pack<2, 16>(c, keys, values, n, n_complete, st); break;
+    case 2032: launch_pack<2, 32>(c, keys, values, n, n_complete, st); break;
+    case 2064: launch_pack<2, 64>(c, keys, values, n, n_complete, st); break;
+    default: return fail(TKV_ERR_PARAMETER, "unsupported (bits, group_size) for the CUDA pack");
   }
   if (n > n_complete) {
     dim3 grid((unsigned)(n - n_complete), c.units);
     copy_residual_kernel<<<grid, 128, 0, st>>>(c, keys, n, n_complete);
-  }
-  {
-    const int nb = (c.d + c.g - 1) / c.g;
-    const size_t sm = (size_t)32 * c.d * 3 + (size_t)32 * nb * 4;
-    cudaFuncSetAttribute(pack_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((unsigned)((n + 31) / 32), c.units);
-    pack_values_kernel<<<grid, 256, sm, st>>>(c, values, n, 0, n);
   }
   set_len_kernel<<<1, 1, 0, st>>>(c.len, n);
   return check_launch("tkv_qcache_pack");
@@ -232,15 +361,11 @@ __global__ void __launch_bounds__(256) append_kernel(QC c, const uint16_t *__res
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     const int c0 = b * g, c1 = min(d, c0 + g);
     uint16_t lob = vrow[c0], hib = lob;
-    float lo = h2f(lob), hi = lo;
     for (int ch = c0 + 1; ch < c1; ++ch) {
       const uint16_t xb = vrow[ch];
-      const float x = h2f(xb);
-      if (x < lo) { lo = x; lob = xb; }
-      if (x > hi) { hi = x; hib = xb; }
+      lob = hmin_bits(lob, xb);
+      hib = hmax_bits(hib, xb);
     }
-    if (lo == 0.0f) lob = 0;
-    if (hi == 0.0f) hib = 0;
     vlohi[b] = pack_lohi(lob, hib);
     c.val_lohi[((size_t)u * c.capacity + n) * nb + b] = vlohi[b];
   }
@@ -276,12 +401,11 @@ __global__ void __launch_bounds__(256) append_kernel(QC c, const uint16_t *__res
       float lo = h2f(lob), hi = lo;
       for (int rr = 1; rr < g; ++rr) {
         const uint16_t xb = res[rr * d + ch];
-        const float x = h2f(xb);
-        if (x < lo) { lo = x; lob = xb; }
-        if (x > hi) { hi = x; hib = xb; }
+        lob = hmin_bits(lob, xb);
+        hib = hmax_bits(hib, xb);
       }
-      if (lo == 0.0f) lob = 0;
-      if (hi == 0.0f) hib = 0;
+      lo = h2f(lob);
+      hi = h2f(hib);
       c.key_lohi[((size_t)u * (c.capacity / g) + grp) * d + ch] = pack_lohi(lob, hib);
       atomic_max_pos(&c.val_smax[2 * u + 1], hi > lo ? (hi - lo) / (float)((1 << bits) - 1) : 0.0f);
       for (int rr = 0; rr < g; ++rr)

@@ -69,6 +69,85 @@ def test_pack_multi_unit_each_head_exact(tkv):
                 assert q.to_bytes(u, "values") == O.quantize_values(values[u], bits, 64).to_bytes()
 
 
+def _boundary_groups(rng, ngroups, glen, bits):
+    """Groups whose members sit on and next to the codec's rounding boundaries
+    lo + (k - 1/2) (hi - lo) / (2^b - 1): the fp16 values nearest each boundary
+    and 1-2 ulps either side, plus lo and hi; spans include mixed signs,
+    subnormals, +-0 and wide magnitude ranges."""
+    out = np.zeros((ngroups, glen), np.float16)
+    for i in range(ngroups):
+        kind = i % 5
+        if kind == 0:
+            lo, hi = sorted(rng.normal(size=2) * 3)
+        elif kind == 1:
+            lo, hi = sorted(rng.normal(size=2) * 1e-5)  # subnormal fp16
+        elif kind == 2:
+            lo, hi = -abs(rng.normal()) * 1e4, abs(rng.normal()) * 1e-3
+        elif kind == 3:
+            lo, hi = 0.0, abs(rng.normal()) + 0.1
+        else:
+            lo, hi = -abs(rng.normal()) - 0.1, -0.0
+        lo16, hi16 = np.float16(lo), np.float16(hi)
+        if lo16 == hi16:
+            hi16 = np.nextafter(hi16, np.float16(np.inf))
+        cand = [lo16, hi16]
+        nl = (1 << bits) - 1
+        for k in range(1, nl + 1):
+            b = np.float16(float(lo16) + (k - 0.5) * (float(hi16) - float(lo16)) / nl)
+            x = b
+            for _ in range(3):
+                cand.append(x)
+                x = np.nextafter(x, np.float16(np.inf))
+            x = b
+            for _ in range(2):
+                x = np.nextafter(x, np.float16(-np.inf))
+                cand.append(x)
+        cand = np.clip(np.array(cand, np.float16), lo16, hi16)
+        row = rng.choice(cand, size=glen)
+        row[rng.integers(glen)], row[rng.integers(glen)] = lo16, hi16
+        if lo16 == 0:  # one zero sign per group (with both, numpy's min picks by reduction order)
+            row[row == 0] = lo16
+        out[i] = row
+    return out
+
+
+@pytest.mark.parametrize("bits", [1, 2])
+def test_pack_negative_zero_minimum(tkv, bits):
+    # a group whose minimum is -0.0 stores the zero-point as -0.0 (0x8000), as
+    # the reference's float64 min does; prefill and append agree
+    g, d, n = 16, 32, 64
+    rng = np.random.default_rng(9)
+    keys = np.abs(cases.f16(rng.normal(size=(n, d))))
+    values = np.abs(cases.f16(rng.normal(size=(n, d))))
+    keys[::5, ::3] = np.float16(-0.0)
+    values[::3, ::5] = np.float16(-0.0)
+    q = tkv.quantize_layer_kv(keys[None], values[None], bits, g)
+    assert q.to_bytes(0, "keys") == O.quantize_keys(keys, bits, g).to_bytes()
+    assert q.to_bytes(0, "values") == O.quantize_values(values, bits, g).to_bytes()
+    qa = tkv.QuantizedLayerKV.from_kv(keys[None, :20], values[None, :20], bits, g, capacity=n)
+    for t in range(20, n):
+        qa.append_token(keys[None, t], values[None, t])
+    assert qa.to_bytes(0, "keys") == O.quantize_keys(keys, bits, g).to_bytes()
+    assert qa.to_bytes(0, "values") == O.quantize_values(values, bits, g).to_bytes()
+
+
+@pytest.mark.parametrize("bits", [1, 2])
+@pytest.mark.parametrize("g", [16, 64])
+def test_pack_rounding_boundaries_exact(tkv, bits, g):
+    # the pack encodes by per-group fp16 thresholds; every value on or next to
+    # a rounding boundary must still get the reference's float64 code
+    rng = np.random.default_rng(40 + bits + g)
+    d, n = 128, 4 * 128 + g + 5  # complete tiles, a partial key tile, a residual
+    kg = _boundary_groups(rng, (n // g) * d, g, bits)  # [(group, ch)][token in group]
+    keys = np.zeros((n, d), np.float16)
+    keys[: (n // g) * g] = kg.reshape(n // g, d, g).transpose(0, 2, 1).reshape(-1, d)
+    keys[(n // g) * g:] = cases.f16(rng.normal(size=(n - (n // g) * g, d)))
+    values = _boundary_groups(rng, n * (d // g), g, bits).reshape(n, d)
+    q = tkv.quantize_layer_kv(keys[None], values[None], bits, g)
+    assert q.to_bytes(0, "keys") == O.quantize_keys(keys, bits, g).to_bytes()
+    assert q.to_bytes(0, "values") == O.quantize_values(values, bits, g).to_bytes()
+
+
 @pytest.mark.parametrize("bits", [1, 2])
 def test_append_matches_batch_quantization(tkv, bits):
     # quantizer.py:445-451 + test_quantizer.py:204-222: incremental == batch
