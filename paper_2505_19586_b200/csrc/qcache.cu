@@ -32,16 +32,6 @@ __device__ __forceinline__ void block_max_pos(float v, float *sm, float *gaddr) 
   if (threadIdx.x == 0 && *sm > 0.0f) atomic_max_pos(gaddr, *sm);
 }
 
-// The reference code of x (quantizer.py:66-117) in float64, without encode_code's fp32 fast path.
-__device__ __noinline__ int ref_code(float xf, float lof, float hif, int bits) {
-  if (bits == 1) return 2.0 * (double)xf >= __dadd_rn((double)hif, (double)lof) ? 1 : 0;
-  const double sd = __ddiv_rn(__dsub_rn((double)hif, (double)lof), 3.0);
-  const double vd = __ddiv_rn(__dsub_rn((double)xf, (double)lof), sd);
-  double r = floor(__dadd_rn(fabs(vd), 0.5));
-  if (vd < 0) r = -r;
-  return min(max((int)r, 0), 3);
-}
-
 // Group min/max with fp16 min/max, which order -0 below +0: a zero minimum is
 // stored as -0 when the group holds a -0 (the reference's float64 min keeps
 // the sign of the zero it meets; with both signs present its pick follows
@@ -59,19 +49,34 @@ __device__ __forceinline__ int h_ord(uint16_t h) { return (h & 0x8000u) ? -(int)
 __device__ __forceinline__ uint16_t h_unord(int o) { return o < 0 ? (uint16_t)(0x8000u | (uint32_t)(-o)) : (uint16_t)o; }
 
 // T_k for one group (lo <= hi as fp16 bits), k = 1 .. 2^b - 1.
-__device__ uint16_t code_threshold(uint16_t lob, uint16_t hib, int bits, int k) {
-  const float lof = h2f(lob), hif = h2f(hib);
-  if (!(hif > lof)) return 0x7fffu;  // degenerate: code 0 everywhere
-  const float est = fminf(fmaxf(lof + ((float)k - 0.5f) * ((hif - lof) / (float)((1 << bits) - 1)), lof), hif);
-  const int olo = h_ord(lob), ohi = h_ord(hib);
-  int o = min(max(h_ord(__half_as_ushort(__float2half_rn(est))), olo), ohi);
-  if (ref_code(h2f(h_unord(o)), lof, hif, bits) >= k) {
-    while (o > olo && ref_code(h2f(h_unord(o - 1)), lof, hif, bits) >= k) --o;
-  } else {
-    do ++o;
-    while (o < ohi && ref_code(h2f(h_unord(o)), lof, hif, bits) < k);
-  }
-  return h_unord(o);
+//   b = 1: code(x) = [2x >= hi + lo] (float64, exact: fp16 sums are exact there), so T_1 is the
+//          fp16 round-up of the exact midpoint (hi + lo) / 2.
+//   b = 2: code(x) >= k  <=>  (x - lo) / sd >= k - 1/2 up to float64 rounding, sd = (hi - lo) / 3
+//          rounded as the reference does.  With m = lo + (k - 1/2) sd, T_k is the fp16 round-up c of
+//          m, unless c or its fp16 predecessor p lies within 1e-12 (relative) of m -- an exact or
+//          near tie, common because group bounds share the fp16 grid -- where the reference's
+//          float64 code of that one candidate decides between it and its neighbour.
+__device__ __forceinline__ uint16_t ceil_f16(double m) {  // the smallest fp16 >= m
+  const uint16_t c = __half_as_ushort(__double2half(m));
+  return h2d(c) < m ? h_unord(h_ord(c) + 1) : c;
+}
+
+__device__ __forceinline__ uint16_t code_threshold(uint16_t lob, uint16_t hib, int bits, int k) {
+  const double lo = h2d(lob), hi = h2d(hib);
+  if (!(hi > lo)) return 0x7fffu;  // degenerate: code 0 everywhere
+  if (bits == 1) return ceil_f16(__dmul_rn(__dadd_rn(hi, lo), 0.5));
+  const double sd = __ddiv_rn(__dsub_rn(hi, lo), 3.0);
+  const double m = __fma_rn((double)k - 0.5, sd, lo);
+  const uint16_t c = ceil_f16(m);
+  const int oc = h_ord(c);
+  const uint16_t p = h_unord(oc - 1);
+  const double band = 1e-12 * (fabs(lo) + fabs(m) + sd);
+  const bool p_near = m - h2d(p) <= band, c_near = h2d(c) - m <= band;
+  if (!p_near && !c_near) return c;
+  // quantizer.py:99-107 on one candidate: round_half_away((x - lo) / sd) >= k
+  const uint16_t cand = p_near ? p : c, alt = p_near ? c : h_unord(oc + 1);
+  const double vd = __ddiv_rn(__dsub_rn(h2d(cand), lo), sd);
+  return floor(__dadd_rn(fabs(vd), 0.5)) >= (double)k ? cand : alt;
 }
 
 __device__ __forceinline__ uint32_t hge2_mask(uint32_t x, uint32_t t) {
@@ -88,6 +93,23 @@ __device__ __forceinline__ uint32_t code_bits2(uint32_t x, const uint32_t *t, in
   } else {
     const uint32_t m1 = hge2_mask(x, t[0]), m2 = hge2_mask(x, t[1]), m3 = hge2_mask(x, t[2]);
     return ((m1 ^ m2 ^ m3) & (0x00010001u << sh)) | (m2 & (0x00020002u << sh));
+  }
+}
+
+// Stage rows x (8*vpr) fp16 from global (dense) into SMEM rows of stride RS, 16 bytes per thread per step.
+__device__ __forceinline__ void tile_load(uint16_t *tile, int RS, const uint16_t *src, int rows, int vpr) {
+  const int step_r = blockDim.x / vpr, step_c = blockDim.x % vpr;
+  int r = threadIdx.x / vpr, col = threadIdx.x % vpr;
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+#pragma unroll 4
+  for (int v = threadIdx.x; v < rows * vpr; v += blockDim.x) {
+    *reinterpret_cast<uint4 *>(tile + (size_t)r * RS + col * 8) = __ldg(s4 + v);
+    r += step_r;
+    col += step_c;
+    if (col >= vpr) {
+      col -= vpr;
+      ++r;
+    }
   }
 }
 
@@ -113,10 +135,7 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
   if (threadIdx.x == 0) bmax = 0.0f;
   const uint16_t *src = keys + ((size_t)u * n + t0) * d;
   const int vpr = d / 8;
-#pragma unroll 4
-  for (int v = threadIdx.x; v < rows * vpr; v += blockDim.x)
-    *reinterpret_cast<uint4 *>(tile + (size_t)(v / vpr) * RS + (v % vpr) * 8) =
-        __ldg(reinterpret_cast<const uint4 *>(src) + v);
+  tile_load(tile, RS, src, rows, vpr);
   // groups past `rows` (a partial last tile) get NaN thresholds: code 0
   for (int i = rows / G * NT * P2 + threadIdx.x; i < GR * NT * P2; i += blockDim.x) thr[i] = 0x7fff7fffu;
   __syncthreads();
@@ -137,8 +156,8 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
   __syncthreads();
   float smax = 0.0f;
   uint16_t *thr16 = reinterpret_cast<uint16_t *>(thr);
-  for (int it = threadIdx.x; it < groups * d; it += blockDim.x) {
-    const int ch = it % d, grp = it / d;
+  for (int it = threadIdx.x; it < NT * groups * d; it += blockDim.x) {
+    const int ch = it % d, grp = (it / d) % groups, k = it / (groups * d) + 1;
     const int e = ch & 1;
     uint16_t lb = 0, hb = 0;
 #pragma unroll
@@ -148,11 +167,12 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
       lb = sg ? hmin_bits(lb, l) : l;
       hb = sg ? hmax_bits(hb, h) : h;
     }
-    const float lf = h2f(lb), hf = h2f(hb);
-    c.key_lohi[((size_t)u * (c.capacity / G) + (t0 / G) + grp) * d + ch] = pack_lohi(lb, hb);  // zero signs: hmin_bits
-    smax = fmaxf(smax, hf > lf ? (hf - lf) / (float)NT : 0.0f);
-#pragma unroll
-    for (int k = 1; k <= NT; ++k) thr16[((size_t)grp * NT + k - 1) * d + ch] = code_threshold(lb, hb, BITS, k);
+    if (k == 1) {
+      const float lf = h2f(lb), hf = h2f(hb);
+      c.key_lohi[((size_t)u * (c.capacity / G) + (t0 / G) + grp) * d + ch] = pack_lohi(lb, hb);  // zero signs: hmin_bits
+      smax = fmaxf(smax, hf > lf ? (hf - lf) / (float)NT : 0.0f);
+    }
+    thr16[((size_t)grp * NT + k - 1) * d + ch] = code_threshold(lb, hb, BITS, k);
   }
   block_max_pos(smax, &bmax, &c.val_smax[2 * u + 1]);  // (its __syncthreads also publishes thr)
   // native words: thread (ks, lane, role pair rp) writes roles 2rp, 2rp+1 (tokens +0 / +8) of
@@ -208,10 +228,7 @@ __global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *
   if (threadIdx.x == 0) bmax = 0.0f;
   const uint16_t *src = values + ((size_t)u * n + t0) * d;
   const int vpr = d / 8;
-#pragma unroll 4
-  for (int v = threadIdx.x; v < rows * vpr; v += blockDim.x)
-    *reinterpret_cast<uint4 *>(tile + (size_t)(v / vpr) * RS + (v % vpr) * 8) =
-        __ldg(reinterpret_cast<const uint4 *>(src) + v);
+  tile_load(tile, RS, src, rows, vpr);
   __syncthreads();
   float smax = 0.0f;
   for (int p = threadIdx.x; p < PV_TOK * nb; p += blockDim.x) {

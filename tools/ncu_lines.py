@@ -1,35 +1,41 @@
-"""Per-CUDA-source-line warp-stall samples of an ncu report (needs -lineinfo):
-    python tools/ncu_lines.py report.ncu-rep [top]"""
+"""Per-source-line instruction and stall-sample totals from
+`ncu -i REP --page source --csv --print-source cuda,sass --kernel-name K`.
+    python tools/ncu_lines.py export.csv [top]"""
 import csv
-import io
-import subprocess
 import sys
+from collections import defaultdict
 
-rep = sys.argv[1]
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
-agg = {}
-cur_file = "?"
-head = None
-for r in csv.reader(io.StringIO(out)):
+rows = list(csv.reader(open(sys.argv[1])))
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+inst, samp, src = defaultdict(float), defaultdict(float), {}
+f = "?"
+hdr = None
+for r in rows:
     if not r:
         continue
     if r[0] == "File Path":
-        cur_file = r[1].split("/")[-1]
+        f = r[1].split("/")[-1]
         continue
     if r[0] == "Line No":
-        head = r
+        hdr = r
         continue
-    if head is None or not r[0].isdigit():
+    if hdr is None or len(r) < len(hdr):
         continue
     try:
-        samp = int(r[4])
-    except (ValueError, IndexError):
+        ln = int(r[0])
+    except ValueError:
         continue
-    key = (cur_file, int(r[0]))
-    a = agg.setdefault(key, [0, r[1].strip()[:100]])
-    a[0] += samp
-tot = sum(v[0] for v in agg.values()) or 1
-for (f, ln), (smp, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{100 * smp / tot:5.1f}%  {f}:{ln:<5} {src}")
+    key = (f, ln)
+    ie = hdr.index("Instructions Executed")
+    ss = hdr.index("Warp Stall Sampling (All Samples)")
+    try:
+        a, b = float(r[ie] or 0), float(r[ss] or 0)
+    except ValueError:
+        continue
+    inst[key] += a
+    samp[key] += b
+    src[key] = r[1][:70]
+ti, ts = sum(inst.values()), sum(samp.values())
+print(f"total warp instructions {ti:.4g}, stall samples {ts:.0f}")
+for k in sorted(inst, key=lambda k: -inst[k])[:top]:
+    print(f"{k[0]}:{k[1]:<5} inst {100 * inst[k] / ti:5.1f}%  stall {100 * samp[k] / max(ts, 1):5.1f}%  {src[k]}")
