@@ -18,20 +18,13 @@ namespace tkv {
 // division and no float64 per element; code(x) = sum_k [x >= T_k] is exactly
 // the reference's code for every fp16 x in the group.  A degenerate group
 // (hi == lo, code 0) gets NaN thresholds, which no compare passes.
-// Tiles are staged with 16-byte loads into padded rows (conflict-free SMEM),
-// group min/max uses fp16x2 min/max (exact), the MMA-native words are
-// assembled straight from the tile and written 8 bytes per thread
+// Persistent CTAs stage tiles with 16-byte cp.async into padded rows
+// (conflict-free SMEM), double-buffered so the next tile's copy overlaps this
+// tile's work; group min/max uses fp16x2 min/max (exact), the MMA-native words
+// are assembled straight from the tile and written 8 bytes per thread
 // (consecutive threads, consecutive words), and the largest group scale is
-// reduced per CTA and published with one atomic per CTA.
+// kept per thread and published with one atomic per warp per unit.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void block_max_pos(float v, float *sm, float *gaddr) {
-  // v >= 0: the int bits are monotone
-  const int vi = __reduce_max_sync(0xffffffffu, __float_as_int(v));
-  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int *>(sm), vi);
-  __syncthreads();
-  if (threadIdx.x == 0 && *sm > 0.0f) atomic_max_pos(gaddr, *sm);
-}
-
 // Group min/max with fp16 min/max, which order -0 below +0: a zero minimum is
 // stored as -0 when the group holds a -0 (the reference's float64 min keeps
 // the sign of the zero it meets; with both signs present its pick follows
@@ -96,14 +89,15 @@ __device__ __forceinline__ uint32_t code_bits2(uint32_t x, const uint32_t *t, in
   }
 }
 
-// Stage rows x (8*vpr) fp16 from global (dense) into SMEM rows of stride RS, 16 bytes per thread per step.
-__device__ __forceinline__ void tile_load(uint16_t *tile, int RS, const uint16_t *src, int rows, int vpr) {
+// Stage rows x (8*vpr) fp16 from global (dense) into SMEM rows of stride RS with 16-byte cp.async
+// (no registers held: the copy of the next tile overlaps this tile's work), one commit group.
+__device__ __forceinline__ void tile_load_async(uint16_t *tile, int RS, const uint16_t *src, int rows, int vpr) {
   const int step_r = blockDim.x / vpr, step_c = blockDim.x % vpr;
   int r = threadIdx.x / vpr, col = threadIdx.x % vpr;
   const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-#pragma unroll 4
   for (int v = threadIdx.x; v < rows * vpr; v += blockDim.x) {
-    *reinterpret_cast<uint4 *>(tile + (size_t)r * RS + col * 8) = __ldg(s4 + v);
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + (size_t)r * RS + col * 8);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(s4 + v) : "memory");
     r += step_r;
     col += step_c;
     if (col >= vpr) {
@@ -111,200 +105,277 @@ __device__ __forceinline__ void tile_load(uint16_t *tile, int RS, const uint16_t
       ++r;
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Publish a running per-unit scale maximum (v >= 0): warp max, one atomic per warp.
+__device__ __forceinline__ void flush_max(float v, float *gaddr) {
+  const int vi = __reduce_max_sync(0xffffffffu, __float_as_int(v));
+  if ((threadIdx.x & 31) == 0 && vi > 0) atomicMax(reinterpret_cast<int *>(gaddr), vi);
 }
 
 constexpr int PK_PAD = 16;  // key tile row padding (fp16): rows 8 banks apart for 8-byte loads
 constexpr int PK_SEG = 4;   // row segments per key group in the min/max
 
-// Pack keys: one CTA per (key tile of Tk = 16*8/b tokens, unit); groups are G tokens x 1 channel.
-template <int BITS, int G>
+// Pack keys: persistent CTAs over (unit, key tile of Tk = 16*8/b tokens) items, double-buffered;
+// groups are G tokens x 1 channel.  D = head_dim when specialised, 0 = runtime c.d.
+template <int BITS, int G, int D>
 __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__restrict__ keys, int64_t n,
-                                                         int64_t n_complete) {
+                                                         int64_t n_complete, int tiles) {
   constexpr int Tk = 16 * (8 / BITS), NT = (1 << BITS) - 1, KS = 8 / BITS, GR = Tk / G, SR = G / PK_SEG;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ float bmax;
-  const int d = c.d;
-  const int u = blockIdx.y;
-  const int64_t t0 = (int64_t)blockIdx.x * Tk;
-  if (t0 >= n_complete) return;
-  const int rows = (int)imin64(Tk, n_complete - t0);  // complete groups only
-  const int RS = d + PK_PAD, P2 = d / 2;               // row stride (fp16), channel pairs
-  uint16_t *tile = reinterpret_cast<uint16_t *>(smem);                                      // [Tk][RS]
-  uint32_t *thr = reinterpret_cast<uint32_t *>(tile + (size_t)Tk * RS);                    // [GR][NT][d/2] fp16x2
+  const int d = D ? D : c.d;
+  const int RS = d + PK_PAD, P2 = d / 2, vpr = d / 8;  // row stride (fp16), channel pairs, 16-byte vectors
+  uint16_t *tiles2 = reinterpret_cast<uint16_t *>(smem);                                    // [2][Tk][RS]
+  uint32_t *thr = reinterpret_cast<uint32_t *>(tiles2 + (size_t)2 * Tk * RS);              // [GR][NT][d/2] fp16x2
   uint2 *red = reinterpret_cast<uint2 *>(thr + (size_t)GR * NT * P2);                      // [GR][SEG][d/2]
-  if (threadIdx.x == 0) bmax = 0.0f;
-  const uint16_t *src = keys + ((size_t)u * n + t0) * d;
-  const int vpr = d / 8;
-  tile_load(tile, RS, src, rows, vpr);
-  // groups past `rows` (a partial last tile) get NaN thresholds: code 0
-  for (int i = rows / G * NT * P2 + threadIdx.x; i < GR * NT * P2; i += blockDim.x) thr[i] = 0x7fff7fffu;
-  __syncthreads();
-  const int groups = rows / G;
-  for (int it = threadIdx.x; it < groups * PK_SEG * P2; it += blockDim.x) {
-    const int p = it % P2, r0 = (it / P2) * SR;  // (grp, seg) rows are contiguous
-    const uint32_t *col = reinterpret_cast<const uint32_t *>(tile) + (size_t)r0 * (RS / 2) + p;
-    uint32_t w = col[0];
-    __half2 lo = *reinterpret_cast<__half2 *>(&w), hi = lo;
-#pragma unroll
-    for (int r = 1; r < SR; ++r) {
-      w = col[r * (RS / 2)];
-      lo = __hmin2(lo, *reinterpret_cast<__half2 *>(&w));
-      hi = __hmax2(hi, *reinterpret_cast<__half2 *>(&w));
-    }
-    red[it] = make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
-  }
-  __syncthreads();
-  float smax = 0.0f;
   uint16_t *thr16 = reinterpret_cast<uint16_t *>(thr);
-  for (int it = threadIdx.x; it < NT * groups * d; it += blockDim.x) {
-    const int ch = it % d, grp = (it / d) % groups, k = it / (groups * d) + 1;
-    const int e = ch & 1;
-    uint16_t lb = 0, hb = 0;
-#pragma unroll
-    for (int sg = 0; sg < PK_SEG; ++sg) {
-      const uint2 lh = red[((size_t)grp * PK_SEG + sg) * P2 + (ch >> 1)];
-      const uint16_t l = (uint16_t)(e ? lh.x >> 16 : lh.x), h = (uint16_t)(e ? lh.y >> 16 : lh.y);
-      lb = sg ? hmin_bits(lb, l) : l;
-      hb = sg ? hmax_bits(hb, h) : h;
-    }
-    if (k == 1) {
-      const float lf = h2f(lb), hf = h2f(hb);
-      c.key_lohi[((size_t)u * (c.capacity / G) + (t0 / G) + grp) * d + ch] = pack_lohi(lb, hb);  // zero signs: hmin_bits
-      smax = fmaxf(smax, hf > lf ? (hf - lf) / (float)NT : 0.0f);
-    }
-    thr16[((size_t)grp * NT + k - 1) * d + ch] = code_threshold(lb, hb, BITS, k);
-  }
-  block_max_pos(smax, &bmax, &c.val_smax[2 * u + 1]);  // (its __syncthreads also publishes thr)
-  // native words: thread (ks, lane, role pair rp) writes roles 2rp, 2rp+1 (tokens +0 / +8) of
-  // channels ch0 .. ch0+3; token 16k + g8 + 8r lies in group 16k / G
-  uint2 *dst = reinterpret_cast<uint2 *>(c.key_codes + ((size_t)u * (c.capacity / Tk) + blockIdx.x) * (d / 32) * 128);
-  for (int q = threadIdx.x; q < d * 2; q += blockDim.x) {
-    const int rp = q & 1, lane = (q >> 1) & 31, ks = q >> 6;
-    const int g8 = lane >> 2, tq = lane & 3;
-    const int ch0 = 32 * ks + 16 * rp + 4 * tq;
-    uint32_t a0[2] = {0u, 0u}, a1[2] = {0u, 0u};  // channels (0,1) and (2,3): code of slot k at bit k*b (+16)
-#pragma unroll
-    for (int k = 0; k < KS; ++k) {
-      const uint2 *tk = reinterpret_cast<const uint2 *>(thr + (size_t)((16 * k) / G) * NT * P2 + ch0 / 2);
-      uint32_t tx[NT], ty[NT];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const uint2 tt = tk[j * (P2 / 2)];
-        tx[j] = tt.x;
-        ty[j] = tt.y;
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint2 x = *reinterpret_cast<const uint2 *>(tile + (size_t)(16 * k + g8 + 8 * r) * RS + ch0);
-        a0[r] |= code_bits2<BITS>(x.x, tx, k * BITS);
-        a1[r] |= code_bits2<BITS>(x.y, ty, k * BITS);
-      }
-    }
-    dst[(ks * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(a0[0], a1[0], 0x6420), __byte_perm(a0[1], a1[1], 0x6420));
-  }
-}
-
-constexpr int PV_TOK = 128;  // tokens per value CTA (4 value tiles)
-constexpr int PV_PAD = 8;    // value tile row padding (fp16): conflict-free 16-byte row loads and 2-byte gathers
-
-// Pack values: one CTA per 128 tokens of one unit; groups are 1 token x G channels (a ragged last block
-// allowed).  Thread (token, block) takes the group's min/max and thresholds; thread (tile, set, lane, role
-// pair) then encodes and assembles its two words straight from the tile.
-template <int BITS, int G>
-__global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *__restrict__ values, int64_t n) {
-  constexpr int NT = (1 << BITS) - 1, KS = 8 / BITS, PER = 16 * KS;
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ float bmax;
-  const int d = c.d;
-  const int nb = (d + G - 1) / G;
-  const int TS = (nb * NT) | 1;  // threshold words per token (odd: 4 tokens on distinct banks)
-  const int u = blockIdx.y;
-  const int64_t t0 = (int64_t)blockIdx.x * PV_TOK;
-  if (t0 >= n) return;
-  const int rows = (int)imin64(PV_TOK, n - t0);
-  const int RS = d + PV_PAD;
-  uint16_t *tile = reinterpret_cast<uint16_t *>(smem);                          // [PV_TOK][RS]
-  uint32_t *thr = reinterpret_cast<uint32_t *>(tile + (size_t)PV_TOK * RS);     // [PV_TOK][TS] fp16x2 (broadcast)
-  if (threadIdx.x == 0) bmax = 0.0f;
-  const uint16_t *src = values + ((size_t)u * n + t0) * d;
-  const int vpr = d / 8;
-  tile_load(tile, RS, src, rows, vpr);
-  __syncthreads();
+  const int items = tiles * c.units;
+  auto issue = [&](int w, int buf) {
+    const int u = w / tiles, ti = w % tiles;
+    const int64_t t0 = (int64_t)ti * Tk;
+    tile_load_async(tiles2 + (size_t)buf * Tk * RS, RS, keys + ((size_t)u * n + t0) * d,
+                    (int)imin64(Tk, n_complete - t0), vpr);
+  };
+  int w = blockIdx.x;
+  if (w >= items) return;
+  issue(w, 0);
+  int buf = 0, cur_u = w / tiles;
   float smax = 0.0f;
-  for (int p = threadIdx.x; p < PV_TOK * nb; p += blockDim.x) {
-    const int t = p % PV_TOK, b = p / PV_TOK;
-    uint32_t *tt = thr + (size_t)t * TS + b * NT;
-    if (t >= rows) {
-#pragma unroll
-      for (int k = 0; k < NT; ++k) tt[k] = 0x7fff7fffu;  // code 0
-      continue;
+  for (; w < items; w += gridDim.x, buf ^= 1) {
+    if (w + (int)gridDim.x < items) issue(w + gridDim.x, buf ^ 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    cp_async_wait_prev();
+    __syncthreads();
+    const int u = w / tiles, ti = w % tiles;
+    const int64_t t0 = (int64_t)ti * Tk;
+    const int groups = (int)imin64(Tk, n_complete - t0) / G;  // complete groups only
+    if (u != cur_u) {
+      flush_max(smax, &c.val_smax[2 * cur_u + 1]);
+      cur_u = u;
+      smax = 0.0f;
     }
-    const int c0 = b * G, c1 = min(d, c0 + G);  // a multiple of 16 channels (d % 32 == 0, G % 16 == 0)
-    const uint4 *row = reinterpret_cast<const uint4 *>(tile + (size_t)t * RS + c0);
-    __half2 lo, hi;
-    for (int v = 0; v < (c1 - c0) / 8; ++v) {
-      const uint4 x = row[v];
-      const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+    const uint16_t *tile = tiles2 + (size_t)buf * Tk * RS;
+    for (int it = threadIdx.x; it < groups * PK_SEG * P2; it += blockDim.x) {
+      const int p = it % P2, r0 = (it / P2) * SR;  // (grp, seg) rows are contiguous
+      const uint32_t *col = reinterpret_cast<const uint32_t *>(tile) + (size_t)r0 * (RS / 2) + p;
+      uint32_t x = col[0];
+      __half2 lo = *reinterpret_cast<__half2 *>(&x), hi = lo;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const __half2 h = *reinterpret_cast<const __half2 *>(&xs[j]);
-        lo = (v | j) ? __hmin2(lo, h) : h;
-        hi = (v | j) ? __hmax2(hi, h) : h;
+      for (int r = 1; r < SR; ++r) {
+        x = col[r * (RS / 2)];
+        lo = __hmin2(lo, *reinterpret_cast<__half2 *>(&x));
+        hi = __hmax2(hi, *reinterpret_cast<__half2 *>(&x));
       }
+      red[it] = make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
     }
-    const __half l = __hmin(__low2half(lo), __high2half(lo)), h = __hmax(__low2half(hi), __high2half(hi));
-    const uint16_t lb = __half_as_ushort(l), hb = __half_as_ushort(h);  // zero signs: see hmin_bits
-    c.val_lohi[((size_t)u * c.capacity + t0 + t) * nb + b] = pack_lohi(lb, hb);
-    smax = fmaxf(smax, group_scale_f(__half2float(l), __half2float(h), BITS));
+    __syncthreads();
+    // one thread per (threshold k, group, channel); groups past a partial tile get NaN (code 0)
+    for (int it = threadIdx.x; it < NT * GR * d; it += blockDim.x) {
+      const int ch = it % d, grp = (it / d) % GR, k = it / (GR * d) + 1;
+      uint16_t tk = 0x7fffu;
+      if (grp < groups) {
+        const int e = ch & 1;
+        uint16_t lb = 0, hb = 0;
 #pragma unroll
-    for (int k = 1; k <= NT; ++k) {
-      const uint32_t tk = code_threshold(lb, hb, BITS, k);
-      tt[k - 1] = tk | (tk << 16);
+        for (int sg = 0; sg < PK_SEG; ++sg) {
+          const uint2 lh = red[((size_t)grp * PK_SEG + sg) * P2 + (ch >> 1)];
+          const uint16_t l = (uint16_t)(e ? lh.x >> 16 : lh.x), h = (uint16_t)(e ? lh.y >> 16 : lh.y);
+          lb = sg ? hmin_bits(lb, l) : l;
+          hb = sg ? hmax_bits(hb, h) : h;
+        }
+        if (k == 1) {
+          const float lf = h2f(lb), hf = h2f(hb);
+          c.key_lohi[((size_t)u * (c.capacity / G) + (t0 / G) + grp) * d + ch] = pack_lohi(lb, hb);  // zero signs: hmin_bits
+          smax = fmaxf(smax, hf > lf ? (hf - lf) / (float)NT : 0.0f);
+        }
+        tk = code_threshold(lb, hb, BITS, k);
+      }
+      thr16[((size_t)grp * NT + k - 1) * d + ch] = tk;
     }
-  }
-  block_max_pos(smax, &bmax, &c.val_smax[2 * u]);  // (its __syncthreads also publishes thr)
-  const int sets = val_sets(d, BITS);
-  const int ntiles = (rows + 31) / 32;
-  uint2 *dst = reinterpret_cast<uint2 *>(c.val_codes + ((size_t)u * (c.capacity / 32) + t0 / 32) * sets * 128);
-  // thread (tile vt, set, lane, role pair rp) writes roles 2rp, 2rp+1 (channels +0 / +8): byte i holds token
-  // 4tq + i + 16rp, bits k*b channel set*PER + 16k + g8 (+8); both channels of a pair lie in one group
-  for (int q = threadIdx.x; q < ntiles * sets * 64; q += blockDim.x) {
-    const int rp = q & 1, lane = (q >> 1) & 31, set = (q >> 6) % sets, vt = q / (sets * 64);
-    const int g8 = lane >> 2, tq = lane & 3;
-    const int tb = vt * 32 + 4 * tq + 16 * rp;
-    uint32_t acc[4] = {0u, 0u, 0u, 0u};  // token i: channel +0 code at bit k*b, channel +8 at 16 + k*b
+    __syncthreads();
+    // native words: thread (ks, lane, role pair rp) writes roles 2rp, 2rp+1 (tokens +0 / +8)
+    // of channels ch0 .. ch0+3; token 16k + g8 + 8r lies in group 16k / G
+    uint2 *dst = reinterpret_cast<uint2 *>(c.key_codes + ((size_t)u * (c.capacity / Tk) + ti) * (d / 32) * 128);
+    for (int q = threadIdx.x; q < d * 2; q += blockDim.x) {
+      const int rp = q & 1, lane = (q >> 1) & 31, ks = q >> 6;
+      const int g8 = lane >> 2, tq = lane & 3;
+      const int ch0 = 32 * ks + 16 * rp + 4 * tq;
+      uint32_t a0[2] = {0u, 0u}, a1[2] = {0u, 0u};  // channels (0,1) and (2,3): slot k's code at bit k*b (+16)
 #pragma unroll
-    for (int k = 0; k < KS; ++k) {
-      const int ch = set * PER + 16 * k + g8;
-      if (ch < d) {
+      for (int k = 0; k < KS; ++k) {
+        const uint2 *tk = reinterpret_cast<const uint2 *>(thr + (size_t)((16 * k) / G) * NT * P2 + ch0 / 2);
+        uint32_t tx[NT], ty[NT];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint16_t *xr = tile + (size_t)(tb + i) * RS + ch;
-          const uint32_t x = (uint32_t)xr[0] | ((uint32_t)xr[8] << 16);
-          acc[i] |= code_bits2<BITS>(x, thr + (size_t)(tb + i) * TS + (ch / G) * NT, k * BITS);
+        for (int j = 0; j < NT; ++j) {
+          const uint2 tt = tk[j * (P2 / 2)];
+          tx[j] = tt.x;
+          ty[j] = tt.y;
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const uint2 x = *reinterpret_cast<const uint2 *>(tile + (size_t)(16 * k + g8 + 8 * r) * RS + ch0);
+          a0[r] |= code_bits2<BITS>(x.x, tx, k * BITS);
+          a1[r] |= code_bits2<BITS>(x.y, ty, k * BITS);
         }
       }
+      dst[(ks * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(a0[0], a1[0], 0x6420), __byte_perm(a0[1], a1[1], 0x6420));
     }
-    const uint32_t p01 = __byte_perm(acc[0], acc[1], 0x6420), p23 = __byte_perm(acc[2], acc[3], 0x6420);
-    dst[((vt * sets + set) * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(p01, p23, 0x6420), __byte_perm(p01, p23, 0x7531));
+    __syncthreads();  // the tile, red and thr are reused
   }
+  flush_max(smax, &c.val_smax[2 * cur_u + 1]);
 }
 
-template <int BITS, int G>
+constexpr int PV_TOK = 128;  // tokens per value item (4 value tiles)
+constexpr int PV_PAD = 8;    // value tile row padding (fp16): conflict-free 16-byte row loads and 2-byte gathers
+
+// Pack values: persistent CTAs over (unit, 128-token) items, double-buffered; groups are 1 token x G
+// channels (a ragged last block allowed).  Thread (token, block) takes the group's min/max and thresholds;
+// thread (tile, set, lane, role pair) then encodes and assembles its two words straight from the tile.
+template <int BITS, int G, int D>
+__global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *__restrict__ values, int64_t n,
+                                                           int chunks) {
+  constexpr int NT = (1 << BITS) - 1, KS = 8 / BITS, PER = 16 * KS;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int d = D ? D : c.d;
+  const int nb = (d + G - 1) / G;
+  const int TS = (nb * NT) | 1;  // threshold words per token (odd: 4 tokens on distinct banks)
+  const int RS = d + PV_PAD, vpr = d / 8;
+  const int sets = val_sets(d, BITS);
+  uint16_t *tiles2 = reinterpret_cast<uint16_t *>(smem);                         // [2][PV_TOK][RS]
+  uint32_t *thr = reinterpret_cast<uint32_t *>(tiles2 + (size_t)2 * PV_TOK * RS);  // [PV_TOK][TS] fp16x2 (broadcast)
+  const int items = chunks * c.units;
+  auto issue = [&](int w, int buf) {
+    const int u = w / chunks;
+    const int64_t t0 = (int64_t)(w % chunks) * PV_TOK;
+    tile_load_async(tiles2 + (size_t)buf * PV_TOK * RS, RS, values + ((size_t)u * n + t0) * d,
+                    (int)imin64(PV_TOK, n - t0), vpr);
+  };
+  int w = blockIdx.x;
+  if (w >= items) return;
+  issue(w, 0);
+  int buf = 0, cur_u = w / chunks;
+  float smax = 0.0f;
+  for (; w < items; w += gridDim.x, buf ^= 1) {
+    if (w + (int)gridDim.x < items) issue(w + gridDim.x, buf ^ 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    cp_async_wait_prev();
+    __syncthreads();
+    const int u = w / chunks;
+    const int64_t t0 = (int64_t)(w % chunks) * PV_TOK;
+    const int rows = (int)imin64(PV_TOK, n - t0);
+    if (u != cur_u) {
+      flush_max(smax, &c.val_smax[2 * cur_u]);
+      cur_u = u;
+      smax = 0.0f;
+    }
+    const uint16_t *tile = tiles2 + (size_t)buf * PV_TOK * RS;
+    for (int p = threadIdx.x; p < PV_TOK * nb; p += blockDim.x) {
+      const int t = p % PV_TOK, b = p / PV_TOK;
+      uint32_t *tt = thr + (size_t)t * TS + b * NT;
+      if (t >= rows) {
+#pragma unroll
+        for (int k = 0; k < NT; ++k) tt[k] = 0x7fff7fffu;  // code 0
+        continue;
+      }
+      const int c0 = b * G, c1 = min(d, c0 + G);  // a multiple of 16 channels (d % 32 == 0, G % 16 == 0)
+      const uint4 *row = reinterpret_cast<const uint4 *>(tile + (size_t)t * RS + c0);
+      __half2 lo, hi;
+#pragma unroll
+      for (int v = 0; v < G / 8; ++v) {
+        if (v < (c1 - c0) / 8) {
+          const uint4 x = row[v];
+          const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const __half2 h = *reinterpret_cast<const __half2 *>(&xs[j]);
+            lo = (v | j) ? __hmin2(lo, h) : h;
+            hi = (v | j) ? __hmax2(hi, h) : h;
+          }
+        }
+      }
+      const __half l = __hmin(__low2half(lo), __high2half(lo)), h = __hmax(__low2half(hi), __high2half(hi));
+      const uint16_t lb = __half_as_ushort(l), hb = __half_as_ushort(h);  // zero signs: see hmin_bits
+      c.val_lohi[((size_t)u * c.capacity + t0 + t) * nb + b] = pack_lohi(lb, hb);
+      smax = fmaxf(smax, group_scale_f(__half2float(l), __half2float(h), BITS));
+#pragma unroll
+      for (int k = 1; k <= NT; ++k) {
+        const uint32_t tk = code_threshold(lb, hb, BITS, k);
+        tt[k - 1] = tk | (tk << 16);
+      }
+    }
+    __syncthreads();
+    const int ntiles = (rows + 31) / 32;
+    uint2 *dst = reinterpret_cast<uint2 *>(c.val_codes + ((size_t)u * (c.capacity / 32) + t0 / 32) * sets * 128);
+    // thread (tile vt, set, lane, role pair rp) writes roles 2rp, 2rp+1 (channels +0 / +8): byte i holds
+    // token 4tq + i + 16rp, bits k*b channel set*PER + 16k + g8 (+8); both channels of a pair share a group
+    for (int q = threadIdx.x; q < ntiles * sets * 64; q += blockDim.x) {
+      const int rp = q & 1, lane = (q >> 1) & 31, set = (q >> 6) % sets, vt = q / (sets * 64);
+      const int g8 = lane >> 2, tq = lane & 3;
+      const int tb = vt * 32 + 4 * tq + 16 * rp;
+      uint32_t acc[4] = {0u, 0u, 0u, 0u};  // token i: channel +0 code at bit k*b, channel +8 at 16 + k*b
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        const int ch = set * PER + 16 * k + g8;
+        if (ch < d) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint16_t *xr = tile + (size_t)(tb + i) * RS + ch;
+            const uint32_t x = (uint32_t)xr[0] | ((uint32_t)xr[8] << 16);
+            acc[i] |= code_bits2<BITS>(x, thr + (size_t)(tb + i) * TS + (ch / G) * NT, k * BITS);
+          }
+        }
+      }
+      const uint32_t p01 = __byte_perm(acc[0], acc[1], 0x6420), p23 = __byte_perm(acc[2], acc[3], 0x6420);
+      dst[((vt * sets + set) * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(p01, p23, 0x6420), __byte_perm(p01, p23, 0x7531));
+    }
+    __syncthreads();  // the tile and thr are reused
+  }
+  flush_max(smax, &c.val_smax[2 * cur_u]);
+}
+
+static int pack_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <typename K>
+static unsigned persistent_grid(K kernel, size_t sm, int64_t items) {
+  int per_sm = 0;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+  return (unsigned)std::min<int64_t>(items, (int64_t)per_sm * pack_sms());
+}
+
+template <int BITS, int G, int D>
 static void launch_pack(const QC &c, const uint16_t *keys, const uint16_t *values, int64_t n, int64_t n_complete,
                         cudaStream_t st) {
   constexpr int Tk = 16 * (8 / BITS), NT = (1 << BITS) - 1, GR = Tk / G;
   if (n_complete > 0) {
-    const size_t sm = (size_t)Tk * (c.d + PK_PAD) * 2 + (size_t)GR * NT * c.d * 2 + (size_t)GR * PK_SEG * (c.d / 2) * 8;
-    cudaFuncSetAttribute(pack_keys_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((unsigned)((n_complete + Tk - 1) / Tk), c.units);
-    pack_keys_kernel<BITS, G><<<grid, 256, sm, st>>>(c, keys, n, n_complete);
+    const int tiles = (int)((n_complete + Tk - 1) / Tk);
+    const size_t sm = (size_t)2 * Tk * (c.d + PK_PAD) * 2 + (size_t)GR * NT * c.d * 2 + (size_t)GR * PK_SEG * (c.d / 2) * 8;
+    const unsigned grid = persistent_grid(pack_keys_kernel<BITS, G, D>, sm, (int64_t)tiles * c.units);
+    pack_keys_kernel<BITS, G, D><<<grid, 256, sm, st>>>(c, keys, n, n_complete, tiles);
   }
   const int nb = (c.d + G - 1) / G;
-  const size_t sm = (size_t)PV_TOK * (c.d + PV_PAD) * 2 + (size_t)PV_TOK * ((nb * NT) | 1) * 4;
-  cudaFuncSetAttribute(pack_values_kernel<BITS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid((unsigned)((n + PV_TOK - 1) / PV_TOK), c.units);
-  pack_values_kernel<BITS, G><<<grid, 256, sm, st>>>(c, values, n);
+  const int chunks = (int)((n + PV_TOK - 1) / PV_TOK);
+  const size_t sm = (size_t)2 * PV_TOK * (c.d + PV_PAD) * 2 + (size_t)PV_TOK * ((nb * NT) | 1) * 4;
+  const unsigned grid = persistent_grid(pack_values_kernel<BITS, G, D>, sm, (int64_t)chunks * c.units);
+  pack_values_kernel<BITS, G, D><<<grid, 256, sm, st>>>(c, values, n, chunks);
+}
+
+template <int BITS, int G>
+static void launch_pack_d(const QC &c, const uint16_t *keys, const uint16_t *values, int64_t n, int64_t n_complete,
+                          cudaStream_t st) {
+  if (c.d == 128) launch_pack<BITS, G, 128>(c, keys, values, n, n_complete, st);
+  else if (c.d == 64) launch_pack<BITS, G, 64>(c, keys, values, n, n_complete, st);
+  else launch_pack<BITS, G, 0>(c, keys, values, n, n_complete, st);
 }
 
 __global__ void copy_residual_kernel(QC c, const uint16_t *__restrict__ keys, int64_t n, int64_t n_complete) {
@@ -341,13 +412,13 @@ int pack(const QC &c, const uint16_t *keys, const uint16_t *values, int64_t n, i
   const int64_t n_complete = (n / c.g) * c.g;
   cudaMemsetAsync(c.val_smax, 0, sizeof(float) * 2 * c.units, st);
   switch (c.bits * 1000 + c.g) {
-    case 1016: launch_pack<1, 16>(c, keys, values, n, n_complete, st); break;
-    case 1032: launch_pack<1, 32>(c, keys, values, n, n_complete, st); break;
-    case 1064: launch_pack<1, 64>(c, keys, values, n, n_complete, st); break;
-    case 1128: launch_pack<1, 128>(c, keys, values, n, n_complete, st); break;
-    case 2016: launch_pack<2, 16>(c, keys, values, n, n_complete, st); break;
-    case 2032: launch_pack<2, 32>(c, keys, values, n, n_complete, st); break;
-    case 2064: launch_pack<2, 64>(c, keys, values, n, n_complete, st); break;
+    case 1016: launch_pack_d<1, 16>(c, keys, values, n, n_complete, st); break;
+    case 1032: launch_pack_d<1, 32>(c, keys, values, n, n_complete, st); break;
+    case 1064: launch_pack_d<1, 64>(c, keys, values, n, n_complete, st); break;
+    case 1128: launch_pack_d<1, 128>(c, keys, values, n, n_complete, st); break;
+    case 2016: launch_pack_d<2, 16>(c, keys, values, n, n_complete, st); break;
+    case 2032: launch_pack_d<2, 32>(c, keys, values, n, n_complete, st); break;
+    case 2064: launch_pack_d<2, 64>(c, keys, values, n, n_complete, st); break;
     default: return fail(TKV_ERR_PARAMETER, "unsupported (bits, group_size) for the CUDA pack");
   }
   if (n > n_complete) {
