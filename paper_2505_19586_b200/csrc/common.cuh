@@ -110,6 +110,30 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// ---- TMA 1-D bulk copies into shared memory, completion on an mbarrier ----
+__device__ __forceinline__ uint32_t sm_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm_addr(dst)),
+      "l"(src), "r"(bytes), "r"(sm_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @p bra.uni DONE_%=;\n"
+      " bra.uni WAIT_%=;\n DONE_%=:\n}\n" ::"r"(sm_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // ---- quantization codec, bit-exact with quantizer.py:66-117 ----
 // Codes are computed in float64 exactly as the reference (inputs are fp16,
 // so x-lo, hi-lo, hi+lo are exact in float64).

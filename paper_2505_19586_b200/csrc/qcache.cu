@@ -109,6 +109,15 @@ __device__ __forceinline__ void tile_load_async(uint16_t *tile, int RS, const ui
 }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+// (u, i) += step over items laid out unit-major with `per` items per unit
+__device__ __forceinline__ void item_advance(int &u, int &i, int step, int per) {
+  i += step;
+  while (i >= per) {
+    i -= per;
+    ++u;
+  }
+}
+
 // Publish a running per-unit scale maximum (v >= 0): warp max, one atomic per warp.
 __device__ __forceinline__ void flush_max(float v, float *gaddr) {
   const int vi = __reduce_max_sync(0xffffffffu, __float_as_int(v));
@@ -132,23 +141,24 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
   uint2 *red = reinterpret_cast<uint2 *>(thr + (size_t)GR * NT * P2);                      // [GR][SEG][d/2]
   uint16_t *thr16 = reinterpret_cast<uint16_t *>(thr);
   const int items = tiles * c.units;
-  auto issue = [&](int w, int buf) {
-    const int u = w / tiles, ti = w % tiles;
-    const int64_t t0 = (int64_t)ti * Tk;
-    tile_load_async(tiles2 + (size_t)buf * Tk * RS, RS, keys + ((size_t)u * n + t0) * d,
-                    (int)imin64(Tk, n_complete - t0), vpr);
+  if ((int)blockIdx.x >= items) return;
+  auto issue = [&](int uu, int tt, int bb) {
+    const int64_t s0 = (int64_t)tt * Tk;
+    tile_load_async(tiles2 + (size_t)bb * Tk * RS, RS, keys + ((size_t)uu * n + s0) * d, (int)imin64(Tk, n_complete - s0),
+                    vpr);
   };
-  int w = blockIdx.x;
-  if (w >= items) return;
-  issue(w, 0);
-  int buf = 0, cur_u = w / tiles;
+  int u = 0, ti = 0;
+  item_advance(u, ti, blockIdx.x, tiles);
+  issue(u, ti, 0);
+  int cur_u = u;
   float smax = 0.0f;
-  for (; w < items; w += gridDim.x, buf ^= 1) {
-    if (w + (int)gridDim.x < items) issue(w + gridDim.x, buf ^ 1);
+  for (int w = blockIdx.x, buf = 0; w < items; w += gridDim.x, buf ^= 1) {
+    int un = u, tn = ti;
+    item_advance(un, tn, gridDim.x, tiles);
+    if (w + (int)gridDim.x < items) issue(un, tn, buf ^ 1);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     cp_async_wait_prev();
     __syncthreads();
-    const int u = w / tiles, ti = w % tiles;
     const int64_t t0 = (int64_t)ti * Tk;
     const int groups = (int)imin64(Tk, n_complete - t0) / G;  // complete groups only
     if (u != cur_u) {
@@ -223,47 +233,52 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
       dst[(ks * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(a0[0], a1[0], 0x6420), __byte_perm(a0[1], a1[1], 0x6420));
     }
     __syncthreads();  // the tile, red and thr are reused
+    u = un;
+    ti = tn;
   }
   flush_max(smax, &c.val_smax[2 * cur_u + 1]);
 }
 
-constexpr int PV_TOK = 128;  // tokens per value item (4 value tiles)
-constexpr int PV_PAD = 8;    // value tile row padding (fp16): conflict-free 16-byte row loads and 2-byte gathers
+constexpr int PV_TOK = 128;           // tokens per value item (4 value tiles)
+constexpr int PV_PAD = 8;             // value tile row padding (fp16): conflict-free 16-byte row loads
+constexpr int PV_CT = PV_TOK + 16;    // code-byte row stride: 4-byte loads of 4 g8 rows on distinct banks
 
 // Pack values: persistent CTAs over (unit, 128-token) items, double-buffered; groups are 1 token x G
-// channels (a ragged last block allowed).  Thread (token, block) takes the group's min/max and thresholds;
-// thread (tile, set, lane, role pair) then encodes and assembles its two words straight from the tile.
+// channels (a ragged last block allowed).  Thread (token, block) keeps its group in registers: min/max,
+// thresholds, then codes.  Channel 16k + j of a word set (j < 16) contributes bits k*b of byte j, so the
+// thread writes 16 code bytes per block into codes[set][part][j][token] (part = the block's slice of the
+// set); a word then ORs its parts with one 4-token load each.
 template <int BITS, int G, int D>
 __global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *__restrict__ values, int64_t n,
                                                            int chunks) {
-  constexpr int NT = (1 << BITS) - 1, KS = 8 / BITS, PER = 16 * KS;
+  constexpr int NT = (1 << BITS) - 1, KS = 8 / BITS, PER = 16 * KS, PARTS = PER / G;
   extern __shared__ __align__(16) unsigned char smem[];
   const int d = D ? D : c.d;
   const int nb = (d + G - 1) / G;
-  const int TS = (nb * NT) | 1;  // threshold words per token (odd: 4 tokens on distinct banks)
   const int RS = d + PV_PAD, vpr = d / 8;
   const int sets = val_sets(d, BITS);
-  uint16_t *tiles2 = reinterpret_cast<uint16_t *>(smem);                         // [2][PV_TOK][RS]
-  uint32_t *thr = reinterpret_cast<uint32_t *>(tiles2 + (size_t)2 * PV_TOK * RS);  // [PV_TOK][TS] fp16x2 (broadcast)
+  uint16_t *tiles2 = reinterpret_cast<uint16_t *>(smem);                              // [2][PV_TOK][RS]
+  uint8_t *codes = reinterpret_cast<uint8_t *>(tiles2 + (size_t)2 * PV_TOK * RS);    // [sets][PARTS][16][PV_CT]
   const int items = chunks * c.units;
-  auto issue = [&](int w, int buf) {
-    const int u = w / chunks;
-    const int64_t t0 = (int64_t)(w % chunks) * PV_TOK;
-    tile_load_async(tiles2 + (size_t)buf * PV_TOK * RS, RS, values + ((size_t)u * n + t0) * d,
-                    (int)imin64(PV_TOK, n - t0), vpr);
+  if ((int)blockIdx.x >= items) return;
+  auto issue = [&](int uu, int cc, int bb) {
+    const int64_t s0 = (int64_t)cc * PV_TOK;
+    tile_load_async(tiles2 + (size_t)bb * PV_TOK * RS, RS, values + ((size_t)uu * n + s0) * d,
+                    (int)imin64(PV_TOK, n - s0), vpr);
   };
-  int w = blockIdx.x;
-  if (w >= items) return;
-  issue(w, 0);
-  int buf = 0, cur_u = w / chunks;
+  int u = 0, ci = 0;
+  item_advance(u, ci, blockIdx.x, chunks);
+  issue(u, ci, 0);
+  int cur_u = u;
   float smax = 0.0f;
-  for (; w < items; w += gridDim.x, buf ^= 1) {
-    if (w + (int)gridDim.x < items) issue(w + gridDim.x, buf ^ 1);
+  for (int w = blockIdx.x, buf = 0; w < items; w += gridDim.x, buf ^= 1) {
+    int un = u, cn = ci;
+    item_advance(un, cn, gridDim.x, chunks);
+    if (w + (int)gridDim.x < items) issue(un, cn, buf ^ 1);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     cp_async_wait_prev();
     __syncthreads();
-    const int u = w / chunks;
-    const int64_t t0 = (int64_t)(w % chunks) * PV_TOK;
+    const int64_t t0 = (int64_t)ci * PV_TOK;
     const int rows = (int)imin64(PV_TOK, n - t0);
     if (u != cur_u) {
       flush_max(smax, &c.val_smax[2 * cur_u]);
@@ -273,64 +288,73 @@ __global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *
     const uint16_t *tile = tiles2 + (size_t)buf * PV_TOK * RS;
     for (int p = threadIdx.x; p < PV_TOK * nb; p += blockDim.x) {
       const int t = p % PV_TOK, b = p / PV_TOK;
-      uint32_t *tt = thr + (size_t)t * TS + b * NT;
-      if (t >= rows) {
+      const int c0 = b * G, nv = (min(d, c0 + G) - c0) / 8;  // 16-byte vectors in the block (>= 2)
+      uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // acc[q]: bytes j = 2q (bits 0-7), 2q+1 (bits 16-23)
+      if (t < rows) {
+        const uint4 *row = reinterpret_cast<const uint4 *>(tile + (size_t)t * RS + c0);
+        uint32_t xs[G / 2];
+        __half2 lo, hi;
 #pragma unroll
-        for (int k = 0; k < NT; ++k) tt[k] = 0x7fff7fffu;  // code 0
-        continue;
-      }
-      const int c0 = b * G, c1 = min(d, c0 + G);  // a multiple of 16 channels (d % 32 == 0, G % 16 == 0)
-      const uint4 *row = reinterpret_cast<const uint4 *>(tile + (size_t)t * RS + c0);
-      __half2 lo, hi;
+        for (int v = 0; v < G / 8; ++v) {
+          if (v < nv) {
+            const uint4 x = row[v];
+            xs[4 * v] = x.x;
+            xs[4 * v + 1] = x.y;
+            xs[4 * v + 2] = x.z;
+            xs[4 * v + 3] = x.w;
 #pragma unroll
-      for (int v = 0; v < G / 8; ++v) {
-        if (v < (c1 - c0) / 8) {
-          const uint4 x = row[v];
-          const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const __half2 h = *reinterpret_cast<const __half2 *>(&xs[j]);
-            lo = (v | j) ? __hmin2(lo, h) : h;
-            hi = (v | j) ? __hmax2(hi, h) : h;
+            for (int j = 0; j < 4; ++j) {
+              const __half2 h = *reinterpret_cast<const __half2 *>(&xs[4 * v + j]);
+              lo = (v | j) ? __hmin2(lo, h) : h;
+              hi = (v | j) ? __hmax2(hi, h) : h;
+            }
           }
         }
-      }
-      const __half l = __hmin(__low2half(lo), __high2half(lo)), h = __hmax(__low2half(hi), __high2half(hi));
-      const uint16_t lb = __half_as_ushort(l), hb = __half_as_ushort(h);  // zero signs: see hmin_bits
-      c.val_lohi[((size_t)u * c.capacity + t0 + t) * nb + b] = pack_lohi(lb, hb);
-      smax = fmaxf(smax, group_scale_f(__half2float(l), __half2float(h), BITS));
+        const __half l = __hmin(__low2half(lo), __high2half(lo)), h = __hmax(__low2half(hi), __high2half(hi));
+        const uint16_t lb = __half_as_ushort(l), hb = __half_as_ushort(h);  // zero signs: see hmin_bits
+        c.val_lohi[((size_t)u * c.capacity + t0 + t) * nb + b] = pack_lohi(lb, hb);
+        smax = fmaxf(smax, group_scale_f(__half2float(l), __half2float(h), BITS));
+        uint32_t th[NT];
 #pragma unroll
-      for (int k = 1; k <= NT; ++k) {
-        const uint32_t tk = code_threshold(lb, hb, BITS, k);
-        tt[k - 1] = tk | (tk << 16);
+        for (int k = 1; k <= NT; ++k) {
+          const uint32_t tk = code_threshold(lb, hb, BITS, k);
+          th[k - 1] = tk | (tk << 16);
+        }
+        const int kb = (b % PARTS) * (G / 16);  // the block's first k within its set
+#pragma unroll
+        for (int m = 0; m < G / 2; ++m)  // channel pair (2m, 2m+1): j = 2m % 16, k = kb + m / 8
+          if (m < 4 * nv) acc[m % 8] |= code_bits2<BITS>(xs[m], th, (kb + m / 8) * BITS);
+      }
+      uint8_t *cb = codes + ((size_t)(c0 / PER) * PARTS + (b % PARTS)) * 16 * PV_CT + t;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        cb[(2 * q) * PV_CT] = (uint8_t)acc[q];
+        cb[(2 * q + 1) * PV_CT] = (uint8_t)(acc[q] >> 16);
       }
     }
     __syncthreads();
     const int ntiles = (rows + 31) / 32;
     uint2 *dst = reinterpret_cast<uint2 *>(c.val_codes + ((size_t)u * (c.capacity / 32) + t0 / 32) * sets * 128);
     // thread (tile vt, set, lane, role pair rp) writes roles 2rp, 2rp+1 (channels +0 / +8): byte i holds
-    // token 4tq + i + 16rp, bits k*b channel set*PER + 16k + g8 (+8); both channels of a pair share a group
+    // token 4tq + i + 16rp, bits k*b channel set*PER + 16k + g8 (+8)
     for (int q = threadIdx.x; q < ntiles * sets * 64; q += blockDim.x) {
       const int rp = q & 1, lane = (q >> 1) & 31, set = (q >> 6) % sets, vt = q / (sets * 64);
       const int g8 = lane >> 2, tq = lane & 3;
       const int tb = vt * 32 + 4 * tq + 16 * rp;
-      uint32_t acc[4] = {0u, 0u, 0u, 0u};  // token i: channel +0 code at bit k*b, channel +8 at 16 + k*b
+      uint32_t wv[2] = {0u, 0u};
 #pragma unroll
-      for (int k = 0; k < KS; ++k) {
-        const int ch = set * PER + 16 * k + g8;
-        if (ch < d) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint16_t *xr = tile + (size_t)(tb + i) * RS + ch;
-            const uint32_t x = (uint32_t)xr[0] | ((uint32_t)xr[8] << 16);
-            acc[i] |= code_bits2<BITS>(x, thr + (size_t)(tb + i) * TS + (ch / G) * NT, k * BITS);
-          }
+      for (int pt = 0; pt < PARTS; ++pt) {
+        if (set * PER + pt * G < d) {
+          const uint8_t *cb = codes + ((size_t)set * PARTS + pt) * 16 * PV_CT + tb;
+          wv[0] |= *reinterpret_cast<const uint32_t *>(cb + g8 * PV_CT);
+          wv[1] |= *reinterpret_cast<const uint32_t *>(cb + (g8 + 8) * PV_CT);
         }
       }
-      const uint32_t p01 = __byte_perm(acc[0], acc[1], 0x6420), p23 = __byte_perm(acc[2], acc[3], 0x6420);
-      dst[((vt * sets + set) * 32 + lane) * 2 + rp] = make_uint2(__byte_perm(p01, p23, 0x6420), __byte_perm(p01, p23, 0x7531));
+      dst[((vt * sets + set) * 32 + lane) * 2 + rp] = make_uint2(wv[0], wv[1]);
     }
-    __syncthreads();  // the tile and thr are reused
+    __syncthreads();  // the tile and codes are reused
+    u = un;
+    ci = cn;
   }
   flush_max(smax, &c.val_smax[2 * cur_u]);
 }
@@ -363,9 +387,8 @@ static void launch_pack(const QC &c, const uint16_t *keys, const uint16_t *value
     const unsigned grid = persistent_grid(pack_keys_kernel<BITS, G, D>, sm, (int64_t)tiles * c.units);
     pack_keys_kernel<BITS, G, D><<<grid, 256, sm, st>>>(c, keys, n, n_complete, tiles);
   }
-  const int nb = (c.d + G - 1) / G;
   const int chunks = (int)((n + PV_TOK - 1) / PV_TOK);
-  const size_t sm = (size_t)2 * PV_TOK * (c.d + PV_PAD) * 2 + (size_t)PV_TOK * ((nb * NT) | 1) * 4;
+  const size_t sm = (size_t)2 * PV_TOK * (c.d + PV_PAD) * 2 + (size_t)val_sets(c.d, BITS) * (16 * (8 / BITS) / G) * 16 * PV_CT;
   const unsigned grid = persistent_grid(pack_values_kernel<BITS, G, D>, sm, (int64_t)chunks * c.units);
   pack_values_kernel<BITS, G, D><<<grid, 256, sm, st>>>(c, values, n, chunks);
 }
