@@ -50,15 +50,22 @@ __device__ __forceinline__ uint16_t h_unord(int o) { return o < 0 ? (uint16_t)(0
 //          near tie, common because group bounds share the fp16 grid -- where the reference's
 //          float64 code of that one candidate decides between it and its neighbour.
 __device__ __forceinline__ uint16_t ceil_f16(double m) {  // the smallest fp16 >= m
-  const uint16_t c = __half_as_ushort(__double2half(m));
+  // fp32 round-to-nearest keeps every fp16 >= m above it, except when it lands exactly on an fp16 below m
+  const uint16_t c = __half_as_ushort(__float2half_ru(__double2float_rn(m)));
   return h2d(c) < m ? h_unord(h_ord(c) + 1) : c;
 }
 
-__device__ __forceinline__ uint16_t code_threshold(uint16_t lob, uint16_t hib, int bits, int k) {
+// sd = (hi - lo) / 3 as the reference rounds it (b = 2; unused at b = 1)
+template <int BITS>
+__device__ __forceinline__ double group_sd(double lo, double hi) {
+  return BITS == 2 ? __ddiv_rn(__dsub_rn(hi, lo), 3.0) : 0.0;
+}
+
+template <int BITS>
+__device__ __forceinline__ uint16_t code_threshold(uint16_t lob, uint16_t hib, double sd, int k) {
   const double lo = h2d(lob), hi = h2d(hib);
   if (!(hi > lo)) return 0x7fffu;  // degenerate: code 0 everywhere
-  if (bits == 1) return ceil_f16(__dmul_rn(__dadd_rn(hi, lo), 0.5));
-  const double sd = __ddiv_rn(__dsub_rn(hi, lo), 3.0);
+  if (BITS == 1) return ceil_f16(__dmul_rn(__dadd_rn(hi, lo), 0.5));
   const double m = __fma_rn((double)k - 0.5, sd, lo);
   const uint16_t c = ceil_f16(m);
   const int oc = h_ord(c);
@@ -139,6 +146,8 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
   uint16_t *tiles2 = reinterpret_cast<uint16_t *>(smem);                                    // [2][Tk][RS]
   uint32_t *thr = reinterpret_cast<uint32_t *>(tiles2 + (size_t)2 * Tk * RS);              // [GR][NT][d/2] fp16x2
   uint2 *red = reinterpret_cast<uint2 *>(thr + (size_t)GR * NT * P2);                      // [GR][SEG][d/2]
+  double *gsd = reinterpret_cast<double *>(red + (size_t)GR * PK_SEG * P2);                 // [GR][d]
+  uint32_t *bounds = reinterpret_cast<uint32_t *>(gsd + (size_t)GR * d);                    // [GR][d]
   uint16_t *thr16 = reinterpret_cast<uint16_t *>(thr);
   const int items = tiles * c.units;
   if ((int)blockIdx.x >= items) return;
@@ -181,28 +190,35 @@ __global__ void __launch_bounds__(256) pack_keys_kernel(QC c, const uint16_t *__
       red[it] = make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
     }
     __syncthreads();
-    // one thread per (threshold k, group, channel); groups past a partial tile get NaN (code 0)
-    for (int it = threadIdx.x; it < NT * GR * d; it += blockDim.x) {
-      const int ch = it % d, grp = (it / d) % GR, k = it / (GR * d) + 1;
-      uint16_t tk = 0x7fffu;
-      if (grp < groups) {
-        const int e = ch & 1;
-        uint16_t lb = 0, hb = 0;
+    // (group, channel): bounds, sd; then one thread per (threshold k, group, channel); groups past a partial
+    // tile get NaN thresholds (code 0)
+    for (int it = threadIdx.x; it < groups * d; it += blockDim.x) {
+      const int ch = it % d, grp = it / d;
+      const int e = ch & 1;
+      uint16_t lb = 0, hb = 0;
 #pragma unroll
-        for (int sg = 0; sg < PK_SEG; ++sg) {
-          const uint2 lh = red[((size_t)grp * PK_SEG + sg) * P2 + (ch >> 1)];
-          const uint16_t l = (uint16_t)(e ? lh.x >> 16 : lh.x), h = (uint16_t)(e ? lh.y >> 16 : lh.y);
-          lb = sg ? hmin_bits(lb, l) : l;
-          hb = sg ? hmax_bits(hb, h) : h;
-        }
-        if (k == 1) {
-          const float lf = h2f(lb), hf = h2f(hb);
-          c.key_lohi[((size_t)u * (c.capacity / G) + (t0 / G) + grp) * d + ch] = pack_lohi(lb, hb);  // zero signs: hmin_bits
-          smax = fmaxf(smax, hf > lf ? (hf - lf) / (float)NT : 0.0f);
-        }
-        tk = code_threshold(lb, hb, BITS, k);
+      for (int sg = 0; sg < PK_SEG; ++sg) {
+        const uint2 lh = red[((size_t)grp * PK_SEG + sg) * P2 + (ch >> 1)];
+        const uint16_t l = (uint16_t)(e ? lh.x >> 16 : lh.x), h = (uint16_t)(e ? lh.y >> 16 : lh.y);
+        lb = sg ? hmin_bits(lb, l) : l;
+        hb = sg ? hmax_bits(hb, h) : h;
       }
-      thr16[((size_t)grp * NT + k - 1) * d + ch] = tk;
+      const uint32_t w2 = pack_lohi(lb, hb);  // zero signs: hmin_bits
+      bounds[it] = w2;
+      if (BITS == 2) gsd[it] = group_sd<BITS>(h2d(lb), h2d(hb));
+      c.key_lohi[((size_t)u * (c.capacity / G) + (t0 / G) + grp) * d + ch] = w2;
+      const float lf = h2f(lb), hf = h2f(hb);
+      smax = fmaxf(smax, hf > lf ? (hf - lf) / (float)NT : 0.0f);
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < NT * GR * d; it += blockDim.x) {
+      const int gc = it % (GR * d), k = it / (GR * d) + 1;
+      uint16_t tk = 0x7fffu;
+      if (gc < groups * d) {
+        const uint32_t w2 = bounds[gc];
+        tk = code_threshold<BITS>((uint16_t)(w2 & 0xffffu), (uint16_t)(w2 >> 16), BITS == 2 ? gsd[gc] : 0.0, k);
+      }
+      thr16[((size_t)(gc / d) * NT + k - 1) * d + gc % d] = tk;
     }
     __syncthreads();
     // native words: thread (ks, lane, role pair rp) writes roles 2rp, 2rp+1 (tokens +0 / +8)
@@ -315,9 +331,10 @@ __global__ void __launch_bounds__(256) pack_values_kernel(QC c, const uint16_t *
         c.val_lohi[((size_t)u * c.capacity + t0 + t) * nb + b] = pack_lohi(lb, hb);
         smax = fmaxf(smax, group_scale_f(__half2float(l), __half2float(h), BITS));
         uint32_t th[NT];
+        const double sd = group_sd<BITS>(h2d(lb), h2d(hb));
 #pragma unroll
         for (int k = 1; k <= NT; ++k) {
-          const uint32_t tk = code_threshold(lb, hb, BITS, k);
+          const uint32_t tk = code_threshold<BITS>(lb, hb, sd, k);
           th[k - 1] = tk | (tk << 16);
         }
         const int kb = (b % PARTS) * (G / 16);  // the block's first k within its set
@@ -383,7 +400,8 @@ static void launch_pack(const QC &c, const uint16_t *keys, const uint16_t *value
   constexpr int Tk = 16 * (8 / BITS), NT = (1 << BITS) - 1, GR = Tk / G;
   if (n_complete > 0) {
     const int tiles = (int)((n_complete + Tk - 1) / Tk);
-    const size_t sm = (size_t)2 * Tk * (c.d + PK_PAD) * 2 + (size_t)GR * NT * c.d * 2 + (size_t)GR * PK_SEG * (c.d / 2) * 8;
+    const size_t sm = (size_t)2 * Tk * (c.d + PK_PAD) * 2 + (size_t)GR * NT * c.d * 2 + (size_t)GR * PK_SEG * (c.d / 2) * 8 +
+                      (size_t)GR * c.d * 12;
     const unsigned grid = persistent_grid(pack_keys_kernel<BITS, G, D>, sm, (int64_t)tiles * c.units);
     pack_keys_kernel<BITS, G, D><<<grid, 256, sm, st>>>(c, keys, n, n_complete, tiles);
   }
