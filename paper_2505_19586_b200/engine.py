@@ -229,6 +229,14 @@ class DecodeEngine:
         self.keys_from_hbm = config.keys_from_hbm
         self.last_channels: dict[int, torch.Tensor] = {}
         self.last_selection: dict[int, tuple] = {}
+        # host I/O inside the captured step (capture(host_io=True)): pinned staging for the step inputs and
+        # outputs, copied by the graph on its own stream, overlapped with the layers
+        self._host_io = False
+        self._io_capture = None  # capture-time state while capturing with host I/O
+        self.io = None
+        self.host_inputs = None  # (hidden, queries, new_keys, new_values) pinned, shaped like the device buffers
+        self.host_out = None     # pinned copy of `out`, written by the graph every step
+        self._inputs_read = None  # event: the graph has copied the staged inputs (staging may be rewritten)
 
     # -- prefill ---------------------------------------------------------------
     def _slice_kv(self, x):
@@ -335,17 +343,78 @@ class DecodeEngine:
                 and self.cfg.bits in (1, 2) and self.G <= 16)
         return q * (2 if pipe else 3) + s * per_s
 
+    def _io_inputs(self, main) -> None:
+        """Host I/O capture: copy the staged inputs on the io stream in two phases -- the first two layers'
+        slices (needed at once), then the rest, which lands while those two run -- each ending in an event
+        the consumers wait on."""
+        L = self.model.num_layers
+        A = min(L, 2)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        self.io.wait_event(fork)
+        evs = []
+        with torch.cuda.stream(self.io):
+            for lo, hi in ((0, A), (A, L)):
+                if lo >= hi:
+                    continue
+                for dst, src in zip((self.hidden, self.queries, self.new_keys, self.new_values), self.host_inputs):
+                    dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.io)
+                evs.append((hi, ev))
+            # an external event-record node: the host may rewrite the staging once it has fired
+            check(_lib.load().tkv_event_record(C.c_void_p(self._inputs_read.cuda_event),
+                                               C.c_void_p(self.io.cuda_stream), 1))
+        self._io_capture = {"evs": evs, "waited": set()}
+
+    def _io_wait(self, stream, layer: int) -> None:
+        """Make `stream` wait until layer `layer`'s inputs are on the device (host I/O capture only)."""
+        st = self._io_capture
+        if st is None:
+            return
+        for i, (hi, ev) in enumerate(st["evs"]):
+            if layer < hi:
+                if (id(stream), i) not in st["waited"]:
+                    stream.wait_event(ev)
+                    st["waited"].add((id(stream), i))
+                return
+
+    def _io_output(self, main, l: int) -> None:
+        """Host I/O capture: copy the outputs back on the io stream in two pieces -- every layer but the last
+        L/8 once those are done (overlapped with the rest of the step), then the tail at the end.  (One copy
+        per layer costs more than it hides: each extra dependency on a layer's kernel breaks the programmatic
+        launch overlap with the next one.)"""
+        if self._io_capture is None:
+            return
+        L = self.model.num_layers
+        tail = max(1, L // 8)
+        if l == L - 1:
+            lo = L - tail if L > tail else 0
+        elif l == L - tail - 1:
+            lo = 0
+        else:
+            return
+        done = torch.cuda.Event()
+        done.record(main)
+        self.io.wait_event(done)
+        with torch.cuda.stream(self.io):
+            self.host_out[lo:l + 1].copy_(self.out[lo:l + 1], non_blocking=True)
+
     def _run_step(self) -> None:
         main = torch.cuda.current_stream(self.device)
         L = self.model.num_layers
+        if self._io_capture is not None:
+            self._io_inputs(main)
         begin = [torch.cuda.Event() for _ in range(L)]
         for l in range(L):
+            self._io_wait(main, l)
             begin[l].record(main)
             nxt = [j for j in ((0, 1) if l == 0 else (l + 1,)) if j < L and self.labels[j] == "s"]
             if not self.cfg.overlap_stage1:
                 nxt = [l] if self.labels[l] == "s" else []
             for j in nxt:
                 self.side.wait_event(begin[l])
+                self._io_wait(self.side, max(j - 1, 0))  # stage 1 of layer j reads hidden[j - 1]
                 with torch.cuda.stream(self.side):
                     self._stage1(j)
             lay = self.layers[l]
@@ -389,7 +458,10 @@ class DecodeEngine:
                     self._span("sparse_append", l, t0, main)
             if self.world > 1 and not self._no_collective:
                 self._all_gather(l)
+            self._io_output(main, l)
         main.wait_stream(self.side)
+        if self._io_capture is not None:
+            main.wait_stream(self.io)
 
     def _all_gather(self, l: int) -> None:
         """The layer's one exchange: head outputs of every rank.
@@ -411,7 +483,10 @@ class DecodeEngine:
         """Run one decode step; returns this rank's outputs [L, units*G, d]
         (fp32, device).  With inputs None the static buffers are used."""
         if hidden is not None:
-            self.load_step(hidden, queries, new_keys, new_values)
+            if self._host_io and self.graph is not None:
+                self._stage_inputs(hidden, queries, new_keys, new_values)
+            else:
+                self.load_step(hidden, queries, new_keys, new_values)
         if self.steps_done >= self.max_steps:
             raise ConfigError("engine max_steps exhausted")
         if self.graph is not None:
@@ -423,6 +498,30 @@ class DecodeEngine:
             self._run_step()
             self.steps_done += 1
         return self.out
+
+    def _stage_inputs(self, hidden, queries, new_keys, new_values) -> None:
+        """Write one step's host inputs (full or rank slice, as load_step) into the pinned staging that the
+        host-I/O graph copies from, once the previous replay has read it."""
+        self._inputs_read.synchronize()
+
+        def sl(x, heads_per_unit):
+            if not isinstance(x, torch.Tensor):
+                x = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float16)))
+            return slice_step_input(x, self.shard, self.batch, self.model.num_kv_heads, heads_per_unit, self.world)
+
+        for dst, x, hpu in zip(self.host_inputs, (hidden, queries, new_keys, new_values), (0, self.G, 1, 1)):
+            dst.copy_(sl(x, hpu).reshape(dst.shape))
+
+    def step_host(self, hidden, queries, new_keys, new_values) -> torch.Tensor:
+        """One decode step with host inputs and host outputs through the host-I/O graph
+        (``capture(host_io=True)``): the inputs are staged in pinned memory, the graph copies them in
+        (the first two layers' slices first) and copies every layer's output back as soon as the layer is
+        done, both on their own stream beside the layers.  Returns the pinned host output [L, units*G, d]
+        (fp32), complete once the stream has reached the end of the step."""
+        if not (self._host_io and self.graph is not None):
+            raise ConfigError("step_host needs capture(host_io=True)")
+        self.step(hidden, queries, new_keys, new_values)
+        return self.host_out
 
     def step_profiled(self, hidden=None, queries=None, new_keys=None, new_values=None) -> dict:
         """One eager step with CUDA events around every kernel group; returns
@@ -439,19 +538,34 @@ class DecodeEngine:
         self.profile = None
         return res
 
-    def capture(self) -> None:
+    def capture(self, host_io: bool = False) -> None:
         """Capture one decode step in a CUDA graph; ``step`` then replays it.
         Capturing executes nothing, so the caches do not advance; the host
-        mirrors of the token counts are restored afterwards."""
+        mirrors of the token counts are restored afterwards.  With
+        ``host_io`` the graph also copies the step's inputs in from pinned
+        host staging and its outputs back to pinned host memory
+        (``step_host``)."""
         if self._host_collective:
             raise ConfigError("capture needs the nccl backend (the gloo all-gather is host-staged)")
+        if host_io and self.host_inputs is None:
+            self.host_inputs = tuple(torch.empty(x.shape, dtype=x.dtype).pin_memory()
+                                     for x in (self.hidden, self.queries, self.new_keys, self.new_values))
+            self.host_out = torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()
+            self.io = torch.cuda.Stream(device=self.device)
+            self._inputs_read = torch.cuda.Event()
+            self._inputs_read.record()  # materialise the CUDA event outside the capture
         saved = [lay.n for lay in self.layers]
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph(keep_graph=True)
-        with torch.cuda.graph(g):
-            self._run_step()
+        self._io_capture = {} if host_io else None
+        try:
+            with torch.cuda.graph(g):
+                self._run_step()
+        finally:
+            self._io_capture = None
         for lay, n in zip(self.layers, saved):
             lay.n = n
+        self._host_io = host_io
         self.graph = _PriorityGraph(g)
 
     def capture_profiled(self) -> None:

@@ -177,3 +177,33 @@ def test_engine_two_ranks_match_one_rank(tkv, batch):
                 assert np.array_equal(cnt, rcnt.reshape(-1)) and np.array_equal(fc, rfc.reshape(-1))
                 for u in range(cnt.shape[0]):
                     assert np.array_equal(idx[u, :cnt[u]], ridx.reshape(-1, ridx.shape[-1])[u, :cnt[u]])
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_engine_host_io_graph_matches_device_graph(tkv, batch):
+    """DecodeEngine.step_host (capture(host_io=True): the graph copies the
+    staged host inputs in and every layer's output back, on a copy stream
+    beside the layers) gives bit-identical outputs to the device-resident
+    graph fed the same inputs, step after step."""
+    from paper_2505_19586_b200.synth import make_workload
+
+    L, hq, h, d, n, T = 4, 8, 2, 128, 3000, 5
+    hidden = hq * d
+    w = make_workload(L, [1], hq, h, d, n, T, batch=batch, seed=23)
+    cfg = tkv.EngineConfig(bits=1, n_local=64, n_topk=96, critical_channels=8)
+    model = tkv.ModelConfig(L, hq, h, d, hidden)
+    engs = []
+    for host_io in (False, True):
+        eng = tkv.DecodeEngine(model, w.labels, cfg, batch=batch, max_steps=T)
+        for l in range(L):
+            eng.prefill(l, w.prefill_keys[l], w.prefill_values[l], w.w_q[l])
+        eng.capture(host_io=host_io)
+        engs.append(eng)
+    dev, hio = engs
+    for t in range(T):
+        ref = dev.step(w.hidden[t], w.queries[t], w.new_keys[t], w.new_values[t]).cpu().numpy()
+        host = hio.step_host(w.hidden[t].cpu(), w.queries[t].cpu(), w.new_keys[t].cpu(), w.new_values[t].cpu())
+        torch.cuda.synchronize()
+        assert host.device.type == "cpu" and host.is_pinned()
+        np.testing.assert_array_equal(host.numpy(), ref, err_msg=f"step {t}")
+        np.testing.assert_array_equal(hio.out.cpu().numpy(), ref, err_msg=f"step {t}")
