@@ -7,7 +7,7 @@ set -u
 OUT=gpurun_out
 mkdir -p $OUT
 TAG=${1:-r2}
-BENCH="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-fidelity"
+BENCH="python bench.py --steps 5 --warmup 3 --cache-warm 0 --no-cpu-baseline --no-fidelity"
 NCU=ncu
 # only this repo's kernels (matched on their base names); the keys-over-PCIe variant runs first
 # (2 + 5 + 2 steps x 64 launches = 576), so -s 700 -c 64 is one step of the main mode
