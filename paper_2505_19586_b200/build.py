@@ -17,8 +17,9 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtailorkv.so"
 SOURCES = ["abi.cu", "qcache.cu", "decode.cu", "decode_imma.cu", "sparse.cu", "sparse_fused.cu", "calibrate.cu", "fidelity.cu", "refops.cu", "sparse_wide.cu"]
-# extra objects: (source, object stem, defines) -- the fused sparse kernel again with 4-CTA clusters
-VARIANTS = [("sparse_fused.cu", "sparse_fused4", ["-DTKV_FZ_CTAS=4"])]
+# extra objects: (source, object stem, defines) -- the fused sparse kernel again with 4- and 2-CTA clusters
+VARIANTS = [("sparse_fused.cu", "sparse_fused4", ["-DTKV_FZ_CTAS=4"]),
+            ("sparse_fused.cu", "sparse_fused2", ["-DTKV_FZ_CTAS=2"])]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

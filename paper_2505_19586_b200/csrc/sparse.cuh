@@ -20,12 +20,20 @@ int64_t sparse_attn_workspace(int units, int G, int d, int max_rows);
 int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t *sel_idx, const int32_t *sel_count,
                      int n_local, int max_rows, int keys_from_device, float *out, void *ws, cudaStream_t st);
 bool sparse_decode_supported(const SL &s, int G, int n_local);
+int max_active_clusters(int d, int G);
+#define TKV_FZ_VARIANT_DECLS                                                                                      \
+  bool sparse_decode_supported(const SL &s, int G, int n_local);                                                 \
+  int max_active_clusters(int d, int G);                                                                         \
+  int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s,          \
+                          int n_local, int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count,    \
+                          int keys_from_device, float *out, const uint16_t *new_keys, const uint16_t *new_values, \
+                          cudaStream_t st);
 namespace fz4 {  // the same kernel with 4-CTA clusters (sparse_fused.cu built with TKV_FZ_CTAS=4)
-bool sparse_decode_supported(const SL &s, int G, int n_local);
-int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
-                        int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
-                        float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st);
+TKV_FZ_VARIANT_DECLS
 }  // namespace fz4
+namespace fz2 {  // and with 2-CTA clusters (TKV_FZ_CTAS=2)
+TKV_FZ_VARIANT_DECLS
+}  // namespace fz2
 namespace wide {  // the wide decode (sparse_wide.cu): P CTAs per unit, for few units per GPU
 bool supported(const SL &s, int G, int n_local, int d_s, int keys_from_device, bool cluster_ok);
 int64_t ctl_bytes(int units, int d);      // per-unit counters + histograms (zero between launches)

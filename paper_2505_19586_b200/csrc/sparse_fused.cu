@@ -30,6 +30,7 @@
 // returns; the 1 MB of keys of a 128k-token head stays on chip.
 #include <cooperative_groups.h>
 
+#include <climits>
 #include <string>
 
 #include "common.cuh"
@@ -42,11 +43,13 @@ namespace cg = cooperative_groups;
 #endif
 
 namespace tkv {
-// This file is compiled twice (build.py): 8-CTA clusters in namespace tkv, and 4-CTA
-// clusters in tkv::fz4 for many units at shorter contexts (batch decode: twice the
-// co-resident units per wave).
+// This file is compiled three times (build.py): 8-CTA clusters in namespace tkv, and 4- and
+// 2-CTA clusters in tkv::fz4 / tkv::fz2 for many units at shorter contexts (batch decode:
+// more co-resident units per wave).
 #if TKV_FZ_CTAS != 8
-namespace fz4 {
+#define TKV_FZ_NS_(n) fz##n
+#define TKV_FZ_NS(n) TKV_FZ_NS_(n)
+namespace TKV_FZ_NS(TKV_FZ_CTAS) {
 #endif
 constexpr int FZ_CTAS = TKV_FZ_CTAS;
 constexpr int FZ_THREADS = 512;
@@ -2178,18 +2181,68 @@ bool sparse_decode_supported(const SL &s, int G, int n_local) {
   return (s.d == 128 && G <= 8) || (s.d == 64 && G <= 8) || (s.d == 256 && G <= 4) || (s.d == 32 && G <= 8);
 }
 
+// clusters of this size that can be resident at once (cudaOccupancyMaxActiveClusters), per kernel instance
+template <int D, int GMAX>
+static int active_clusters() {
+  static int n = -1;
+  if (n < 0) {
+    auto kern = sparse_fused_kernel<true, D, GMAX>;
+    const size_t sm = sizeof(FzShared);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(FZ_CTAS, 1024);
+    cfg.blockDim = dim3(FZ_THREADS);
+    cfg.dynamicSmemBytes = sm;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = FZ_CTAS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    n = c;
+  }
+  return n;
+}
+
+int max_active_clusters(int d, int G) {
+  if (d == 128 && G <= 4) return active_clusters<128, 4>();
+  if (d == 128 && G <= 8) return active_clusters<128, 8>();
+  if (d == 64 && G <= 8) return active_clusters<64, 8>();
+  if (d == 32 && G <= 8) return active_clusters<32, 8>();
+  if (d == 256 && G <= 4) return active_clusters<256, 4>();
+  return 0;
+}
+
 // fused select + gather + attention (tkv_sparse_decode)
 int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
                         float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st) {
 #if TKV_FZ_CTAS == 8
-  // More units than 8-CTA clusters fit at once (15 on a B200) and a context that 4 CTAs
-  // cover: 4-CTA clusters run twice the units per wave.  TKV_FZ4=0/1 overrides.
+  // Cluster size: the fewest waves of co-resident clusters over the units (a launch takes about the same
+  // time per wave whatever the cluster size: DESIGN.md 4.7), larger clusters on ties; a size is eligible when
+  // its CTAs can hold a unit's candidate slice.  B200, d 128: 8-CTA clusters 15 at once, 4-CTA 33, 2-CTA 74.
+  // TKV_FZ_CLUSTER=8|4|2 forces a size (when eligible).
   {
-    static const int force = getenv("TKV_FZ4") ? atoi(getenv("TKV_FZ4")) : -1;
-    const bool fits4 = fz4::sparse_decode_supported(s, G, n_local);
-    if (fits4 && (force == 1 || (force < 0 && s.units > 15)))
+    static const int force = getenv("TKV_FZ_CLUSTER") ? atoi(getenv("TKV_FZ_CLUSTER")) : 0;
+    const int m8 = max_active_clusters(s.d, G);
+    const bool ok4 = fz4::sparse_decode_supported(s, G, n_local), ok2 = fz2::sparse_decode_supported(s, G, n_local);
+    const int m4 = ok4 ? fz4::max_active_clusters(s.d, G) : 0, m2 = ok2 ? fz2::max_active_clusters(s.d, G) : 0;
+    auto waves = [&](int m) { return m > 0 ? (s.units + m - 1) / m : INT_MAX; };
+    int c = 8, w = waves(m8);
+    if (waves(m4) < w) c = 4, w = waves(m4);
+    if (waves(m2) < w) c = 2, w = waves(m2);
+    if (force == 8 || (force == 4 && ok4) || (force == 2 && ok2)) c = force;
+    if (c == 4)
       return fz4::sparse_decode_fused(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
+                                      keys_from_device, out, new_keys, new_values, st);
+    if (c == 2)
+      return fz2::sparse_decode_fused(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                                       keys_from_device, out, new_keys, new_values, st);
   }
 #endif
@@ -2209,7 +2262,7 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
 }
 
 #if TKV_FZ_CTAS != 8
-}  // namespace fz4
+}  // namespace fz4 / fz2
 }  // namespace tkv
 #else
 }  // namespace tkv
