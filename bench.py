@@ -544,10 +544,17 @@ def main():
     raw = (C.c_ulonglong * (128 * 3))()
     cnt = lib.tkv_debug_sparse_launches(raw, 0)
     stamps = [(raw[i * 3], raw[i * 3 + 1], raw[i * 3 + 2]) for i in range(min(cnt, 128))]
-    sparse_kernel = "cluster (sparse_fused_kernel, one 8-CTA cluster per unit)"
-    if not stamps:  # the wide decode ran (few units per GPU)
+    path = lib.tkv_debug_sparse_path()  # what the dispatch chose: cluster size, 0 wide, -1 unfused
+    if path == 0:  # the wide decode
         stamps = wide_launches(lib)
         sparse_kernel = f"wide (sparse_wide_kernel, {_lib.wide_parts(eng.units)} CTAs per unit)"
+    elif path > 0:
+        sparse_kernel = f"cluster (sparse_fused_kernel, one {path}-CTA cluster per unit)"
+        if path != 8:
+            stamps = []  # (the launch stamps are recorded by the 8-CTA build only)
+    else:
+        sparse_kernel = "unfused (select, gather + attention, append)"
+        stamps = []
     plain = None
     if len(stamps) >= 2 and not args.unfused:
         ends = [x[2] for x in stamps]

@@ -320,6 +320,11 @@ static void decode_ws_parts(int units, int d, int64_t *ctl_b, int64_t *scr_b) {
   *scr_b = (wide::scratch_bytes(units, d) + 255) / 256 * 256;
 }
 
+// which kernel the last tkv_sparse_decode dispatched: cluster size (8, 4, 2) of the fused cluster kernel,
+// 0 the wide decode, -1 the unfused three-launch path (host-side dispatch; a captured graph keeps it)
+static int g_sparse_path = -2;
+int tkv_debug_sparse_path(void) { return g_sparse_path; }
+
 int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *channels,
                       int32_t d_s, int32_t n_local, int32_t n_topk, int32_t *sel_idx, int32_t *sel_count,
                       int32_t *fetch_count, int32_t keys_from_device, const uint16_t *new_keys,
@@ -335,12 +340,18 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
   int64_t ctl_b, scr_b;
   decode_ws_parts(s->units, s->d, &ctl_b, &scr_b);
   char *ws0 = static_cast<char *>(workspace);
-  if (wide::supported(*s, G, n_local, d_s, keys_from_device, sparse_decode_supported(*s, G, n_local)))
+  if (wide::supported(*s, G, n_local, d_s, keys_from_device, sparse_decode_supported(*s, G, n_local))) {
+    g_sparse_path = 0;
     return wide::decode(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                         keys_from_device, out, new_keys, new_values, ws0, ws0 + ctl_b, as_stream(stream));
-  if (sparse_decode_supported(*s, G, n_local))
-    return sparse_decode_fused(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
-                               keys_from_device, out, new_keys, new_values, as_stream(stream));
+  }
+  if (sparse_decode_supported(*s, G, n_local)) {
+    const int r = sparse_decode_fused(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count,
+                                      fetch_count, keys_from_device, out, new_keys, new_values, as_stream(stream));
+    g_sparse_path = last_cluster_size();
+    return r;
+  }
+  g_sparse_path = -1;
   // shapes outside the fused kernels: select, then gather + attention, then the append (three launches)
   TKV_REQUIRE(s->n_sink == 0, TKV_ERR_PARAMETER, "attention sinks need the fused sparse decode (shape unsupported)");
   pdl_note(as_stream(stream), s->len);

@@ -21,6 +21,7 @@ int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t 
                      int n_local, int max_rows, int keys_from_device, float *out, void *ws, cudaStream_t st);
 bool sparse_decode_supported(const SL &s, int G, int n_local);
 int max_active_clusters(int d, int G);
+int last_cluster_size();  // cluster size the last sparse_decode_fused dispatch chose (8, 4 or 2)
 #define TKV_FZ_VARIANT_DECLS                                                                                      \
   bool sparse_decode_supported(const SL &s, int G, int n_local);                                                 \
   int max_active_clusters(int d, int G);                                                                         \

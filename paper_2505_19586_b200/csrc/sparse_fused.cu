@@ -2219,6 +2219,11 @@ int max_active_clusters(int d, int G) {
   return 0;
 }
 
+#if TKV_FZ_CTAS == 8
+static int g_last_cluster = 0;
+int last_cluster_size() { return g_last_cluster; }
+#endif
+
 // fused select + gather + attention (tkv_sparse_decode)
 int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32_t *channels, int d_s, int n_local,
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
@@ -2238,6 +2243,7 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
     if (waves(m4) < w) c = 4, w = waves(m4);
     if (waves(m2) < w) c = 2, w = waves(m2);
     if (force == 8 || (force == 4 && ok4) || (force == 2 && ok2)) c = force;
+    g_last_cluster = c;
     if (c == 4)
       return fz4::sparse_decode_fused(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                                       keys_from_device, out, new_keys, new_values, st);
