@@ -234,9 +234,14 @@ class DecodeEngine:
         self._host_io = False
         self._io_capture = None  # capture-time state while capturing with host I/O
         self.io = None
-        self.host_inputs = None  # (hidden, queries, new_keys, new_values) pinned, shaped like the device buffers
-        self.host_out = None     # pinned copy of `out`, written by the graph every step
-        self._inputs_read = None  # event: the graph has copied the staged inputs (staging may be rewritten)
+        # two staging sets, each with its own captured graph, used alternately: the host fills set k % 2
+        # while the graph of the previous step (the other set) runs
+        self._hio_sets = None    # [(inputs (hidden, queries, new_keys, new_values) pinned, outputs pinned)] x 2
+        self._hio_graphs = None
+        self._hio_done = None    # per set: host-recorded event after its last replay
+        self._hio_next = 0
+        self.host_inputs = None  # the staging set being captured / filled
+        self.host_out = None     # the pinned output of the last step_host
 
     # -- prefill ---------------------------------------------------------------
     def _slice_kv(self, x):
@@ -290,6 +295,7 @@ class DecodeEngine:
             if self.dec_ws is None or self.dec_ws.numel() < need_dec:
                 self.dec_ws = torch.zeros(need_dec, dtype=torch.uint8, device=self.device)
         self.graph = self.prof_graph = None  # a captured step holds the old buffers: capture again
+        self._hio_graphs = None
 
     # -- one step --------------------------------------------------------------
     def load_step(self, hidden, queries, new_keys, new_values, non_blocking: bool = True) -> None:
@@ -362,9 +368,6 @@ class DecodeEngine:
                 ev = torch.cuda.Event()
                 ev.record(self.io)
                 evs.append((hi, ev))
-            # an external event-record node: the host may rewrite the staging once it has fired
-            check(_lib.load().tkv_event_record(C.c_void_p(self._inputs_read.cuda_event),
-                                               C.c_void_p(self.io.cuda_stream), 1))
         self._io_capture = {"evs": evs, "waited": set()}
 
     def _io_wait(self, stream, layer: int) -> None:
@@ -483,13 +486,24 @@ class DecodeEngine:
         """Run one decode step; returns this rank's outputs [L, units*G, d]
         (fp32, device).  With inputs None the static buffers are used."""
         if hidden is not None:
-            if self._host_io and self.graph is not None:
+            if self._host_io and self._hio_graphs is not None:
                 self._stage_inputs(hidden, queries, new_keys, new_values)
             else:
                 self.load_step(hidden, queries, new_keys, new_values)
+        elif self._host_io and self._hio_graphs is not None:
+            raise ConfigError("the host-I/O graph takes its inputs from the host: pass them (step_host)")
         if self.steps_done >= self.max_steps:
             raise ConfigError("engine max_steps exhausted")
-        if self.graph is not None:
+        if self._host_io and self._hio_graphs is not None and hidden is not None:
+            i = self._hio_next
+            self._hio_graphs[i].replay()
+            self._hio_done[i].record(torch.cuda.current_stream(self.device))
+            self.host_out = self._hio_sets[i][1]
+            self._hio_next = 1 - i
+            for lay in self.layers:
+                lay.n += 1
+            self.steps_done += 1
+        elif self.graph is not None:
             self.graph.replay()
             for lay in self.layers:
                 lay.n += 1
@@ -500,25 +514,28 @@ class DecodeEngine:
         return self.out
 
     def _stage_inputs(self, hidden, queries, new_keys, new_values) -> None:
-        """Write one step's host inputs (full or rank slice, as load_step) into the pinned staging that the
-        host-I/O graph copies from, once the previous replay has read it."""
-        self._inputs_read.synchronize()
+        """Write one step's host inputs (full or rank slice, as load_step) into the next staging set, once
+        that set's previous replay (two steps back) has finished."""
+        i = self._hio_next
+        self._hio_done[i].synchronize()
 
         def sl(x, heads_per_unit):
             if not isinstance(x, torch.Tensor):
                 x = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float16)))
             return slice_step_input(x, self.shard, self.batch, self.model.num_kv_heads, heads_per_unit, self.world)
 
-        for dst, x, hpu in zip(self.host_inputs, (hidden, queries, new_keys, new_values), (0, self.G, 1, 1)):
+        for dst, x, hpu in zip(self._hio_sets[i][0], (hidden, queries, new_keys, new_values), (0, self.G, 1, 1)):
             dst.copy_(sl(x, hpu).reshape(dst.shape))
 
     def step_host(self, hidden, queries, new_keys, new_values) -> torch.Tensor:
         """One decode step with host inputs and host outputs through the host-I/O graph
         (``capture(host_io=True)``): the inputs are staged in pinned memory, the graph copies them in
-        (the first two layers' slices first) and copies every layer's output back as soon as the layer is
-        done, both on their own stream beside the layers.  Returns the pinned host output [L, units*G, d]
-        (fp32), complete once the stream has reached the end of the step."""
-        if not (self._host_io and self.graph is not None):
+        (the first two layers' slices first) and the outputs back (all but the last L/8 layers as soon as
+        those are done), on a copy stream beside the layers.  Two staging sets alternate, so the host fills
+        the next step's inputs while this one runs.  Returns this step's pinned host output
+        [L, units*G, d] (fp32), complete once the stream has reached the end of the step and valid until
+        the step after next."""
+        if not (self._host_io and self._hio_graphs is not None):
             raise ConfigError("step_host needs capture(host_io=True)")
         self.step(hidden, queries, new_keys, new_values)
         return self.host_out
@@ -547,26 +564,37 @@ class DecodeEngine:
         (``step_host``)."""
         if self._host_collective:
             raise ConfigError("capture needs the nccl backend (the gloo all-gather is host-staged)")
-        if host_io and self.host_inputs is None:
-            self.host_inputs = tuple(torch.empty(x.shape, dtype=x.dtype).pin_memory()
-                                     for x in (self.hidden, self.queries, self.new_keys, self.new_values))
-            self.host_out = torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()
-            self.io = torch.cuda.Stream(device=self.device)
-            self._inputs_read = torch.cuda.Event()
-            self._inputs_read.record()  # materialise the CUDA event outside the capture
         saved = [lay.n for lay in self.layers]
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph(keep_graph=True)
-        self._io_capture = {} if host_io else None
-        try:
-            with torch.cuda.graph(g):
-                self._run_step()
-        finally:
-            self._io_capture = None
-        for lay, n in zip(self.layers, saved):
-            lay.n = n
+
+        def one(io_set):
+            g = torch.cuda.CUDAGraph(keep_graph=True)
+            self._io_capture = {} if io_set is not None else None
+            if io_set is not None:
+                self.host_inputs, self.host_out = io_set
+            try:
+                with torch.cuda.graph(g):
+                    self._run_step()
+            finally:
+                self._io_capture = None
+            for lay, n in zip(self.layers, saved):
+                lay.n = n
+            return _PriorityGraph(g)
+
+        if host_io:
+            if self._hio_sets is None:
+                self._hio_sets = [(tuple(torch.empty(x.shape, dtype=x.dtype).pin_memory()
+                                         for x in (self.hidden, self.queries, self.new_keys, self.new_values)),
+                                   torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()) for _ in range(2)]
+                self.io = torch.cuda.Stream(device=self.device)
+                self._hio_done = [torch.cuda.Event(), torch.cuda.Event()]
+            self._hio_graphs = [one(st) for st in self._hio_sets]
+            self._hio_next = 0
+            self.graph = self._hio_graphs[0]
+        else:
+            self._hio_graphs = None
+            self.graph = one(None)
         self._host_io = host_io
-        self.graph = _PriorityGraph(g)
 
     def capture_profiled(self) -> None:
         """Capture the decode step with an event-record node around every
