@@ -677,6 +677,19 @@ int64_t stage1_workspace(int B, int hq, int H, int d) {
 
 int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, int d, int G, const float *chmax,
            int d_s, double *q_hat, int32_t *channels, void *ws, cudaStream_t st, const SL *pf) {
+  // The scorer-column L2 prefetch pays while the columns are a small part of L2 (config 2: 16.8 MB, 1.55 vs
+  // 1.61 ms/token without); at config 3's 67 MB per layer it evicts more than it brings (4.51 ms/token
+  // without it, 5.84 with).  Above L2/4 it is skipped.
+  if (pf) {
+    static int64_t l2 = 0;
+    if (!l2) {
+      int v = 0;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      l2 = (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess && v > 0) ? v : (126ll << 20);
+    }
+    if ((int64_t)pf->units * pf->capacity * d_s * 2 > l2 / 4) pf = nullptr;
+  }
   SL pfs = {};
   if (pf) pfs = *pf;
   if (G > 16 || G * d > 2048) return fail(TKV_ERR_SHAPE, "stage 1 supports G*head_dim <= 2048 (G <= 16)");
