@@ -209,6 +209,14 @@ typedef struct tkv_sparse_layer {
    * threshold against that partition's own score moments, running mean of
    * its step-to-step change).  Like `thresh`, it only aims the search. */
   float *part_hint;
+  /* Optional [units] int32, zero-initialised: a device-side handshake with stage 1 that replaces a
+   * stream/graph dependency of the decode on stage 1.  tkv_stage1 (given this layer as prefetch_layer)
+   * stores 1 for a unit once its critical channels are written; the fused cluster decode waits for 1
+   * before it reads the channels and stores 0 when it is done.  Only for decodes that leave SMs free for
+   * stage 1 (the caller's choice; the wait is bounded: an error flag, never a hang).  NULL = none. */
+  int32_t *s1_ready;
+  /* stage-1 options for this layer: bit 0 = no scorer-column L2 prefetch */
+  int32_t s1_flags;
 } tkv_sparse_layer;
 
 /* Token partitions per unit of the wide sparse decode (and slot_hand stride). */
@@ -269,6 +277,14 @@ int64_t tkv_sparse_attn_workspace(int32_t units, int32_t G, int32_t d, int32_t m
 int tkv_sparse_attention(const tkv_sparse_layer *s, const uint16_t *queries, int32_t G, const int32_t *sel_idx,
                          const int32_t *sel_count, int32_t n_local, int32_t max_rows, int32_t keys_from_device,
                          float *out, void *workspace, void *stream);
+
+/* Which kernel tkv_sparse_decode would run for these arguments (nothing is launched): the cluster size
+ * (8, 4 or 2) of the fused cluster kernel, 0 the wide decode, -1 the unfused three-launch path, -2 an
+ * invalid layer.  (A caller enabling the stage-1 handshake, tkv_sparse_layer.s1_ready, uses it to check
+ * that the decode leaves SMs free.) */
+int tkv_sparse_decode_plan(const tkv_sparse_layer *s, int32_t G, int32_t d_s, int32_t n_local,
+                           int32_t keys_from_device);
+
 
 /* One decode step of a sparsity-friendly layer in ONE launch (replaces
  * pipeline.py:351-376: approx_scores retriever.py:166-189 + select_topk_tokens

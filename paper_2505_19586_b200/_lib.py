@@ -60,6 +60,7 @@ class SparseLayer(C.Structure):
         ("cache_slots", C.c_int32), ("cache_window", C.c_int32), ("slot_tok", C.c_void_p), ("slot_stamp", C.c_void_p),
         ("slot_v", C.c_void_p), ("tok_slot", C.c_void_p), ("cache_stats", C.c_void_p), ("thresh", C.c_void_p),
         ("slot_hand", C.c_void_p), ("n_sink", C.c_int32), ("part_hint", C.c_void_p),
+        ("s1_ready", C.c_void_p), ("s1_flags", C.c_int32),
     ]
 
 
@@ -92,6 +93,7 @@ _SIGS = {
     "tkv_approx_scores_f64": (C.c_int, [_P, _I32, _P, _I64, _I32, _P, _P]),
     "tkv_channel_select_f64": (C.c_int, [_P, _I32, _P, _I32, _I32, _P, _P, _P]),
     "tkv_host_gather": (C.c_int, [C.POINTER(SparseLayer), _I32, _P, _I64, _P, _P, _P]),
+    "tkv_sparse_decode_plan": (C.c_int, [C.POINTER(SparseLayer), _I32, _I32, _I32, _I32]),
     "tkv_sum_at": (C.c_int, [_P, _P, _P, _P, _P]),
     "tkv_sparse_prefill": (C.c_int, [C.POINTER(SparseLayer), _P, _P, _I64, _P]),
     "tkv_sparse_append": (C.c_int, [C.POINTER(SparseLayer), _P, _P, _P]),

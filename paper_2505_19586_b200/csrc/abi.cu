@@ -320,6 +320,15 @@ static void decode_ws_parts(int units, int d, int64_t *ctl_b, int64_t *scr_b) {
   *scr_b = (wide::scratch_bytes(units, d) + 255) / 256 * 256;
 }
 
+// which kernel tkv_sparse_decode would dispatch for these arguments (same encoding as below), no launch
+int tkv_sparse_decode_plan(const tkv_sparse_layer *s, int32_t G, int32_t d_s, int32_t n_local,
+                           int32_t keys_from_device) {
+  if (validate_sparse(s)) return -2;
+  const bool cl = sparse_decode_supported(*s, G, n_local);
+  if (wide::supported(*s, G, n_local, d_s, keys_from_device, cl)) return 0;
+  return cl ? choose_cluster(*s, G, n_local) : -1;
+}
+
 // which kernel the last tkv_sparse_decode dispatched: cluster size (8, 4, 2) of the fused cluster kernel,
 // 0 the wide decode, -1 the unfused three-launch path (host-side dispatch; a captured graph keeps it)
 static int g_sparse_path = -2;

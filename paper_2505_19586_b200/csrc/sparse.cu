@@ -186,6 +186,12 @@ __device__ void stage1_select_unit(const double *__restrict__ part, int splits, 
   __syncthreads();
 }
 
+// stage 1 -> decode handshake (tkv_sparse_layer.s1_ready): channels written before the flag
+__device__ __forceinline__ void s1_signal(int32_t *flag) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
+}
+
 // Arrival counter + channel selection (+ optional scorer-column L2 prefetch)
 // run by the last CTA to finish its partials of one KV head: sequences
 // [b0, b0+nb).  qs: G*D doubles of shared memory.
@@ -208,10 +214,14 @@ __device__ __forceinline__ void stage1_tail(const double *__restrict__ part, int
   __threadfence();
   for (int b = 0; b < nb; ++b) {
     stage1_select_unit(part, splits, B, hq, D, G, chmax, d_s, q_hat, channels, b0 + b, kvh, qs, score, flags);
+    const int u = (b0 + b) * hkv + kvh;
+    if (pf.s1_ready) {  // the decode's handshake: this unit's channels are written
+      __syncthreads();
+      if (threadIdx.x == 0) s1_signal(&pf.s1_ready[u]);
+    }
     if (prefetch) {
       // start moving the selected channel rows of the layer's scorer keys into L2: the
       // layer's decode kernel (next on the main stream) then scores from L2, not HBM
-      const int u = (b0 + b) * hkv + kvh;
       const int64_t len = *pf.len;
       const int64_t bytes = len * 2;
       const int64_t nch = (bytes + 32767) / 32768;
@@ -429,6 +439,7 @@ __device__ __forceinline__ void stage1_warp_select(const double *__restrict__ qg
     before += __popc(m);
   }
   __syncwarp();
+  if (pf.s1_ready && lane == 0) s1_signal(&pf.s1_ready[(b_off + b) * hkv + kvh]);
   if (prefetch) {
     // start moving the selected channel rows of the layer's scorer keys into L2: the
     // layer's decode kernel (next on the main stream) then scores from L2, not HBM
@@ -680,7 +691,9 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
   // The scorer-column L2 prefetch pays while the columns are a small part of L2 (config 2: 16.8 MB, 1.55 vs
   // 1.61 ms/token without); at config 3's 67 MB per layer it evicts more than it brings (4.51 ms/token
   // without it, 5.84 with).  Above L2/4 it is skipped.
-  if (pf) {
+  // (the layer also carries the decode handshake flags, tkv_sparse_layer.s1_ready, set whatever the prefetch)
+  bool do_pf = pf != nullptr && !(pf->s1_flags & 1);
+  if (do_pf) {
     static int64_t l2 = 0;
     if (!l2) {
       int v = 0;
@@ -688,7 +701,7 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
       cudaGetDevice(&dev);
       l2 = (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess && v > 0) ? v : (126ll << 20);
     }
-    if ((int64_t)pf->units * pf->capacity * d_s * 2 > l2 / 4) pf = nullptr;
+    if ((int64_t)pf->units * pf->capacity * d_s * 2 > l2 / 4) do_pf = false;
   }
   SL pfs = {};
   if (pf) pfs = *pf;
@@ -741,7 +754,7 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
       attr = true;                                                                                          \
     }                                                                                                       \
     e = cudaLaunchKernelEx(&cfg, stage1_mma_kernel<DD>, hb, w_q, nb, H, rows, part, arrive, G, mb, d_s, qb,  \
-                           cbp, pfs, pf ? 1 : 0, b0);                                                       \
+                           cbp, pfs, do_pf ? 1 : 0, b0);                                                       \
   }
       if (smem > 160 * 1024) return fail(TKV_ERR_SHAPE, "stage 1: hidden size too large for the split plan");
       switch (d) {
@@ -776,9 +789,9 @@ int stage1(const uint16_t *hidden, const uint16_t *w_q, int B, int hq, int H, in
   }
 #define TKV_S1(DD)                                                                                              \
   (B == 1 ? launch_prio(stage1_fused_kernel<DD, 1, 256>, grid, dim3(256), 0, st, false, hidden, w_q, B, H, rows,  \
-                        part, arrive, G, chmax, d_s, q_hat, channels, pfs, pf ? 1 : 0)                           \
+                        part, arrive, G, chmax, d_s, q_hat, channels, pfs, do_pf ? 1 : 0)                           \
           : launch_prio(stage1_fused_kernel<DD, S1_BG>, grid, dim3(S1_THREADS), 0, st, false, hidden, w_q, B, H,  \
-                        rows, part, arrive, G, chmax, d_s, q_hat, channels, pfs, pf ? 1 : 0))
+                        rows, part, arrive, G, chmax, d_s, q_hat, channels, pfs, do_pf ? 1 : 0))
   switch (d) {
     case 128: TKV_S1(128); break;
     case 64: TKV_S1(64); break;

@@ -22,6 +22,7 @@ int sparse_attention(const SL &s, const uint16_t *queries, int G, const int32_t 
 bool sparse_decode_supported(const SL &s, int G, int n_local);
 int max_active_clusters(int d, int G);
 int last_cluster_size();  // cluster size the last sparse_decode_fused dispatch chose (8, 4 or 2)
+int choose_cluster(const SL &s, int G, int n_local);  // the cluster size sparse_decode_fused picks
 #define TKV_FZ_VARIANT_DECLS                                                                                      \
   bool sparse_decode_supported(const SL &s, int G, int n_local);                                                 \
   int max_active_clusters(int d, int G);                                                                         \

@@ -474,6 +474,25 @@ __device__ __forceinline__ void fz_bulk_commit_wait_read() {
 
 // phase timestamps of unit 0, every CTA (debug: tkv_debug_sparse_phases)
 constexpr int FZ_NMARK = 40;
+// stage-1 handshake wait, bounded (~2 s): a missing signal becomes an error flag, never a hang
+__device__ unsigned g_fz_s1_timeout = 0;
+__device__ __forceinline__ void fz_wait_ready(const int32_t *flag) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  if (v) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(100);
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!v && t - t0 > 2000000000ull) {
+      atomicExch(&g_fz_s1_timeout, 1u);
+      return;
+    }
+  } while (!v);
+}
+
 __device__ unsigned long long g_fz_phase[FZ_CTAS][FZ_NMARK];
 __device__ int g_fz_trace;  // set by tkv_debug_sparse_trace
 __device__ double g_fz_dbg[2][8];  // list-path attempts of unit 0 (debug)
@@ -569,6 +588,11 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     const uint16_t *src = (half ? new_values : new_keys) + (size_t)u * D + c8;
     *reinterpret_cast<uint4 *>(s.host_kv + (((size_t)u * s.capacity + n) * 2 + half) * D + c8) =
         *reinterpret_cast<const uint4 *>(src);
+  }
+  // stage-1 handshake (tkv_sparse_layer.s1_ready): wait until this unit's channels are written
+  if (ATTEND && s.s1_ready) {
+    if (tid == 0) fz_wait_ready(&s.s1_ready[u]);
+    __syncthreads();
   }
   bool listed = false;                 // candidate-list path: flags come from keys32 + bitmap
   uint32_t ord_def = 0xffffffffu;      // (list path) keys above this orderable value are selected
@@ -1983,6 +2007,8 @@ __global__ void __launch_bounds__(FZ_THREADS, 1)
     }
     FZ_MARK(16);
     asm volatile("griddepcontrol.launch_dependents;");  // the next layer's kernel may start its prologue
+    // every CTA of the cluster read its channels before the selection's cluster barriers: re-arm the handshake
+    if (s.s1_ready && rank == 0 && tid == 0) s.s1_ready[u] = 0;
     __syncthreads();  // the staging area (aliased by the partials) is no longer read
     FZ_MARK(17);
     float *pm = reinterpret_cast<float *>(S.k.raw), *pl = pm + FZ_WARPS * GMAX, *pa = pl + FZ_WARPS * GMAX;
@@ -2222,6 +2248,23 @@ int max_active_clusters(int d, int G) {
 #if TKV_FZ_CTAS == 8
 static int g_last_cluster = 0;
 int last_cluster_size() { return g_last_cluster; }
+
+// Cluster size: the fewest waves of co-resident clusters over the units (a launch takes about the same
+// time per wave whatever the cluster size: DESIGN.md 4.7), larger clusters on ties; a size is eligible when
+// its CTAs can hold a unit's candidate slice.  B200, d 128: 8-CTA clusters 15 at once, 4-CTA 33, 2-CTA 74.
+// TKV_FZ_CLUSTER=8|4|2 forces a size (when eligible).
+int choose_cluster(const SL &s, int G, int n_local) {
+  static const int force = getenv("TKV_FZ_CLUSTER") ? atoi(getenv("TKV_FZ_CLUSTER")) : 0;
+  const int m8 = max_active_clusters(s.d, G);
+  const bool ok4 = fz4::sparse_decode_supported(s, G, n_local), ok2 = fz2::sparse_decode_supported(s, G, n_local);
+  const int m4 = ok4 ? fz4::max_active_clusters(s.d, G) : 0, m2 = ok2 ? fz2::max_active_clusters(s.d, G) : 0;
+  auto waves = [&](int m) { return m > 0 ? (s.units + m - 1) / m : INT_MAX; };
+  int c = 8, w = waves(m8);
+  if (waves(m4) < w) c = 4, w = waves(m4);
+  if (waves(m2) < w) c = 2, w = waves(m2);
+  if (force == 8 || (force == 4 && ok4) || (force == 2 && ok2)) c = force;
+  return c;
+}
 #endif
 
 // fused select + gather + attention (tkv_sparse_decode)
@@ -2229,20 +2272,8 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
                         int n_topk, int32_t *sel_idx, int32_t *sel_count, int32_t *fetch_count, int keys_from_device,
                         float *out, const uint16_t *new_keys, const uint16_t *new_values, cudaStream_t st) {
 #if TKV_FZ_CTAS == 8
-  // Cluster size: the fewest waves of co-resident clusters over the units (a launch takes about the same
-  // time per wave whatever the cluster size: DESIGN.md 4.7), larger clusters on ties; a size is eligible when
-  // its CTAs can hold a unit's candidate slice.  B200, d 128: 8-CTA clusters 15 at once, 4-CTA 33, 2-CTA 74.
-  // TKV_FZ_CLUSTER=8|4|2 forces a size (when eligible).
-  {
-    static const int force = getenv("TKV_FZ_CLUSTER") ? atoi(getenv("TKV_FZ_CLUSTER")) : 0;
-    const int m8 = max_active_clusters(s.d, G);
-    const bool ok4 = fz4::sparse_decode_supported(s, G, n_local), ok2 = fz2::sparse_decode_supported(s, G, n_local);
-    const int m4 = ok4 ? fz4::max_active_clusters(s.d, G) : 0, m2 = ok2 ? fz2::max_active_clusters(s.d, G) : 0;
-    auto waves = [&](int m) { return m > 0 ? (s.units + m - 1) / m : INT_MAX; };
-    int c = 8, w = waves(m8);
-    if (waves(m4) < w) c = 4, w = waves(m4);
-    if (waves(m2) < w) c = 2, w = waves(m2);
-    if (force == 8 || (force == 4 && ok4) || (force == 2 && ok2)) c = force;
+  {  // cluster size (choose_cluster)
+    const int c = choose_cluster(s, G, n_local);
     g_last_cluster = c;
     if (c == 4)
       return fz4::sparse_decode_fused(s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
@@ -2272,6 +2303,14 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
 }  // namespace tkv
 #else
 }  // namespace tkv
+
+// 1 when a fused decode (8-CTA build) gave up waiting for the stage-1 handshake (then reset to 0)
+extern "C" int tkv_debug_sparse_s1_timeout(void) {
+  unsigned v = 0, z = 0;
+  if (cudaMemcpyFromSymbol(&v, tkv::g_fz_s1_timeout, sizeof(v)) != cudaSuccess) return -1;
+  cudaMemcpyToSymbol(tkv::g_fz_s1_timeout, &z, sizeof(z));
+  return (int)v;
+}
 
 extern "C" int tkv_debug_sparse_trace(int on) {
   return cudaMemcpyToSymbol(tkv::g_fz_trace, &on, sizeof(int)) == cudaSuccess ? 0 : 7;

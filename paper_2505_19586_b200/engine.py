@@ -58,6 +58,8 @@ class EngineConfig:
     fused_sparse: bool = True      # one launch per sparse layer (select + gather + attention); else two
     scorer_l2_prefetch: bool = True  # stage 1 starts moving the chosen scorer columns into L2
     overlap_stage1: bool = True    # stage 1 of layer l+1 runs on a side stream during layer l (else in line)
+    stage1_handshake: bool | None = None  # decode waits for stage 1 on a device flag, not a stream edge
+                                          # (None: when the fused decode leaves half the SMs free)
     quant_impl: int = 0            # 0 auto, 1 SIMT, 2 tensor-core
 
     def validate(self) -> None:
@@ -227,6 +229,7 @@ class DecodeEngine:
         self._event_pool = None
         self.prof_graph = None
         self.keys_from_hbm = config.keys_from_hbm
+        self._s1_sync = None  # decided at the first sparse prefill (stage-1 handshake on/off)
         self.last_channels: dict[int, torch.Tensor] = {}
         self.last_selection: dict[int, tuple] = {}
         # host I/O inside the captured step (capture(host_io=True)): pinned staging for the step inputs and
@@ -286,6 +289,9 @@ class DecodeEngine:
             chans = torch.zeros((self.units, self.retrieval.d_s), dtype=torch.int32, device=self.device)
             self.sparse[layer] = _SparseState(lay, w, chans, ws)
             self.layers[layer] = lay
+            if self._s1_sync is None:
+                self._s1_sync = self._stage1_handshake_ok(lay)
+            lay.set_stage1_handshake(self._s1_sync, l2_prefetch=self.cfg.scorer_l2_prefetch)
             # workspaces follow the largest layer capacity seen so far (prefill lengths may differ per layer)
             kmax = self.retrieval.max_selected
             need_sel = int(lib.tkv_select_workspace(self.units, lay.capacity))
@@ -296,6 +302,19 @@ class DecodeEngine:
                 self.dec_ws = torch.zeros(need_dec, dtype=torch.uint8, device=self.device)
         self.graph = self.prof_graph = None  # a captured step holds the old buffers: capture again
         self._hio_graphs = None
+
+    def _stage1_handshake_ok(self, lay) -> bool:
+        """The decode may wait for stage 1 on a device flag when stage 1 is overlapped and the fused
+        cluster decode leaves at least half of the SMs free (stage 1 then always finds room to run)."""
+        c = self.cfg
+        if c.stage1_handshake is not None:
+            return bool(c.stage1_handshake) and c.fused_sparse and c.overlap_stage1
+        if not (c.fused_sparse and c.overlap_stage1):
+            return False
+        plan = int(_lib.load().tkv_sparse_decode_plan(C.byref(lay.struct), self.G, self.retrieval.d_s,
+                                                      self.retrieval.n_local, int(self.keys_from_hbm)))
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        return plan > 0 and self.units * plan <= sms // 2
 
     # -- one step --------------------------------------------------------------
     def load_step(self, hidden, queries, new_keys, new_values, non_blocking: bool = True) -> None:
@@ -317,9 +336,10 @@ class DecodeEngine:
         src = l - 1 if l >= 1 else 0  # pipeline.py:273
         t0 = self._mark(self.side)
         if not _SKIP_STAGE1:
+            # the layer goes to stage 1 for its L2 prefetch and/or the handshake flags (s1_flags says which)
             stage1_select(self.hidden[src], st.w_q, st.layer.chmax, self.G, self.retrieval.d_s,
                           channels=st.channels, workspace=st.s1_ws, stream=self.side,
-                          prefetch_layer=st.layer if self.cfg.scorer_l2_prefetch else None)
+                          prefetch_layer=st.layer if (self.cfg.scorer_l2_prefetch or self._s1_sync) else None)
         self._span("stage1", l, t0, self.side)
         st.s1_done.record(self.side)
 
@@ -436,7 +456,8 @@ class DecodeEngine:
                     self._span("quant_append", l, t0, self.side)
             else:
                 st = self.sparse[l]
-                main.wait_event(st.s1_done)
+                if not self._s1_sync:  # (with the handshake the decode waits on the device flag)
+                    main.wait_event(st.s1_done)
                 if self.cfg.fused_sparse:
                     t0 = self._mark(main)
                     lay.decode(self.queries[l], st.channels, self.G, self.retrieval, self.sel_idx, self.sel_count,

@@ -107,6 +107,7 @@ class OffloadedLayerKV:
             self.slot_hand = None
         self.thresh = torch.full((units, 4), float("nan"), dtype=torch.float32, device=dev)  # top-k threshold hint
         self.part_hint = torch.full((units, _lib.MAX_PARTS, 2), float("nan"), dtype=torch.float32, device=dev)
+        self.s1_ready = None
         self.struct = SparseLayer(units, d, self.capacity, self.local_offset, self.local_capacity,
                                   self.kt.data_ptr(), self.chmax.data_ptr(), self.loc_k.data_ptr(),
                                   self.loc_v.data_ptr(), ptr(self.kdev), self.arena.addr,
@@ -149,6 +150,17 @@ class OffloadedLayerKV:
     def _check_sinks(self, cfg: RetrievalConfig) -> None:
         if cfg.n_sink != self.n_sink:
             raise ParameterError(f"RetrievalConfig.n_sink={cfg.n_sink} but the layer was built with n_sink={self.n_sink}")
+
+    def set_stage1_handshake(self, enabled: bool, l2_prefetch: bool = True) -> None:
+        """Device-side stage-1 handshake (tkv_sparse_layer.s1_ready): stage 1, given this layer as its
+        prefetch layer, flags each unit's channels as written, and the fused cluster decode waits for the
+        flag instead of a stream dependency on stage 1 (which costs a programmatic-launch overlap per
+        layer).  Only for decodes that leave SMs free for stage 1.  ``l2_prefetch`` False keeps stage 1's
+        scorer-column L2 prefetch off while the layer is passed for the handshake."""
+        if enabled and self.s1_ready is None:
+            self.s1_ready = torch.zeros(self.units, dtype=torch.int32, device=self.kt.device)
+        self.struct.s1_ready = self.s1_ready.data_ptr() if enabled else None
+        self.struct.s1_flags = 0 if l2_prefetch else 1
 
     def set_row_cache(self, enabled: bool) -> None:
         """Switch the HBM row cache on or off for later launches (a captured

@@ -207,3 +207,31 @@ def test_engine_host_io_graph_matches_device_graph(tkv, batch):
         assert host.device.type == "cpu" and host.is_pinned()
         np.testing.assert_array_equal(host.numpy(), ref, err_msg=f"step {t}")
         np.testing.assert_array_equal(hio.out.cpu().numpy(), ref, err_msg=f"step {t}")
+
+
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "graph"])
+def test_engine_stage1_handshake_matches_stream_edge(tkv, graph):
+    """The device-side stage-1 handshake (the decode waits on tkv_sparse_layer.s1_ready instead of a
+    stream dependency on stage 1) gives bit-identical outputs and selections to the stream edge, with
+    stage 1 overlapped, and never times out."""
+    from paper_2505_19586_b200 import _lib
+    from paper_2505_19586_b200.synth import make_workload
+
+    L, hq, h, d, n, T = 5, 8, 2, 128, 3000, 5
+    w = make_workload(L, [1], hq, h, d, n, T, batch=1, seed=29)
+    model = tkv.ModelConfig(L, hq, h, d, hq * d)
+    outs = {}
+    for hs in (False, True):
+        cfg = tkv.EngineConfig(bits=1, n_local=64, n_topk=96, critical_channels=8, stage1_handshake=hs)
+        eng = tkv.DecodeEngine(model, w.labels, cfg, batch=1, max_steps=T)
+        for l in range(L):
+            eng.prefill(l, w.prefill_keys[l], w.prefill_values[l], w.w_q[l])
+        assert eng._s1_sync is hs
+        if graph:
+            eng.capture()
+        outs[hs] = [eng.step(w.hidden[t], w.queries[t], w.new_keys[t], w.new_values[t]).cpu().numpy().copy()
+                    for t in range(T)]
+        torch.cuda.synchronize()
+    assert _lib.load().tkv_debug_sparse_s1_timeout() == 0
+    for t in range(T):
+        np.testing.assert_array_equal(outs[True][t], outs[False][t], err_msg=f"step {t}")
