@@ -145,6 +145,9 @@ def wide_show(lib, parts=18):
     mk = (C.c_ulonglong * (32 * 32))()
     lib.tkv_debug_wide_marks(mk)
     t = [list(mk)[p * 32:(p + 1) * 32] for p in range(min(parts, 32))]
+    if not any(x[1] for x in t):
+        print("  (the wide decode did not run)")
+        return
     t0 = min(x[1] for x in t if x[1])
     for p, x in enumerate(t):
         parts_s, prev = [], x[1]
