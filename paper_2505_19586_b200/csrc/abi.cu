@@ -350,6 +350,8 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
   decode_ws_parts(s->units, s->d, &ctl_b, &scr_b);
   char *ws0 = static_cast<char *>(workspace);
   if (wide::supported(*s, G, n_local, d_s, keys_from_device, sparse_decode_supported(*s, G, n_local))) {
+    TKV_REQUIRE(s->s1_ready == nullptr, TKV_ERR_PARAMETER,
+                "the stage-1 handshake (s1_ready) needs the fused cluster decode, not the wide decode");
     g_sparse_path = 0;
     return wide::decode(*s, queries, G, channels, d_s, n_local, n_topk, sel_idx, sel_count, fetch_count,
                         keys_from_device, out, new_keys, new_values, ws0, ws0 + ctl_b, as_stream(stream));
@@ -362,6 +364,8 @@ int tkv_sparse_decode(const tkv_sparse_layer *s, const uint16_t *queries, int32_
   }
   g_sparse_path = -1;
   // shapes outside the fused kernels: select, then gather + attention, then the append (three launches)
+  TKV_REQUIRE(s->s1_ready == nullptr, TKV_ERR_PARAMETER,
+              "the stage-1 handshake (s1_ready) needs the fused cluster decode");
   TKV_REQUIRE(s->n_sink == 0, TKV_ERR_PARAMETER, "attention sinks need the fused sparse decode (shape unsupported)");
   pdl_note(as_stream(stream), s->len);
   char *ws = ws0 + ctl_b + scr_b;

@@ -423,7 +423,18 @@ class DecodeEngine:
         with torch.cuda.stream(self.io):
             self.host_out[lo:l + 1].copy_(self.out[lo:l + 1], non_blocking=True)
 
+    def _recheck_handshake(self) -> None:
+        """The dispatch can change after prefill (set_sparse_kernel / TKV_WIDE): keep the stage-1 handshake
+        only while the fused cluster decode still runs (the wide decode neither waits nor re-arms)."""
+        if self._s1_sync and self.sparse:
+            lay = next(iter(self.sparse.values())).layer
+            if not self._stage1_handshake_ok(lay) and self.cfg.stage1_handshake is None:
+                self._s1_sync = False
+                for st in self.sparse.values():
+                    st.layer.set_stage1_handshake(False, l2_prefetch=self.cfg.scorer_l2_prefetch)
+
     def _run_step(self) -> None:
+        self._recheck_handshake()
         main = torch.cuda.current_stream(self.device)
         L = self.model.num_layers
         if self._io_capture is not None:
