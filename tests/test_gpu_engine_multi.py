@@ -217,6 +217,8 @@ def test_engine_stage1_handshake_matches_stream_edge(tkv, graph):
     from paper_2505_19586_b200 import _lib
     from paper_2505_19586_b200.synth import make_workload
 
+    if os.environ.get("TKV_WIDE") == "1":  # forced wide decode: the library rejects the handshake (tested below)
+        pytest.skip("the stage-1 handshake needs the cluster decode")
     L, hq, h, d, n, T = 5, 8, 2, 128, 3000, 5
     w = make_workload(L, [1], hq, h, d, n, T, batch=1, seed=29)
     model = tkv.ModelConfig(L, hq, h, d, hq * d)
@@ -235,3 +237,28 @@ def test_engine_stage1_handshake_matches_stream_edge(tkv, graph):
     assert _lib.load().tkv_debug_sparse_s1_timeout() == 0
     for t in range(T):
         np.testing.assert_array_equal(outs[True][t], outs[False][t], err_msg=f"step {t}")
+
+
+def test_stage1_handshake_rejected_on_the_wide_decode(tkv, sparse_kernel):
+    """With the wide decode dispatched, a layer carrying the stage-1 handshake is refused (it neither waits
+    nor re-arms), and the auto engine drops the handshake instead."""
+    from paper_2505_19586_b200.synth import make_workload
+
+    if sparse_kernel != "wide":
+        pytest.skip("wide decode only")
+    L, hq, h, d, n, T = 3, 8, 2, 128, 3000, 2
+    w = make_workload(L, [0], hq, h, d, n, T, batch=1, seed=31)
+    model = tkv.ModelConfig(L, hq, h, d, hq * d)
+    eng = tkv.DecodeEngine(model, w.labels, tkv.EngineConfig(bits=1, n_local=64, n_topk=96, critical_channels=8),
+                           batch=1, max_steps=T)
+    for l in range(L):
+        eng.prefill(l, w.prefill_keys[l], w.prefill_values[l], w.w_q[l])
+    assert eng._s1_sync is False
+    eng.step(w.hidden[0], w.queries[0], w.new_keys[0], w.new_values[0])
+    forced = tkv.DecodeEngine(model, w.labels, tkv.EngineConfig(bits=1, n_local=64, n_topk=96, critical_channels=8,
+                                                                stage1_handshake=True), batch=1, max_steps=T)
+    for l in range(L):
+        forced.prefill(l, w.prefill_keys[l], w.prefill_values[l], w.w_q[l])
+    with pytest.raises(tkv.ParameterError):
+        forced.step(w.hidden[0], w.queries[0], w.new_keys[0], w.new_values[0])
+    torch.cuda.synchronize()
