@@ -111,6 +111,22 @@ def _boundary_groups(rng, ngroups, glen, bits):
     return out
 
 
+@pytest.mark.parametrize("d", [32, 64, 96, 128, 256])
+@pytest.mark.parametrize("bits,g", [(1, 16), (1, 32), (1, 64), (1, 128), (2, 16), (2, 32), (2, 64)])
+def test_pack_every_instantiation_exact(tkv, d, bits, g):
+    # every (bits, group, head_dim) pack kernel instance -- the d = 64 / 128 specialisations and the
+    # generic one -- against the oracle, with a partial key tile, a residual and a partial value chunk
+    rng = np.random.default_rng(1000 + d + 10 * g + bits)
+    Tk = 16 * (8 // bits)
+    n = 2 * Tk + g + 7 if g < Tk else Tk + g + 7
+    keys = cases.f16(rng.normal(size=(2, n, d)))
+    values = cases.f16(rng.normal(size=(2, n, d)) * 3.0)
+    q = tkv.quantize_layer_kv(keys, values, bits, g)
+    for u in range(2):
+        assert q.to_bytes(u, "keys") == O.quantize_keys(keys[u], bits, g).to_bytes(), (u, "keys")
+        assert q.to_bytes(u, "values") == O.quantize_values(values[u], bits, g).to_bytes(), (u, "values")
+
+
 @pytest.mark.parametrize("bits", [1, 2])
 def test_pack_negative_zero_minimum(tkv, bits):
     # a group whose minimum is -0.0 stores the zero-point as -0.0 (0x8000), as
