@@ -2253,8 +2253,10 @@ int last_cluster_size() { return g_last_cluster; }
 // time per wave whatever the cluster size: DESIGN.md 4.7), larger clusters on ties; a size is eligible when
 // its CTAs can hold a unit's candidate slice.  B200, d 128: 8-CTA clusters 15 at once, 4-CTA 33, 2-CTA 74.
 // TKV_FZ_CLUSTER=8|4|2 forces a size (when eligible).
+static int g_cluster_force = -1;  // tkv_debug_sparse_cluster: runtime override of TKV_FZ_CLUSTER (tests)
 int choose_cluster(const SL &s, int G, int n_local) {
-  static const int force = getenv("TKV_FZ_CLUSTER") ? atoi(getenv("TKV_FZ_CLUSTER")) : 0;
+  static const int env_force = getenv("TKV_FZ_CLUSTER") ? atoi(getenv("TKV_FZ_CLUSTER")) : 0;
+  const int force = g_cluster_force >= 0 ? g_cluster_force : env_force;
   const int m8 = max_active_clusters(s.d, G);
   const bool ok4 = fz4::sparse_decode_supported(s, G, n_local), ok2 = fz2::sparse_decode_supported(s, G, n_local);
   const int m4 = ok4 ? fz4::max_active_clusters(s.d, G) : 0, m2 = ok2 ? fz2::max_active_clusters(s.d, G) : 0;
@@ -2303,6 +2305,12 @@ int sparse_decode_fused(const SL &s, const uint16_t *queries, int G, const int32
 }  // namespace tkv
 #else
 }  // namespace tkv
+
+// force the fused decode's cluster size (8, 4 or 2 when eligible; 0 = auto; -1 = TKV_FZ_CLUSTER)
+extern "C" int tkv_debug_sparse_cluster(int c) {
+  tkv::g_cluster_force = c;
+  return 0;
+}
 
 // 1 when a fused decode (8-CTA build) gave up waiting for the stage-1 handshake (then reset to 0)
 extern "C" int tkv_debug_sparse_s1_timeout(void) {

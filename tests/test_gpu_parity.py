@@ -405,6 +405,31 @@ def test_select_and_sparse_attention_match_oracle(tkv, kod, path, monkeypatch):
     assert rel_err(out.cpu().numpy(), ref_out) <= 1e-5
 
 
+@pytest.mark.parametrize("cluster", [8, 4, 2])
+@pytest.mark.parametrize("dist", ["normal", "ties", "outliers"])
+def test_fused_decode_every_cluster_size(tkv, cluster, dist):
+    """The fused decode built with 8-, 4- and 2-CTA clusters (the dispatch picks by units): selections,
+    fetch counts and outputs against the oracle, with the row cache, over two steps."""
+    import paper_2505_19586_b200._lib as L
+    rng = np.random.default_rng(300 + cluster)
+    units, n, d, G = 3, 9000, 128, 4
+    keys = cases.f16(_keys_for(dist, rng, (units, n, d)))
+    values = cases.f16(rng.normal(size=(units, n, d)))
+    cfg = tkv.RetrievalConfig(64, 300, 8)
+    lay = _sparse_layer(tkv, keys, values, cfg.n_local, keys_on_device=True, cache_rows=cfg.n_local + cfg.n_topk,
+                        cache_window=2)
+    L.load().tkv_debug_sparse_cluster(cluster)
+    try:
+        for step in range(2):
+            queries = cases.f16(rng.normal(size=(units * G, d)))
+            chans = np.stack([np.sort(rng.choice(d, 8, replace=False)) for _ in range(units)]).astype(np.int32)
+            res = _decode_once(tkv, lay, queries, chans, G, cfg, True)
+            assert L.load().tkv_debug_sparse_path() == cluster
+            assert _check_decode(keys, values, queries, chans, G, cfg, res, n) <= 1e-5
+    finally:
+        L.load().tkv_debug_sparse_cluster(-1)
+
+
 @pytest.mark.parametrize("dist", ["ties", "zeros", "normal"])
 def test_cluster_select_ties_and_sizes(tkv, dist):
     """Scorer + top-k on inputs with massive exact score ties (the cluster
