@@ -294,14 +294,9 @@ __global__ void __launch_bounds__(T, T == 256 ? 4 : 2) stage1_fused_kernel(const
   for (int b = 0; b < BG; ++b)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[b][e] = 0.0f;
+  // software pipeline: each slot is refilled with the row BATCH ahead as soon as it is consumed, so
+  // BATCH loads stay in flight through the whole stream (rows are still summed in order)
   for (int k0 = 0; k0 * RG < nrow; k0 += BATCH) {
-    if (k0 > 0) {  // next batch (the first one was issued before the barrier)
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
-        const int i = rg + RG * (k0 + k);
-        if (i < nrow) v[k] = s1_ld_nc_v4(&w[(size_t)i * TPR + cg8]);
-      }
-    }
 #pragma unroll
     for (int k = 0; k < BATCH; ++k) {
       const int i = rg + RG * (k0 + k);
@@ -310,6 +305,8 @@ __global__ void __launch_bounds__(T, T == 256 ? 4 : 2) stage1_fused_kernel(const
       float wf[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) wf[e] = h2f((uint16_t)(wv[e >> 1] >> (16 * (e & 1))));
+      const int inext = i + RG * BATCH;
+      if (inext < nrow) v[k] = s1_ld_nc_v4(&w[(size_t)inext * TPR + cg8]);
 #pragma unroll
       for (int b = 0; b < BG; ++b) {
         const float hv = hs[b][i];
